@@ -1,0 +1,424 @@
+"""Pins of the fp64 CPU oracle (runs without a GPU).
+
+Each test pins the oracle to something other than itself:
+hand-worked examples (tests/golden/*.json, cited), closed forms, invariants,
+an independent library route (torch CPU fp64 cross_entropy / autograd), finite
+differences, and brute force.  Chosen so a dropped term, wrong sign, wrong index
+or transposed operand in the oracle fails at least one of them.
+"""
+import json
+import math
+import os
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import LossParams
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ----------------------------------------------------------------------------- c3 log-probs
+def test_e1_worked_logprob():
+    # V=3, x=[0, ln2, ln3], y=2 -> lse = ln 6, logp = -ln 2, p = [1/6,1/3,1/2]
+    x = np.array([[0.0, math.log(2.0), math.log(3.0)]])
+    logp, lse = oracle.token_logprob(x, [2])
+    assert abs(lse[0] - math.log(6.0)) <= 2e-16 * 4
+    assert abs(logp[0] + math.log(2.0)) <= 2e-16 * 4
+    for y, pv in enumerate([1 / 6, 1 / 3, 1 / 2]):
+        lp, _ = oracle.token_logprob(x, [y])
+        assert abs(math.exp(lp[0]) - pv) < 1e-15
+
+
+@pytest.mark.parametrize("V", [1, 7, 1024, 128256, 151936])
+def test_constant_row_is_minus_log_v(V):
+    # closed form: uniform logits give log(1/V) (BASELINE.json north_star)
+    x = np.full((2, V), 3.25)
+    logp, _ = oracle.token_logprob(x, [0, V - 1])
+    assert np.allclose(logp, -math.log(V), atol=1e-12, rtol=0)
+
+
+def test_logp_matches_torch_cross_entropy_fp64():
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(0)
+    x = rng.normal(size=(37, 53)) * 4
+    y = rng.integers(0, 53, size=37)
+    logp, _ = oracle.token_logprob(x, y)
+    ref = -torch.nn.functional.cross_entropy(torch.tensor(x, dtype=torch.float64),
+                                             torch.tensor(y), reduction="none").numpy()
+    assert np.allclose(logp, ref, atol=1e-13, rtol=0)
+
+
+def test_logp_shift_and_permutation_invariance():
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=(9, 31)) * 3
+    y = rng.integers(0, 31, size=9)
+    base, _ = oracle.token_logprob(x, y)
+    shifted, _ = oracle.token_logprob(x + 123.5, y)
+    assert np.allclose(base, shifted, atol=1e-12)
+    perm = rng.permutation(31)
+    inv = np.argsort(perm)
+    permuted, _ = oracle.token_logprob(x[:, perm], inv[y])
+    assert np.allclose(base, permuted, atol=1e-13)
+
+
+def test_logp_ignore_and_bad_targets():
+    x = np.zeros((3, 4))
+    logp, _ = oracle.token_logprob(x, [-100, 4, 1])
+    assert logp[0] == 0.0 and math.isnan(logp[1]) and abs(logp[2] + math.log(4)) < 1e-15
+
+
+def test_temperature_scales_logits():
+    rng = np.random.default_rng(2)
+    x = rng.normal(size=(5, 11))
+    y = rng.integers(0, 11, size=5)
+    a, _ = oracle.token_logprob(x, y, inv_temperature=0.5)
+    # closed form at T -> infinity (inv_T = 0): uniform -> -ln V
+    b, _ = oracle.token_logprob(x, y, inv_temperature=0.0)
+    c, _ = oracle.token_logprob(x * 0.5, y, inv_temperature=1.0)
+    assert np.allclose(a, c, atol=1e-14)
+    assert np.allclose(b, -math.log(11), atol=1e-14)
+
+
+def test_all_neg_inf_row_gives_nan():
+    x = np.full((1, 5), -np.inf)
+    logp, _ = oracle.token_logprob(x, [2])
+    assert math.isnan(logp[0])
+
+
+def test_neg_inf_entries_are_probability_zero():
+    x = np.array([[0.0, -np.inf, 0.0]])
+    logp, _ = oracle.token_logprob(x, [0])
+    assert abs(logp[0] + math.log(2)) < 1e-15
+
+
+# ----------------------------------------------------------------------------- c1 advantages
+def test_zero_advantage_spec_examples():
+    g = _gold("spec_examples.json")
+    for ex in g["zero_advantage"]:
+        r = ex["rewards"]
+        adv, zv = oracle.group_advantage(r, [0, len(r)])
+        assert bool(zv[0]) == ex["zero"]
+        if ex["zero"]:
+            assert np.all(adv == 0) and not np.any(np.signbit(adv))
+
+
+def test_zero_var_eight_tenths_is_exactly_zero():
+    # eight copies of 0.1: sequential mean is 0.09999999999999999, d != 0 without the
+    # special case (reading Z5); with it A must be exactly +0.0
+    r = [0.1] * 8
+    acc = 0.0
+    for v in r:
+        acc += v
+    assert acc / 8 != 0.1          # the hazard the special case exists for
+    adv, zv = oracle.group_advantage(r, [0, 8])
+    assert zv[0] == 1 and np.all(adv == 0.0)
+
+
+def test_empty_group_is_invalid():
+    with pytest.raises(ValueError):
+        oracle.group_advantage([1.0, 0.0], [0, 0, 2])
+
+
+@pytest.mark.parametrize("k", range(0, 9))
+def test_binary_closed_form_n8(k):
+    # closed form for binary rewards: mean k/n, sum of squared deviations k(n-k)/n
+    n, eps = 8, 1e-6
+    r = [1.0] * k + [0.0] * (n - k)
+    for mode, ddof in ((oracle.STD_UNBIASED, 1), (oracle.STD_BIASED, 0)):
+        adv, zv = oracle.group_advantage(r, [0, n], std_mode=mode, eps=eps)
+        if k in (0, n):
+            assert zv[0] == 1 and np.all(adv == 0)
+            continue
+        sigma = math.sqrt(k * (n - k) / n / (n - ddof))
+        ap, am = (1 - k / n) / (sigma + eps), (-k / n) / (sigma + eps)
+        assert np.allclose(adv[:k], ap, rtol=2e-7) and np.allclose(adv[k:], am, rtol=2e-7)
+    g = _gold("spec_examples.json")
+    if str(k) in g["closed_form_binary_n8_unbiased_eps1e-6"]:
+        ap, am = g["closed_form_binary_n8_unbiased_eps1e-6"][str(k)]
+        adv, _ = oracle.group_advantage(r, [0, n])
+        assert abs(adv[0] - ap) < 1e-6 and abs(adv[-1] - am) < 1e-6
+    if str(k) in g["closed_form_binary_n8_biased_eps1e-6"]:
+        ap, am = g["closed_form_binary_n8_biased_eps1e-6"][str(k)]
+        adv, _ = oracle.group_advantage(r, [0, n], std_mode=oracle.STD_BIASED)
+        assert abs(adv[0] - ap) < 1e-6 and abs(adv[-1] - am) < 1e-6
+
+
+def test_pair_values():
+    g = _gold("spec_examples.json")["pair_01"]
+    a, _ = oracle.group_advantage([0.0, 1.0], [0, 2])
+    assert a[1] == np.float32(g["unbiased"]) and a[0] == np.float32(-g["unbiased"])
+    b, _ = oracle.group_advantage([0.0, 1.0], [0, 2], std_mode=oracle.STD_BIASED)
+    assert b[1] == np.float32(g["biased"])
+
+
+def test_std_none_is_mean_centering():
+    a, _ = oracle.group_advantage([0.0, 1.0, 1.0, 1.0], [0, 4], std_mode=oracle.STD_NONE)
+    assert np.allclose(a, [-0.75, 0.25, 0.25, 0.25])
+
+
+def test_zero_predicate_brute_force_10000_groups():
+    # agrees with brute-force pairwise equality on 10,000 random groups
+    rng = random.Random(7)
+    for _ in range(10000):
+        n = rng.randint(1, 8)
+        pool = [0.0, 1.0, 0.5, 0.1, 0.1 + 1e-17, 1e-300, -0.0]
+        r = [rng.choice(pool) for _ in range(n)]
+        brute = all(r[i] == r[j] for i in range(n) for j in range(n))
+        _, zv = oracle.group_advantage(r, [0, n])
+        assert bool(zv[0]) == brute
+
+
+def test_advantages_sum_to_zero_and_affine_invariance():
+    rng = np.random.default_rng(3)
+    sizes = rng.integers(2, 17, size=50)
+    cu = np.concatenate([[0], np.cumsum(sizes)])
+    r = rng.normal(size=cu[-1])
+    adv, _ = oracle.group_advantage(r, cu, eps=0.0)
+    adv2, _ = oracle.group_advantage(3.5 * r - 2.0, cu, eps=0.0)
+    for g in range(len(sizes)):
+        seg = adv[cu[g]:cu[g + 1]].astype(np.float64)
+        assert abs(seg.sum()) < 1e-5
+        # unbiased std of standardized values is 1
+        assert abs(np.std(seg, ddof=1) - 1.0) < 1e-5
+    assert np.allclose(adv, adv2, atol=1e-5)
+
+
+def test_batch_norm_token_weighted_moments():
+    rng = np.random.default_rng(4)
+    cu = np.arange(0, 65, 8)
+    r = (rng.uniform(size=64) < 0.4).astype(np.float64)
+    r[:8] = 1.0            # a zero-variance group (shifted by batch norm by design, Z6)
+    L = rng.integers(0, 300, size=64)
+    adv, zv = oracle.group_advantage(r, cu, batch_norm=True, bn_eps=0.0, seq_weight=L)
+    a = adv.astype(np.float64)
+    W = L.sum()
+    mu = (L * a).sum() / W
+    var = (L * (a - mu) ** 2).sum() / W
+    assert abs(mu) < 1e-6 and abs(var - 1.0) < 1e-5
+    assert zv[0] == 1 and adv[0] != 0.0
+
+
+# ----------------------------------------------------------------------------- c2 bookkeeping
+def test_staleness_spec_example():
+    for ex in _gold("spec_examples.json")["staleness"]:
+        bk = oracle.seq_bookkeeping([0, 3], [1, 1, 1], [0, 1, 2], 4, [ex["produced_at"]],
+                                    ex["trainer_version"], ex["max_staleness"])
+        assert (bk["active_tokens"] == 0) == ex["discarded"]
+        assert bk["stale_masked"] == (3 if ex["discarded"] else 0)
+
+
+def test_bookkeeping_brute_force():
+    rng = np.random.default_rng(5)
+    lens = rng.integers(0, 20, size=30)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    N = int(cu[-1])
+    mask = (rng.uniform(size=N) < 0.7).astype(np.uint8)
+    V = 50
+    y = rng.integers(-3, V + 3, size=N)
+    ver = rng.integers(5, 14, size=30)
+    bk = oracle.seq_bookkeeping(cu, mask, y, V, ver, 12, 4)
+    seq = np.repeat(np.arange(30), lens)
+    assert np.array_equal(bk["token_seq"], seq)
+    stale = 12 - ver
+    ok = (stale >= 0) & (stale <= 4)
+    valid = (mask != 0) & (y >= 0) & (y < V) & ok[seq]
+    assert np.array_equal(bk["valid"], valid.astype(np.uint8))
+    assert np.array_equal(bk["seq_active"], np.bincount(seq[valid], minlength=30))
+    assert bk["active_tokens"] == bk["seq_active"].sum() == valid.sum()
+    assert bk["neg_staleness"] == (stale < 0).sum()
+    assert bk["bad_targets"] == (y >= V).sum()
+    assert bk["stale_masked"] == ((mask != 0) & (y >= 0) & (y < V) & (stale[seq] > 4)).sum()
+
+
+# ----------------------------------------------------------------------------- c4-c7 loss
+def _e5():
+    g = _gold("e5_policy_loss.json")
+    x = np.array([[0.0 if k == 0 else math.log(k) for k in row] for row in g["logits_ln"]])
+    y = np.array(g["targets"])
+    logp, _ = oracle.token_logprob(x, y)
+    old = logp - np.log(np.array(g["ratio"]))
+    return g, x, y, old
+
+
+def test_e5_worked_loss_and_gradient():
+    g, x, y, old = _e5()
+    p = LossParams(clip_eps_low=g["clip_eps"], clip_eps_high=g["clip_eps"], global_active_tokens=3)
+    out = oracle.policy_loss_fwd_bwd(x, y, old, [1, 1, 1], [0, 1, 2], g["adv"], None, None, p)
+    assert abs(out["loss"] - g["expected_loss"]) < 1e-14
+    assert np.allclose(out["scale"], g["expected_scale"], atol=1e-14)
+    assert list(out["clipped"]) == g["expected_clipped"]
+    assert np.allclose(out["dlogits"], g["expected_dlogits"], atol=1e-14)
+
+
+def test_e6_branches():
+    for b in _gold("e5_policy_loss.json")["e6_branches"]:
+        x = np.zeros((1, 4))
+        logp, _ = oracle.token_logprob(x, [1])
+        old = logp - math.log(b["r"])
+        p = LossParams(agg=oracle.AGG_SUM)
+        out = oracle.policy_loss_fwd_bwd(x, [1], old, [1], [0], [b["A"]], None, None, p)
+        assert out["clipped"][0] == b["clipped"]
+        assert abs(out["loss"] - b["L"]) < 1e-12
+        assert (np.abs(out["dlogits"]).max() == 0) == b["grad_zero"]
+
+
+def test_ratio_one_loss_is_minus_weighted_mean_adv():
+    # E4 closed form: old = logp -> r = 1 -> L_t = -A -> loss = -(token-weighted mean of A)
+    rng = np.random.default_rng(6)
+    N, V, S = 40, 17, 5
+    x = rng.normal(size=(N, V))
+    y = rng.integers(0, V, size=N)
+    logp, _ = oracle.token_logprob(x, y)
+    tseq = np.sort(rng.integers(0, S, size=N))
+    adv = rng.normal(size=S).astype(np.float32)
+    mask = (rng.uniform(size=N) < 0.8).astype(np.uint8)
+    p = LossParams(global_active_tokens=float(mask.sum()))
+    out = oracle.policy_loss_fwd_bwd(x, y, logp, mask, tseq, adv, None, None, p)
+    expect = -sum(float(adv[tseq[t]]) for t in range(N) if mask[t]) / mask.sum()
+    assert abs(out["loss"] - expect) < 1e-12
+    ones = np.ones(S, dtype=np.float32)
+    out1 = oracle.policy_loss_fwd_bwd(x, y, logp, mask, tseq, ones, None, None, p)
+    assert abs(out1["loss"] + 1.0) < 1e-15
+
+
+def test_seq_mean_equals_token_mean_for_equal_lengths():
+    rng = np.random.default_rng(8)
+    S, T, V = 4, 6, 9
+    x = rng.normal(size=(S * T, V))
+    y = rng.integers(0, V, size=S * T)
+    logp, _ = oracle.token_logprob(x, y)
+    old = logp + rng.normal(size=S * T) * 0.3
+    tseq = np.repeat(np.arange(S), T)
+    adv = rng.normal(size=S).astype(np.float32)
+    L = np.full(S, T)
+    a = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(S * T), tseq, adv, None, L,
+                                   LossParams(global_active_tokens=S * T))
+    b = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(S * T), tseq, adv, None, L,
+                                   LossParams(agg=oracle.AGG_SEQ_MEAN_TOKEN_MEAN, global_num_seqs=S))
+    assert abs(a["loss"] - b["loss"]) < 1e-14
+    assert np.allclose(a["dlogits"], b["dlogits"], atol=1e-16)
+
+
+def _random_case(seed, N=12, V=13, S=3):
+    rng = np.random.default_rng(seed)
+    x = rng.normal(size=(N, V)) * 2
+    y = rng.integers(0, V, size=N)
+    logp, _ = oracle.token_logprob(x, y)
+    old = logp + rng.normal(size=N) * 0.5
+    tseq = np.sort(rng.integers(0, S, size=N))
+    adv = rng.normal(size=S).astype(np.float32)
+    return x, y, old, tseq, adv
+
+
+def _loss_only(x, y, old, tseq, adv, p, clip_override):
+    return oracle.policy_loss_fwd_bwd(x, y, old, np.ones(len(y)), tseq, adv, None, None, p,
+                                      clip_override=clip_override, want_dlogits=False)["loss"]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_gradient_finite_differences(seed):
+    x, y, old, tseq, adv = _random_case(seed)
+    p = LossParams(global_active_tokens=len(y), inv_temperature=0.7, grad_scale=1.0)
+    out = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(len(y)), tseq, adv, None, None, p)
+    # stay away from the clip kinks: skip tokens within 1e-4 of a clip boundary
+    r = out["ratio"]
+    near = (np.abs(r - 0.8) < 1e-4) | (np.abs(r - 1.2) < 1e-4)
+    h = 1e-6
+    num = np.zeros_like(x)
+    for t in range(x.shape[0]):
+        if near[t]:
+            continue
+        for v in range(x.shape[1]):
+            xp = x.copy(); xp[t, v] += h
+            xm = x.copy(); xm[t, v] -= h
+            num[t, v] = (_loss_only(xp, y, old, tseq, adv, p, out["clipped"]) -
+                         _loss_only(xm, y, old, tseq, adv, p, out["clipped"])) / (2 * h)
+    ok = ~near
+    assert np.allclose(num[ok], out["dlogits"][ok], atol=1e-8)
+
+
+def test_gradient_matches_torch_autograd():
+    torch = pytest.importorskip("torch")
+    x, y, old, tseq, adv = _random_case(11, N=30, V=21, S=4)
+    p = LossParams(global_active_tokens=30, clip_eps_low=0.2, clip_eps_high=0.28)
+    out = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(30), tseq, adv, None, None, p)
+    xt = torch.tensor(x, dtype=torch.float64, requires_grad=True)
+    lp = torch.log_softmax(xt, dim=1).gather(1, torch.tensor(y)[:, None])[:, 0]
+    r = torch.exp(lp - torch.tensor(old))
+    A = torch.tensor(adv.astype(np.float64))[torch.tensor(tseq)]
+    L = -torch.minimum(r * A, torch.clamp(r, 0.8, 1.28) * A)
+    loss = L.sum() / 30
+    loss.backward()
+    assert abs(loss.item() - out["loss"]) < 1e-13
+    assert np.allclose(xt.grad.numpy(), out["dlogits"], atol=1e-14)
+
+
+def test_gradient_rows_sum_to_zero_and_masked_rows_zero():
+    x, y, old, tseq, adv = _random_case(12, N=20, V=30)
+    mask = np.ones(20, dtype=np.uint8); mask[[3, 7]] = 0
+    y = y.copy(); y[5] = -100
+    p = LossParams(global_active_tokens=17)
+    out = oracle.policy_loss_fwd_bwd(x, y, old, mask, tseq, adv, None, None, p)
+    assert np.all(np.abs(out["dlogits"].sum(axis=1)) < 1e-15 * 30)
+    for t in (3, 5, 7):
+        assert np.all(out["dlogits"][t] == 0)
+    assert out["stats"]["active_tokens"] == 17 and out["logp"][5] == 0.0
+
+
+def test_log_ratio_clamp_stops_gradient():
+    x = np.zeros((2, 4))
+    logp, _ = oracle.token_logprob(x, [0, 1])
+    old = logp - np.array([25.0, 19.0])
+    out = oracle.policy_loss_fwd_bwd(x, [0, 1], old, [1, 1], [0, 1], [-1.0, -1.0], None, None,
+                                     LossParams(agg=oracle.AGG_SUM))
+    assert abs(out["ratio"][0] - math.exp(20.0)) < 1e-6 * math.exp(20.0)
+    assert out["stats"]["clamped"] == 1
+    assert np.all(out["dlogits"][0] == 0) and np.any(out["dlogits"][1] != 0)
+
+
+def test_staleness_masks_in_loss():
+    x = np.zeros((4, 3))
+    logp, _ = oracle.token_logprob(x, [0, 1, 2, 0])
+    out = oracle.policy_loss_fwd_bwd(x, [0, 1, 2, 0], logp, [1, 1, 1, 1], [0, 0, 1, 2],
+                                     [1.0, 1.0, 1.0], [20, 11, 21], None,
+                                     LossParams(agg=oracle.AGG_SUM, trainer_version=20, max_staleness=8))
+    assert list(out["valid"]) == [1, 1, 0, 0]
+    assert out["stats"]["stale_masked"] == 1 and out["stats"]["neg_staleness"] == 1
+
+
+def test_grad_scale_and_temperature_linear():
+    x, y, old, tseq, adv = _random_case(13)
+    a = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(12), tseq, adv, None, None,
+                                   LossParams(global_active_tokens=12))
+    b = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(12), tseq, adv, None, None,
+                                   LossParams(global_active_tokens=12, grad_scale=3.0))
+    assert np.allclose(3.0 * a["dlogits"], b["dlogits"], atol=1e-15)
+    assert a["loss"] == b["loss"]
+
+
+# ----------------------------------------------------------------------------- c8 vocab-parallel
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_vocab_split_combine_equals_unsplit(P):
+    rng = np.random.default_rng(20 + P)
+    V = 101
+    x = rng.normal(size=(16, V)) * 5
+    y = rng.integers(0, V, size=16)
+    logp, lse = oracle.token_logprob(x, y)
+    bounds = np.linspace(0, V, P + 1).astype(int)
+    if P == 3:
+        bounds = np.array([0, 0, 60, V])          # includes an empty shard
+    ms, ss, xs = [], [], []
+    for r in range(len(bounds) - 1):
+        m, s, xy, _ = oracle.vocab_shard_stats(x[:, bounds[r]:bounds[r + 1]], y, bounds[r])
+        ms.append(m); ss.append(s); xs.append(xy)
+    lse2, zy = oracle.vocab_combine(ms, ss, xs)
+    assert np.allclose(lse2, lse, atol=1e-12, rtol=0)
+    assert np.allclose(zy - lse2, logp, atol=1e-12, rtol=0)
