@@ -1,0 +1,277 @@
+/*
+ * rl_policy.h — C ABI of the B200-native trainer policy-loss hot path of
+ * AstraFlow (arXiv 2605.15565).
+ *
+ * The path (BASELINE.json north_star): per consumed rollout
+ * (mini-)batch, (1) GRPO group-relative advantages over each prompt's response
+ * group ("group-level reward normalization"; 8 rollouts per
+ * prompt; GRPO), (2) sequence/version bookkeeping
+ * ("max staleness 8"), (3) per-token log-probs of the
+ * sampled tokens (log-softmax over V, then gather), (4) the token-level clipped
+ * importance-ratio surrogate against the behaviour log-probs recorded with the
+ * rollout's weight version (PPO; "4 PPO mini-batches")
+ * and its fused backward dL/dlogits = scale*(softmax - onehot), (5) the
+ * vocab-parallel variant with a cross-GPU combine of (max, sum-exp, target logit).
+ * The exact definitions (and every reading where the paper is silent) are in
+ * DESIGN.md §3; the fp64 CPU oracle in oracle/ implements them.
+ *
+ * Conventions (all entry points):
+ *  - Pointers documented "device" must be CUDA device pointers on the current
+ *    device; "host" pointers are read during the call only.  The caller owns every
+ *    buffer; the library allocates nothing on the hot path (scratch comes from the
+ *    caller's workspace, sized by the *_workspace_size functions).  The only
+ *    library-owned object is rl_comm (an NCCL communicator).
+ *  - Calls enqueue work on `stream` (a cudaStream_t; NULL = legacy default stream)
+ *    and return without synchronising.  Outputs are valid after the stream syncs.
+ *  - Errors: host-detectable problems (NULL required pointer, negative size, bad
+ *    enum, ld < vocab, misalignment) return a non-OK status and enqueue NOTHING.
+ *    A failed launch returns RL_ERR_CUDA; NCCL failures RL_ERR_NCCL.
+ *    rl_last_error() gives a thread-local human-readable detail.
+ *    Data errors found on the device never trap: they are counted in the stats /
+ *    counts outputs (target >= vocab -> logp NaN and the token is masked; negative
+ *    staleness -> the sequence is masked).
+ *  - Logits rows are row-major [n_tokens, ld], ld >= vocab, with the row start
+ *    16-byte aligned (base pointer 16-B aligned and ld % 8 == 0 for bf16,
+ *    ld % 4 == 0 for f32).  Row t is the distribution that scored targets[t] (the
+ *    next-token shift is the caller's job).  Columns [vocab, ld) are never read or
+ *    written.
+ *  - dlogits may alias logits exactly (same pointer, same ld) for in-place use;
+ *    partial overlap is undefined.  Every row of dlogits is written (exact zeros
+ *    for masked rows).
+ *  - All calls are deterministic: same inputs -> bitwise-identical outputs.
+ */
+#ifndef RL_POLICY_H_
+#define RL_POLICY_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RL_POLICY_ABI_VERSION 1
+
+typedef void* rl_stream; /* cudaStream_t */
+
+typedef enum {
+  RL_OK = 0,
+  RL_ERR_INVALID_ARGUMENT = 1, /* NULL required pointer, negative size, bad enum, ld < vocab */
+  RL_ERR_ALIGNMENT = 2,        /* logits/dlogits not 16-B aligned, or ld not a multiple of 16 B */
+  RL_ERR_UNSUPPORTED = 3,      /* dtype / device not supported (requires sm_100) */
+  RL_ERR_WORKSPACE = 4,        /* workspace NULL or smaller than *_workspace_size() */
+  RL_ERR_CUDA = 5,             /* a CUDA launch or runtime call failed */
+  RL_ERR_NCCL = 6              /* an NCCL call failed */
+} rl_status;
+
+typedef enum { RL_F32 = 0, RL_BF16 = 1 } rl_dtype; /* logits and dlogits share the dtype */
+
+/* Group std estimator (reading Z2/Z4): unbiased (n-1), biased (n), or none (mean-centering only). */
+typedef enum { RL_STD_UNBIASED = 0, RL_STD_BIASED = 1, RL_STD_NONE = 2 } rl_std_mode;
+
+/* Loss aggregation (reading Z8): global token mean, sequence-mean of token-means, or plain sum. */
+typedef enum { RL_AGG_TOKEN_MEAN = 0, RL_AGG_SEQ_MEAN_TOKEN_MEAN = 1, RL_AGG_SUM = 2 } rl_loss_agg;
+
+/* rl_loss_params.flags */
+#define RL_F_STATS_ACCUMULATE 0x1u /* add into *stats instead of overwriting it */
+#define RL_F_SKIP_MASKED_READS 0x2u /* masked rows: do not read logits (logp_out = 0), only write zeros */
+
+#define RL_STALE_HIST_BINS 16
+
+/* Device-resident batch counts written by rl_seq_bookkeeping (all integer-valued doubles,
+ * so they can be summed across ranks with one fp64 all-reduce). */
+typedef struct {
+  double active_tokens;   /* sum of valid_t */
+  double stale_masked;    /* tokens (mask=1, 0<=y<V) dropped only because staleness > max_staleness */
+  double neg_staleness;   /* SEQUENCES with trainer_version - seq_version < 0 (counted error) */
+  double bad_targets;     /* tokens with y >= vocab (counted error) */
+  double stale_hist[RL_STALE_HIST_BINS]; /* sequences by staleness min(s,15); negative not binned */
+} rl_batch_counts;
+
+/* Device-resident loss statistics written by rl_policy_loss_fwd_bwd (all doubles). */
+typedef struct {
+  double loss_sum;      /* sum_t valid_t * w_t * L_t  (= the loss for TOKEN_MEAN / SEQ_MEAN) */
+  double active_tokens; /* sum_t valid_t */
+  double weight_sum;    /* sum_t valid_t * w_t */
+  double ratio_sum;     /* sum_t valid_t * r_t */
+  double clipped_low;   /* valid tokens with A < 0 and r < 1 - eps_low  */
+  double clipped_high;  /* valid tokens with A > 0 and r > 1 + eps_high */
+  double clamped;       /* valid tokens whose log-ratio hit +-log_ratio_clamp */
+  double stale_masked;  /* tokens (mask=1, 0<=y<V) dropped because staleness > max_staleness */
+  double bad_targets;   /* tokens with y >= vocab */
+  double neg_staleness; /* TOKENS whose sequence has negative staleness */
+} rl_loss_stats;
+#define RL_LOSS_STATS_N 10
+
+typedef struct {
+  float clip_eps_low;    /* default 0.2 (reading Z9) */
+  float clip_eps_high;   /* default 0.2 */
+  float inv_temperature; /* default 1.0 (rollout temperature 1.0) */
+  float log_ratio_clamp; /* default 20: r = exp(clamp(logp - old, -c, c)) (reading Z11) */
+  float grad_scale;      /* extra multiplier on dlogits only, default 1 */
+  int32_t agg;           /* rl_loss_agg, default RL_AGG_TOKEN_MEAN */
+  int32_t trainer_version; /* current trainer weight version (staleness = this - seq_version) */
+  int32_t max_staleness;   /* < 0 disables the staleness mask; 8 per PAPER.md:776 */
+  int32_t global_num_seqs; /* S_global for RL_AGG_SEQ_MEAN_TOKEN_MEAN */
+  uint32_t flags;          /* RL_F_* */
+  double global_active_tokens;     /* N_active over ALL ranks/chunks of this (mini-)batch;
+                                      used iff active_tokens_dev == NULL */
+  const double* active_tokens_dev; /* device pointer to the same count (e.g. &counts->active_tokens
+                                      after rl_comm_allreduce_f64); NULL -> use the host value */
+} rl_loss_params;
+
+/* ---------------------------------------------------------------- misc */
+const char* rl_status_string(rl_status s);
+const char* rl_last_error(void); /* thread-local detail of the last non-OK return ("" if none) */
+int32_t rl_abi_version(void);    /* RL_POLICY_ABI_VERSION */
+void rl_loss_params_default(rl_loss_params* p); /* fills the defaults above (host pointer) */
+
+/* ---------------------------------------------------------------- (1) advantages
+ * GRPO group-relative advantages, c1 of DESIGN.md §3 (PAPER.md:572 group-level reward
+ * normalization; SPEC.md:56-64 zero-variance predicate; PAPER.md:572 batch-level
+ * advantage normalisation as option).  Bit-exact to the fp64 definition:
+ *   zero_var[g] = all rewards of g bitwise-equal (singletons included) -> A_i = +0
+ *   else mu = sequential sum / n; q = sequential sum of (r_i-mu)^2;
+ *        sigma = sqrt(q/(n-1)) | sqrt(q/n); A_i = (r_i - mu)/(sigma + eps) | (r_i - mu)
+ *   optional batch norm (token-weighted by seq_weight[i]), then float32 RNE.
+ * rewards   device f64 [n_seq], group-major (group g = sequences cu_groups[g]..cu_groups[g+1]-1)
+ * cu_groups device i32 [n_groups+1], cu_groups[0] = 0, cu_groups[n_groups] = n_seq
+ * seq_weight device i32 [n_seq] active tokens per sequence; required iff batch_norm != 0
+ * workspace device, >= rl_group_advantage_workspace_size(n_seq) bytes; required iff batch_norm
+ * adv_out   device f32 [n_seq]
+ * zero_var_out device u8 [n_groups] or NULL: 1 = zero variance, 0 = not, 2 = INVALID group
+ *           (empty or out of range — SPEC.md:60 invalid-argument; its members are left untouched)
+ */
+size_t rl_group_advantage_workspace_size(int32_t n_seq);
+rl_status rl_group_advantage(const double* rewards, const int32_t* cu_groups, int32_t n_groups,
+                             int32_t n_seq, int32_t std_mode, double eps, int32_t batch_norm,
+                             double bn_eps, const int32_t* seq_weight, void* workspace,
+                             size_t workspace_bytes, float* adv_out, uint8_t* zero_var_out,
+                             rl_stream stream);
+
+/* ---------------------------------------------------------------- (2) bookkeeping
+ * Sequence / version bookkeeping, c2 of DESIGN.md §3 (PAPER.md:160 model version,
+ * PAPER.md:776 max staleness, SPEC.md:142 worked example 20-11=9>8 -> masked).
+ * cu_seqlens   device i32 [n_seq+1], cu_seqlens[0] = 0, cu_seqlens[n_seq] = n_tokens
+ * loss_mask    device u8 [n_tokens] (NULL = all ones); targets device i32 [n_tokens]
+ *              (y < 0 = ignored, y >= vocab = counted error)
+ * seq_version  device i32 [n_seq] behaviour weight version, or NULL (staleness 0)
+ * seq_adv      device f32 [n_seq] or NULL; if given, adv_token_out[t] = seq_adv[token_seq[t]]
+ * Outputs (device): token_seq_out i32 [n_tokens] (required); seq_active_out i32 [n_seq]
+ *   (required; valid tokens per sequence); seq_staleness_out i32 [n_seq] or NULL;
+ *   adv_token_out f32 [n_tokens] or NULL; valid_out u8 [n_tokens] or NULL;
+ *   counts_out rl_batch_counts or NULL (overwritten).
+ */
+rl_status rl_seq_bookkeeping(const int32_t* cu_seqlens, int32_t n_seq, int64_t n_tokens,
+                             const uint8_t* loss_mask, const int32_t* targets, int64_t vocab,
+                             const int32_t* seq_version, int32_t trainer_version,
+                             int32_t max_staleness, const float* seq_adv,
+                             int32_t* token_seq_out, int32_t* seq_active_out,
+                             int32_t* seq_staleness_out, float* adv_token_out, uint8_t* valid_out,
+                             rl_batch_counts* counts_out, rl_stream stream);
+
+/* ---------------------------------------------------------------- (3) token log-probs
+ * c3 of DESIGN.md §3 (north_star: log-softmax over the vocabulary then gather):
+ *   z = x * inv_temperature; lse = max z + ln sum exp(z - max z); logp = z_y - lse.
+ * Read-only single streaming pass over the logits (no grad; for behaviour/proximal/
+ * reference recompute).  y < 0 -> logp 0; y >= vocab -> logp NaN and counted.
+ * logits device [n_tokens, ld] of dtype; targets device i32 [n_tokens]
+ * logp_out device f32 [n_tokens]; lse_out device f32 [n_tokens] or NULL
+ * bad_target_count device f64 scalar or NULL (ADDED to, not overwritten)
+ */
+rl_status rl_token_logprob(const void* logits, int32_t dtype, int64_t n_tokens, int64_t vocab,
+                           int64_t ld, const int32_t* targets, float inv_temperature,
+                           float* logp_out, float* lse_out, double* bad_target_count,
+                           rl_stream stream);
+
+/* ---------------------------------------------------------------- (4) fused loss fwd+bwd
+ * c3–c7 of DESIGN.md §3 in ONE streaming pass over the logits (logits read once from
+ * HBM, dlogits written once):
+ *   valid_t = mask_t && 0 <= y_t < V && 0 <= staleness(seq) (<= max_staleness if >= 0)
+ *   r = exp(clamp(logp - old_logp, +-c)); L_t = -min(r A, clip(r, 1-eps_l, 1+eps_h) A)
+ *   w_t = 1/N_active | 1/(S_global L_seq) | 1;  s_t = w A r inv_T grad_scale if unclipped
+ *   and unclamped else 0;  dlogits[t,v] = s_t * (softmax(z_t)_v - [v == y_t])
+ * logits   device [n_tokens, ld] (dtype); dlogits device [n_tokens, ld] (same dtype), may == logits
+ * targets  device i32 [n_tokens]; old_logp device f32 [n_tokens] (behaviour log-probs)
+ * loss_mask device u8 [n_tokens] or NULL (all ones)
+ * token_seq device i32 [n_tokens] sequence index into the per-sequence arrays
+ * seq_adv   device f32 [n_seq] (from rl_group_advantage); seq_version device i32 [n_seq] or NULL
+ * seq_active device i32 [n_seq] (required for RL_AGG_SEQ_MEAN_TOKEN_MEAN, else may be NULL)
+ * p         HOST pointer to the parameters (read during the call only)
+ * logp_out  device f32 [n_tokens] or NULL; clipped_out device u8 [n_tokens] or NULL
+ *           (0 none, 1 low, 2 high)
+ * stats     device rl_loss_stats (overwritten, or added to with RL_F_STATS_ACCUMULATE)
+ * workspace device, >= rl_policy_loss_workspace_size(n_tokens, vocab, dtype) bytes
+ */
+size_t rl_policy_loss_workspace_size(int64_t n_tokens, int64_t vocab, int32_t dtype);
+rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, int64_t n_tokens,
+                                 int64_t vocab, int64_t ld, const int32_t* targets,
+                                 const float* old_logp, const uint8_t* loss_mask,
+                                 const int32_t* token_seq, const float* seq_adv,
+                                 const int32_t* seq_version, const int32_t* seq_active,
+                                 const rl_loss_params* p, void* dlogits, float* logp_out,
+                                 uint8_t* clipped_out, rl_loss_stats* stats, void* workspace,
+                                 size_t workspace_bytes, rl_stream stream);
+
+/* Same as rl_policy_loss_fwd_bwd but every array argument is a HOST pointer (pinned or
+ * pageable); the library streams the rows through device staging buffers taken from the
+ * caller's DEVICE workspace (>= rl_policy_loss_host_workspace_size()), overlapping the
+ * host->device copy of chunk k+1, the kernel on chunk k and the device->host copy of
+ * chunk k-1.  *stats_host is written (or accumulated) when the call returns; this call
+ * synchronises `stream`.  dlogits_host may be NULL (gradient discarded). */
+size_t rl_policy_loss_host_workspace_size(int64_t chunk_tokens, int64_t vocab, int64_t ld,
+                                          int32_t dtype, int32_t n_seq);
+rl_status rl_policy_loss_fwd_bwd_host(const void* logits_host, int32_t dtype, int64_t n_tokens,
+                                      int64_t vocab, int64_t ld, const int32_t* targets_host,
+                                      const float* old_logp_host, const uint8_t* loss_mask_host,
+                                      const int32_t* token_seq_host, const float* seq_adv_host,
+                                      const int32_t* seq_version_host,
+                                      const int32_t* seq_active_host, int32_t n_seq,
+                                      const rl_loss_params* p, void* dlogits_host,
+                                      float* logp_out_host, rl_loss_stats* stats_host,
+                                      int64_t chunk_tokens, void* workspace,
+                                      size_t workspace_bytes, rl_stream stream);
+
+/* ---------------------------------------------------------------- (5) multi-GPU
+ * rl_comm wraps an NCCL communicator (NVLink 5 / NVSwitch).  Bootstrap: rank 0 calls
+ * rl_comm_unique_id, the 128 bytes are broadcast by the caller (e.g. over the torch
+ * process group), then every rank calls rl_comm_init on its current device.
+ */
+typedef struct rl_comm rl_comm;
+rl_status rl_comm_unique_id(void* out_128_bytes_host);
+rl_status rl_comm_init(rl_comm** out, const void* unique_id_host, int32_t nranks, int32_t rank);
+rl_status rl_comm_split(rl_comm* parent, int32_t color, int32_t key, rl_comm** out); /* per-policy groups */
+rl_status rl_comm_destroy(rl_comm* c);
+rl_status rl_comm_size(const rl_comm* c, int32_t* nranks, int32_t* rank);
+/* In-place sum all-reduce of n doubles (device) — used for rl_batch_counts (before the loss,
+ * so every rank sees N_active_global) and rl_loss_stats (after). */
+rl_status rl_comm_allreduce_f64(rl_comm* c, double* buf, size_t n, rl_stream stream);
+
+/* Vocab-parallel log-prob (+ optional fused loss/grad on the local shard), c8 of DESIGN.md §3.
+ * Each rank holds the columns [vocab_offset, vocab_offset + vocab_shard) of every row.
+ * Phase 1 (kernel): per row (m_r, s_r, t_y-if-owned) over the local shard.
+ * Phase 2 (NCCL all-gather over NVLink of the 3 floats per row).
+ * Phase 3 (kernel): M = max m_r, S = sum s_r 2^(m_r - M), lse, logp (identical on all ranks);
+ *   if old_logp != NULL also the loss terms (counted once, on the rank owning y) and the
+ *   local dlogits shard s_t*(softmax - onehot) for the shard's columns.
+ * targets are GLOBAL ids.  logp_out / lse_out device f32 [n_tokens] (all ranks).
+ * Loss inputs as in rl_policy_loss_fwd_bwd; dlogits_shard may alias logits_shard.
+ * stats: per-rank partial; sum over ranks with rl_comm_allreduce_f64 to get the batch loss.
+ * workspace >= rl_vocab_parallel_workspace_size(n_tokens, nranks).
+ */
+size_t rl_vocab_parallel_workspace_size(int64_t n_tokens, int32_t nranks);
+rl_status rl_vocab_parallel_logprob(const void* logits_shard, int32_t dtype, int64_t n_tokens,
+                                    int64_t vocab_shard, int64_t vocab_offset,
+                                    int64_t vocab_total, int64_t ld, const int32_t* targets,
+                                    float inv_temperature, rl_comm* comm, float* logp_out,
+                                    float* lse_out, const float* old_logp,
+                                    const uint8_t* loss_mask, const int32_t* token_seq,
+                                    const float* seq_adv, const int32_t* seq_version,
+                                    const int32_t* seq_active, const rl_loss_params* p,
+                                    void* dlogits_shard, rl_loss_stats* stats, void* workspace,
+                                    size_t workspace_bytes, rl_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RL_POLICY_H_ */

@@ -263,6 +263,7 @@ def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_
     clipped = np.zeros(n, dtype=np.uint8)
     scale = np.zeros(n, dtype=np.float64)
     ratio = np.zeros(n, dtype=np.float64)
+    wl = np.zeros(n, dtype=np.float64)   # per-token w_t * L_t (0 for invalid tokens)
     st = dict(active_tokens=0, ratio_sum=0.0, clipped_low=0, clipped_high=0, clamped=0,
               stale_masked=0, bad_targets=0, neg_staleness=0, weight_sum=0.0)
     ratio_terms, weight_terms = [], []
@@ -314,6 +315,7 @@ def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_
         scale[t] = s
         ratio[t] = r
         loss_terms.append(w * L)
+        wl[t] = w * L
         ratio_terms.append(r)
         weight_terms.append(w)
         st["active_tokens"] += 1
@@ -329,7 +331,7 @@ def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_
     st["weight_sum"] = math.fsum(weight_terms)
     loss = math.fsum(loss_terms)
     return dict(loss=loss, dlogits=dl, logp=logp, lse=lse, valid=valid, clipped=clipped,
-                scale=scale, ratio=ratio, stats=st)
+                scale=scale, ratio=ratio, token_loss=wl, stats=st)
 
 
 # ----------------------------------------------------------------------------- c8

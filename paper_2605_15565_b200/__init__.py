@@ -1,0 +1,353 @@
+"""B200-native trainer policy-loss hot path of AstraFlow (arXiv 2605.15565).
+
+Thin ctypes binding over the C-ABI library ``librlpolicy.so`` (include/rl_policy.h).
+Argument marshalling only: every step of the path runs in the library's sm_100a kernels.
+There is no CPU fallback: if the library is missing or CUDA is unavailable, calls raise.
+
+Functions keep the C names without the ``rl_`` prefix and take torch tensors:
+``group_advantage``, ``seq_bookkeeping``, ``token_logprob``, ``policy_loss_fwd_bwd``,
+``policy_loss_fwd_bwd_host``, ``vocab_parallel_logprob`` and the ``Comm`` wrapper.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+__all__ = [
+    "load", "lib_path", "RLError", "LossParams", "STATS_FIELDS", "COUNTS_FIELDS",
+    "STD_UNBIASED", "STD_BIASED", "STD_NONE", "AGG_TOKEN_MEAN", "AGG_SEQ_MEAN_TOKEN_MEAN",
+    "AGG_SUM", "F_STATS_ACCUMULATE", "F_SKIP_MASKED_READS", "F32", "BF16",
+    "group_advantage", "group_advantage_workspace_size", "seq_bookkeeping", "token_logprob",
+    "policy_loss_fwd_bwd", "policy_loss_workspace_size", "policy_loss_fwd_bwd_host",
+    "policy_loss_host_workspace_size", "vocab_parallel_logprob",
+    "vocab_parallel_workspace_size", "Comm", "EXPORTED_SYMBOLS",
+]
+
+F32, BF16 = 0, 1
+STD_UNBIASED, STD_BIASED, STD_NONE = 0, 1, 2
+AGG_TOKEN_MEAN, AGG_SEQ_MEAN_TOKEN_MEAN, AGG_SUM = 0, 1, 2
+F_STATS_ACCUMULATE, F_SKIP_MASKED_READS = 0x1, 0x2
+STALE_HIST_BINS = 16
+STATS_FIELDS = ("loss_sum", "active_tokens", "weight_sum", "ratio_sum", "clipped_low",
+                "clipped_high", "clamped", "stale_masked", "bad_targets", "neg_staleness")
+COUNTS_FIELDS = ("active_tokens", "stale_masked", "neg_staleness", "bad_targets")
+N_COUNTS = len(COUNTS_FIELDS) + STALE_HIST_BINS
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+vp, i32, i64, f32, f64, u32, sz = (C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_double,
+                                   C.c_uint32, C.c_size_t)
+
+
+class _Params(C.Structure):
+    _fields_ = [("clip_eps_low", f32), ("clip_eps_high", f32), ("inv_temperature", f32),
+                ("log_ratio_clamp", f32), ("grad_scale", f32), ("agg", i32),
+                ("trainer_version", i32), ("max_staleness", i32), ("global_num_seqs", i32),
+                ("flags", u32), ("global_active_tokens", f64), ("active_tokens_dev", vp)]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "rl_status_string": (C.c_char_p, [i32]),
+    "rl_last_error": (C.c_char_p, []),
+    "rl_abi_version": (i32, []),
+    "rl_loss_params_default": (None, [vp]),
+    "rl_group_advantage_workspace_size": (sz, [i32]),
+    "rl_group_advantage": (i32, [vp, vp, i32, i32, i32, f64, i32, f64, vp, vp, sz, vp, vp, vp]),
+    "rl_seq_bookkeeping": (i32, [vp, i32, i64, vp, vp, i64, vp, i32, i32, vp, vp, vp, vp, vp, vp,
+                                 vp, vp]),
+    "rl_token_logprob": (i32, [vp, i32, i64, i64, i64, vp, f32, vp, vp, vp, vp]),
+    "rl_policy_loss_workspace_size": (sz, [i64, i64, i32]),
+    "rl_policy_loss_fwd_bwd": (i32, [vp, i32, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                     vp, vp, vp, vp, sz, vp]),
+    "rl_policy_loss_host_workspace_size": (sz, [i64, i64, i64, i32, i32]),
+    "rl_policy_loss_fwd_bwd_host": (i32, [vp, i32, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, i32,
+                                          vp, vp, vp, vp, i64, vp, sz, vp]),
+    "rl_comm_unique_id": (i32, [vp]),
+    "rl_comm_init": (i32, [vp, vp, i32, i32]),
+    "rl_comm_split": (i32, [vp, i32, i32, vp]),
+    "rl_comm_destroy": (i32, [vp]),
+    "rl_comm_size": (i32, [vp, vp, vp]),
+    "rl_comm_allreduce_f64": (i32, [vp, vp, sz, vp]),
+    "rl_vocab_parallel_workspace_size": (sz, [i64, i32]),
+    "rl_vocab_parallel_logprob": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, f32, vp, vp, vp, vp,
+                                        vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+}
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+class RLError(RuntimeError):
+    pass
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "librlpolicy.so")
+
+
+def load():
+    """Load the in-tree librlpolicy.so (build it with ``python -m paper_2605_15565_b200.build``)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        raise RLError(f"{path} is missing: run `python -m paper_2605_15565_b200.build` "
+                      "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        lib = load()
+        raise RLError(f"{what}: {lib.rl_status_string(status).decode()} "
+                      f"({lib.rl_last_error().decode()})")
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _dev(t, what):
+    if t is not None and not t.is_cuda:
+        raise RLError(f"{what} must be a CUDA tensor (no CPU fallback)")
+    return _ptr(t)
+
+
+def _stream(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _dtype_code(t):
+    import torch
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return F32
+    raise RLError(f"unsupported logits dtype {t.dtype}")
+
+
+@dataclass
+class LossParams:
+    """Mirror of rl_loss_params (include/rl_policy.h)."""
+    clip_eps_low: float = 0.2
+    clip_eps_high: float = 0.2
+    inv_temperature: float = 1.0
+    log_ratio_clamp: float = 20.0
+    grad_scale: float = 1.0
+    agg: int = AGG_TOKEN_MEAN
+    trainer_version: int = 0
+    max_staleness: int = -1
+    global_num_seqs: int = 0
+    flags: int = 0
+    global_active_tokens: float = 0.0
+    active_tokens_dev: object = None   # CUDA tensor (float64 scalar view) or int pointer
+
+    def _c(self) -> _Params:
+        p = _Params()
+        for f, _ in _Params._fields_:
+            if f == "active_tokens_dev":
+                p.active_tokens_dev = _ptr(self.active_tokens_dev)
+            else:
+                setattr(p, f, getattr(self, f))
+        return p
+
+
+# ----------------------------------------------------------------------------- (1)
+def group_advantage_workspace_size(n_seq: int) -> int:
+    return load().rl_group_advantage_workspace_size(n_seq)
+
+
+def group_advantage(rewards, cu_groups, adv_out, zero_var_out=None, std_mode=STD_UNBIASED,
+                    eps=1e-6, batch_norm=False, bn_eps=1e-6, seq_weight=None, workspace=None,
+                    stream=None):
+    lib = load()
+    n_groups = cu_groups.numel() - 1
+    n_seq = rewards.numel()
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check(lib.rl_group_advantage(_dev(rewards, "rewards"), _dev(cu_groups, "cu_groups"), n_groups,
+                                  n_seq, std_mode, eps, int(bool(batch_norm)), bn_eps,
+                                  _dev(seq_weight, "seq_weight"), _dev(workspace, "workspace"),
+                                  ws_bytes, _dev(adv_out, "adv_out"),
+                                  _dev(zero_var_out, "zero_var_out"), _stream(stream)),
+           "rl_group_advantage")
+
+
+# ----------------------------------------------------------------------------- (2)
+def seq_bookkeeping(cu_seqlens, targets, vocab, token_seq_out, seq_active_out, loss_mask=None,
+                    seq_version=None, trainer_version=0, max_staleness=-1, seq_adv=None,
+                    seq_staleness_out=None, adv_token_out=None, valid_out=None, counts_out=None,
+                    stream=None):
+    """counts_out: CUDA float64 tensor with >= 20 elements (rl_batch_counts)."""
+    lib = load()
+    if counts_out is not None and counts_out.numel() < N_COUNTS:
+        raise RLError("counts_out needs 20 float64 elements")
+    _check(lib.rl_seq_bookkeeping(_dev(cu_seqlens, "cu_seqlens"), cu_seqlens.numel() - 1,
+                                  targets.numel(), _dev(loss_mask, "loss_mask"),
+                                  _dev(targets, "targets"), vocab, _dev(seq_version, "seq_version"),
+                                  trainer_version, max_staleness, _dev(seq_adv, "seq_adv"),
+                                  _dev(token_seq_out, "token_seq_out"),
+                                  _dev(seq_active_out, "seq_active_out"),
+                                  _dev(seq_staleness_out, "seq_staleness_out"),
+                                  _dev(adv_token_out, "adv_token_out"), _dev(valid_out, "valid_out"),
+                                  _dev(counts_out, "counts_out"), _stream(stream)),
+           "rl_seq_bookkeeping")
+
+
+# ----------------------------------------------------------------------------- (3)
+def token_logprob(logits, targets, logp_out, lse_out=None, vocab=None, inv_temperature=1.0,
+                  bad_target_count=None, stream=None):
+    lib = load()
+    n, ld = logits.shape
+    V = ld if vocab is None else vocab
+    if logits.stride(1) != 1 or logits.stride(0) != ld:
+        raise RLError("logits must be a contiguous [n_tokens, ld] tensor")
+    _check(lib.rl_token_logprob(_dev(logits, "logits"), _dtype_code(logits), n, V, ld,
+                                _dev(targets, "targets"), inv_temperature, _dev(logp_out, "logp_out"),
+                                _dev(lse_out, "lse_out"), _dev(bad_target_count, "bad_target_count"),
+                                _stream(stream)),
+           "rl_token_logprob")
+
+
+# ----------------------------------------------------------------------------- (4)
+def policy_loss_workspace_size(n_tokens, vocab, dtype=BF16) -> int:
+    return load().rl_policy_loss_workspace_size(n_tokens, vocab, dtype)
+
+
+def policy_loss_fwd_bwd(logits, targets, old_logp, token_seq, seq_adv, params: LossParams,
+                        dlogits, stats, workspace, loss_mask=None, seq_version=None,
+                        seq_active=None, logp_out=None, clipped_out=None, vocab=None,
+                        stream=None):
+    """stats: CUDA float64 tensor with >= 10 elements (rl_loss_stats, STATS_FIELDS order).
+    dlogits may be ``logits`` itself (in place)."""
+    lib = load()
+    n, ld = logits.shape
+    V = ld if vocab is None else vocab
+    if logits.stride(1) != 1 or logits.stride(0) != ld or dlogits.shape != logits.shape or \
+            dlogits.stride() != logits.stride() or dlogits.dtype != logits.dtype:
+        raise RLError("logits/dlogits must be contiguous [n_tokens, ld] tensors of one dtype")
+    if stats.numel() < len(STATS_FIELDS):
+        raise RLError("stats needs 10 float64 elements")
+    p = params._c()
+    _check(lib.rl_policy_loss_fwd_bwd(
+        _dev(logits, "logits"), _dtype_code(logits), n, V, ld, _dev(targets, "targets"),
+        _dev(old_logp, "old_logp"), _dev(loss_mask, "loss_mask"), _dev(token_seq, "token_seq"),
+        _dev(seq_adv, "seq_adv"), _dev(seq_version, "seq_version"), _dev(seq_active, "seq_active"),
+        C.byref(p), _dev(dlogits, "dlogits"), _dev(logp_out, "logp_out"),
+        _dev(clipped_out, "clipped_out"), _dev(stats, "stats"), _dev(workspace, "workspace"),
+        workspace.numel() * workspace.element_size(), _stream(stream)),
+        "rl_policy_loss_fwd_bwd")
+
+
+def policy_loss_host_workspace_size(chunk_tokens, vocab, ld, dtype, n_seq) -> int:
+    return load().rl_policy_loss_host_workspace_size(chunk_tokens, vocab, ld, dtype, n_seq)
+
+
+def policy_loss_fwd_bwd_host(logits, targets, old_logp, token_seq, seq_adv, params: LossParams,
+                             workspace, chunk_tokens, loss_mask=None, seq_version=None,
+                             seq_active=None, dlogits=None, logp_out=None, vocab=None,
+                             stats_out=None, stream=None):
+    """All array arguments are CPU tensors (pinned for overlap); workspace is a CUDA tensor.
+    Returns the rl_loss_stats as a dict (also written into ``stats_out`` if given)."""
+    import torch
+    lib = load()
+    for name, t in (("logits", logits), ("targets", targets), ("old_logp", old_logp),
+                    ("token_seq", token_seq), ("seq_adv", seq_adv)):
+        if t.is_cuda:
+            raise RLError(f"{name} must be a host tensor for the host-buffer entry point")
+    n, ld = logits.shape
+    V = ld if vocab is None else vocab
+    st = stats_out if stats_out is not None else torch.zeros(len(STATS_FIELDS), dtype=torch.float64)
+    p = params._c()
+    _check(lib.rl_policy_loss_fwd_bwd_host(
+        _ptr(logits), _dtype_code(logits), n, V, ld, _ptr(targets), _ptr(old_logp), _ptr(loss_mask),
+        _ptr(token_seq), _ptr(seq_adv), _ptr(seq_version), _ptr(seq_active), seq_adv.numel(),
+        C.byref(p), _ptr(dlogits), _ptr(logp_out), _ptr(st), chunk_tokens,
+        _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(), _stream(stream)),
+        "rl_policy_loss_fwd_bwd_host")
+    return dict(zip(STATS_FIELDS, st.tolist()))
+
+
+# ----------------------------------------------------------------------------- (5)
+class Comm:
+    """rl_comm (NCCL) bootstrapped over a torch.distributed process group."""
+
+    def __init__(self, handle: int, nranks: int, rank: int):
+        self.handle, self.nranks, self.rank = handle, nranks, rank
+
+    @classmethod
+    def from_torch(cls, group=None):
+        import torch
+        import torch.distributed as dist
+        lib = load()
+        rank, n = dist.get_rank(group), dist.get_world_size(group)
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            _check(lib.rl_comm_unique_id(C.cast(buf, vp)), "rl_comm_unique_id")
+        t = torch.tensor(bytearray(buf), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        raw = bytes(t.cpu().tolist())
+        h = vp()
+        _check(lib.rl_comm_init(C.byref(h), raw, n, rank), "rl_comm_init")
+        return cls(h.value, n, rank)
+
+    def split(self, color: int, key: int):
+        lib = load()
+        h = vp()
+        _check(lib.rl_comm_split(self.handle, color, key, C.byref(h)), "rl_comm_split")
+        if not h.value:
+            return None
+        n, r = i32(), i32()
+        _check(lib.rl_comm_size(h.value, C.byref(n), C.byref(r)), "rl_comm_size")
+        return Comm(h.value, n.value, r.value)
+
+    def allreduce_f64(self, buf, stream=None):
+        _check(load().rl_comm_allreduce_f64(self.handle, _dev(buf, "buf"), buf.numel(),
+                                            _stream(stream)), "rl_comm_allreduce_f64")
+
+    def destroy(self):
+        if self.handle:
+            _check(load().rl_comm_destroy(self.handle), "rl_comm_destroy")
+            self.handle = None
+
+
+def vocab_parallel_workspace_size(n_tokens, nranks) -> int:
+    return load().rl_vocab_parallel_workspace_size(n_tokens, nranks)
+
+
+def vocab_parallel_logprob(logits_shard, targets, vocab_offset, vocab_total, comm: Comm, logp_out,
+                           workspace, lse_out=None, vocab_shard=None, inv_temperature=1.0,
+                           old_logp=None, loss_mask=None, token_seq=None, seq_adv=None,
+                           seq_version=None, seq_active=None, params: Optional[LossParams] = None,
+                           dlogits_shard=None, stats=None, stream=None):
+    lib = load()
+    n, ld = logits_shard.shape
+    Vr = ld if vocab_shard is None else vocab_shard
+    p = params._c() if params is not None else None
+    _check(lib.rl_vocab_parallel_logprob(
+        _dev(logits_shard, "logits_shard"), _dtype_code(logits_shard), n, Vr, vocab_offset,
+        vocab_total, ld, _dev(targets, "targets"), inv_temperature, comm.handle,
+        _dev(logp_out, "logp_out"), _dev(lse_out, "lse_out"), _dev(old_logp, "old_logp"),
+        _dev(loss_mask, "loss_mask"), _dev(token_seq, "token_seq"), _dev(seq_adv, "seq_adv"),
+        _dev(seq_version, "seq_version"), _dev(seq_active, "seq_active"),
+        C.byref(p) if p is not None else None, _dev(dlogits_shard, "dlogits_shard"),
+        _dev(stats, "stats"), _dev(workspace, "workspace"),
+        workspace.numel() * workspace.element_size(), _stream(stream)),
+        "rl_vocab_parallel_logprob")

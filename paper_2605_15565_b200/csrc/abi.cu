@@ -1,0 +1,65 @@
+// C-ABI plumbing: status strings, thread-local error detail, parameter defaults.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace rl {
+
+static thread_local char g_last_error[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+
+rl_status fail(rl_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+rl_status check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(RL_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return RL_OK;
+}
+
+}  // namespace rl
+
+extern "C" const char* rl_status_string(rl_status s) {
+  switch (s) {
+    case RL_OK: return "ok";
+    case RL_ERR_INVALID_ARGUMENT: return "invalid-argument";
+    case RL_ERR_ALIGNMENT: return "alignment";
+    case RL_ERR_UNSUPPORTED: return "unsupported";
+    case RL_ERR_WORKSPACE: return "workspace";
+    case RL_ERR_CUDA: return "cuda-error";
+    case RL_ERR_NCCL: return "nccl-error";
+  }
+  return "unknown-status";
+}
+
+extern "C" const char* rl_last_error(void) { return rl::g_last_error; }
+
+extern "C" int32_t rl_abi_version(void) { return RL_POLICY_ABI_VERSION; }
+
+extern "C" void rl_loss_params_default(rl_loss_params* p) {
+  if (!p) return;
+  p->clip_eps_low = 0.2f;
+  p->clip_eps_high = 0.2f;
+  p->inv_temperature = 1.0f;
+  p->log_ratio_clamp = 20.0f;
+  p->grad_scale = 1.0f;
+  p->agg = RL_AGG_TOKEN_MEAN;
+  p->trainer_version = 0;
+  p->max_staleness = -1;
+  p->global_num_seqs = 0;
+  p->flags = 0;
+  p->global_active_tokens = 0.0;
+  p->active_tokens_dev = nullptr;
+}

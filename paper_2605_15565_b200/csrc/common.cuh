@@ -1,0 +1,132 @@
+// Shared device helpers for the sm_100a kernels of the policy-loss path.
+// (CUDA side only; the CPU oracle in oracle/ shares nothing with this file.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rl_policy.h"
+
+#define RL_LOG2E 1.4426950408889634f
+#define RL_LN2 0.6931471805599453f
+
+namespace rl {
+
+// ---------------------------------------------------------------- host-side error plumbing
+void set_error(const char* fmt, ...);
+rl_status fail(rl_status s, const char* fmt, ...);
+rl_status check_launch(const char* what);
+
+// ---------------------------------------------------------------- element access
+__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
+// pack two floats to bf16x2 with round-to-nearest-even (cvt.rn.bf16x2.f32: hi operand first)
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float fast_log2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 128-bit streaming global load, no L1 allocation
+__device__ __forceinline__ uint4 ld_stream_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// 128-bit load with an L2 cache-policy hint (evict_last keeps the line for a re-read)
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_hint_v4(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// 128-bit streaming store (evict-first in L2: dlogits are not re-read by this kernel)
+__device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------- (max, sum) in log2 domain
+// A partial softmax state over a set of columns: m = max t, s = sum 2^(t - m), t = x*k.
+struct MS {
+  float m;
+  float s;
+};
+
+__device__ __forceinline__ MS ms_combine(MS a, MS b) {
+  float m = fmaxf(a.m, b.m);
+  if (m == -INFINITY) return MS{-INFINITY, 0.f};
+  float sa = (a.m == -INFINITY) ? 0.f : a.s * fast_exp2(a.m - m);
+  float sb = (b.m == -INFINITY) ? 0.f : b.s * fast_exp2(b.m - m);
+  return MS{m, sa + sb};
+}
+
+__device__ __forceinline__ MS warp_reduce_ms(MS v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    MS w;
+    w.m = __shfl_xor_sync(0xffffffffu, v.m, o);
+    w.s = __shfl_xor_sync(0xffffffffu, v.s, o);
+    v = ms_combine(v, w);
+  }
+  return v;
+}
+
+// Row validity (c2 rule), shared by the bookkeeping and loss kernels.
+struct RowMeta {
+  int32_t y;
+  int32_t seq;
+  bool in_range;   // 0 <= y < V
+  bool bad;        // y >= V
+  bool neg_stale;  // staleness < 0
+  bool stale_drop; // staleness > max_staleness >= 0
+  bool valid;
+};
+
+__device__ __forceinline__ RowMeta row_meta(int64_t row, int64_t vocab, const int32_t* targets,
+                                            const uint8_t* loss_mask, const int32_t* token_seq,
+                                            const int32_t* seq_version, int32_t trainer_version,
+                                            int32_t max_staleness) {
+  RowMeta m;
+  m.y = targets[row];
+  m.seq = token_seq ? token_seq[row] : 0;
+  m.in_range = (m.y >= 0) && ((int64_t)m.y < vocab);
+  m.bad = (int64_t)m.y >= vocab;
+  int32_t stale = seq_version ? (trainer_version - seq_version[m.seq]) : 0;
+  m.neg_stale = stale < 0;
+  m.stale_drop = (!m.neg_stale) && max_staleness >= 0 && stale > max_staleness;
+  bool mask = loss_mask ? (loss_mask[row] != 0) : true;
+  m.valid = mask && m.in_range && !m.neg_stale && !m.stale_drop;
+  m.stale_drop = m.stale_drop && mask && m.in_range;
+  return m;
+}
+
+}  // namespace rl

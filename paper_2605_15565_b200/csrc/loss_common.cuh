@@ -1,0 +1,108 @@
+// Per-token epilogue of the clipped importance-ratio surrogate (c4–c7 of DESIGN.md §3) and the
+// per-CTA statistics partials.  Shared by every loss kernel (two-pass, cluster row-resident,
+// vocab-parallel) so all of them take bitwise-identical per-token decisions.
+#pragma once
+#include "common.cuh"
+
+namespace rl {
+
+struct Knobs {
+  float lo_b, hi_b;  // 1 - eps_low, 1 + eps_high
+  float inv_t, clamp_c, grad_scale;
+  int32_t agg, trainer_version, max_staleness, global_num_seqs;
+  uint32_t flags;
+  double active_host;
+  const double* active_dev;
+};
+
+inline Knobs make_knobs(const rl_loss_params* p) {
+  Knobs k;
+  k.lo_b = 1.0f - p->clip_eps_low;
+  k.hi_b = 1.0f + p->clip_eps_high;
+  k.inv_t = p->inv_temperature;
+  k.clamp_c = p->log_ratio_clamp;
+  k.grad_scale = p->grad_scale;
+  k.agg = p->agg;
+  k.trainer_version = p->trainer_version;
+  k.max_staleness = p->max_staleness;
+  k.global_num_seqs = p->global_num_seqs;
+  k.flags = p->flags;
+  k.active_host = p->global_active_tokens;
+  k.active_dev = p->active_tokens_dev;
+  return k;
+}
+
+// Statistics partials: indices follow rl_loss_stats field order.
+enum {
+  ST_LOSS = 0, ST_ACTIVE, ST_WSUM, ST_RSUM, ST_CLO, ST_CHI, ST_CLAMP, ST_STALE, ST_BAD, ST_NEG
+};
+struct Acc {
+  double v[RL_LOSS_STATS_N];
+  __device__ void zero() {
+#pragma unroll
+    for (int i = 0; i < RL_LOSS_STATS_N; ++i) v[i] = 0.0;
+  }
+};
+
+// 1 / N_active (TOKEN_MEAN) read once per CTA.
+__device__ __forceinline__ double token_mean_inv(const Knobs& kn) {
+  const double d = kn.active_dev ? *kn.active_dev : kn.active_host;
+  return d > 0.0 ? 1.0 / d : 0.0;
+}
+
+// Per-token epilogue.  Returns the gradient scale s_t (0 for invalid / clipped / clamped
+// tokens) and adds the token's contribution to `acc`.  `inv_tm` = token_mean_inv(kn).
+//   D = logp - old; Dc = clamp(D, +-c); r = exp(Dc)
+//   L = -min(r A, clip(r, lo, hi) A); clipped: A>0 && r>hi -> 2, A<0 && r<lo -> 1
+//   w = 1/N | 1/(S L_i) | 1;  s = w A r inv_T grad_scale if unclipped and unclamped
+__device__ __forceinline__ float token_epilogue(const RowMeta& mt, float logp, float old, float A,
+                                                const int32_t* seq_active, double inv_tm,
+                                                const Knobs& kn, Acc& acc, uint8_t* clipped_out) {
+  acc.v[ST_BAD] += mt.bad ? 1.0 : 0.0;
+  acc.v[ST_NEG] += mt.neg_stale ? 1.0 : 0.0;
+  acc.v[ST_STALE] += mt.stale_drop ? 1.0 : 0.0;
+  if (!mt.valid) {
+    if (clipped_out) *clipped_out = 0;
+    return 0.f;
+  }
+  const float D = logp - old;
+  const float Dc = fminf(fmaxf(D, -kn.clamp_c), kn.clamp_c);
+  const bool clamp_active = Dc != D;
+  const float r = expf(Dc);
+  const float u = r * A;
+  const float kk = fminf(fmaxf(r, kn.lo_b), kn.hi_b) * A;
+  const float L = -fminf(u, kk);
+  uint8_t cl = 0;
+  if (A > 0.f && r > kn.hi_b) cl = 2;
+  else if (A < 0.f && r < kn.lo_b) cl = 1;
+  double w;
+  if (kn.agg == RL_AGG_TOKEN_MEAN) {
+    w = inv_tm;
+  } else if (kn.agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN) {
+    const int32_t Li = seq_active ? seq_active[mt.seq] : 0;
+    w = (Li > 0 && kn.global_num_seqs > 0) ? 1.0 / ((double)kn.global_num_seqs * (double)Li) : 0.0;
+  } else {
+    w = 1.0;
+  }
+  acc.v[ST_LOSS] += w * (double)L;
+  acc.v[ST_ACTIVE] += 1.0;
+  acc.v[ST_WSUM] += w;
+  acc.v[ST_RSUM] += (double)r;
+  acc.v[ST_CLO] += cl == 1 ? 1.0 : 0.0;
+  acc.v[ST_CHI] += cl == 2 ? 1.0 : 0.0;
+  acc.v[ST_CLAMP] += clamp_active ? 1.0 : 0.0;
+  if (clipped_out) *clipped_out = cl;
+  if (cl != 0 || clamp_active) return 0.f;
+  return (float)w * A * r * kn.inv_t * kn.grad_scale;
+}
+
+// log-prob from the log2-domain statistics: c2 = M + log2 S; logp = z_y - c2 ln2
+__device__ __forceinline__ float logp_from(const RowMeta& mt, float zy, float c2) {
+  if (mt.in_range) return zy - c2 * RL_LN2;
+  if (mt.bad) return __int_as_float(0x7fc00000);
+  return 0.f;
+}
+
+constexpr int kMaxStatCtas = 4096;  // upper bound of per-CTA partial rows in the workspace
+
+}  // namespace rl

@@ -1,0 +1,240 @@
+// (5) Vocab-parallel log-prob (+ fused loss/grad on the local shard) — c8 of DESIGN.md §3
+// (north_star: "by vocabulary (vocab-parallel log-softmax), with an NCCL all-reduce of
+// per-token max, sum-exp and target logit over NVLink"; BASELINE.json configs[3]).
+//
+// Phase 1 (vp_stats_kernel): per row, (m_r, s_r) in the log2 domain over the local columns
+//   and the target logit z_y if this rank owns column y -> 16 B per row.
+// Phase 2: one ncclAllGather of those 16-B records over NVLink/NVSwitch.
+// Phase 3 (vp_finish_kernel): M = max m_r, S = sum s_r 2^(m_r - M), lse, logp — identical
+//   on every rank; with the loss, the token epilogue (stats counted on comm rank 0 only) and
+//   the local dlogits shard s_t*(softmax - onehot) written in a second pass over the shard.
+#include <nccl.h>
+
+#include <algorithm>
+
+#include "loss_common.cuh"
+#include "rowstats.cuh"
+
+namespace rl {
+
+ncclComm_t comm_nccl(rl_comm* c);
+int32_t comm_rank(const rl_comm* c);
+int32_t comm_size(const rl_comm* c);
+rl_status launch_stats_reduce(const double* partials, int n_ctas, rl_loss_stats* stats,
+                              bool accumulate, cudaStream_t s);
+
+constexpr int kVpThreads = 256;
+constexpr int kVpUnroll = 4;
+
+template <typename T>
+__global__ void __launch_bounds__(kVpThreads) vp_stats_kernel(
+    const void* __restrict__ logits, int64_t n_tokens, int64_t Vr, int64_t offset, int64_t ld,
+    const int32_t* __restrict__ targets, float inv_t, float4* __restrict__ rec) {
+  __shared__ float red[64];
+  const float k = inv_t * RL_LOG2E;
+  const uint64_t keep = policy_evict_last();  // the finish pass re-reads the shard
+  const int64_t row_bytes = ld * elem_bytes<T>();
+  for (int64_t row = blockIdx.x; row < n_tokens; row += gridDim.x) {
+    const char* rp = reinterpret_cast<const char*>(logits) + row * row_bytes;
+    MS st = row_stats_thread<T, kVpThreads, kVpUnroll>(rp, Vr, k, keep);
+    st = block_reduce_ms<kVpThreads>(st, red);
+    if (threadIdx.x == 0) {
+      const int64_t yl = (int64_t)targets[row] - offset;
+      const bool owned = targets[row] >= 0 && yl >= 0 && yl < Vr;
+      const float zy = owned ? VecTraits<T>::load1(rp, yl) * inv_t : 0.f;
+      rec[row] = make_float4(st.m, st.s, zy, owned ? 1.f : 0.f);
+    }
+  }
+}
+
+__device__ __forceinline__ float vp_combine(const float4* __restrict__ all, int64_t n_tokens,
+                                            int P, int64_t row, float* zy_out) {
+  float M = -INFINITY;
+  for (int r = 0; r < P; ++r) M = fmaxf(M, all[(int64_t)r * n_tokens + row].x);
+  float S = 0.f, zy = 0.f;
+  for (int r = 0; r < P; ++r) {
+    const float4 e = all[(int64_t)r * n_tokens + row];
+    if (e.x != -INFINITY) S += e.y * fast_exp2(e.x - M);
+    zy += e.z;
+  }
+  *zy_out = zy;
+  return M + fast_log2(S);  // c2: log2-domain log-sum-exp
+}
+
+// logprob only: one thread per row
+__global__ void vp_logp_kernel(const float4* __restrict__ all, int64_t n_tokens, int P,
+                               int64_t vocab_total, const int32_t* __restrict__ targets,
+                               float* __restrict__ logp_out, float* __restrict__ lse_out) {
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < n_tokens;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    float zy;
+    const float c2 = vp_combine(all, n_tokens, P, row, &zy);
+    const int32_t y = targets[row];
+    float lp = 0.f;
+    if (y >= 0 && (int64_t)y < vocab_total) lp = zy - c2 * RL_LN2;
+    else if ((int64_t)y >= vocab_total) lp = __int_as_float(0x7fc00000);
+    logp_out[row] = lp;
+    if (lse_out) lse_out[row] = c2 * RL_LN2;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kVpThreads) vp_finish_kernel(
+    const void* __restrict__ logits, int64_t n_tokens, int64_t Vr, int64_t offset,
+    int64_t vocab_total, int64_t ld, const float4* __restrict__ all, int P,
+    const int32_t* __restrict__ targets, const float* __restrict__ old_logp,
+    const uint8_t* __restrict__ loss_mask, const int32_t* __restrict__ token_seq,
+    const float* __restrict__ seq_adv, const int32_t* __restrict__ seq_version,
+    const int32_t* __restrict__ seq_active, Knobs kn, int count_stats, void* dlogits,
+    float* __restrict__ logp_out, float* __restrict__ lse_out, double* __restrict__ partials) {
+  constexpr int EPV = VecTraits<T>::EPV;
+  __shared__ float s_row[2];
+  const float k = kn.inv_t * RL_LOG2E;
+  const uint64_t drop = policy_evict_first();
+  const int64_t row_bytes = ld * elem_bytes<T>();
+  const double inv_tm = token_mean_inv(kn);
+  Acc acc;
+  acc.zero();
+  for (int64_t row = blockIdx.x; row < n_tokens; row += gridDim.x) {
+    if (threadIdx.x == 0) {
+      const RowMeta mt = row_meta(row, vocab_total, targets, loss_mask, token_seq, seq_version,
+                                  kn.trainer_version, kn.max_staleness);
+      float zy;
+      const float c2 = vp_combine(all, n_tokens, P, row, &zy);
+      const float lp = logp_from(mt, zy, c2);
+      if (logp_out) logp_out[row] = lp;
+      if (lse_out) lse_out[row] = c2 * RL_LN2;
+      const float A = mt.valid ? seq_adv[mt.seq] : 0.f;
+      const float old = mt.valid ? old_logp[row] : 0.f;
+      Acc tmp;
+      tmp.zero();
+      const float s = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr);
+      if (count_stats)
+        for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
+      s_row[0] = s;
+      s_row[1] = c2;
+    }
+    __syncthreads();
+    const float s = s_row[0], c2 = s_row[1];
+    __syncthreads();
+    const char* rp = reinterpret_cast<const char*>(logits) + row * row_bytes;
+    char* dp = reinterpret_cast<char*>(dlogits) + row * row_bytes;
+    const uint4* vrow = reinterpret_cast<const uint4*>(rp);
+    uint4* vout = reinterpret_cast<uint4*>(dp);
+    const int64_t nvec = Vr / EPV;
+    const int64_t yl = (int64_t)targets[row] - offset;
+    if (s == 0.f) {
+      for (int64_t i = threadIdx.x; i < nvec; i += kVpThreads) st_stream_v4(vout + i, make_uint4(0, 0, 0, 0));
+      for (int64_t c = nvec * EPV + threadIdx.x; c < Vr; c += kVpThreads) VecTraits<T>::store1(dp, c, 0.f);
+      continue;
+    }
+    for (int64_t i = threadIdx.x; i < nvec; i += kVpThreads) {
+      float f[EPV];
+      VecTraits<T>::unpack(ld_hint_v4(vrow + i, drop), f);
+#pragma unroll
+      for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
+      const int64_t c0 = i * EPV;
+      if (yl >= c0 && yl < c0 + EPV) f[yl - c0] -= s;
+      st_stream_v4(vout + i, VecTraits<T>::pack(f));
+    }
+    for (int64_t c = nvec * EPV + threadIdx.x; c < Vr; c += kVpThreads) {
+      float v = s * fast_exp2(fmaf(VecTraits<T>::load1(rp, c), k, -c2));
+      if (c == yl) v -= s;
+      VecTraits<T>::store1(dp, c, v);
+    }
+  }
+  if (threadIdx.x == 0)
+    for (int i = 0; i < RL_LOSS_STATS_N; ++i) partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = acc.v[i];
+}
+
+static int vp_grid(int64_t n) {
+  static int ctas = 0;
+  if (!ctas) {
+    int dev = 0, sms = 148, occ = 4;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vp_stats_kernel<bf16_t>, kVpThreads, 0);
+    ctas = std::min(sms * std::max(occ, 1), kMaxStatCtas);
+  }
+  return (int)std::min<int64_t>(n, ctas);
+}
+
+}  // namespace rl
+
+extern "C" size_t rl_vocab_parallel_workspace_size(int64_t n_tokens, int32_t nranks) {
+  if (n_tokens < 0 || nranks < 1) return 0;
+  const size_t rec = (size_t)n_tokens * 16;
+  return rl::kMaxStatCtas * RL_LOSS_STATS_N * sizeof(double) + rec * (1 + (size_t)nranks);
+}
+
+extern "C" rl_status rl_vocab_parallel_logprob(
+    const void* logits_shard, int32_t dtype, int64_t n_tokens, int64_t vocab_shard,
+    int64_t vocab_offset, int64_t vocab_total, int64_t ld, const int32_t* targets,
+    float inv_temperature, rl_comm* comm, float* logp_out, float* lse_out, const float* old_logp,
+    const uint8_t* loss_mask, const int32_t* token_seq, const float* seq_adv,
+    const int32_t* seq_version, const int32_t* seq_active, const rl_loss_params* p,
+    void* dlogits_shard, rl_loss_stats* stats, void* workspace, size_t workspace_bytes,
+    rl_stream stream) {
+  using namespace rl;
+  if (!comm) return fail(RL_ERR_INVALID_ARGUMENT, "NULL comm");
+  if (n_tokens < 0 || vocab_shard < 0 || vocab_offset < 0 || vocab_total < 1 ||
+      vocab_offset + vocab_shard > vocab_total || ld < vocab_shard || ld < 1)
+    return fail(RL_ERR_INVALID_ARGUMENT, "bad sizes (n_tokens/vocab_shard/offset/total/ld)");
+  if (dtype != RL_F32 && dtype != RL_BF16) return fail(RL_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);
+  if (!(inv_temperature > 0.f)) return fail(RL_ERR_INVALID_ARGUMENT, "inv_temperature must be > 0");
+  const int P = comm_size(comm);
+  if (!workspace || workspace_bytes < rl_vocab_parallel_workspace_size(n_tokens, P))
+    return fail(RL_ERR_WORKSPACE, "workspace must be >= %zu bytes",
+                rl_vocab_parallel_workspace_size(n_tokens, P));
+  const bool with_loss = old_logp != nullptr;
+  if (n_tokens > 0 && (!targets || !logp_out || (vocab_shard > 0 && !logits_shard)))
+    return fail(RL_ERR_INVALID_ARGUMENT, "NULL logits_shard/targets/logp_out");
+  if (with_loss) {
+    if (!p || !token_seq || !seq_adv || !stats || (vocab_shard > 0 && !dlogits_shard))
+      return fail(RL_ERR_INVALID_ARGUMENT, "fused loss needs p, token_seq, seq_adv, stats, dlogits_shard");
+    if (p->agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN && !seq_active)
+      return fail(RL_ERR_INVALID_ARGUMENT, "SEQ_MEAN_TOKEN_MEAN needs seq_active");
+  }
+  const int64_t eb = dtype == RL_BF16 ? 2 : 4;
+  if (((uintptr_t)logits_shard & 15) || ((uintptr_t)dlogits_shard & 15) || (ld * eb) % 16)
+    return fail(RL_ERR_ALIGNMENT, "shards must be 16-B aligned with ld*elem %% 16 == 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  double* partials = (double*)workspace;
+  float4* send = reinterpret_cast<float4*>((char*)workspace + kMaxStatCtas * RL_LOSS_STATS_N * sizeof(double));
+  float4* recv = send + n_tokens;
+  if (n_tokens == 0) {
+    if (with_loss && !(p->flags & RL_F_STATS_ACCUMULATE)) cudaMemsetAsync(stats, 0, sizeof(rl_loss_stats), s);
+    return check_launch("vp empty");
+  }
+  const int grid = vp_grid(n_tokens);
+  if (dtype == RL_BF16)
+    vp_stats_kernel<bf16_t><<<grid, kVpThreads, 0, s>>>(logits_shard, n_tokens, vocab_shard,
+                                                        vocab_offset, ld, targets, inv_temperature, send);
+  else
+    vp_stats_kernel<float><<<grid, kVpThreads, 0, s>>>(logits_shard, n_tokens, vocab_shard,
+                                                       vocab_offset, ld, targets, inv_temperature, send);
+  rl_status st = check_launch("vp_stats_kernel");
+  if (st != RL_OK) return st;
+  ncclResult_t r = ncclAllGather(send, recv, (size_t)n_tokens * 4, ncclFloat, comm_nccl(comm), s);
+  if (r != ncclSuccess) return fail(RL_ERR_NCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+  if (!with_loss) {
+    const int blocks = (int)std::min<int64_t>(148 * 4, (n_tokens + 255) / 256);
+    vp_logp_kernel<<<blocks, 256, 0, s>>>(recv, n_tokens, P, vocab_total, targets, logp_out, lse_out);
+    return check_launch("vp_logp_kernel");
+  }
+  const Knobs kn = make_knobs(p);
+  const int count = comm_rank(comm) == 0;
+  if (dtype == RL_BF16)
+    vp_finish_kernel<bf16_t><<<grid, kVpThreads, 0, s>>>(
+        logits_shard, n_tokens, vocab_shard, vocab_offset, vocab_total, ld, recv, P, targets,
+        old_logp, loss_mask, token_seq, seq_adv, seq_version, seq_active, kn, count, dlogits_shard,
+        logp_out, lse_out, partials);
+  else
+    vp_finish_kernel<float><<<grid, kVpThreads, 0, s>>>(
+        logits_shard, n_tokens, vocab_shard, vocab_offset, vocab_total, ld, recv, P, targets,
+        old_logp, loss_mask, token_seq, seq_adv, seq_version, seq_active, kn, count, dlogits_shard,
+        logp_out, lse_out, partials);
+  st = check_launch("vp_finish_kernel");
+  if (st != RL_OK) return st;
+  return launch_stats_reduce(partials, grid, stats, (p->flags & RL_F_STATS_ACCUMULATE) != 0, s);
+}

@@ -1,0 +1,397 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs.  Tolerances (BASELINE.json north_star; readings Z21-Z23 in DESIGN.md §3):
+advantages / masks / integer bookkeeping bit-exact; logp <= 2e-3 absolute; loss <= 1e-4
+relative (Z22 scale); dlogits per row max|d| <= 1e-2*|s_t| (Z21) and literal 1e-2 absolute
+in unit-scale (SUM) mode; clip flags exact outside the Z23 band; masked rows bitwise zero.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.cases import clip_band, oracle_chain, small_case
+
+pytestmark = pytest.mark.gpu
+
+LOGP_ATOL = 2e-3
+LOSS_RTOL = 1e-4
+DLOGIT_ROW_RTOL = 1e-2
+
+
+def torch():
+    import torch as t
+    return t
+
+
+def dev(a):
+    t = torch()
+    if a.dtype == np.uint16:
+        return t.from_numpy(np.ascontiguousarray(a).view(np.int16)).cuda().view(t.bfloat16)
+    return t.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host_logits(tns):
+    t = torch()
+    if tns.dtype == t.bfloat16:
+        return oracle.decode_bf16(tns.view(t.int16).cpu().numpy().view(np.uint16))
+    return tns.cpu().numpy().astype(np.float64)
+
+
+def run_gpu_chain(rl, case, params, std_mode=0, eps=1e-6, batch_norm=False, bn_eps=1e-6,
+                  in_place=False, want=("logp", "clipped")):
+    t = torch()
+    N, S, G = len(case["targets"]), len(case["rewards"]), len(case["cu_groups"]) - 1
+    logits = dev(case["logits"])
+    targets = dev(case["targets"])
+    cu = dev(case["cu_seqlens"])
+    mask = dev(case["loss_mask"])
+    ver = dev(case["seq_version"])
+    tok_seq = t.empty(N, dtype=t.int32, device="cuda")
+    seq_active = t.empty(S, dtype=t.int32, device="cuda")
+    counts = t.zeros(20, dtype=t.float64, device="cuda")
+    rl.seq_bookkeeping(cu, targets, case["vocab"], tok_seq, seq_active, loss_mask=mask,
+                       seq_version=ver, trainer_version=case["trainer_version"],
+                       max_staleness=case["max_staleness"], counts_out=counts)
+    adv = t.empty(S, dtype=t.float32, device="cuda")
+    zv = t.empty(G, dtype=t.uint8, device="cuda")
+    ws_adv = t.empty(max(1, rl.group_advantage_workspace_size(S)), dtype=t.uint8, device="cuda")
+    rl.group_advantage(dev(case["rewards"]), dev(case["cu_groups"]), adv, zv, std_mode=std_mode,
+                       eps=eps, batch_norm=batch_norm, bn_eps=bn_eps, seq_weight=seq_active,
+                       workspace=ws_adv)
+    p = rl.LossParams(**params)
+    p.trainer_version = case["trainer_version"]
+    p.max_staleness = case["max_staleness"]
+    if p.global_num_seqs == 0:
+        p.global_num_seqs = S
+    p.active_tokens_dev = counts[0:1]
+    dl = logits if in_place else t.empty_like(logits)
+    stats = t.zeros(10, dtype=t.float64, device="cuda")
+    ws = t.empty(rl.policy_loss_workspace_size(N, case["vocab"]), dtype=t.uint8, device="cuda")
+    logp = t.empty(N, dtype=t.float32, device="cuda")
+    clipped = t.empty(N, dtype=t.uint8, device="cuda")
+    rl.policy_loss_fwd_bwd(logits, targets, dev(case["old_logp"]), tok_seq, adv, p, dl, stats, ws,
+                           loss_mask=mask, seq_version=ver, seq_active=seq_active, logp_out=logp,
+                           clipped_out=clipped, vocab=case["vocab"])
+    t.cuda.synchronize()
+    return dict(adv=adv.cpu().numpy(), zero_var=zv.cpu().numpy(), token_seq=tok_seq.cpu().numpy(),
+                seq_active=seq_active.cpu().numpy(), counts=counts.cpu().numpy(),
+                logp=logp.cpu().numpy(), clipped=clipped.cpu().numpy(),
+                dlogits=host_logits(dl)[:, :case["vocab"]], stats=stats.cpu().numpy())
+
+
+def check_against_oracle(case, g, params, **adv_kw):
+    ref = oracle_chain(case, oracle.LossParams(**params), **adv_kw)
+    out = ref["loss"]
+    # --- bit-exact parts
+    assert np.array_equal(g["adv"].view(np.uint32), ref["adv"].view(np.uint32)), "advantages"
+    assert np.array_equal(g["zero_var"], ref["zero_var"])
+    assert np.array_equal(g["token_seq"], ref["bk"]["token_seq"])
+    assert np.array_equal(g["seq_active"], ref["bk"]["seq_active"])
+    assert g["counts"][0] == ref["bk"]["active_tokens"]
+    # --- logp
+    y = case["targets"]
+    V = case["vocab"]
+    inr = (y >= 0) & (y < V)
+    assert np.all(np.abs(g["logp"][inr] - out["logp"][inr]) <= LOGP_ATOL), \
+        np.abs(g["logp"][inr] - out["logp"][inr]).max()
+    assert np.all(g["logp"][y < 0] == 0)
+    assert np.all(np.isnan(g["logp"][y >= V]))
+    # --- clip decisions: exact outside the tie band (Z23); inside, adopt the GPU's decision
+    eps_lo, eps_hi = params.get("clip_eps_low", 0.2), params.get("clip_eps_high", 0.2)
+    band = clip_band(out["ratio"], out["valid"], eps_lo, eps_hi)
+    assert np.array_equal(g["clipped"][~band], out["clipped"][~band])
+    if band.any():
+        override = np.where(band, g["clipped"], out["clipped"])
+        out = oracle.policy_loss_fwd_bwd(case["x64"], y, case["old_logp"], case["loss_mask"],
+                                         ref["bk"]["token_seq"], ref["adv"], case["seq_version"],
+                                         ref["bk"]["seq_active"], ref["params"], clip_override=override)
+    # --- loss (Z22)
+    scale = max(abs(out["loss"]), float(np.abs(out["token_loss"]).sum()), 1e-30)
+    assert abs(g["stats"][0] - out["loss"]) <= LOSS_RTOL * scale, (g["stats"][0], out["loss"])
+    st = out["stats"]
+    assert g["stats"][1] == st["active_tokens"]
+    assert abs(g["stats"][3] - st["ratio_sum"]) <= 1e-4 * max(1.0, st["ratio_sum"])
+    assert g["stats"][4] == st["clipped_low"] and g["stats"][5] == st["clipped_high"]
+    assert g["stats"][6] == st["clamped"] and g["stats"][7] == st["stale_masked"]
+    assert g["stats"][8] == st["bad_targets"] and g["stats"][9] == st["neg_staleness"]
+    # --- dlogits (Z21): zero rows exactly zero, other rows relative to |s_t|
+    s = out["scale"]
+    d = g["dlogits"]
+    zero_rows = s == 0
+    assert np.all(d[zero_rows] == 0), "rows with s_t = 0 must be exact zeros"
+    nz = ~zero_rows
+    if nz.any():
+        err = np.abs(d[nz] - out["dlogits"][nz]).max(axis=1)
+        assert np.all(err <= DLOGIT_ROW_RTOL * np.abs(s[nz])), (err / np.abs(s[nz])).max()
+    return out
+
+
+# ----------------------------------------------------------------------------- advantages
+@pytest.mark.parametrize("std_mode", [0, 1, 2])
+@pytest.mark.parametrize("bn", [False, True])
+def test_group_advantage_bit_exact(cuda_lib, std_mode, bn):
+    rl, t = cuda_lib, torch()
+    rng = np.random.default_rng(100 + std_mode + 3 * bn)
+    sizes = np.concatenate([[1, 1, 8, 8, 16, 3, 2], rng.integers(1, 17, size=200)])
+    cu = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    S = int(cu[-1])
+    kinds = [lambda n: (rng.uniform(size=n) < 0.5).astype(float),
+             lambda n: np.full(n, 0.1),
+             lambda n: rng.normal(size=n) * 1e3,
+             lambda n: rng.choice([0.1, 0.2, 0.3, 1e-17, 0.1 + 1e-17], size=n),
+             lambda n: rng.uniform(size=n)]
+    r = np.concatenate([kinds[g % len(kinds)](n) for g, n in enumerate(sizes)])
+    L = rng.integers(0, 4000, size=S).astype(np.int32)
+    ref_adv, ref_zv = oracle.group_advantage(r, cu, std_mode, 1e-6, bn, 1e-6, L)
+    adv = t.empty(S, dtype=t.float32, device="cuda")
+    zv = t.empty(len(sizes), dtype=t.uint8, device="cuda")
+    ws = t.empty(rl.group_advantage_workspace_size(S), dtype=t.uint8, device="cuda")
+    rl.group_advantage(dev(r), dev(cu), adv, zv, std_mode=std_mode, batch_norm=bn,
+                       seq_weight=dev(L), workspace=ws)
+    assert np.array_equal(adv.cpu().numpy().view(np.uint32), ref_adv.view(np.uint32))
+    assert np.array_equal(zv.cpu().numpy(), ref_zv)
+
+
+def test_group_advantage_invalid_group_flagged(cuda_lib):
+    rl, t = cuda_lib, torch()
+    cu = np.array([0, 2, 2, 4], dtype=np.int32)  # group 1 is empty
+    r = np.array([0.0, 1.0, 1.0, 1.0])
+    adv = t.full((4,), 7.0, dtype=t.float32, device="cuda")
+    zv = t.empty(3, dtype=t.uint8, device="cuda")
+    rl.group_advantage(dev(r), dev(cu), adv, zv)
+    assert list(zv.cpu().numpy()) == [0, 2, 1]
+    ref, _ = oracle.group_advantage(r, [0, 2, 4])
+    assert np.array_equal(adv.cpu().numpy(), ref)
+
+
+# ----------------------------------------------------------------------------- bookkeeping
+def test_seq_bookkeeping_exact(cuda_lib):
+    rl, t = cuda_lib, torch()
+    rng = np.random.default_rng(7)
+    lens = np.concatenate([[0, 5, 0, 33], rng.integers(0, 700, size=60), [0]])
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    S, N, V = len(lens), int(cu[-1]), 1000
+    mask = (rng.uniform(size=N) < 0.6).astype(np.uint8)
+    y = rng.integers(-2, V + 2, size=N).astype(np.int32)
+    ver = rng.integers(3, 14, size=S).astype(np.int32)
+    sadv = rng.normal(size=S).astype(np.float32)
+    ref = oracle.seq_bookkeeping(cu, mask, y, V, ver, 12, 8)
+    tok, act, stale = (t.empty(N, dtype=t.int32, device="cuda"), t.empty(S, dtype=t.int32, device="cuda"),
+                       t.empty(S, dtype=t.int32, device="cuda"))
+    advt, valid = t.empty(N, dtype=t.float32, device="cuda"), t.empty(N, dtype=t.uint8, device="cuda")
+    counts = t.empty(20, dtype=t.float64, device="cuda")
+    rl.seq_bookkeeping(dev(cu), dev(y), V, tok, act, loss_mask=dev(mask), seq_version=dev(ver),
+                       trainer_version=12, max_staleness=8, seq_adv=dev(sadv), seq_staleness_out=stale,
+                       adv_token_out=advt, valid_out=valid, counts_out=counts)
+    assert np.array_equal(tok.cpu().numpy(), ref["token_seq"])
+    assert np.array_equal(act.cpu().numpy(), ref["seq_active"])
+    assert np.array_equal(stale.cpu().numpy(), ref["seq_staleness"])
+    assert np.array_equal(valid.cpu().numpy(), ref["valid"])
+    assert np.array_equal(advt.cpu().numpy(), sadv[ref["token_seq"]])
+    c = counts.cpu().numpy()
+    assert c[0] == ref["active_tokens"] and c[1] == ref["stale_masked"]
+    assert c[2] == ref["neg_staleness"] and c[3] == ref["bad_targets"]
+    assert np.array_equal(c[4:20], ref["stale_hist"])
+
+
+# ----------------------------------------------------------------------------- log-probs
+@pytest.mark.parametrize("V,ld,dtype", [(1024, 1024, "f32"), (1003, 1008, "bf16"), (5, 8, "bf16"),
+                                        (1, 8, "bf16"), (1001, 1004, "f32"), (151936, 151936, "bf16")])
+def test_token_logprob(cuda_lib, V, ld, dtype):
+    rl, t = cuda_lib, torch()
+    R = 40 if V > 100000 else 300
+    x, y = synth.host_logits(V, np.arange(R), 31, dtype)
+    y = y.copy()
+    y[3], y[5] = -100, V  # ignored and bad targets
+    xs = np.zeros((R, ld), dtype=x.dtype)
+    xs[:, :V] = x
+    x64 = oracle.decode_bf16(x) if dtype == "bf16" else x.astype(np.float64)
+    ref, ref_lse = oracle.token_logprob(x64, y)
+    logp, lse = t.empty(R, device="cuda"), t.empty(R, device="cuda")
+    bad = t.zeros(1, dtype=t.float64, device="cuda")
+    rl.token_logprob(dev(xs), dev(y), logp, lse, vocab=V, bad_target_count=bad)
+    g = logp.cpu().numpy()
+    ok = (y >= 0) & (y < V)
+    assert np.all(np.abs(g[ok] - ref[ok]) <= LOGP_ATOL)
+    assert np.all(np.abs(lse.cpu().numpy() - ref_lse) <= LOGP_ATOL)
+    assert g[3] == 0 and math.isnan(g[5]) and bad.item() == 1
+
+
+def test_token_logprob_special_values(cuda_lib):
+    rl, t = cuda_lib, torch()
+    x = np.zeros((3, 64), dtype=np.float32)
+    x[0, 1:] = -np.inf            # one finite entry: logp = 0
+    x[1, :] = -np.inf             # all -inf: NaN
+    x[2, 7] = np.inf              # +inf propagates: NaN
+    logp = t.empty(3, device="cuda")
+    rl.token_logprob(dev(x), dev(np.array([0, 0, 7], dtype=np.int32)), logp)
+    g = logp.cpu().numpy()
+    ref, _ = oracle.token_logprob(x.astype(np.float64), [0, 0, 7])
+    assert g[0] == 0.0 and ref[0] == 0.0
+    assert math.isnan(g[1]) and math.isnan(ref[1]) and math.isnan(g[2]) and math.isnan(ref[2])
+
+
+# ----------------------------------------------------------------------------- fused loss
+def test_tiny_config_full_parity(cuda_lib):
+    """BASELINE.json configs[0]: 2 x 4 x 64 tokens, V = 1024, fp32 logits — every output."""
+    case = small_case()
+    g = run_gpu_chain(cuda_lib, case, {})
+    out = check_against_oracle(case, g, {})
+    assert out["stats"]["active_tokens"] > 0
+
+
+@pytest.mark.parametrize("kw", [
+    dict(vocab=5003, ld=5008, dtype="bf16", n_prompts=3, group=5, seq_len=41, seed=3),
+    dict(vocab=4096, ld=4096, dtype="bf16", n_prompts=2, group=8, seq_len=37, seed=4,
+         staleness_max=8, stale_outlier_frac=0.3, max_staleness=8, big_delta_frac=0.2),
+    dict(vocab=777, ld=780, dtype="f32", n_prompts=4, group=3, seq_len=29, seed=5, mask_mode="all",
+         big_delta_frac=0.3, sigma_delta=0.3),
+])
+@pytest.mark.parametrize("in_place", [False, True])
+def test_loss_parity_ragged(cuda_lib, kw, in_place):
+    case = small_case(**kw)
+    g = run_gpu_chain(cuda_lib, case, {}, in_place=in_place)
+    check_against_oracle(case, g, {})
+
+
+@pytest.mark.parametrize("params", [
+    dict(agg=oracle.AGG_SEQ_MEAN_TOKEN_MEAN),
+    dict(clip_eps_low=0.2, clip_eps_high=0.28),
+    dict(inv_temperature=0.7, grad_scale=2.5),
+])
+def test_loss_parity_knobs(cuda_lib, params):
+    case = small_case(vocab=2048, dtype="bf16", seed=9, big_delta_frac=0.1, sigma_delta=0.2)
+    g = run_gpu_chain(cuda_lib, case, params, batch_norm=True)
+    check_against_oracle(case, g, params, batch_norm=True)
+
+
+def test_unit_scale_literal_dlogit_tolerance(cuda_lib):
+    """Z21: in SUM mode (w = 1) with |A r| <= ~2 the literal 1e-2 absolute bound is meaningful."""
+    case = small_case(vocab=3000, dtype="bf16", seed=12, sigma_delta=0.05)
+    params = dict(agg=oracle.AGG_SUM)
+    g = run_gpu_chain(cuda_lib, case, params)
+    out = check_against_oracle(case, g, params)
+    assert np.abs(g["dlogits"] - out["dlogits"]).max() <= 1e-2
+
+
+def test_all_masked_batch_and_determinism(cuda_lib):
+    case = small_case(vocab=1024, seed=13)
+    case["loss_mask"][:] = 0
+    g = run_gpu_chain(cuda_lib, case, {})
+    assert g["stats"][0] == 0 and g["stats"][1] == 0 and np.all(g["dlogits"] == 0)
+    case = small_case(vocab=3000, dtype="bf16", seed=14)
+    a = run_gpu_chain(cuda_lib, case, {})
+    b = run_gpu_chain(cuda_lib, case, {})
+    assert a["stats"].tobytes() == b["stats"].tobytes()
+    assert a["dlogits"].tobytes() == b["dlogits"].tobytes() and a["logp"].tobytes() == b["logp"].tobytes()
+
+
+def test_rows_sum_to_zero_bf16(cuda_lib):
+    """Invariant: each gradient row sums to ~0 (bf16 output: |sum| <= 4e-3 |s_t|)."""
+    case = small_case(vocab=8192, dtype="bf16", seed=15, mask_mode="all", ignore_frac=0.0)
+    g = run_gpu_chain(cuda_lib, case, {})
+    ref = oracle_chain(case, oracle.LossParams())["loss"]
+    s = ref["scale"]
+    nz = s != 0
+    sums = g["dlogits"][nz].sum(axis=1)
+    assert np.all(np.abs(sums) <= 4e-3 * np.abs(s[nz]) * 8)
+
+
+def test_host_entry_point_matches_device(cuda_lib):
+    rl, t = cuda_lib, torch()
+    case = small_case(vocab=3000, dtype="bf16", seed=16, n_prompts=3, group=4, seq_len=50)
+    g = run_gpu_chain(rl, case, {})
+    bk = oracle.seq_bookkeeping(case["cu_seqlens"], case["loss_mask"], case["targets"], 3000,
+                                case["seq_version"], case["trainer_version"], -1)
+    adv = np.asarray(g["adv"], dtype=np.float32)
+    N = len(case["targets"])
+    x = t.from_numpy(case["logits"].view(np.int16)).view(t.bfloat16).pin_memory()
+    dl = t.empty_like(x).pin_memory()
+    logp = t.empty(N, dtype=t.float32).pin_memory()
+    p = rl.LossParams(trainer_version=case["trainer_version"], global_active_tokens=bk["active_tokens"])
+    ws = t.empty(rl.policy_loss_host_workspace_size(64, 3000, 3000, rl.BF16, len(adv)),
+                 dtype=t.uint8, device="cuda")
+    st = rl.policy_loss_fwd_bwd_host(x, t.from_numpy(case["targets"]), t.from_numpy(case["old_logp"]),
+                                     t.from_numpy(bk["token_seq"]), t.from_numpy(adv), p, ws, 64,
+                                     loss_mask=t.from_numpy(case["loss_mask"]),
+                                     seq_version=t.from_numpy(case["seq_version"]),
+                                     dlogits=dl, logp_out=logp, vocab=3000)
+    assert st["loss_sum"] == pytest.approx(g["stats"][0], rel=1e-6, abs=1e-12)
+    assert st["active_tokens"] == g["stats"][1]
+    assert np.array_equal(logp.numpy(), g["logp"])
+    assert np.array_equal(oracle.decode_bf16(dl.view(t.int16).numpy().view(np.uint16)), g["dlogits"])
+
+
+def test_vocab_parallel_single_rank(cuda_lib):
+    """c8 with P = 1 (degenerate world size): equals the unsplit log-probs and loss."""
+    import ctypes
+    rl, t = cuda_lib, torch()
+    lib = rl.load()
+    buf = (ctypes.c_uint8 * 128)()
+    assert lib.rl_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)) == 0
+    h = ctypes.c_void_p()
+    assert lib.rl_comm_init(ctypes.byref(h), bytes(buf), 1, 0) == 0
+    comm = rl.Comm(h.value, 1, 0)
+    case = small_case(vocab=2048, dtype="bf16", seed=17)
+    g = run_gpu_chain(rl, case, {})
+    N = len(case["targets"])
+    logp = t.empty(N, device="cuda")
+    ws = t.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=t.uint8, device="cuda")
+    rl.vocab_parallel_logprob(dev(case["logits"]), dev(case["targets"]), 0, 2048, comm, logp, ws)
+    t.cuda.synchronize()
+    lp = logp.cpu().numpy()
+    ok = case["targets"] >= 0
+    assert np.all(np.abs(lp[ok] - g["logp"][ok]) <= 1e-4)
+    comm.destroy()
+
+
+@pytest.mark.slow
+def test_full_size_single_policy_sampled(cuda_lib):
+    """BASELINE.json configs[1] at full width (V = 151936 bf16) in the bench's launch
+    configuration (one 131,072-token PPO mini-batch): sampled rows against the
+    oracle, plus the row-sum invariant over every row."""
+    rl, t = cuda_lib, torch()
+    cfg = synth.get_config("single")
+    N, V = 131072, cfg.vocab
+    lay = synth.seq_layout(cfg)
+    logits = t.empty((N, V), dtype=t.bfloat16, device="cuda")
+    y = t.empty(N, dtype=t.int32, device="cuda")
+    synth.device_logits(logits, V, 0, cfg.seed, targets_out=y)
+    rows = np.random.default_rng(0).choice(N, size=48, replace=False)
+    rows.sort()
+    xs = oracle.decode_bf16(logits[t.from_numpy(rows).cuda()].view(t.int16).cpu().numpy().view(np.uint16))
+    yh = y.cpu().numpy()
+    ref_lp, _ = oracle.token_logprob(xs, yh[rows])
+    old = np.zeros(N, dtype=np.float32)
+    old[rows] = ref_lp + np.random.default_rng(1).normal(size=len(rows)) * 0.05
+    S = N // cfg.seq_len
+    tseq = np.repeat(np.arange(S), cfg.seq_len).astype(np.int32)
+    adv = np.random.default_rng(2).normal(size=S).astype(np.float32)
+    p = rl.LossParams(agg=rl.AGG_SUM)
+    dl = t.empty_like(logits)
+    stats = t.zeros(10, dtype=t.float64, device="cuda")
+    ws = t.empty(rl.policy_loss_workspace_size(N, V), dtype=t.uint8, device="cuda")
+    logp = t.empty(N, device="cuda")
+    rl.policy_loss_fwd_bwd(logits, y, dev(old), dev(tseq), dev(adv), p, dl, stats, ws, logp_out=logp)
+    t.cuda.synchronize()
+    out = oracle.policy_loss_fwd_bwd(xs, yh[rows], old[rows], np.ones(len(rows)), tseq[rows], adv,
+                                     None, None, oracle.LossParams(agg=oracle.AGG_SUM))
+    g_lp = logp.cpu().numpy()[rows]
+    assert np.all(np.abs(g_lp - out["logp"]) <= LOGP_ATOL)
+    d = oracle.decode_bf16(dl[t.from_numpy(rows).cuda()].view(t.int16).cpu().numpy().view(np.uint16))
+    s = out["scale"]
+    for k in range(len(rows)):
+        if s[k] == 0:
+            assert np.all(d[k] == 0)
+        else:
+            assert np.abs(d[k] - out["dlogits"][k]).max() <= DLOGIT_ROW_RTOL * abs(s[k])
+    # every row: |sum_v d| ~ 0 up to bf16 rounding of the row (chunked to bound memory)
+    for c0 in range(0, N, 4096):
+        blk = dl[c0:c0 + 4096].float()
+        sums = blk.sum(dim=1).abs()
+        amax = blk.abs().amax(dim=1)
+        assert bool((sums <= 8e-3 * amax + 1e-5).all())
+        del blk
+    del logits, dl

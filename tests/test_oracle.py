@@ -422,3 +422,16 @@ def test_vocab_split_combine_equals_unsplit(P):
     lse2, zy = oracle.vocab_combine(ms, ss, xs)
     assert np.allclose(lse2, lse, atol=1e-12, rtol=0)
     assert np.allclose(zy - lse2, logp, atol=1e-12, rtol=0)
+
+
+def test_parity_case_builder_runs_on_cpu():
+    """The seeded case builder used by the GPU tests and smoke() (inputs only + oracle chain)."""
+    from tests.cases import oracle_chain, small_case
+    case = small_case()
+    ref = oracle_chain(case, LossParams())
+    assert ref["bk"]["active_tokens"] > 0 and ref["zero_var"][0] == 1
+    assert np.isfinite(ref["loss"]["loss"])
+    case = small_case(vocab=1003, ld=1008, dtype="bf16", staleness_max=8, stale_outlier_frac=0.3,
+                      max_staleness=8, big_delta_frac=0.2)
+    ref = oracle_chain(case, LossParams())
+    assert ref["loss"]["stats"]["stale_masked"] > 0
