@@ -9,6 +9,7 @@
 // (1 HBM read + 1 write, one MUFU.EX2 per element) lives in policy_loss_cluster.cu.
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "loss_common.cuh"
@@ -220,10 +221,14 @@ extern "C" rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, i
     st = launch_loss_cluster(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
                              token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,
                              clipped_out, partials, &n_ctas, s);
+  const char* which = st == RL_OK ? "cluster" : "two_pass";
   if (st == RL_ERR_UNSUPPORTED)
     st = launch_loss_two_pass(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
                               token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,
                               clipped_out, partials, &n_ctas, s);
   if (st != RL_OK) return st;
+  static const bool debug = getenv("RL_DEBUG") != nullptr;
+  if (debug) fprintf(stderr, "[rl] rl_policy_loss_fwd_bwd: %s kernel, %d CTAs, n=%lld V=%lld\n", which,
+                     n_ctas, (long long)n_tokens, (long long)vocab);
   return launch_stats_reduce(partials, n_ctas, stats, acc, s);
 }

@@ -1,12 +1,542 @@
-// Row-resident cluster kernel "R" of the fused loss — placeholder until the
-// kernel lands; the entry point falls back to the two-pass kernel on RL_ERR_UNSUPPORTED.
+// Row-resident cluster kernel "R" of the fused policy loss — the hot kernel.
+//
+// North_star: "a single streaming pass over bf16 logits with online max and sum-exp, using
+// vectorised 128-bit coalesced loads staged through TMA or shared memory ... the gather,
+// ratio, clip, mask and gradient write fused into that same pass, so logits are read once
+// and dlogits written once."
+//
+// A row of V = 151936 bf16 logits is 297 KB, more than one SM's shared memory, so each row is
+// split over a thread-block CLUSTER of CL CTAs (CL = 2 at V = 151936: 148 KB per CTA).  Per CTA:
+//   producer warp : cp.async.bulk (TMA bulk copy) of 7.5 KB chunks of this CTA's column slice
+//                   into a ring of shared-memory slots (mbarrier full/empty pipeline), running
+//                   ahead into the next rows as slots free up.
+//   consumer warps (15), per row i, software-pipelined so the cross-CTA exchange of row i
+//   overlaps the arrival / max pass of row i+1:
+//     pass B(i)  e' = 2^(x k - m_c + 15) from the ring, sum e' (the only MUFU.EX2 per element);
+//                e' is kept as fp16 in REGISTERS (20 x 16 B per thread) and the ring slot is
+//                released immediately -> the ring refills with the next rows during the rest.
+//     send(i)    (m_c, s_c, z_y) record -> peer CTA(s): st.shared::cluster + remote mbarrier arrive
+//     pass A(i+1) max over row i+1's slice as its chunks land (packed bf16 max)
+//     recv(i)    combine in rank order -> lse, logp, ratio, clip, s_t (c3-c7; identical in every
+//                CTA of the cluster, rank 0 records the statistics)
+//     pass C(i)  dlogits = s_t 2^(m_c - 15 - lse2) e'  (target column: s_t (p_y - 1)), bf16 RNE,
+//                128-bit streaming stores straight from the register cache.
+// HBM traffic: logits read once (TMA), dlogits written once.  dlogits may alias logits: a CTA
+// writes only its own slice of row i, after that slice is fully resident.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
 #include "loss_common.cuh"
+#include "rowstats.cuh"
+#include "sm100.cuh"
 
 namespace rl {
-rl_status launch_loss_cluster(const void*, int32_t, int64_t, int64_t, int64_t, const int32_t*,
-                              const float*, const uint8_t*, const int32_t*, const float*,
-                              const int32_t*, const int32_t*, const Knobs&, void*, float*,
-                              uint8_t*, double*, int*, cudaStream_t) {
-  return RL_ERR_UNSUPPORTED;
+
+constexpr int kNcw = 15;  // consumer warps: 15 + 1 producer = 16 warps = 4 per SMSP -> 128 regs/thread
+constexpr int kCons = kNcw * 32;              // consumer threads (one 16-B vector each per chunk)
+constexpr int kChunkVec = kCons;              // vectors per chunk
+constexpr int kChunkBytes = kChunkVec * 16;   // 7.5 KB
+constexpr int kClThreads = kCons + 32;        // + producer warp
+constexpr int kSmemMax = 232448;              // 227 KB opt-in per CTA on sm_100
+
+// fp16 cache of e' = 2^(x k - m + kCacheShift) in (0, 2^15]: the shift keeps the bulk of a
+// peaked row (e ~ 1e-7 .. 1e-9) out of the fp16 subnormal range (abs. precision 2^-39 instead
+// of 2^-24), so the cached probabilities lose no mass; 2^-15 is folded into the pass-C scale.
+constexpr float kCacheShift = 15.f;
+
+struct ClArgs {
+  const void* logits;
+  void* dlogits;
+  int64_t n_tokens, V, ld, nvec;
+  int64_t h_vec;  // vectors per CTA slice
+  const int32_t* targets;
+  const float* old_logp;
+  const uint8_t* mask;
+  const int32_t* token_seq;
+  const float* seq_adv;
+  const int32_t* seq_version;
+  const int32_t* seq_active;
+  float* logp_out;
+  uint8_t* clipped_out;
+  double* partials;
+  Knobs kn;
+  int32_t nslots;
+};
+
+struct __align__(16) ClShared {
+  double acc[RL_LOSS_STATS_N];  // per-CTA statistics (thread 0; kept out of registers)
+  float4 xch[2][8];             // [row parity][cluster rank]: (m_c log2 units, s_c, z_y, owned)
+  float red_max[kNcw];
+  float red_sum[kNcw];
+  float row_sc[3];              // q, s_t, d_y
+  int ycol;                     // target column if inside this CTA's slice, else -1
+  uint64_t xbar[2];
+  // followed by full[nslots], empty[nslots] (uint64) then the ring (128-B aligned)
+};
+
+// ------------------------------------------------------------------ packed fp32x2 helpers
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
 }
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t cvt_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint64_t h2_to_f2(uint32_t h) {
+  float lo, hi;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+      : "=f"(lo), "=f"(hi)
+      : "r"(h));
+  return f2pack(lo, hi);
+}
+__device__ __forceinline__ uint32_t f2_to_bf2(uint64_t v) {
+  float lo, hi;
+  f2unpack(v, lo, hi);
+  return pack_bf16x2(lo, hi);
+}
+
+// ------------------------------------------------------------------ per-vector kernels
+template <typename T>
+struct ClVec;
+
+template <>
+struct ClVec<bf16_t> {
+  static constexpr int EPV = 8;
+  using MaxT = __nv_bfloat162;
+  __device__ static __forceinline__ MaxT max_init() { return __bfloat162bfloat162(__ushort_as_bfloat16(0xff80)); }
+  // pass A: running packed max
+  __device__ static __forceinline__ void max_acc(const uint4& v, MaxT& m) {
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+    m = __hmax2(m, __hmax2(__hmax2(p[0], p[1]), __hmax2(p[2], p[3])));
+  }
+  __device__ static __forceinline__ float max_to_float(MaxT m) { return fmaxf(__low2float(m), __high2float(m)); }
+  // pass B: e' = 2^(x k + mneg); accumulates packed partial sums, fills the fp16 cache words
+  __device__ static __forceinline__ uint64_t exp_cache(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
+                                                       uint4& c) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t t = ffma2(f2pack(bf16_lo(w[i]), bf16_hi(w[i])), k2, mn2);
+      float a, b;
+      f2unpack(t, a, b);
+      a = fast_exp2(a);
+      b = fast_exp2(b);
+      acc = fadd2(acc, f2pack(a, b));
+      o[i] = cvt_h2(a, b);
+    }
+    c = make_uint4(o[0], o[1], o[2], o[3]);
+    return acc;
+  }
+  // pass C: q * e' -> bf16
+  __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t q2) {
+    return make_uint4(f2_to_bf2(fmul2(h2_to_f2(c.x), q2)), f2_to_bf2(fmul2(h2_to_f2(c.y), q2)),
+                      f2_to_bf2(fmul2(h2_to_f2(c.z), q2)), f2_to_bf2(fmul2(h2_to_f2(c.w), q2)));
+  }
+};
+
+template <>
+struct ClVec<float> {
+  static constexpr int EPV = 4;
+  using MaxT = float;
+  __device__ static __forceinline__ MaxT max_init() { return -INFINITY; }
+  __device__ static __forceinline__ void max_acc(const uint4& v, MaxT& m) {
+    m = fmaxf(fmaxf(m, fmaxf(__uint_as_float(v.x), __uint_as_float(v.y))),
+              fmaxf(__uint_as_float(v.z), __uint_as_float(v.w)));
+  }
+  __device__ static __forceinline__ float max_to_float(MaxT m) { return m; }
+  __device__ static __forceinline__ uint64_t exp_cache(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
+                                                       uint4& c) {
+    uint32_t o[2];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint64_t t = ffma2(f2pack(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1])), k2, mn2);
+      float a, b;
+      f2unpack(t, a, b);
+      a = fast_exp2(a);
+      b = fast_exp2(b);
+      acc = fadd2(acc, f2pack(a, b));
+      o[i] = cvt_h2(a, b);
+    }
+    c.x = o[0];
+    c.y = o[1];
+    return acc;
+  }
+  __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t q2) {
+    float a, b, d, e;
+    f2unpack(fmul2(h2_to_f2(c.x), q2), a, b);
+    f2unpack(fmul2(h2_to_f2(c.y), q2), d, e);
+    return make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(d), __float_as_uint(e));
+  }
+};
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Ring position of the first chunk of a row (slot index + phase parity), advanced per row.
+struct RingPos {
+  uint32_t slot, phase;
+  __device__ __forceinline__ void advance(int n, int nslots) {
+    slot += n;
+    while (slot >= (uint32_t)nslots) {
+      slot -= nslots;
+      phase ^= 1u;
+    }
+  }
+};
+
+// NCH = compile-time upper bound of chunks per CTA slice (the register cache is uint4[NCH]).
+template <typename T, int CL, int NCH>
+__global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArgs a) {
+  constexpr int EPV = ClVec<T>::EPV;
+  using MaxT = typename ClVec<T>::MaxT;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  ClShared& sh = *reinterpret_cast<ClShared*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + sizeof(ClShared));
+  uint64_t* empty = full + a.nslots;
+  const size_t ring_off = (sizeof(ClShared) + 2 * sizeof(uint64_t) * a.nslots + 127) & ~(size_t)127;
+  uint4* ring = reinterpret_cast<uint4*>(smem_raw + ring_off);
+  const int nslots = a.nslots;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t crank = sm100::cluster_ctarank();
+  const int64_t cid = sm100::cluster_id_x();
+  const int64_t ncl = sm100::nclusters_x();
+  const int64_t v0 = (int64_t)crank * a.h_vec;
+  const int64_t v1 = min(a.nvec, v0 + a.h_vec);
+  const int my_nv = (int)max((int64_t)0, v1 - v0);
+  const int nfull = my_nv / kChunkVec;             // full chunks
+  const int last_nv = my_nv - nfull * kChunkVec;   // vectors of the partial last chunk
+  const int nch = nfull + (last_nv > 0);           // <= NCH (checked at launch)
+  const bool tail_owner = crank == CL - 1;
+  const int n_tail = (int)(a.V - a.nvec * EPV);    // < EPV scalar columns after the vectors
+  const int64_t row_bytes = a.ld * elem_bytes<T>();
+
+  if (tid == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], kNcw);
+    }
+    sm100::mbar_init(&sh.xbar[0], CL - 1);
+    sm100::mbar_init(&sh.xbar[1], CL - 1);
+    sm100::fence_mbar_init();
+  }
+  sm100::cluster_sync();  // barriers initialised before any remote arrive / TMA
+
+  if (warp == kNcw) {
+    // ------------------------------------------------------------ producer warp
+    if (lane == 0 && nch > 0) {
+      const uint64_t pol = policy_evict_first();
+      RingPos rp{0, 0};
+      for (int64_t row = cid; row < a.n_tokens; row += ncl) {
+        const char* src = reinterpret_cast<const char*>(a.logits) + row * row_bytes + v0 * 16;
+        for (int j = 0; j < nch; ++j) {
+          sm100::mbar_wait(&empty[rp.slot], rp.phase ^ 1);
+          const uint32_t bytes = (j < nfull ? kChunkVec : last_nv) * 16u;
+          sm100::mbar_arrive_expect_tx(&full[rp.slot], bytes);
+          sm100::bulk_g2s(ring + (size_t)rp.slot * kChunkVec, src + (size_t)j * kChunkBytes, bytes,
+                          &full[rp.slot], pol);
+          rp.advance(1, nslots);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumer warps
+    const float k = a.kn.inv_t * RL_LOG2E;
+    const uint64_t k2 = f2pack(k, k);
+    const double inv_tm = token_mean_inv(a.kn);
+    if (tid == 0)
+      for (int i = 0; i < RL_LOSS_STATS_N; ++i) sh.acc[i] = 0.0;
+    uint4 cache[NCH];  // this thread's fp16 e' values for the current row (registers)
+    RingPos pos{0, 0};
+
+    // pass A of `row` at ring position `p`: waits for each chunk, returns the log2-domain max
+    // (block-reduced; -inf for an empty / all -inf slice) and this thread's tail column in xt.
+    auto pass_a = [&](int64_t row, RingPos p, float& xt) -> float {
+      MaxT mx = ClVec<T>::max_init();
+      uint32_t slot = p.slot, ph = p.phase;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        if (j < nch) {
+          sm100::mbar_wait(&full[slot], ph);
+          if (j < nfull || tid < last_nv) ClVec<T>::max_acc(ring[(size_t)slot * kChunkVec + tid], mx);
+          if (++slot == (uint32_t)nslots) {
+            slot = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+      float m = ClVec<T>::max_to_float(mx);
+      xt = -INFINITY;
+      if (tail_owner && tid < n_tail) {
+        xt = VecTraits<T>::load1(reinterpret_cast<const char*>(a.logits) + row * row_bytes, a.nvec * EPV + tid);
+        m = fmaxf(m, xt);
+      }
+      m = warp_max(m);
+      if (lane == 0) sh.red_max[warp] = m;
+      sm100::named_bar_sync(1, kCons);
+      m = sh.red_max[0];
+#pragma unroll
+      for (int w = 1; w < kNcw; ++w) m = fmaxf(m, sh.red_max[w]);
+      return m * k;
+    };
+
+    int64_t row = cid;
+    uint32_t it = 0;
+    float xt = -INFINITY, xt_next = -INFINITY;
+    float m = row < a.n_tokens ? pass_a(row, pos, xt) : 0.f;
+    for (; row < a.n_tokens; row += ncl, ++it) {
+      const char* rp = reinterpret_cast<const char*>(a.logits) + row * row_bytes;
+      char* dp = reinterpret_cast<char*>(a.dlogits) + row * row_bytes;
+      // row scalars (thread 0 only; their latency is hidden behind pass B and pass A(next))
+      RowMeta mt;
+      float A = 0.f, old = 0.f, zy = 0.f;
+      bool owned = false;
+      if (tid == 0) {
+        mt = row_meta(row, a.V, a.targets, a.mask, a.token_seq, a.seq_version, a.kn.trainer_version,
+                      a.kn.max_staleness);
+        if (mt.valid) {
+          A = a.seq_adv[mt.seq];
+          old = a.old_logp[row];
+        }
+        if (mt.in_range) {
+          const int64_t vy = mt.y / EPV;
+          owned = (vy >= v0 && vy < v1) || (tail_owner && vy >= a.nvec);
+          if (owned) zy = VecTraits<T>::load1(rp, mt.y) * a.kn.inv_t;
+        }
+      }
+      // ---- pass B: e' = 2^(x k - m + 15) -> sum, fp16 register cache; slots released at once
+      const bool live = m != -INFINITY;
+      const uint64_t mn2 = f2pack(kCacheShift - m, kCacheShift - m);
+      uint64_t acc2 = f2pack(0.f, 0.f);
+      {
+        uint32_t slot = pos.slot;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          if (j < nch) {
+            if (live && (j < nfull || tid < last_nv))
+              acc2 = ClVec<T>::exp_cache(ring[(size_t)slot * kChunkVec + tid], k2, mn2, acc2, cache[j]);
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&empty[slot]);
+            if (++slot == (uint32_t)nslots) slot = 0;
+          }
+        }
+      }
+      pos.advance(nch, nslots);
+      float s0, s1;
+      f2unpack(acc2, s0, s1);
+      float sum = s0 + s1;
+      if (tail_owner && tid < n_tail && live) {
+        xt = fast_exp2(fmaf(xt, k, kCacheShift - m));
+        sum += xt;
+      }
+      sum = warp_sum(sum);
+      if (lane == 0) sh.red_sum[warp] = sum;
+      sm100::named_bar_sync(1, kCons);
+      const int par = it & 1;
+      if (tid == 0) {  // send this CTA's record of row i to the peers
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kNcw; ++w) s += sh.red_sum[w];
+        s *= 1.f / 32768.f;  // undo the 2^15 cache shift (exact)
+        const float4 rec = make_float4(m, s, owned ? zy : 0.f, owned ? 1.f : 0.f);
+        sh.xch[par][crank] = rec;
+#pragma unroll
+        for (int r = 0; r < CL; ++r)
+          if (r != (int)crank) {
+            sm100::st_remote_v4(&sh.xch[par][crank], r, rec.x, rec.y, rec.z, rec.w);
+            sm100::mbar_arrive_remote(&sh.xbar[par], r);
+          }
+      }
+      // ---- pass A of the next row overlaps the exchange latency of this one
+      const int64_t next = row + ncl;
+      const float m_next = next < a.n_tokens ? pass_a(next, pos, xt_next) : 0.f;
+      if (tid == 0) {
+        if (CL > 1) sm100::mbar_wait_cluster(&sh.xbar[par], (it >> 1) & 1);
+        // combine in rank order (bitwise identical in every CTA of the cluster)
+        float M = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) M = fmaxf(M, sh.xch[par][r].x);
+        float S = 0.f, z = 0.f;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {
+          const float4 e = sh.xch[par][r];
+          if (e.x != -INFINITY) S += e.y * fast_exp2(e.x - M);
+          z += e.z;
+        }
+        const float c2 = M + fast_log2(S);
+        const float lp = logp_from(mt, z, c2);
+        uint8_t cl = 0;
+        Acc tmp;
+        tmp.zero();
+        const float st = token_epilogue(mt, lp, old, A, a.seq_active, inv_tm, a.kn, tmp, &cl);
+        if (crank == 0) {
+#pragma unroll
+          for (int i = 0; i < RL_LOSS_STATS_N; ++i) sh.acc[i] += tmp.v[i];
+          if (a.logp_out) a.logp_out[row] = lp;
+          if (a.clipped_out) a.clipped_out[row] = cl;
+        }
+        // q = s_t 2^(m_c - 15 - lse2): p_v = (q / s_t) e'_v.  An all -inf / empty slice has no
+        // cache (pass B skipped) and q = 0.
+        sh.row_sc[0] = (st == 0.f || !live) ? 0.f : st * fast_exp2(m - kCacheShift - c2);
+        sh.row_sc[1] = st;
+        sh.row_sc[2] = st * (fast_exp2(z * RL_LOG2E - c2) - 1.f);  // target column: s_t (p_y - 1)
+        sh.ycol = owned ? mt.y : -1;
+      }
+      sm100::named_bar_sync(1, kCons);
+      const float q = sh.row_sc[0], st = sh.row_sc[1], dy = sh.row_sc[2];
+      const int ycol = sh.ycol;
+      // ---- pass C: dlogits for this slice straight from the register cache
+      uint4* out = reinterpret_cast<uint4*>(dp) + v0;
+      const uint64_t q2 = f2pack(q, q);
+      const bool zero = (st == 0.f) || (q == 0.f);
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        if (j < nch && (j < nfull || tid < last_nv)) {
+          const uint4 o = zero ? make_uint4(0, 0, 0, 0) : ClVec<T>::grad(cache[j], q2);
+          st_stream_v4(out + j * kChunkVec + tid, o);
+        }
+      }
+      if (tail_owner && tid < n_tail) {
+        const float o = zero ? 0.f : xt * q;
+        VecTraits<T>::store1(dp, a.nvec * EPV + tid, o);
+      }
+      // target column d_y = s_t (p_y - 1): rewritten by the thread that stored its vector (or
+      // tail column) above — same-thread program order to the same address.
+      if (st != 0.f && ycol >= 0) {
+        const bool in_tail = ycol >= a.nvec * EPV;
+        const int owner = in_tail ? (int)(ycol - a.nvec * EPV) : (int)((ycol / EPV - v0) % kChunkVec);
+        if (tid == owner) VecTraits<T>::store1(dp, ycol, dy);
+      }
+      xt = xt_next;
+      m = m_next;
+    }
+    if (tid == 0) {
+#pragma unroll
+      for (int i = 0; i < RL_LOSS_STATS_N; ++i)
+        a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = crank == 0 ? sh.acc[i] : 0.0;
+    }
+  }
+  __syncwarp();
+  sm100::cluster_sync();  // no CTA leaves while a peer may still arrive on / write its smem
+}
+
+template <typename T, int CL, int NCH>
+static rl_status launch_cl(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_ctas) {
+  ClArgs a = a0;
+  auto kern = loss_cluster_kernel<T, CL, NCH>;
+  const size_t head = (sizeof(ClShared) + 127) & ~(size_t)127;
+  int nslots = (int)((kSmemMax - head - 256) / (kChunkBytes + 16));
+  const int nch = (int)((a.h_vec + kChunkVec - 1) / kChunkVec);
+  if (nch > nslots || nch > NCH) return RL_ERR_UNSUPPORTED;
+  a.nslots = nslots;
+  const size_t smem = ((sizeof(ClShared) + 2 * sizeof(uint64_t) * nslots + 127) & ~(size_t)127) +
+                      (size_t)nslots * kChunkBytes;
+  static bool attr_done = false;
+  if (!attr_done) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return check_launch("cudaFuncSetAttribute(max dynamic smem)");
+    attr_done = true;
+  }
+  static int max_clusters = 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kClThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (!max_clusters) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cfg.gridDim = dim3(sms / CL * CL);
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+      cudaGetLastError();
+      max_clusters = sms / CL;
+    }
+  }
+  const int64_t ncl = std::min<int64_t>(std::min<int64_t>(n, max_clusters), kMaxStatCtas / CL);
+  cfg.gridDim = dim3((unsigned)(ncl * CL));
+  *n_ctas = (int)(ncl * CL);
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return check_launch("loss_cluster_kernel");
+  return check_launch("loss_cluster_kernel");
+}
+
+rl_status launch_loss_cluster(const void* logits, int32_t dtype, int64_t n, int64_t V, int64_t ld,
+                              const int32_t* targets, const float* old_logp, const uint8_t* mask,
+                              const int32_t* token_seq, const float* seq_adv,
+                              const int32_t* seq_version, const int32_t* seq_active,
+                              const Knobs& kn, void* dlogits, float* logp_out, uint8_t* clipped_out,
+                              double* partials, int* n_ctas, cudaStream_t s) {
+  if (kn.flags & RL_F_SKIP_MASKED_READS) return RL_ERR_UNSUPPORTED;
+  ClArgs a;
+  a.logits = logits;
+  a.dlogits = dlogits;
+  a.n_tokens = n;
+  a.V = V;
+  a.ld = ld;
+  const int epv = dtype == RL_BF16 ? 8 : 4;
+  a.nvec = V / epv;
+  a.targets = targets;
+  a.old_logp = old_logp;
+  a.mask = mask;
+  a.token_seq = token_seq;
+  a.seq_adv = seq_adv;
+  a.seq_version = seq_version;
+  a.seq_active = seq_active;
+  a.logp_out = logp_out;
+  a.clipped_out = clipped_out;
+  a.partials = partials;
+  a.kn = kn;
+  a.nslots = 0;
+  // the smallest cluster (and register-cache size) whose per-CTA slice fits
+  const int64_t h2 = (a.nvec + 1) / 2, nch2 = (h2 + kChunkVec - 1) / kChunkVec;
+  const bool bf = dtype == RL_BF16;
+  a.h_vec = h2;
+  if (nch2 <= 2) return bf ? launch_cl<bf16_t, 2, 2>(a, n, s, n_ctas) : launch_cl<float, 2, 2>(a, n, s, n_ctas);
+  if (nch2 <= 5) return bf ? launch_cl<bf16_t, 2, 5>(a, n, s, n_ctas) : launch_cl<float, 2, 5>(a, n, s, n_ctas);
+  if (nch2 <= 10) return bf ? launch_cl<bf16_t, 2, 10>(a, n, s, n_ctas) : launch_cl<float, 2, 10>(a, n, s, n_ctas);
+  if (nch2 <= 20) return bf ? launch_cl<bf16_t, 2, 20>(a, n, s, n_ctas) : launch_cl<float, 2, 20>(a, n, s, n_ctas);
+  a.h_vec = (a.nvec + 3) / 4;
+  return bf ? launch_cl<bf16_t, 4, 20>(a, n, s, n_ctas) : launch_cl<float, 4, 20>(a, n, s, n_ctas);
+}
+
 }  // namespace rl
