@@ -66,13 +66,14 @@ struct ClArgs {
 };
 
 struct __align__(16) ClShared {
-  double acc[RL_LOSS_STATS_N];  // per-CTA statistics (thread 0; kept out of registers)
   float4 xch[2][8];             // [row parity][cluster rank]: (m_c log2 units, s_c, z_y, owned)
-  float red_max[kNcw];
-  float red_sum[kNcw];
-  float row_sc[3];              // q, s_t, d_y
-  int ycol;                     // target column if inside this CTA's slice, else -1
-  uint64_t xbar[2];
+  float red_max[2][kNcw];       // [pass-A call parity][warp] block reduction
+  float red_sum[2][kNcw];       // [row parity][warp] pass-B partial sums (2^15-scaled)
+  float mrow[2];                // [row parity] slice max m_c (log2 units)
+  float4 row_sc[2];             // [row parity] (q, s_t, d_y, target column as int bits or -1)
+  uint64_t xbar[2];             // peer records landed (CL - 1 remote arrivals)
+  uint64_t sumbar[2];           // consumers finished pass B (kNcw arrivals)
+  uint64_t scalebar[2];         // epilogue published row_sc (1 arrival)
   // followed by full[nslots], empty[nslots] (uint64) then the ring (128-B aligned)
 };
 
@@ -218,6 +219,10 @@ struct RingPos {
 };
 
 // NCH = compile-time upper bound of chunks per CTA slice (the register cache is uint4[NCH]).
+//
+// Warp roles: warps 0..14 consume (passes A/B/C); warp 15 is the service warp: lane 0 issues the
+// TMA bulk copies, lane 1 runs the per-row epilogue (DSMEM exchange with the peer CTA(s),
+// combine, ratio/clip/scale, statistics) off the consumers' critical path.
 template <typename T, int CL, int NCH>
 __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArgs a) {
   constexpr int EPV = ClVec<T>::EPV;
@@ -229,6 +234,8 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
   const size_t ring_off = (sizeof(ClShared) + 2 * sizeof(uint64_t) * a.nslots + 127) & ~(size_t)127;
   uint4* ring = reinterpret_cast<uint4*>(smem_raw + ring_off);
   const int nslots = a.nslots;
+  const uint32_t full_s = sm100::smem_u32(full), empty_s = sm100::smem_u32(empty);
+  const uint32_t ring_s = sm100::smem_u32(ring);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -250,21 +257,24 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
       sm100::mbar_init(&full[i], 1);
       sm100::mbar_init(&empty[i], kNcw);
     }
-    sm100::mbar_init(&sh.xbar[0], CL - 1);
-    sm100::mbar_init(&sh.xbar[1], CL - 1);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&sh.xbar[i], CL - 1);
+      sm100::mbar_init(&sh.sumbar[i], kNcw);
+      sm100::mbar_init(&sh.scalebar[i], 1);
+    }
     sm100::fence_mbar_init();
   }
   sm100::cluster_sync();  // barriers initialised before any remote arrive / TMA
 
   if (warp == kNcw) {
-    // ------------------------------------------------------------ producer warp
     if (lane == 0 && nch > 0) {
+      // ---------------------------------------------------------- TMA producer (lane 0)
       const uint64_t pol = policy_evict_first();
       RingPos rp{0, 0};
       for (int64_t row = cid; row < a.n_tokens; row += ncl) {
         const char* src = reinterpret_cast<const char*>(a.logits) + row * row_bytes + v0 * 16;
         for (int j = 0; j < nch; ++j) {
-          sm100::mbar_wait(&empty[rp.slot], rp.phase ^ 1);
+          sm100::mbar_wait_a(empty_s + rp.slot * 8, rp.phase ^ 1);
           const uint32_t bytes = (j < nfull ? kChunkVec : last_nv) * 16u;
           sm100::mbar_arrive_expect_tx(&full[rp.slot], bytes);
           sm100::bulk_g2s(ring + (size_t)rp.slot * kChunkVec, src + (size_t)j * kChunkBytes, bytes,
@@ -272,62 +282,20 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
           rp.advance(1, nslots);
         }
       }
-    }
-  } else {
-    // ------------------------------------------------------------ consumer warps
-    const float k = a.kn.inv_t * RL_LOG2E;
-    const uint64_t k2 = f2pack(k, k);
-    const double inv_tm = token_mean_inv(a.kn);
-    if (tid == 0)
-      for (int i = 0; i < RL_LOSS_STATS_N; ++i) sh.acc[i] = 0.0;
-    uint4 cache[NCH];  // this thread's fp16 e' values for the current row (registers)
-    RingPos pos{0, 0};
-
-    // pass A of `row` at ring position `p`: waits for each chunk, returns the log2-domain max
-    // (block-reduced; -inf for an empty / all -inf slice) and this thread's tail column in xt.
-    auto pass_a = [&](int64_t row, RingPos p, float& xt) -> float {
-      MaxT mx = ClVec<T>::max_init();
-      uint32_t slot = p.slot, ph = p.phase;
-#pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        if (j < nch) {
-          sm100::mbar_wait(&full[slot], ph);
-          if (j < nfull || tid < last_nv) ClVec<T>::max_acc(ring[(size_t)slot * kChunkVec + tid], mx);
-          if (++slot == (uint32_t)nslots) {
-            slot = 0;
-            ph ^= 1u;
-          }
-        }
-      }
-      float m = ClVec<T>::max_to_float(mx);
-      xt = -INFINITY;
-      if (tail_owner && tid < n_tail) {
-        xt = VecTraits<T>::load1(reinterpret_cast<const char*>(a.logits) + row * row_bytes, a.nvec * EPV + tid);
-        m = fmaxf(m, xt);
-      }
-      m = warp_max(m);
-      if (lane == 0) sh.red_max[warp] = m;
-      sm100::named_bar_sync(1, kCons);
-      m = sh.red_max[0];
-#pragma unroll
-      for (int w = 1; w < kNcw; ++w) m = fmaxf(m, sh.red_max[w]);
-      return m * k;
-    };
-
-    int64_t row = cid;
-    uint32_t it = 0;
-    float xt = -INFINITY, xt_next = -INFINITY;
-    float m = row < a.n_tokens ? pass_a(row, pos, xt) : 0.f;
-    for (; row < a.n_tokens; row += ncl, ++it) {
-      const char* rp = reinterpret_cast<const char*>(a.logits) + row * row_bytes;
-      char* dp = reinterpret_cast<char*>(a.dlogits) + row * row_bytes;
-      // row scalars (thread 0 only; their latency is hidden behind pass B and pass A(next))
-      RowMeta mt;
-      float A = 0.f, old = 0.f, zy = 0.f;
-      bool owned = false;
-      if (tid == 0) {
-        mt = row_meta(row, a.V, a.targets, a.mask, a.token_seq, a.seq_version, a.kn.trainer_version,
-                      a.kn.max_staleness);
+    } else if (lane == 1) {
+      // ---------------------------------------------------------- row epilogue (lane 1)
+      const double inv_tm = token_mean_inv(a.kn);
+      Acc acc;
+      acc.zero();
+      uint32_t it = 0;
+      for (int64_t row = cid; row < a.n_tokens; row += ncl, ++it) {
+        const int par = it & 1;
+        const uint32_t ph = (it >> 1) & 1;
+        const char* rp = reinterpret_cast<const char*>(a.logits) + row * row_bytes;
+        const RowMeta mt = row_meta(row, a.V, a.targets, a.mask, a.token_seq, a.seq_version,
+                                    a.kn.trainer_version, a.kn.max_staleness);
+        float A = 0.f, old = 0.f, zy = 0.f;
+        bool owned = false;
         if (mt.valid) {
           A = a.seq_adv[mt.seq];
           old = a.old_logp[row];
@@ -337,41 +305,12 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
           owned = (vy >= v0 && vy < v1) || (tail_owner && vy >= a.nvec);
           if (owned) zy = VecTraits<T>::load1(rp, mt.y) * a.kn.inv_t;
         }
-      }
-      // ---- pass B: e' = 2^(x k - m + 15) -> sum, fp16 register cache; slots released at once
-      const bool live = m != -INFINITY;
-      const uint64_t mn2 = f2pack(kCacheShift - m, kCacheShift - m);
-      uint64_t acc2 = f2pack(0.f, 0.f);
-      {
-        uint32_t slot = pos.slot;
-#pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-          if (j < nch) {
-            if (live && (j < nfull || tid < last_nv))
-              acc2 = ClVec<T>::exp_cache(ring[(size_t)slot * kChunkVec + tid], k2, mn2, acc2, cache[j]);
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(&empty[slot]);
-            if (++slot == (uint32_t)nslots) slot = 0;
-          }
-        }
-      }
-      pos.advance(nch, nslots);
-      float s0, s1;
-      f2unpack(acc2, s0, s1);
-      float sum = s0 + s1;
-      if (tail_owner && tid < n_tail && live) {
-        xt = fast_exp2(fmaf(xt, k, kCacheShift - m));
-        sum += xt;
-      }
-      sum = warp_sum(sum);
-      if (lane == 0) sh.red_sum[warp] = sum;
-      sm100::named_bar_sync(1, kCons);
-      const int par = it & 1;
-      if (tid == 0) {  // send this CTA's record of row i to the peers
+        sm100::mbar_wait(&sh.sumbar[par], ph);
         float s = 0.f;
 #pragma unroll
-        for (int w = 0; w < kNcw; ++w) s += sh.red_sum[w];
+        for (int w = 0; w < kNcw; ++w) s += sh.red_sum[par][w];
         s *= 1.f / 32768.f;  // undo the 2^15 cache shift (exact)
+        const float m = sh.mrow[par];
         const float4 rec = make_float4(m, s, owned ? zy : 0.f, owned ? 1.f : 0.f);
         sh.xch[par][crank] = rec;
 #pragma unroll
@@ -380,12 +319,7 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
             sm100::st_remote_v4(&sh.xch[par][crank], r, rec.x, rec.y, rec.z, rec.w);
             sm100::mbar_arrive_remote(&sh.xbar[par], r);
           }
-      }
-      // ---- pass A of the next row overlaps the exchange latency of this one
-      const int64_t next = row + ncl;
-      const float m_next = next < a.n_tokens ? pass_a(next, pos, xt_next) : 0.f;
-      if (tid == 0) {
-        if (CL > 1) sm100::mbar_wait_cluster(&sh.xbar[par], (it >> 1) & 1);
+        if (CL > 1) sm100::mbar_wait_cluster(&sh.xbar[par], ph);
         // combine in rank order (bitwise identical in every CTA of the cluster)
         float M = -INFINITY;
 #pragma unroll
@@ -405,20 +339,110 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
         const float st = token_epilogue(mt, lp, old, A, a.seq_active, inv_tm, a.kn, tmp, &cl);
         if (crank == 0) {
 #pragma unroll
-          for (int i = 0; i < RL_LOSS_STATS_N; ++i) sh.acc[i] += tmp.v[i];
+          for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
           if (a.logp_out) a.logp_out[row] = lp;
           if (a.clipped_out) a.clipped_out[row] = cl;
         }
         // q = s_t 2^(m_c - 15 - lse2): p_v = (q / s_t) e'_v.  An all -inf / empty slice has no
-        // cache (pass B skipped) and q = 0.
-        sh.row_sc[0] = (st == 0.f || !live) ? 0.f : st * fast_exp2(m - kCacheShift - c2);
-        sh.row_sc[1] = st;
-        sh.row_sc[2] = st * (fast_exp2(z * RL_LOG2E - c2) - 1.f);  // target column: s_t (p_y - 1)
-        sh.ycol = owned ? mt.y : -1;
+        // cache (pass B skipped) and q = 0.  Target column: d_y = s_t (p_y - 1).
+        const float q = (st == 0.f || m == -INFINITY) ? 0.f : st * fast_exp2(m - kCacheShift - c2);
+        const float dy = st * (fast_exp2(z * RL_LOG2E - c2) - 1.f);
+        sh.row_sc[par] = make_float4(q, st, dy, __int_as_float(owned ? mt.y : -1));
+        sm100::mbar_arrive(&sh.scalebar[par]);
       }
+#pragma unroll
+      for (int i = 0; i < RL_LOSS_STATS_N; ++i)
+        a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = crank == 0 ? acc.v[i] : 0.0;
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ consumer warps
+    const float k = a.kn.inv_t * RL_LOG2E;
+    const uint64_t k2 = f2pack(k, k);
+    const uint32_t my_off = (uint32_t)tid * 16u;
+    uint4 cache[NCH];  // this thread's fp16 e' values for the current row (registers)
+    RingPos pos{0, 0};
+
+    // pass A of `row` at ring position `p`: waits for each chunk, returns the log2-domain max
+    // (block-reduced; -inf for an empty / all -inf slice) and this thread's tail column in xt.
+    uint32_t acall = 0;  // pass-A call counter (red_max double buffer)
+    auto pass_a = [&](int64_t row, RingPos p, float& xt) -> float {
+      MaxT mx = ClVec<T>::max_init();
+      const int ab = (acall++) & 1;
+      uint32_t slot = p.slot, ph = p.phase;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        if (j < nch) {
+          sm100::mbar_wait_a(full_s + slot * 8, ph);
+          if (j < nfull || tid < last_nv)
+            ClVec<T>::max_acc(sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off), mx);
+          if (++slot == (uint32_t)nslots) {
+            slot = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+      float m = ClVec<T>::max_to_float(mx);
+      xt = -INFINITY;
+      if (tail_owner && tid < n_tail) {
+        xt = VecTraits<T>::load1(reinterpret_cast<const char*>(a.logits) + row * row_bytes, a.nvec * EPV + tid);
+        m = fmaxf(m, xt);
+      }
+      m = warp_max(m);
+      if (lane == 0) sh.red_max[ab][warp] = m;
       sm100::named_bar_sync(1, kCons);
-      const float q = sh.row_sc[0], st = sh.row_sc[1], dy = sh.row_sc[2];
-      const int ycol = sh.ycol;
+      m = sh.red_max[ab][0];
+#pragma unroll
+      for (int w = 1; w < kNcw; ++w) m = fmaxf(m, sh.red_max[ab][w]);
+      return m * k;
+    };
+
+    int64_t row = cid;
+    uint32_t it = 0;
+    float xt = -INFINITY, xt_next = -INFINITY;
+    float m = row < a.n_tokens ? pass_a(row, pos, xt) : 0.f;
+    for (; row < a.n_tokens; row += ncl, ++it) {
+      const int par = it & 1;
+      char* dp = reinterpret_cast<char*>(a.dlogits) + row * row_bytes;
+      // ---- pass B: e' = 2^(x k - m + 15) -> sum, fp16 register cache; slots released at once
+      const bool live = m != -INFINITY;
+      const uint64_t mn2 = f2pack(kCacheShift - m, kCacheShift - m);
+      uint64_t acc2 = f2pack(0.f, 0.f);
+      {
+        uint32_t slot = pos.slot;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          if (j < nch) {
+            if (live && (j < nfull || tid < last_nv))
+              acc2 = ClVec<T>::exp_cache(sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off), k2,
+                                         mn2, acc2, cache[j]);
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive_a(empty_s + slot * 8);
+            if (++slot == (uint32_t)nslots) slot = 0;
+          }
+        }
+      }
+      pos.advance(nch, nslots);
+      float s0, s1;
+      f2unpack(acc2, s0, s1);
+      float sum = s0 + s1;
+      if (tail_owner && tid < n_tail && live) {
+        xt = fast_exp2(fmaf(xt, k, kCacheShift - m));
+        sum += xt;
+      }
+      sum = warp_sum(sum);
+      if (lane == 0) {
+        sh.red_sum[par][warp] = sum;
+        if (warp == 0) sh.mrow[par] = m;
+        sm100::mbar_arrive(&sh.sumbar[par]);
+      }
+      // ---- pass A of the next row overlaps the epilogue / exchange of this one
+      const int64_t next = row + ncl;
+      const float m_next = next < a.n_tokens ? pass_a(next, pos, xt_next) : 0.f;
+      sm100::mbar_wait(&sh.scalebar[par], (it >> 1) & 1);
+      const float4 sc = sh.row_sc[par];
+      const float q = sc.x, st = sc.y, dy = sc.z;
+      const int ycol = __float_as_int(sc.w);
       // ---- pass C: dlogits for this slice straight from the register cache
       uint4* out = reinterpret_cast<uint4*>(dp) + v0;
       const uint64_t q2 = f2pack(q, q);
@@ -434,8 +458,8 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
         const float o = zero ? 0.f : xt * q;
         VecTraits<T>::store1(dp, a.nvec * EPV + tid, o);
       }
-      // target column d_y = s_t (p_y - 1): rewritten by the thread that stored its vector (or
-      // tail column) above — same-thread program order to the same address.
+      // target column: rewritten by the thread that stored its vector (or tail column) above —
+      // same-thread program order to the same address.
       if (st != 0.f && ycol >= 0) {
         const bool in_tail = ycol >= a.nvec * EPV;
         const int owner = in_tail ? (int)(ycol - a.nvec * EPV) : (int)((ycol / EPV - v0) % kChunkVec);
@@ -443,11 +467,6 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
       }
       xt = xt_next;
       m = m_next;
-    }
-    if (tid == 0) {
-#pragma unroll
-      for (int i = 0; i < RL_LOSS_STATS_N; ++i)
-        a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = crank == 0 ? sh.acc[i] : 0.0;
     }
   }
   __syncwarp();
