@@ -134,6 +134,7 @@ struct ClVec<bf16_t> {
     m = __hmax2(m, __hmax2(__hmax2(p[0], p[1]), __hmax2(p[2], p[3])));
   }
   __device__ static __forceinline__ float max_to_float(MaxT m) { return fmaxf(__low2float(m), __high2float(m)); }
+  __device__ static __forceinline__ uint4 neg_inf_vec() { return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u); }
   // pass B: e' = 2^(x k + mneg); accumulates packed partial sums, fills the fp16 cache words
   __device__ static __forceinline__ uint64_t exp_cache(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
                                                        uint4& c) {
@@ -169,6 +170,7 @@ struct ClVec<float> {
               fmaxf(__uint_as_float(v.z), __uint_as_float(v.w)));
   }
   __device__ static __forceinline__ float max_to_float(MaxT m) { return m; }
+  __device__ static __forceinline__ uint4 neg_inf_vec() { return make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u); }
   __device__ static __forceinline__ uint64_t exp_cache(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
                                                        uint4& c) {
     uint32_t o[2];
@@ -223,7 +225,7 @@ struct RingPos {
 // Warp roles: warps 0..14 consume (passes A/B/C); warp 15 is the service warp: lane 0 issues the
 // TMA bulk copies, lane 1 runs the per-row epilogue (DSMEM exchange with the peer CTA(s),
 // combine, ratio/clip/scale, statistics) off the consumers' critical path.
-template <typename T, int CL, int NCH>
+template <typename T, int CL, int NCH, bool EXACT>
 __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArgs a) {
   constexpr int EPV = ClVec<T>::EPV;
   using MaxT = typename ClVec<T>::MaxT;
@@ -360,8 +362,13 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
     const float k = a.kn.inv_t * RL_LOG2E;
     const uint64_t k2 = f2pack(k, k);
     const uint32_t my_off = (uint32_t)tid * 16u;
+    const bool last_mine = tid < last_nv;  // this thread's vector exists in the partial last chunk
     uint4 cache[NCH];  // this thread's fp16 e' values for the current row (registers)
     RingPos pos{0, 0};
+    // chunk j of a row: present (uniform), partial (uniform: the ragged last chunk), mine (per thread)
+#define RL_PRESENT(j) (EXACT ? true : ((j) < nch))
+#define RL_PARTIAL(j) (EXACT ? ((j) == NCH - 1 && last_nv > 0) : ((j) == nfull))
+#define RL_MINE(j) (!RL_PARTIAL(j) || last_mine)
 
     // pass A of `row` at ring position `p`: waits for each chunk, returns the log2-domain max
     // (block-reduced; -inf for an empty / all -inf slice) and this thread's tail column in xt.
@@ -372,10 +379,11 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
       uint32_t slot = p.slot, ph = p.phase;
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
-        if (j < nch) {
+        if (RL_PRESENT(j)) {
           sm100::mbar_wait_a(full_s + slot * 8, ph);
-          if (j < nfull || tid < last_nv)
-            ClVec<T>::max_acc(sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off), mx);
+          uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off);
+          if (!RL_MINE(j)) v = ClVec<T>::neg_inf_vec();  // stale bytes past the slice
+          ClVec<T>::max_acc(v, mx);
           if (++slot == (uint32_t)nslots) {
             slot = 0;
             ph ^= 1u;
@@ -397,29 +405,36 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
       return m * k;
     };
 
+    // pass B of the first row (no pass C to fuse with yet)
+    auto send_sum = [&](uint32_t itn, float mm, float sum) {
+      sum = warp_sum(sum);
+      if (lane == 0) {
+        sh.red_sum[itn & 1][warp] = sum;
+        if (warp == 0) sh.mrow[itn & 1] = mm;
+        sm100::mbar_arrive(&sh.sumbar[itn & 1]);
+      }
+    };
+
     int64_t row = cid;
     uint32_t it = 0;
     float xt = -INFINITY, xt_next = -INFINITY;
-    float m = row < a.n_tokens ? pass_a(row, pos, xt) : 0.f;
-    for (; row < a.n_tokens; row += ncl, ++it) {
-      const int par = it & 1;
-      char* dp = reinterpret_cast<char*>(a.dlogits) + row * row_bytes;
-      // ---- pass B: e' = 2^(x k - m + 15) -> sum, fp16 register cache; slots released at once
+    float m = 0.f;
+    if (row < a.n_tokens) {
+      m = pass_a(row, pos, xt);
       const bool live = m != -INFINITY;
       const uint64_t mn2 = f2pack(kCacheShift - m, kCacheShift - m);
       uint64_t acc2 = f2pack(0.f, 0.f);
-      {
-        uint32_t slot = pos.slot;
+      uint32_t slot = pos.slot;
 #pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-          if (j < nch) {
-            if (live && (j < nfull || tid < last_nv))
-              acc2 = ClVec<T>::exp_cache(sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off), k2,
-                                         mn2, acc2, cache[j]);
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive_a(empty_s + slot * 8);
-            if (++slot == (uint32_t)nslots) slot = 0;
+      for (int j = 0; j < NCH; ++j) {
+        if (RL_PRESENT(j)) {
+          if (live) {
+            const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off);
+            const uint64_t nacc = ClVec<T>::exp_cache(v, k2, mn2, acc2, cache[j]);
+            acc2 = RL_MINE(j) ? nacc : acc2;
           }
+          sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+          if (++slot == (uint32_t)nslots) slot = 0;
         }
       }
       pos.advance(nch, nslots);
@@ -430,28 +445,42 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
         xt = fast_exp2(fmaf(xt, k, kCacheShift - m));
         sum += xt;
       }
-      sum = warp_sum(sum);
-      if (lane == 0) {
-        sh.red_sum[par][warp] = sum;
-        if (warp == 0) sh.mrow[par] = m;
-        sm100::mbar_arrive(&sh.sumbar[par]);
-      }
+      send_sum(0, m, sum);
+    }
+    for (; row < a.n_tokens; row += ncl, ++it) {
+      const int par = it & 1;
+      char* dp = reinterpret_cast<char*>(a.dlogits) + row * row_bytes;
       // ---- pass A of the next row overlaps the epilogue / exchange of this one
       const int64_t next = row + ncl;
-      const float m_next = next < a.n_tokens ? pass_a(next, pos, xt_next) : 0.f;
+      const bool has_next = next < a.n_tokens;
+      const float m_next = has_next ? pass_a(next, pos, xt_next) : 0.f;
       sm100::mbar_wait(&sh.scalebar[par], (it >> 1) & 1);
       const float4 sc = sh.row_sc[par];
       const float q = sc.x, st = sc.y, dy = sc.z;
       const int ycol = __float_as_int(sc.w);
-      // ---- pass C: dlogits for this slice straight from the register cache
-      uint4* out = reinterpret_cast<uint4*>(dp) + v0;
-      const uint64_t q2 = f2pack(q, q);
       const bool zero = (st == 0.f) || (q == 0.f);
+      const uint64_t q2 = f2pack(q, q);
+      uint4* out = reinterpret_cast<uint4*>(dp) + v0 + tid;
+      // ---- fused pass C(row) + pass B(next), chunk by chunk: the dlogits stores of this row
+      // drain while the exp2 work of the next row runs; each register-cache entry is emptied
+      // (stored) and refilled in place.
+      const bool live = has_next && m_next != -INFINITY;
+      const uint64_t mn2 = f2pack(kCacheShift - m_next, kCacheShift - m_next);
+      uint64_t acc2 = f2pack(0.f, 0.f);
+      uint32_t slot = pos.slot;
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
-        if (j < nch && (j < nfull || tid < last_nv)) {
-          const uint4 o = zero ? make_uint4(0, 0, 0, 0) : ClVec<T>::grad(cache[j], q2);
-          st_stream_v4(out + j * kChunkVec + tid, o);
+        if (RL_PRESENT(j)) {
+          if (RL_MINE(j)) st_stream_v4(out + j * kChunkVec, zero ? make_uint4(0, 0, 0, 0) : ClVec<T>::grad(cache[j], q2));
+          if (has_next) {
+            if (live) {
+              const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off);
+              const uint64_t nacc = ClVec<T>::exp_cache(v, k2, mn2, acc2, cache[j]);
+              acc2 = RL_MINE(j) ? nacc : acc2;
+            }
+            sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+            if (++slot == (uint32_t)nslots) slot = 0;
+          }
         }
       }
       if (tail_owner && tid < n_tail) {
@@ -465,22 +494,36 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
         const int owner = in_tail ? (int)(ycol - a.nvec * EPV) : (int)((ycol / EPV - v0) % kChunkVec);
         if (tid == owner) VecTraits<T>::store1(dp, ycol, dy);
       }
+      if (has_next) {
+        pos.advance(nch, nslots);
+        float s0, s1;
+        f2unpack(acc2, s0, s1);
+        float sum = s0 + s1;
+        if (tail_owner && tid < n_tail && live) {
+          xt_next = fast_exp2(fmaf(xt_next, k, kCacheShift - m_next));
+          sum += xt_next;
+        }
+        send_sum(it + 1, m_next, sum);
+      }
       xt = xt_next;
       m = m_next;
     }
+#undef RL_PRESENT
+#undef RL_PARTIAL
+#undef RL_MINE
   }
   __syncwarp();
   sm100::cluster_sync();  // no CTA leaves while a peer may still arrive on / write its smem
 }
 
-template <typename T, int CL, int NCH>
+template <typename T, int CL, int NCH, bool EXACT = false>
 static rl_status launch_cl(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_ctas) {
   ClArgs a = a0;
-  auto kern = loss_cluster_kernel<T, CL, NCH>;
+  auto kern = loss_cluster_kernel<T, CL, NCH, EXACT>;
   const size_t head = (sizeof(ClShared) + 127) & ~(size_t)127;
   int nslots = (int)((kSmemMax - head - 256) / (kChunkBytes + 16));
   const int nch = (int)((a.h_vec + kChunkVec - 1) / kChunkVec);
-  if (nch > nslots || nch > NCH) return RL_ERR_UNSUPPORTED;
+  if (nch > nslots || nch > NCH || (EXACT && nch != NCH)) return RL_ERR_UNSUPPORTED;
   a.nslots = nslots;
   const size_t smem = ((sizeof(ClShared) + 2 * sizeof(uint64_t) * nslots + 127) & ~(size_t)127) +
                       (size_t)nslots * kChunkBytes;
@@ -550,6 +593,8 @@ rl_status launch_loss_cluster(const void* logits, int32_t dtype, int64_t n, int6
   const int64_t h2 = (a.nvec + 1) / 2, nch2 = (h2 + kChunkVec - 1) / kChunkVec;
   const bool bf = dtype == RL_BF16;
   a.h_vec = h2;
+  if (bf && nch2 == 20) return launch_cl<bf16_t, 2, 20, true>(a, n, s, n_ctas);  // V = 151936
+  if (bf && nch2 == 17) return launch_cl<bf16_t, 2, 17, true>(a, n, s, n_ctas);  // V = 128256
   if (nch2 <= 2) return bf ? launch_cl<bf16_t, 2, 2>(a, n, s, n_ctas) : launch_cl<float, 2, 2>(a, n, s, n_ctas);
   if (nch2 <= 5) return bf ? launch_cl<bf16_t, 2, 5>(a, n, s, n_ctas) : launch_cl<float, 2, 5>(a, n, s, n_ctas);
   if (nch2 <= 10) return bf ? launch_cl<bf16_t, 2, 10>(a, n, s, n_ctas) : launch_cl<float, 2, 10>(a, n, s, n_ctas);

@@ -154,3 +154,18 @@ __device__ __forceinline__ uint4 lds128_a(uint32_t addr) {
 }
 }  // namespace sm100
 }  // namespace rl
+
+namespace rl {
+namespace sm100 {
+// mbarrier arrive by lane 0 of a converged warp, predicated (no branch / no warp-sync): the
+// preceding ld.shared of every lane is the same warp instruction as lane 0's, whose result the
+// arrive is ordered after.
+__device__ __forceinline__ void mbar_arrive_lane0(uint32_t bar, uint32_t lane) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\t"
+      "@p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar),
+      "r"(lane)
+      : "memory");
+}
+}  // namespace sm100
+}  // namespace rl
