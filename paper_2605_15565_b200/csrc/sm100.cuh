@@ -169,3 +169,24 @@ __device__ __forceinline__ void mbar_arrive_lane0(uint32_t bar, uint32_t lane) {
 }
 }  // namespace sm100
 }  // namespace rl
+
+namespace rl {
+namespace sm100 {
+// bulk L2 prefetch of [src, src+bytes) (bytes % 16 == 0): pulls a future row slice into L2 so the
+// later TMA load of each chunk is an L2 hit (lookahead beyond the shared-memory ring).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
+}
+}  // namespace sm100
+}  // namespace rl
+
+namespace rl {
+namespace sm100 {
+// shared-memory atomic add with acquire-release semantics at CTA scope; returns the old value
+__device__ __forceinline__ uint32_t atom_add_acqrel(uint32_t addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  return old;
+}
+}  // namespace sm100
+}  // namespace rl
