@@ -40,7 +40,7 @@ SIDE_BYTES = 17          # target 4 + old_logp 4 + mask 1 + logp out 4 + token_s
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default=None, choices=[None, "cluster", "two_pass"])
@@ -355,7 +355,7 @@ def main():
         yy = pool_y[0][:64].cpu().numpy()
         oo = pool_old[0][:64].cpu().numpy()
         workers = host_cores()
-        rate, secs, done = time_oracle(x16, yy, oo, 4096, workers)
+        rate, secs, done = time_oracle(x16, yy, oo, 8192, workers)
         cpu = {"value": rate, "unit": "tokens/s", "cores": workers, "kind": "oracle",
                "sample": f"{done} token rows (64 distinct rows of mini-batch 0) x V=151936 fwd+bwd "
                          f"in {secs:.1f} s wall over {workers} processes"}
