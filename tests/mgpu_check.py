@@ -1,0 +1,150 @@
+"""Multi-GPU parity check (one process per GPU; launched by tests/test_gpu_multi.py):
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_check.py
+
+token parallel: whole-sequence shards, rl_batch_counts all-reduced through rl_comm before the
+loss, rl_loss_stats after it -> global loss / counts equal the unsplit oracle, each rank's dlogits
+rows equal the oracle's rows.  vocab parallel: column shards, NCCL all-gather combine -> logp on
+every rank and each dlogits shard equal the oracle.  comm split by colour.
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    import paper_2605_15565_b200 as rl
+    from paper_2605_15565_b200.parallel import shard_sequences, shard_vocab
+    from tests.cases import oracle_chain, small_case
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    rl.load()
+    comm = rl.Comm.from_torch()
+
+    def d(a):
+        if a.dtype == np.uint16:
+            return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).to(dev).view(torch.bfloat16)
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    case = small_case(n_prompts=4, group=4, seq_len=48, vocab=5003, ld=5008, dtype="bf16", seed=77,
+                      staleness_max=3, max_staleness=2, big_delta_frac=0.1, sigma_delta=0.1)
+    V, S = case["vocab"], len(case["rewards"])
+    ref = oracle_chain(case, oracle.LossParams())
+    out_ref = ref["loss"]
+    fails = []
+
+    # ------------------------------------------------------------------ token parallel
+    sh = shard_sequences(case["cu_seqlens"], world, rank)
+    t0, t1, s0, s1 = sh.tok_begin, sh.tok_end, sh.seq_begin, sh.seq_end
+    n = t1 - t0
+    adv = torch.empty(S, dtype=torch.float32, device=dev)
+    rl.group_advantage(d(case["rewards"]), d(case["cu_groups"]), adv)       # replicated
+    counts = torch.zeros(20, dtype=torch.float64, device=dev)
+    tok = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    act = torch.empty(max(s1 - s0, 1), dtype=torch.int32, device=dev)
+    cu_local = (np.asarray(case["cu_seqlens"][s0:s1 + 1]) - t0).astype(np.int32)
+    rl.seq_bookkeeping(d(cu_local), d(case["targets"][t0:t1]), V, tok[:n], act[:s1 - s0],
+                       loss_mask=d(case["loss_mask"][t0:t1]), seq_version=d(case["seq_version"][s0:s1]),
+                       trainer_version=case["trainer_version"], max_staleness=case["max_staleness"],
+                       counts_out=counts)
+    comm.allreduce_f64(counts)                        # N_active over all ranks
+    logits = d(case["logits"][t0:t1])
+    dl = torch.empty_like(logits)
+    stats = torch.zeros(10, dtype=torch.float64, device=dev)
+    ws = torch.empty(rl.policy_loss_workspace_size(n, V), dtype=torch.uint8, device=dev)
+    p = rl.LossParams(trainer_version=case["trainer_version"], max_staleness=case["max_staleness"],
+                      active_tokens_dev=counts[0:1])
+    rl.policy_loss_fwd_bwd(logits, d(case["targets"][t0:t1]), d(case["old_logp"][t0:t1]), tok[:n],
+                           adv[s0:], p, dl, stats, ws, loss_mask=d(case["loss_mask"][t0:t1]),
+                           seq_version=d(case["seq_version"][s0:s1]), vocab=V)
+    comm.allreduce_f64(stats)
+    torch.cuda.synchronize()
+    st = stats.cpu().numpy()
+    scale = max(abs(out_ref["loss"]), float(np.abs(out_ref["token_loss"]).sum()))
+    if abs(st[0] - out_ref["loss"]) > 1e-4 * scale:
+        fails.append(f"tp loss {st[0]} vs {out_ref['loss']}")
+    if st[1] != out_ref["stats"]["active_tokens"] or counts[0].item() != ref["bk"]["active_tokens"]:
+        fails.append(f"tp active {st[1]} vs {out_ref['stats']['active_tokens']}")
+    g = oracle.decode_bf16(dl.view(torch.int16).cpu().numpy().view(np.uint16))[:, :V]
+    s_ref = out_ref["scale"][t0:t1]
+    for i in range(n):
+        if s_ref[i] == 0:
+            if np.any(g[i] != 0):
+                fails.append(f"tp row {t0 + i} not zero")
+        elif np.abs(g[i] - out_ref["dlogits"][t0 + i]).max() > 1e-2 * abs(s_ref[i]):
+            fails.append(f"tp row {t0 + i} dlogits")
+
+    # ------------------------------------------------------------------ vocab parallel
+    vs = shard_vocab(V, world, rank)
+    N = len(case["targets"])
+    ld_s = max(8, (vs.size + 7) // 8 * 8)
+    shard = np.zeros((N, ld_s), dtype=np.uint16)
+    shard[:, :vs.size] = case["logits"][:, vs.offset:vs.offset + vs.size]
+    shard_t = d(shard)
+    dls = torch.empty_like(shard_t)
+    logp = torch.empty(N, dtype=torch.float32, device=dev)
+    lse = torch.empty(N, dtype=torch.float32, device=dev)
+    stats_v = torch.zeros(10, dtype=torch.float64, device=dev)
+    ws_v = torch.empty(rl.vocab_parallel_workspace_size(N, world), dtype=torch.uint8, device=dev)
+    p_v = rl.LossParams(trainer_version=case["trainer_version"], max_staleness=case["max_staleness"],
+                        global_active_tokens=float(ref["bk"]["active_tokens"]))
+    tok_full = d(ref["bk"]["token_seq"])
+    rl.vocab_parallel_logprob(shard_t, d(case["targets"]), vs.offset, V, comm, logp, ws_v, lse_out=lse,
+                              vocab_shard=vs.size, old_logp=d(case["old_logp"]),
+                              loss_mask=d(case["loss_mask"]), token_seq=tok_full, seq_adv=adv,
+                              seq_version=d(case["seq_version"]), params=p_v, dlogits_shard=dls,
+                              stats=stats_v)
+    comm.allreduce_f64(stats_v)
+    torch.cuda.synchronize()
+    lp = logp.cpu().numpy()
+    y = case["targets"]
+    ok = (y >= 0) & (y < V)
+    if np.abs(lp[ok] - out_ref["logp"][ok]).max() > 2e-3:
+        fails.append(f"vp logp max err {np.abs(lp[ok] - out_ref['logp'][ok]).max()}")
+    sv = stats_v.cpu().numpy()
+    if abs(sv[0] - out_ref["loss"]) > 1e-4 * scale or sv[1] != out_ref["stats"]["active_tokens"]:
+        fails.append(f"vp loss {sv[0]} vs {out_ref['loss']} active {sv[1]}")
+    gv = oracle.decode_bf16(dls.view(torch.int16).cpu().numpy().view(np.uint16))[:, :vs.size]
+    s_all = out_ref["scale"]
+    for i in range(N):
+        refrow = out_ref["dlogits"][i, vs.offset:vs.offset + vs.size]
+        if s_all[i] == 0:
+            if np.any(gv[i] != 0):
+                fails.append(f"vp row {i} not zero")
+        elif vs.size and np.abs(gv[i] - refrow).max() > 1e-2 * abs(s_all[i]):
+            fails.append(f"vp row {i} dlogits")
+
+    # ------------------------------------------------------------------ comm split
+    sub = comm.split(rank % 2, rank)
+    one = torch.ones(1, dtype=torch.float64, device=dev)
+    sub.allreduce_f64(one)
+    torch.cuda.synchronize()
+    if one.item() != sub.nranks or sub.nranks != len(range(rank % 2, world, 2)):
+        fails.append(f"split group size {one.item()} vs {sub.nranks}")
+    sub.destroy()
+
+    flag = torch.tensor([len(fails)], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag)
+    for f in fails[:10]:
+        print(f"[rank {rank}] FAIL {f}", flush=True)
+    comm.destroy()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("MGPU_OK" if flag.item() == 0 else "MGPU_FAIL", flush=True)
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

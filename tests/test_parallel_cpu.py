@@ -1,0 +1,121 @@
+"""Host logic of the N > 1 path on CPU (no GPU): sharding plans, and the shard algebra of the
+two parallel modes exercised with a world_size-2 gloo process group — each rank computes its
+shard with the oracle, the ranks exchange exactly what the GPU path exchanges (batch counts
+before, loss statistics after; vocab-parallel (m, s, z_y) records), and the result must equal the
+unsplit oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2605_15565_b200.parallel import shard_sequences, shard_vocab
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_sequences_partition(world):
+    rng = np.random.default_rng(world)
+    lens = rng.integers(0, 4000, size=64)
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    shards = [shard_sequences(cu, world, r) for r in range(world)]
+    assert shards[0].seq_begin == 0 and shards[-1].seq_end == 64
+    for a, b in zip(shards, shards[1:]):
+        assert a.seq_end == b.seq_begin and a.tok_end == b.tok_begin
+    assert sum(s.n_tokens for s in shards) == cu[-1]
+    ideal = cu[-1] / world
+    assert max(abs(s.n_tokens - ideal) for s in shards) <= lens.max()
+
+
+def test_shard_sequences_equal_lengths_even_split():
+    cu = np.arange(65) * 32768          # config 2: 64 sequences x 32768
+    for world in (2, 4, 8):
+        assert {shard_sequences(cu, world, r).n_seq for r in range(world)} == {64 // world}
+
+
+@pytest.mark.parametrize("V,world", [(151936, 8), (128256, 4), (1024, 3), (13, 2), (5, 8)])
+def test_shard_vocab_partition(V, world):
+    shards = [shard_vocab(V, world, r) for r in range(world)]
+    assert shards[0].offset == 0
+    assert sum(s.size for s in shards) == V
+    for a, b in zip(shards, shards[1:]):
+        assert a.offset + a.size == b.offset and (b.size == 0 or b.offset % 8 == 0)
+    if V == 151936 and world == 8:
+        assert all(s.size == 18992 for s in shards)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from tests.cases import small_case
+        case = small_case(n_prompts=3, group=4, seq_len=40, vocab=301, dtype="f32", seed=42,
+                          staleness_max=3, max_staleness=2, big_delta_frac=0.2, sigma_delta=0.2)
+        # ---------------- token parallel
+        sh = shard_sequences(case["cu_seqlens"], world, rank)
+        t0, t1, s0, s1 = sh.tok_begin, sh.tok_end, sh.seq_begin, sh.seq_end
+        cu_local = np.asarray(case["cu_seqlens"][s0:s1 + 1]) - t0
+        bk = oracle.seq_bookkeeping(cu_local, case["loss_mask"][t0:t1], case["targets"][t0:t1],
+                                    case["vocab"], case["seq_version"][s0:s1], case["trainer_version"],
+                                    case["max_staleness"])
+        cnt = torch.tensor([float(bk["active_tokens"])], dtype=torch.float64)
+        dist.all_reduce(cnt)                                   # rl_batch_counts all-reduce
+        adv, _ = oracle.group_advantage(case["rewards"], case["cu_groups"])   # replicated
+        p = oracle.LossParams(global_active_tokens=cnt.item(), trainer_version=case["trainer_version"],
+                              max_staleness=case["max_staleness"])
+        out = oracle.policy_loss_fwd_bwd(case["x64"][t0:t1], case["targets"][t0:t1],
+                                         case["old_logp"][t0:t1], case["loss_mask"][t0:t1],
+                                         bk["token_seq"] + s0, adv, case["seq_version"], None, p)
+        st = torch.tensor([out["loss"], out["stats"]["active_tokens"], out["stats"]["ratio_sum"],
+                           out["stats"]["clipped_low"], out["stats"]["clipped_high"]], dtype=torch.float64)
+        dist.all_reduce(st)                                    # rl_loss_stats all-reduce
+        # ---------------- vocab parallel
+        vs = shard_vocab(case["vocab"], world, rank)
+        m, s, xy, owned = oracle.vocab_shard_stats(case["x64"][:, vs.offset:vs.offset + vs.size],
+                                                   case["targets"], vs.offset)
+        rec = torch.tensor(np.stack([m, s, xy]), dtype=torch.float64)
+        allrec = [torch.zeros_like(rec) for _ in range(world)]
+        dist.all_gather(allrec, rec)                           # the vp record all-gather
+        lse, zy = oracle.vocab_combine([r[0].numpy() for r in allrec], [r[1].numpy() for r in allrec],
+                                       [r[2].numpy() for r in allrec])
+        if rank == 0:
+            q.put(dict(stats=st.numpy(), lse=lse, zy=zy))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_gloo_shard_algebra():
+    torch = pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+    from tests.cases import oracle_chain, small_case
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    case = small_case(n_prompts=3, group=4, seq_len=40, vocab=301, dtype="f32", seed=42,
+                      staleness_max=3, max_staleness=2, big_delta_frac=0.2, sigma_delta=0.2)
+    ref = oracle_chain(case, oracle.LossParams())["loss"]
+    st = res["stats"]
+    assert abs(st[0] - ref["loss"]) <= 1e-12 * max(1.0, abs(ref["loss"]))
+    assert st[1] == ref["stats"]["active_tokens"]
+    assert abs(st[2] - ref["stats"]["ratio_sum"]) < 1e-9
+    assert st[3] == ref["stats"]["clipped_low"] and st[4] == ref["stats"]["clipped_high"]
+    logp, lse = oracle.token_logprob(case["x64"], case["targets"])
+    ok = case["targets"] >= 0
+    assert np.allclose(res["lse"], lse, atol=1e-12)
+    assert np.allclose((res["zy"] - res["lse"])[ok], logp[ok], atol=1e-12)
