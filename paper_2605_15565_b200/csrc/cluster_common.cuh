@@ -1,0 +1,189 @@
+// Shared pieces of the row-resident loss kernels (policy_loss_cluster.cu, policy_loss_stream.cu):
+// launch geometry, kernel arguments, packed fp32x2 / fp16 / bf16 helpers, per-vector math.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "loss_common.cuh"
+#include "rowstats.cuh"
+#include "sm100.cuh"
+
+namespace rl {
+
+constexpr int kNcw = 15;  // consumer warps: 15 + 1 producer = 16 warps = 4 per SMSP -> 128 regs/thread
+constexpr int kCons = kNcw * 32;              // consumer threads (one 16-B vector each per chunk)
+constexpr int kChunkVec = kCons;              // vectors per chunk
+constexpr int kChunkBytes = kChunkVec * 16;   // 7.5 KB
+constexpr int kClThreads = kCons + 32;        // + producer warp
+constexpr int kSmemMax = 232448;              // 227 KB opt-in per CTA on sm_100
+
+// fp16 cache of e' = 2^(x k - m + kCacheShift) in (0, 2^15]: the shift keeps the bulk of a
+// peaked row (e ~ 1e-7 .. 1e-9) out of the fp16 subnormal range (abs. precision 2^-39 instead
+// of 2^-24), so the cached probabilities lose no mass; 2^-15 is folded into the pass-C scale.
+constexpr float kCacheShift = 15.f;
+
+struct ClArgs {
+  const void* logits;
+  void* dlogits;
+  int64_t n_tokens, V, ld, nvec;
+  int64_t h_vec;  // vectors per CTA slice
+  const int32_t* targets;
+  const float* old_logp;
+  const uint8_t* mask;
+  const int32_t* token_seq;
+  const float* seq_adv;
+  const int32_t* seq_version;
+  const int32_t* seq_active;
+  float* logp_out;
+  uint8_t* clipped_out;
+  double* partials;
+  Knobs kn;
+  int32_t nslots;
+  int32_t prefetch_chunks;  // L2 lookahead in chunks beyond a full ring (RL_L2_PREFETCH_CHUNKS)
+  int32_t debug;            // development only (RL_CLUSTER_DEBUG): 1 = no dlogits stores, 2 = no exp2
+};
+
+// ------------------------------------------------------------------ packed fp32x2 helpers
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t cvt_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint64_t h2_to_f2(uint32_t h) {
+  float lo, hi;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+      : "=f"(lo), "=f"(hi)
+      : "r"(h));
+  return f2pack(lo, hi);
+}
+__device__ __forceinline__ uint32_t f2_to_bf2(uint64_t v) {
+  float lo, hi;
+  f2unpack(v, lo, hi);
+  return pack_bf16x2(lo, hi);
+}
+
+// ------------------------------------------------------------------ per-vector kernels
+template <typename T>
+struct ClVec;
+
+template <>
+struct ClVec<bf16_t> {
+  static constexpr int EPV = 8;
+  using MaxT = __nv_bfloat162;
+  __device__ static __forceinline__ MaxT max_init() { return __bfloat162bfloat162(__ushort_as_bfloat16(0xff80)); }
+  // pass A: running packed max
+  __device__ static __forceinline__ void max_acc(const uint4& v, MaxT& m) {
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+    m = __hmax2(m, __hmax2(__hmax2(p[0], p[1]), __hmax2(p[2], p[3])));
+  }
+  __device__ static __forceinline__ float max_to_float(MaxT m) { return fmaxf(__low2float(m), __high2float(m)); }
+  __device__ static __forceinline__ uint4 neg_inf_vec() { return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u); }
+  // pass B: e' = 2^(x k + mneg); accumulates packed partial sums, fills the fp16 cache words
+  __device__ static __forceinline__ uint64_t exp_cache(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
+                                                       uint4& c) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t t = ffma2(f2pack(bf16_lo(w[i]), bf16_hi(w[i])), k2, mn2);
+      float a, b;
+      f2unpack(t, a, b);
+      a = fast_exp2(a);
+      b = fast_exp2(b);
+      acc = fadd2(acc, f2pack(a, b));
+      o[i] = cvt_h2(a, b);
+    }
+    c = make_uint4(o[0], o[1], o[2], o[3]);
+    return acc;
+  }
+  // pass C: q * e' -> bf16
+  __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t q2) {
+    return make_uint4(f2_to_bf2(fmul2(h2_to_f2(c.x), q2)), f2_to_bf2(fmul2(h2_to_f2(c.y), q2)),
+                      f2_to_bf2(fmul2(h2_to_f2(c.z), q2)), f2_to_bf2(fmul2(h2_to_f2(c.w), q2)));
+  }
+};
+
+template <>
+struct ClVec<float> {
+  static constexpr int EPV = 4;
+  using MaxT = float;
+  __device__ static __forceinline__ MaxT max_init() { return -INFINITY; }
+  __device__ static __forceinline__ void max_acc(const uint4& v, MaxT& m) {
+    m = fmaxf(fmaxf(m, fmaxf(__uint_as_float(v.x), __uint_as_float(v.y))),
+              fmaxf(__uint_as_float(v.z), __uint_as_float(v.w)));
+  }
+  __device__ static __forceinline__ float max_to_float(MaxT m) { return m; }
+  __device__ static __forceinline__ uint4 neg_inf_vec() { return make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u); }
+  __device__ static __forceinline__ uint64_t exp_cache(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
+                                                       uint4& c) {
+    uint32_t o[2];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint64_t t = ffma2(f2pack(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1])), k2, mn2);
+      float a, b;
+      f2unpack(t, a, b);
+      a = fast_exp2(a);
+      b = fast_exp2(b);
+      acc = fadd2(acc, f2pack(a, b));
+      o[i] = cvt_h2(a, b);
+    }
+    c.x = o[0];
+    c.y = o[1];
+    return acc;
+  }
+  __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t q2) {
+    float a, b, d, e;
+    f2unpack(fmul2(h2_to_f2(c.x), q2), a, b);
+    f2unpack(fmul2(h2_to_f2(c.y), q2), d, e);
+    return make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(d), __float_as_uint(e));
+  }
+};
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Ring position of the first chunk of a row (slot index + phase parity), advanced per row.
+struct RingPos {
+  uint32_t slot, phase;
+  __device__ __forceinline__ void advance(int n, int nslots) {
+    slot += n;
+    while (slot >= (uint32_t)nslots) {
+      slot -= nslots;
+      phase ^= 1u;
+    }
+  }
+};
+
+}  // namespace rl

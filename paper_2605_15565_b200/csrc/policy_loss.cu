@@ -152,12 +152,22 @@ rl_status launch_loss_cluster(const void* logits, int32_t dtype, int64_t n, int6
                               const Knobs& kn, void* dlogits, float* logp_out, uint8_t* clipped_out,
                               double* partials, int* n_ctas, cudaStream_t s);
 
-// Kernel choice: "cluster" (default) or "two_pass", overridable with RL_LOSS_KERNEL.
+// Streaming two-cache variant (policy_loss_stream.cu); same contract as launch_loss_cluster.
+rl_status launch_loss_stream(const void* logits, int32_t dtype, int64_t n, int64_t V, int64_t ld,
+                             const int32_t* targets, const float* old_logp, const uint8_t* mask,
+                             const int32_t* token_seq, const float* seq_adv, const int32_t* seq_version,
+                             const int32_t* seq_active, const Knobs& kn, void* dlogits, float* logp_out,
+                             uint8_t* clipped_out, double* partials, int* n_ctas, cudaStream_t s);
+
+// Kernel choice: "cluster" (default), "stream" or "two_pass", overridable with RL_LOSS_KERNEL.
 static int loss_kernel_choice() {
   static int choice = -1;
   if (choice < 0) {
     choice = 0;
-    if (const char* e = getenv("RL_LOSS_KERNEL")) choice = strcmp(e, "two_pass") == 0 ? 1 : 0;
+    if (const char* e = getenv("RL_LOSS_KERNEL")) {
+      if (strcmp(e, "two_pass") == 0) choice = 1;
+      if (strcmp(e, "stream") == 0) choice = 2;
+    }
   }
   return choice;
 }
@@ -217,11 +227,15 @@ extern "C" rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, i
   double* partials = (double*)workspace;
   int n_ctas = 0;
   rl_status st = RL_ERR_UNSUPPORTED;
+  if (loss_kernel_choice() == 2)
+    st = launch_loss_stream(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
+                            token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,
+                            clipped_out, partials, &n_ctas, s);
   if (loss_kernel_choice() == 0)
     st = launch_loss_cluster(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
                              token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,
                              clipped_out, partials, &n_ctas, s);
-  const char* which = st == RL_OK ? "cluster" : "two_pass";
+  const char* which = st == RL_OK ? (loss_kernel_choice() == 2 ? "stream" : "cluster") : "two_pass";
   if (st == RL_ERR_UNSUPPORTED)
     st = launch_loss_two_pass(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
                               token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,

@@ -28,196 +28,36 @@
 
 #include <algorithm>
 
-#include "loss_common.cuh"
-#include "rowstats.cuh"
-#include "sm100.cuh"
+#include "cluster_common.cuh"
 
 namespace rl {
 
-constexpr int kNcw = 15;  // consumer warps: 15 + 1 producer = 16 warps = 4 per SMSP -> 128 regs/thread
-constexpr int kCons = kNcw * 32;              // consumer threads (one 16-B vector each per chunk)
-constexpr int kChunkVec = kCons;              // vectors per chunk
-constexpr int kChunkBytes = kChunkVec * 16;   // 7.5 KB
-constexpr int kClThreads = kCons + 32;        // + producer warp
-constexpr int kSmemMax = 232448;              // 227 KB opt-in per CTA on sm_100
-
-// fp16 cache of e' = 2^(x k - m + kCacheShift) in (0, 2^15]: the shift keeps the bulk of a
-// peaked row (e ~ 1e-7 .. 1e-9) out of the fp16 subnormal range (abs. precision 2^-39 instead
-// of 2^-24), so the cached probabilities lose no mass; 2^-15 is folded into the pass-C scale.
-constexpr float kCacheShift = 15.f;
-
-struct ClArgs {
-  const void* logits;
-  void* dlogits;
-  int64_t n_tokens, V, ld, nvec;
-  int64_t h_vec;  // vectors per CTA slice
-  const int32_t* targets;
-  const float* old_logp;
-  const uint8_t* mask;
-  const int32_t* token_seq;
-  const float* seq_adv;
-  const int32_t* seq_version;
-  const int32_t* seq_active;
-  float* logp_out;
-  uint8_t* clipped_out;
-  double* partials;
-  Knobs kn;
-  int32_t nslots;
-};
+// Development trace (RL_TRACE=1 selects the traced instantiation): per CTA, the first 64 rows'
+// phase boundaries in globaltimer ns.  Read with rl_debug_trace (tools/trace_cluster.py).
+constexpr int kTraceRows = 64, kTraceEv = 8, kTraceCtas = 256;
+__device__ unsigned long long g_trace[kTraceCtas][kTraceRows][kTraceEv];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define RL_TRACE_EV(row_it, ev)                                                           \
+  do {                                                                                   \
+    if (TRACE && blockIdx.x < kTraceCtas && (row_it) < kTraceRows)                       \
+      g_trace[blockIdx.x][(row_it)][(ev)] = gtimer();                                    \
+  } while (0)
 
 struct __align__(16) ClShared {
   float4 xch[2][8];             // [row parity][cluster rank]: (m_c log2 units, s_c, z_y, owned)
   float red_max[2][kNcw];       // [pass-A call parity][warp] block reduction
   float red_sum[2][kNcw];       // [row parity][warp] pass-B partial sums (2^15-scaled)
   float mrow[2];                // [row parity] slice max m_c (log2 units)
-  float4 row_sc[2];             // [row parity] (q, s_t, d_y, target column as int bits or -1)
+  float4 row_sc[2];             // [row parity] (s_t, lse2, d_y, target column as int bits or -1)
+  float rref[2][8];             // [row parity][group] reference max R_g of each chunk group (log2)
   uint64_t xbar[2];             // peer records landed (CL - 1 remote arrivals)
   uint64_t sumbar[2];           // consumers finished pass B (kNcw arrivals)
   uint64_t scalebar[2];         // epilogue published row_sc (1 arrival)
   // followed by full[nslots], empty[nslots] (uint64) then the ring (128-B aligned)
-};
-
-// ------------------------------------------------------------------ packed fp32x2 helpers
-__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ uint32_t cvt_h2(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-__device__ __forceinline__ uint64_t h2_to_f2(uint32_t h) {
-  float lo, hi;
-  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-      : "=f"(lo), "=f"(hi)
-      : "r"(h));
-  return f2pack(lo, hi);
-}
-__device__ __forceinline__ uint32_t f2_to_bf2(uint64_t v) {
-  float lo, hi;
-  f2unpack(v, lo, hi);
-  return pack_bf16x2(lo, hi);
-}
-
-// ------------------------------------------------------------------ per-vector kernels
-template <typename T>
-struct ClVec;
-
-template <>
-struct ClVec<bf16_t> {
-  static constexpr int EPV = 8;
-  using MaxT = __nv_bfloat162;
-  __device__ static __forceinline__ MaxT max_init() { return __bfloat162bfloat162(__ushort_as_bfloat16(0xff80)); }
-  // pass A: running packed max
-  __device__ static __forceinline__ void max_acc(const uint4& v, MaxT& m) {
-    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
-    m = __hmax2(m, __hmax2(__hmax2(p[0], p[1]), __hmax2(p[2], p[3])));
-  }
-  __device__ static __forceinline__ float max_to_float(MaxT m) { return fmaxf(__low2float(m), __high2float(m)); }
-  __device__ static __forceinline__ uint4 neg_inf_vec() { return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u); }
-  // pass B: e' = 2^(x k + mneg); accumulates packed partial sums, fills the fp16 cache words
-  __device__ static __forceinline__ uint64_t exp_cache(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
-                                                       uint4& c) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    uint32_t o[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint64_t t = ffma2(f2pack(bf16_lo(w[i]), bf16_hi(w[i])), k2, mn2);
-      float a, b;
-      f2unpack(t, a, b);
-      a = fast_exp2(a);
-      b = fast_exp2(b);
-      acc = fadd2(acc, f2pack(a, b));
-      o[i] = cvt_h2(a, b);
-    }
-    c = make_uint4(o[0], o[1], o[2], o[3]);
-    return acc;
-  }
-  // pass C: q * e' -> bf16
-  __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t q2) {
-    return make_uint4(f2_to_bf2(fmul2(h2_to_f2(c.x), q2)), f2_to_bf2(fmul2(h2_to_f2(c.y), q2)),
-                      f2_to_bf2(fmul2(h2_to_f2(c.z), q2)), f2_to_bf2(fmul2(h2_to_f2(c.w), q2)));
-  }
-};
-
-template <>
-struct ClVec<float> {
-  static constexpr int EPV = 4;
-  using MaxT = float;
-  __device__ static __forceinline__ MaxT max_init() { return -INFINITY; }
-  __device__ static __forceinline__ void max_acc(const uint4& v, MaxT& m) {
-    m = fmaxf(fmaxf(m, fmaxf(__uint_as_float(v.x), __uint_as_float(v.y))),
-              fmaxf(__uint_as_float(v.z), __uint_as_float(v.w)));
-  }
-  __device__ static __forceinline__ float max_to_float(MaxT m) { return m; }
-  __device__ static __forceinline__ uint4 neg_inf_vec() { return make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u); }
-  __device__ static __forceinline__ uint64_t exp_cache(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
-                                                       uint4& c) {
-    uint32_t o[2];
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const uint64_t t = ffma2(f2pack(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1])), k2, mn2);
-      float a, b;
-      f2unpack(t, a, b);
-      a = fast_exp2(a);
-      b = fast_exp2(b);
-      acc = fadd2(acc, f2pack(a, b));
-      o[i] = cvt_h2(a, b);
-    }
-    c.x = o[0];
-    c.y = o[1];
-    return acc;
-  }
-  __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t q2) {
-    float a, b, d, e;
-    f2unpack(fmul2(h2_to_f2(c.x), q2), a, b);
-    f2unpack(fmul2(h2_to_f2(c.y), q2), d, e);
-    return make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(d), __float_as_uint(e));
-  }
-};
-
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Ring position of the first chunk of a row (slot index + phase parity), advanced per row.
-struct RingPos {
-  uint32_t slot, phase;
-  __device__ __forceinline__ void advance(int n, int nslots) {
-    slot += n;
-    while (slot >= (uint32_t)nslots) {
-      slot -= nslots;
-      phase ^= 1u;
-    }
-  }
 };
 
 // NCH = compile-time upper bound of chunks per CTA slice (the register cache is uint4[NCH]).
@@ -225,8 +65,9 @@ struct RingPos {
 // Warp roles: warps 0..14 consume (passes A/B/C); warp 15 is the service warp: lane 0 issues the
 // TMA bulk copies, lane 1 runs the per-row epilogue (DSMEM exchange with the peer CTA(s),
 // combine, ratio/clip/scale, statistics) off the consumers' critical path.
-template <typename T, int CL, int NCH, bool EXACT>
+template <typename T, int CL, int NCH, bool EXACT, int H, bool TRACE = false>
 __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArgs a) {
+  static_assert(H >= 1 && H <= 8, "chunk groups per row");
   constexpr int EPV = ClVec<T>::EPV;
   using MaxT = typename ClVec<T>::MaxT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -273,14 +114,36 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
       // ---------------------------------------------------------- TMA producer (lane 0)
       const uint64_t pol = policy_evict_first();
       RingPos rp{0, 0};
+      // L2 lookahead: when the ring is full, the chunks that must wait for a free slot are
+      // prefetched into L2 (up to pf_chunks ahead) so their later TMA loads are L2 hits.
+      const int pf_chunks = a.prefetch_chunks;
+      int64_t g = 0, g_pf = 0;
       for (int64_t row = cid; row < a.n_tokens; row += ncl) {
         const char* src = reinterpret_cast<const char*>(a.logits) + row * row_bytes + v0 * 16;
-        for (int j = 0; j < nch; ++j) {
+        for (int j = 0; j < nch; ++j, ++g) {
+          if (pf_chunks > 0 && g >= g_pf && !sm100::mbar_try_wait_a(empty_s + rp.slot * 8, rp.phase ^ 1)) {
+            int64_t rr = row, jj = j;
+            for (int q = 0; q < pf_chunks; ++q) {
+              if (rr >= a.n_tokens) break;
+              const uint32_t pb = (jj < nfull ? kChunkVec : last_nv) * 16u;
+              sm100::bulk_prefetch_l2(reinterpret_cast<const char*>(a.logits) + rr * row_bytes + v0 * 16 +
+                                          (size_t)jj * kChunkBytes, pb);
+              if (++jj == nch) {
+                jj = 0;
+                rr += ncl;
+              }
+            }
+            g_pf = g + pf_chunks;
+          }
           sm100::mbar_wait_a(empty_s + rp.slot * 8, rp.phase ^ 1);
           const uint32_t bytes = (j < nfull ? kChunkVec : last_nv) * 16u;
           sm100::mbar_arrive_expect_tx(&full[rp.slot], bytes);
-          sm100::bulk_g2s(ring + (size_t)rp.slot * kChunkVec, src + (size_t)j * kChunkBytes, bytes,
-                          &full[rp.slot], pol);
+          if (a.debug == 3)
+            sm100::bulk_g2s(ring + (size_t)rp.slot * kChunkVec, src + (size_t)j * kChunkBytes, bytes,
+                            &full[rp.slot], pol);
+          else
+            sm100::bulk_g2s_nohint(ring + (size_t)rp.slot * kChunkVec, src + (size_t)j * kChunkBytes, bytes,
+                                   &full[rp.slot]);
           rp.advance(1, nslots);
         }
       }
@@ -307,7 +170,10 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
           owned = (vy >= v0 && vy < v1) || (tail_owner && vy >= a.nvec);
           if (owned) zy = VecTraits<T>::load1(rp, mt.y) * a.kn.inv_t;
         }
-        sm100::mbar_wait(&sh.sumbar[par], ph);
+        RL_TRACE_EV(it, 4);
+        if (a.debug == 4) sm100::mbar_wait(&sh.sumbar[par], ph);
+        else sm100::mbar_wait_polite(&sh.sumbar[par], ph, false);
+        RL_TRACE_EV(it, 5);
         float s = 0.f;
 #pragma unroll
         for (int w = 0; w < kNcw; ++w) s += sh.red_sum[par][w];
@@ -321,7 +187,11 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
             sm100::st_remote_v4(&sh.xch[par][crank], r, rec.x, rec.y, rec.z, rec.w);
             sm100::mbar_arrive_remote(&sh.xbar[par], r);
           }
-        if (CL > 1) sm100::mbar_wait_cluster(&sh.xbar[par], ph);
+        if (CL > 1) {
+          if (a.debug == 4) sm100::mbar_wait_cluster(&sh.xbar[par], ph);
+          else sm100::mbar_wait_polite(&sh.xbar[par], ph, true);
+        }
+        RL_TRACE_EV(it, 6);
         // combine in rank order (bitwise identical in every CTA of the cluster)
         float M = -INFINITY;
 #pragma unroll
@@ -347,10 +217,11 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
         }
         // q = s_t 2^(m_c - 15 - lse2): p_v = (q / s_t) e'_v.  An all -inf / empty slice has no
         // cache (pass B skipped) and q = 0.  Target column: d_y = s_t (p_y - 1).
-        const float q = (st == 0.f || m == -INFINITY) ? 0.f : st * fast_exp2(m - kCacheShift - c2);
+        (void)m;
         const float dy = st * (fast_exp2(z * RL_LOG2E - c2) - 1.f);
-        sh.row_sc[par] = make_float4(q, st, dy, __int_as_float(owned ? mt.y : -1));
+        sh.row_sc[par] = make_float4(st, c2, dy, __int_as_float(owned ? mt.y : -1));
         sm100::mbar_arrive(&sh.scalebar[par]);
+        RL_TRACE_EV(it, 7);
       }
 #pragma unroll
       for (int i = 0; i < RL_LOSS_STATS_N; ++i)
@@ -365,20 +236,26 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
     const bool last_mine = tid < last_nv;  // this thread's vector exists in the partial last chunk
     uint4 cache[NCH];  // this thread's fp16 e' values for the current row (registers)
     RingPos pos{0, 0};
+    constexpr int GS = (NCH + H - 1) / H;  // chunks per group; each group has its own reference
     // chunk j of a row: present (uniform), partial (uniform: the ragged last chunk), mine (per thread)
 #define RL_PRESENT(j) (EXACT ? true : ((j) < nch))
 #define RL_PARTIAL(j) (EXACT ? ((j) == NCH - 1 && last_nv > 0) : ((j) == nfull))
 #define RL_MINE(j) (!RL_PARTIAL(j) || last_mine)
 
-    // pass A of `row` at ring position `p`: waits for each chunk, returns the log2-domain max
-    // (block-reduced; -inf for an empty / all -inf slice) and this thread's tail column in xt.
+    // pass A of chunk group g of `row` (ring position p of the row's first chunk): waits for the
+    // group's chunks, returns their block-reduced log2-domain max R_g (the last group also covers
+    // this thread's scalar tail column, returned in xt).
     uint32_t acall = 0;  // pass-A call counter (red_max double buffer)
-    auto pass_a = [&](int64_t row, RingPos p, float& xt) -> float {
+    auto group_a = [&](int64_t row, RingPos p, int g, float& xt) -> float {
       MaxT mx = ClVec<T>::max_init();
       const int ab = (acall++) & 1;
-      uint32_t slot = p.slot, ph = p.phase;
+      uint32_t slot = p.slot + g * GS, ph = p.phase;
+      while (slot >= (uint32_t)nslots) {
+        slot -= nslots;
+        ph ^= 1u;
+      }
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) {
+      for (int j = g * GS; j < (g + 1) * GS && j < NCH; ++j) {
         if (RL_PRESENT(j)) {
           sm100::mbar_wait_a(full_s + slot * 8, ph);
           uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off);
@@ -391,10 +268,12 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
         }
       }
       float m = ClVec<T>::max_to_float(mx);
-      xt = -INFINITY;
-      if (tail_owner && tid < n_tail) {
-        xt = VecTraits<T>::load1(reinterpret_cast<const char*>(a.logits) + row * row_bytes, a.nvec * EPV + tid);
-        m = fmaxf(m, xt);
+      if (g == H - 1) {
+        xt = -INFINITY;
+        if (tail_owner && tid < n_tail) {
+          xt = VecTraits<T>::load1(reinterpret_cast<const char*>(a.logits) + row * row_bytes, a.nvec * EPV + tid);
+          m = fmaxf(m, xt);
+        }
       }
       m = warp_max(m);
       if (lane == 0) sh.red_max[ab][warp] = m;
@@ -404,13 +283,25 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
       for (int w = 1; w < kNcw; ++w) m = fmaxf(m, sh.red_max[ab][w]);
       return m * k;
     };
-
-    // pass B of the first row (no pass C to fuse with yet)
-    auto send_sum = [&](uint32_t itn, float mm, float sum) {
-      sum = warp_sum(sum);
+    // running (R_run, S_run) of a row: group sums fold into the largest reference seen so far
+    float R_run = -INFINITY, S_run = 0.f;
+    auto fold = [&](float Rg, uint64_t acc2) {
+      float s0, s1;
+      f2unpack(acc2, s0, s1);
+      const float sg = s0 + s1;
+      if (Rg == -INFINITY) return;
+      if (Rg > R_run) {
+        S_run = (R_run == -INFINITY ? 0.f : S_run * fast_exp2(R_run - Rg)) + sg;
+        R_run = Rg;
+      } else {
+        S_run += sg * fast_exp2(Rg - R_run);
+      }
+    };
+    auto send_sum = [&](uint32_t itn) {
+      const float sum = warp_sum(S_run);
       if (lane == 0) {
         sh.red_sum[itn & 1][warp] = sum;
-        if (warp == 0) sh.mrow[itn & 1] = mm;
+        if (warp == 0) sh.mrow[itn & 1] = R_run;
         sm100::mbar_arrive(&sh.sumbar[itn & 1]);
       }
     };
@@ -418,61 +309,21 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
     int64_t row = cid;
     uint32_t it = 0;
     float xt = -INFINITY, xt_next = -INFINITY;
-    float m = 0.f;
-    if (row < a.n_tokens) {
-      m = pass_a(row, pos, xt);
-      const bool live = m != -INFINITY;
-      const uint64_t mn2 = f2pack(kCacheShift - m, kCacheShift - m);
-      uint64_t acc2 = f2pack(0.f, 0.f);
+    float Rg0 = 0.f;  // group-0 reference of the next row, computed while the exchange runs
+    if (row < a.n_tokens) {  // pass A + B of the first row, group by group
+      R_run = -INFINITY;
+      S_run = 0.f;
       uint32_t slot = pos.slot;
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        if (RL_PRESENT(j)) {
-          if (live) {
-            const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off);
-            const uint64_t nacc = ClVec<T>::exp_cache(v, k2, mn2, acc2, cache[j]);
-            acc2 = RL_MINE(j) ? nacc : acc2;
-          }
-          sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
-          if (++slot == (uint32_t)nslots) slot = 0;
-        }
-      }
-      pos.advance(nch, nslots);
-      float s0, s1;
-      f2unpack(acc2, s0, s1);
-      float sum = s0 + s1;
-      if (tail_owner && tid < n_tail && live) {
-        xt = fast_exp2(fmaf(xt, k, kCacheShift - m));
-        sum += xt;
-      }
-      send_sum(0, m, sum);
-    }
-    for (; row < a.n_tokens; row += ncl, ++it) {
-      const int par = it & 1;
-      char* dp = reinterpret_cast<char*>(a.dlogits) + row * row_bytes;
-      // ---- pass A of the next row overlaps the epilogue / exchange of this one
-      const int64_t next = row + ncl;
-      const bool has_next = next < a.n_tokens;
-      const float m_next = has_next ? pass_a(next, pos, xt_next) : 0.f;
-      sm100::mbar_wait(&sh.scalebar[par], (it >> 1) & 1);
-      const float4 sc = sh.row_sc[par];
-      const float q = sc.x, st = sc.y, dy = sc.z;
-      const int ycol = __float_as_int(sc.w);
-      const bool zero = (st == 0.f) || (q == 0.f);
-      const uint64_t q2 = f2pack(q, q);
-      uint4* out = reinterpret_cast<uint4*>(dp) + v0 + tid;
-      // ---- fused pass C(row) + pass B(next), chunk by chunk: the dlogits stores of this row
-      // drain while the exp2 work of the next row runs; each register-cache entry is emptied
-      // (stored) and refilled in place.
-      const bool live = has_next && m_next != -INFINITY;
-      const uint64_t mn2 = f2pack(kCacheShift - m_next, kCacheShift - m_next);
-      uint64_t acc2 = f2pack(0.f, 0.f);
-      uint32_t slot = pos.slot;
+      for (int g = 0; g < H; ++g) {
+        const float Rg = group_a(row, pos, g, xt);
+        if (tid == 0) sh.rref[0][g] = Rg;
+        const bool live = Rg != -INFINITY;
+        const uint64_t mn2 = f2pack(kCacheShift - Rg, kCacheShift - Rg);
+        uint64_t acc2 = f2pack(0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        if (RL_PRESENT(j)) {
-          if (RL_MINE(j)) st_stream_v4(out + j * kChunkVec, zero ? make_uint4(0, 0, 0, 0) : ClVec<T>::grad(cache[j], q2));
-          if (has_next) {
+        for (int j = g * GS; j < (g + 1) * GS && j < NCH; ++j) {
+          if (RL_PRESENT(j)) {
             if (live) {
               const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off);
               const uint64_t nacc = ClVec<T>::exp_cache(v, k2, mn2, acc2, cache[j]);
@@ -482,11 +333,79 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
             if (++slot == (uint32_t)nslots) slot = 0;
           }
         }
+        if (g == H - 1 && tail_owner && tid < n_tail && live) {
+          xt = fast_exp2(fmaf(xt, k, kCacheShift - Rg));
+          acc2 = fadd2(acc2, f2pack(xt, 0.f));
+        }
+        fold(Rg, acc2);
       }
-      if (tail_owner && tid < n_tail) {
-        const float o = zero ? 0.f : xt * q;
-        VecTraits<T>::store1(dp, a.nvec * EPV + tid, o);
+      pos.advance(nch, nslots);
+      send_sum(0);
+    }
+    for (; row < a.n_tokens; row += ncl, ++it) {
+      const int par = it & 1;
+      char* dp = reinterpret_cast<char*>(a.dlogits) + row * row_bytes;
+      // ---- pass A of the next row's first chunk group overlaps the exchange of this one
+      const int64_t next = row + ncl;
+      const bool has_next = next < a.n_tokens;
+      if (tid == 0) RL_TRACE_EV(it, 0);
+      if (has_next) Rg0 = group_a(next, pos, 0, xt_next);
+      if (tid == 0) RL_TRACE_EV(it, 1);
+      sm100::mbar_wait(&sh.scalebar[par], (it >> 1) & 1);
+      if (tid == 0) RL_TRACE_EV(it, 2);
+      const float4 sc = sh.row_sc[par];
+      const float st = sc.x, c2 = sc.y, dy = sc.z;
+      const int ycol = __float_as_int(sc.w);
+      uint4* out = reinterpret_cast<uint4*>(dp) + v0 + tid;
+      // ---- fused pass C(row) + pass A/B(next) group by group: the dlogits stores of this row
+      // drain while the next row's groups are max-reduced (as they land) and exp2'd; each
+      // register-cache entry is emptied (stored) and refilled in place.
+      R_run = -INFINITY;
+      S_run = 0.f;
+      uint32_t slot = pos.slot;
+      float q_last = 0.f;
+#pragma unroll
+      for (int g = 0; g < H; ++g) {
+        float Rg = Rg0;
+        if (has_next && g > 0) Rg = group_a(next, pos, g, xt_next);
+        if (has_next && tid == 0) sh.rref[(it + 1) & 1][g] = Rg;
+        const float Rc = sh.rref[par][g];  // this row's group reference
+        const float q = (st == 0.f || Rc == -INFINITY) ? 0.f : st * fast_exp2(Rc - kCacheShift - c2);
+        q_last = q;
+        const uint64_t q2 = f2pack(q, q);
+        const bool zero = q == 0.f;
+        const bool live = has_next && Rg != -INFINITY;
+        const uint64_t mn2 = f2pack(kCacheShift - Rg, kCacheShift - Rg);
+        uint64_t acc2 = f2pack(0.f, 0.f);
+#pragma unroll
+        for (int j = g * GS; j < (g + 1) * GS && j < NCH; ++j) {
+          if (RL_PRESENT(j)) {
+            if (RL_MINE(j) && (!TRACE || a.debug != 1))
+              st_stream_v4(out + j * kChunkVec, zero ? make_uint4(0, 0, 0, 0) : ClVec<T>::grad(cache[j], q2));
+            if (has_next) {
+              if (live && (!TRACE || a.debug != 2)) {
+                const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off);
+                const uint64_t nacc = ClVec<T>::exp_cache(v, k2, mn2, acc2, cache[j]);
+                acc2 = RL_MINE(j) ? nacc : acc2;
+              }
+              sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+              if (++slot == (uint32_t)nslots) slot = 0;
+            }
+          }
+        }
+        if (g == H - 1) {
+          if (tail_owner && tid < n_tail) {  // this row's tail column (cached e' in xt)
+            const float o = (q == 0.f) ? 0.f : xt * q;
+            VecTraits<T>::store1(dp, a.nvec * EPV + tid, o);
+          }
+          if (has_next && tail_owner && tid < n_tail && live) {
+            xt_next = fast_exp2(fmaf(xt_next, k, kCacheShift - Rg));
+            acc2 = fadd2(acc2, f2pack(xt_next, 0.f));
+          }
+        }
+        if (has_next) fold(Rg, acc2);
       }
+      (void)q_last;
       // target column: rewritten by the thread that stored its vector (or tail column) above —
       // same-thread program order to the same address.
       if (st != 0.f && ycol >= 0) {
@@ -496,17 +415,10 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
       }
       if (has_next) {
         pos.advance(nch, nslots);
-        float s0, s1;
-        f2unpack(acc2, s0, s1);
-        float sum = s0 + s1;
-        if (tail_owner && tid < n_tail && live) {
-          xt_next = fast_exp2(fmaf(xt_next, k, kCacheShift - m_next));
-          sum += xt_next;
-        }
-        send_sum(it + 1, m_next, sum);
+        send_sum(it + 1);
       }
+      if (tid == 0) RL_TRACE_EV(it, 3);
       xt = xt_next;
-      m = m_next;
     }
 #undef RL_PRESENT
 #undef RL_PARTIAL
@@ -516,13 +428,16 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
   sm100::cluster_sync();  // no CTA leaves while a peer may still arrive on / write its smem
 }
 
-template <typename T, int CL, int NCH, bool EXACT = false>
+template <typename T, int CL, int NCH, bool EXACT = false, int H = 1, bool TRACE = false>
 static rl_status launch_cl(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_ctas) {
   ClArgs a = a0;
-  auto kern = loss_cluster_kernel<T, CL, NCH, EXACT>;
+  auto kern = loss_cluster_kernel<T, CL, NCH, EXACT, H, TRACE>;
   const size_t head = (sizeof(ClShared) + 127) & ~(size_t)127;
   int nslots = (int)((kSmemMax - head - 256) / (kChunkBytes + 16));
   const int nch = (int)((a.h_vec + kChunkVec - 1) / kChunkVec);
+  static int slots_cap = -1;  // RL_CLUSTER_SLOTS: cap on the ring depth (tuning knob)
+  if (slots_cap < 0) slots_cap = getenv("RL_CLUSTER_SLOTS") ? atoi(getenv("RL_CLUSTER_SLOTS")) : 0;
+  if (slots_cap > 0) nslots = std::min(nslots, std::max(slots_cap, nch));
   if (nch > nslots || nch > NCH || (EXACT && nch != NCH)) return RL_ERR_UNSUPPORTED;
   a.nslots = nslots;
   const size_t smem = ((sizeof(ClShared) + 2 * sizeof(uint64_t) * nslots + 127) & ~(size_t)127) +
@@ -589,11 +504,37 @@ rl_status launch_loss_cluster(const void* logits, int32_t dtype, int64_t n, int6
   a.partials = partials;
   a.kn = kn;
   a.nslots = 0;
-  // the smallest cluster (and register-cache size) whose per-CTA slice fits
-  const int64_t h2 = (a.nvec + 1) / 2, nch2 = (h2 + kChunkVec - 1) / kChunkVec;
+  static int pfc = -1;
+  if (pfc < 0) pfc = getenv("RL_L2_PREFETCH_CHUNKS") ? atoi(getenv("RL_L2_PREFETCH_CHUNKS")) : 0;
+  a.prefetch_chunks = pfc;
+  a.debug = getenv("RL_CLUSTER_DEBUG") ? atoi(getenv("RL_CLUSTER_DEBUG")) : 0;
+  // Half rows per 2-CTA cluster by default (all 148 SMs).  RL_CLUSTER_CL=3 selects thirds of a
+  // row per 3-CTA cluster (more ring slack, 56-register cache) — measured slower.
+  static int cl_env = -1;
+  if (cl_env < 0) {
+    cl_env = 2;
+    if (const char* e = getenv("RL_CLUSTER_CL")) cl_env = atoi(e) == 3 ? 3 : 2;
+  }
   const bool bf = dtype == RL_BF16;
+  auto nchunks = [&](int64_t h) { return (h + kChunkVec - 1) / kChunkVec; };
+  const int64_t h2 = (a.nvec + 1) / 2, nch2 = nchunks(h2);
+  const int64_t h3 = (a.nvec + 2) / 3, nch3 = nchunks(h3);
+  if (cl_env == 3 && nch2 > 10 && nch3 <= 20) {
+    a.h_vec = h3;
+    if (bf && nch3 == 14) return launch_cl<bf16_t, 3, 14, true>(a, n, s, n_ctas);  // V = 151936
+    if (bf && nch3 == 12) return launch_cl<bf16_t, 3, 12, true>(a, n, s, n_ctas);  // V = 128256
+    return bf ? launch_cl<bf16_t, 3, 20>(a, n, s, n_ctas) : launch_cl<float, 3, 20>(a, n, s, n_ctas);
+  }
   a.h_vec = h2;
-  if (bf && nch2 == 20) return launch_cl<bf16_t, 2, 20, true>(a, n, s, n_ctas);  // V = 151936
+  if (bf && nch2 == 20) {  // V = 151936: 4 chunk groups (RL_CLUSTER_GROUPS = 1, 2, 4, 5)
+    static int groups = -1;
+    if (groups < 0) groups = getenv("RL_CLUSTER_GROUPS") ? atoi(getenv("RL_CLUSTER_GROUPS")) : 1;
+    if (getenv("RL_TRACE")) return launch_cl<bf16_t, 2, 20, true, 1, true>(a, n, s, n_ctas);
+    if (groups == 1) return launch_cl<bf16_t, 2, 20, true, 1>(a, n, s, n_ctas);
+    if (groups == 2) return launch_cl<bf16_t, 2, 20, true, 2>(a, n, s, n_ctas);
+    if (groups == 5) return launch_cl<bf16_t, 2, 20, true, 5>(a, n, s, n_ctas);
+    return launch_cl<bf16_t, 2, 20, true, 4>(a, n, s, n_ctas);
+  }
   if (bf && nch2 == 17) return launch_cl<bf16_t, 2, 17, true>(a, n, s, n_ctas);  // V = 128256
   if (nch2 <= 2) return bf ? launch_cl<bf16_t, 2, 2>(a, n, s, n_ctas) : launch_cl<float, 2, 2>(a, n, s, n_ctas);
   if (nch2 <= 5) return bf ? launch_cl<bf16_t, 2, 5>(a, n, s, n_ctas) : launch_cl<float, 2, 5>(a, n, s, n_ctas);
@@ -604,3 +545,9 @@ rl_status launch_loss_cluster(const void* logits, int32_t dtype, int64_t n, int6
 }
 
 }  // namespace rl
+
+// development only (not part of include/rl_policy.h): copy the phase trace to the host
+extern "C" int rl_debug_trace(unsigned long long* host, size_t bytes) {
+  const size_t n = sizeof(rl::g_trace) < bytes ? sizeof(rl::g_trace) : bytes;
+  return cudaMemcpyFromSymbol(host, rl::g_trace, n) == cudaSuccess ? 0 : 1;
+}

@@ -190,3 +190,33 @@ __device__ __forceinline__ uint32_t atom_add_acqrel(uint32_t addr, uint32_t v) {
 }
 }  // namespace sm100
 }  // namespace rl
+
+namespace rl {
+namespace sm100 {
+// TMA bulk copy global -> shared without an L2 cache hint (measured 3-4 % faster than evict_first
+// for this streaming pattern, tools/copy_probe.cu "hints")
+__device__ __forceinline__ void bulk_g2s_nohint(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// polite polling wait (test_wait + nanosleep): for a lane that shares its warp with another
+// lane's loop, so the other divergent path keeps getting issue slots
+__device__ __forceinline__ void mbar_wait_polite(uint64_t* bar, uint32_t parity, bool cluster_acquire) {
+  for (;;) {
+    uint32_t ok;
+    if (cluster_acquire)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    else
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
+}
+}  // namespace sm100
+}  // namespace rl
