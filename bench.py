@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
+    ap.add_argument("--config", default="single", choices=["single", "long", "vocabpar", "multi"],
+                    help="BASELINE.json config (single = the headline metric's workload, the default)")
     return ap.parse_args()
 
 
@@ -191,6 +193,206 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+def make_pool(torch, synth, dev, n_buf, MB, V, seed, rank, cfg_seed_row0=0):
+    """`n_buf` distinct resident [MB, V] bf16 logits buffers (device generator), their sampled
+    targets and behaviour log-probs (torch fp32 log-softmax + seeded drift: input synthesis)."""
+    pool, pool_y, pool_old = [], [], []
+    for b in range(n_buf):
+        x = torch.empty((MB, V), dtype=torch.bfloat16, device=dev)
+        y = torch.empty(MB, dtype=torch.int32, device=dev)
+        synth.device_logits(x, V, row0=(rank * n_buf + b + cfg_seed_row0) * MB, seed=seed, targets_out=y)
+        old = torch.empty(MB, dtype=torch.float32, device=dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(77 + b + 10 * rank)
+        for c0 in range(0, MB, 4096):
+            blk = x[c0:c0 + 4096].float()
+            lp = blk.gather(1, y[c0:c0 + 4096, None].long())[:, 0] - torch.logsumexp(blk, dim=1)
+            old[c0:c0 + 4096] = lp + 0.02 * torch.randn(lp.shape, generator=g, device=dev)
+            del blk
+        pool.append(x)
+        pool_y.append(y)
+        pool_old.append(old)
+    return pool, pool_y, pool_old
+
+
+class TokenParallelWorkload:
+    """Configs single / long / multi: whole sequences per rank, each rank's share processed as
+    mini-batch calls of MB tokens streaming through a pool of 2 resident logits buffers.
+    One step: bookkeeping of every call (counts all-reduced over the policy's ranks) ->
+    advantages (group + batch normalisation) -> fused loss of every call (stats all-reduced)."""
+
+    def __init__(self, rl, torch, np, synth, dev, comm, cfg, seqs, MB, n_calls, rank, max_staleness,
+                 n_pool=2, dlogits_buf=None):
+        self.rl, self.torch, self.comm = rl, torch, comm
+        V, T = cfg.vocab, cfg.seq_len
+        self.V, self.MB, self.n_calls = V, MB, n_calls
+        lay = synth.seq_layout(cfg)
+        s0, s1 = seqs                     # this rank's sequences [s0, s1) of the policy batch
+        self.trainer_version, self.max_staleness = lay["trainer_version"], max_staleness
+        self.pool, self.pool_y, self.pool_old = make_pool(torch, synth, dev, n_pool, MB, V, cfg.seed, rank)
+        if dlogits_buf is not None:  # shared [MB * V_max] bf16 buffer viewed as [MB, V]
+            self.dlogits = dlogits_buf[:MB * V].view(MB, V)
+        else:
+            self.dlogits = torch.empty((MB, V), dtype=torch.bfloat16, device=dev)
+        S_all = cfg.n_seq
+        G = S_all // cfg.group
+        self.rewards = torch.from_numpy(lay["rewards"]).to(dev)
+        self.cu_groups = torch.from_numpy(lay["cu_groups"]).to(dev)
+        self.seq_version = torch.from_numpy(lay["seq_version"]).to(dev)
+        self.adv = torch.empty(S_all, dtype=torch.float32, device=dev)
+        self.zero_var = torch.empty(G, dtype=torch.uint8, device=dev)
+        self.seq_active = torch.zeros(S_all, dtype=torch.int32, device=dev)
+        self.ws_adv = torch.empty(rl.group_advantage_workspace_size(S_all), dtype=torch.uint8, device=dev)
+        # per call: a contiguous token range of this rank's sequences (MB tokens = MB/T sequences)
+        tok0 = s0 * T
+        self.calls = []
+        mask_all = lay["loss_mask"]
+        for c in range(n_calls):
+            t0 = tok0 + c * MB
+            sa = t0 // T
+            sb = sa + MB // T
+            self.calls.append(dict(
+                cu=torch.from_numpy((np.arange(MB // T + 1) * T).astype(np.int32)).to(dev),
+                mask=torch.from_numpy(mask_all[t0:t0 + MB]).to(dev), sa=sa, sb=sb,
+                tok=torch.empty(MB, dtype=torch.int32, device=dev),
+                counts=torch.zeros(20, dtype=torch.float64, device=dev),
+                stats=torch.zeros(10, dtype=torch.float64, device=dev),
+                logp=torch.empty(MB, dtype=torch.float32, device=dev)))
+        self.total_counts = torch.zeros(20, dtype=torch.float64, device=dev)
+        self.ws = torch.empty(rl.policy_loss_workspace_size(MB, V), dtype=torch.uint8, device=dev)
+        self.tokens_per_step = n_calls * MB
+        self.bytes_per_token = 2 * V * 2 + SIDE_BYTES
+        self.launches = 0
+        self.ev = []
+
+    def step(self, record):
+        rl, torch = self.rl, self.torch
+        P = len(self.pool)
+        for c, cl in enumerate(self.calls):
+            rl.seq_bookkeeping(cl["cu"], self.pool_y[c % P], self.V, cl["tok"], self.seq_active[cl["sa"]:cl["sb"]],
+                               loss_mask=cl["mask"], seq_version=self.seq_version[cl["sa"]:cl["sb"]],
+                               trainer_version=self.trainer_version, max_staleness=self.max_staleness,
+                               counts_out=cl["counts"])
+            self.launches += 2
+        # N_active of the whole (policy) batch: the calls' counts summed, then over ranks
+        torch.sum(torch.stack([cl["counts"] for cl in self.calls]), dim=0, out=self.total_counts)
+        if self.comm is not None:
+            self.comm.allreduce_f64(self.total_counts)
+        rl.group_advantage(self.rewards, self.cu_groups, self.adv, self.zero_var, batch_norm=True,
+                           seq_weight=self.seq_active, workspace=self.ws_adv)
+        self.launches += 1
+        stream = torch.cuda.current_stream()
+        for c, cl in enumerate(self.calls):
+            p = rl.LossParams(trainer_version=self.trainer_version, max_staleness=self.max_staleness,
+                              active_tokens_dev=self.total_counts[0:1])
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            rl.policy_loss_fwd_bwd(self.pool[c % P], self.pool_y[c % P], self.pool_old[c % P], cl["tok"],
+                                   self.adv[cl["sa"]:cl["sb"]], p, self.dlogits, cl["stats"], self.ws,
+                                   loss_mask=cl["mask"], seq_version=self.seq_version[cl["sa"]:cl["sb"]],
+                                   logp_out=cl["logp"])
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                self.ev.append((e0, e1))
+            self.launches += 2
+            if self.comm is not None:
+                self.comm.allreduce_f64(cl["stats"])
+
+    def kernel_ms(self):
+        ms = [a.elapsed_time(b) for a, b in self.ev]
+        return sum(ms) / len(ms)
+
+
+class VocabParallelWorkload:
+    """Config vocabpar (BASELINE.json configs[3]): 65,536 tokens, V split over the ranks; one step
+    = rl_vocab_parallel_logprob with the fused loss on the rank's column shard."""
+
+    def __init__(self, rl, torch, np, synth, dev, comm, cfg, world, rank):
+        from paper_2605_15565_b200.parallel import shard_vocab
+        self.rl, self.torch, self.comm = rl, torch, comm
+        V = cfg.vocab
+        N = cfg.n_tokens
+        sh = shard_vocab(V, world, rank)
+        self.off, self.Vr = sh.offset, sh.size
+        ld = max(8, (self.Vr + 7) // 8 * 8)
+        full = torch.empty((4096, V), dtype=torch.bfloat16, device=dev)
+        self.shard = torch.empty((N, ld), dtype=torch.bfloat16, device=dev)
+        self.y = torch.empty(N, dtype=torch.int32, device=dev)
+        self.old = torch.empty(N, dtype=torch.float32, device=dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(99)
+        for c0 in range(0, N, 4096):   # identical full rows on every rank, each keeps its columns
+            synth.device_logits(full, V, row0=c0, seed=cfg.seed, targets_out=self.y[c0:c0 + 4096])
+            self.shard[c0:c0 + 4096, :self.Vr].copy_(full[:, self.off:self.off + self.Vr])
+            blk = full.float()
+            lp = blk.gather(1, self.y[c0:c0 + 4096, None].long())[:, 0] - torch.logsumexp(blk, dim=1)
+            self.old[c0:c0 + 4096] = lp + 0.02 * torch.randn(lp.shape, generator=g, device=dev)
+        del full, blk
+        lay = synth.seq_layout(cfg)
+        self.lay = lay
+        self.dl = torch.empty_like(self.shard)
+        self.logp = torch.empty(N, dtype=torch.float32, device=dev)
+        self.mask = torch.from_numpy(lay["loss_mask"]).to(dev)
+        self.cu = torch.from_numpy(lay["cu_seqlens"]).to(dev)
+        self.tok = torch.empty(N, dtype=torch.int32, device=dev)
+        S = cfg.n_seq
+        self.seq_active = torch.empty(S, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(20, dtype=torch.float64, device=dev)
+        self.rewards = torch.from_numpy(lay["rewards"]).to(dev)
+        self.cu_groups = torch.from_numpy(lay["cu_groups"]).to(dev)
+        self.seq_version = torch.from_numpy(lay["seq_version"]).to(dev)
+        self.adv = torch.empty(S, dtype=torch.float32, device=dev)
+        self.ws_adv = torch.empty(rl.group_advantage_workspace_size(S), dtype=torch.uint8, device=dev)
+        self.stats = torch.zeros(10, dtype=torch.float64, device=dev)
+        self.ws = torch.empty(rl.vocab_parallel_workspace_size(N, world), dtype=torch.uint8, device=dev)
+        self.V, self.N = V, N
+        self.tokens_per_step = N
+        # algorithmic bytes per token on this rank: read + write of the shard row + side data
+        self.bytes_per_token = 2 * self.Vr * 2 + SIDE_BYTES
+        self.launches = 0
+        self.ev = []
+
+    def step(self, record):
+        rl, torch = self.rl, self.torch
+        rl.seq_bookkeeping(self.cu, self.y, self.V, self.tok, self.seq_active, loss_mask=self.mask,
+                           seq_version=self.seq_version, trainer_version=self.lay["trainer_version"],
+                           counts_out=self.counts)
+        rl.group_advantage(self.rewards, self.cu_groups, self.adv, batch_norm=True, seq_weight=self.seq_active,
+                           workspace=self.ws_adv)
+        p = rl.LossParams(trainer_version=self.lay["trainer_version"], active_tokens_dev=self.counts[0:1])
+        stream = torch.cuda.current_stream()
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        rl.vocab_parallel_logprob(self.shard, self.y, self.off, self.V, self.comm, self.logp, self.ws,
+                                  vocab_shard=self.Vr, old_logp=self.old, loss_mask=self.mask, token_seq=self.tok,
+                                  seq_adv=self.adv, seq_version=self.seq_version, params=p,
+                                  dlogits_shard=self.dl, stats=self.stats)
+        if record:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+            self.ev.append((e0, e1))
+        self.comm.allreduce_f64(self.stats)
+        self.launches += 2 + 1 + 3
+
+    def kernel_ms(self):
+        ms = [a.elapsed_time(b) for a, b in self.ev]
+        return sum(ms) / len(ms)
+
+
+CONFIG_WORKLOADS = {
+    "single": "single-policy GRPO batch (BASELINE.json configs[1]): 32 prompts x 8 responses x 2048 tokens, "
+              "V=151936, bf16 logits, per GPU",
+    "long": "long agentic trajectories (BASELINE.json configs[2]): 8 prompts x 8 responses x 32768 tokens, "
+            "multi-turn with tool output masked, V=151936, token-sharded over the GPUs",
+    "vocabpar": "vocab-parallel (BASELINE.json configs[3]): 65,536 tokens, V=151936 split across the GPUs",
+    "multi": "multi-policy step (BASELINE.json configs[4]): 2 policies (V 151936 / 128256), 128 x 8 x 4096 "
+             "tokens, staleness <= 8, one GPU group per policy",
+}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -203,6 +405,7 @@ def main():
 
     import paper_2605_15565_b200 as rl
     import synth
+    from paper_2605_15565_b200.parallel import shard_sequences
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -211,91 +414,77 @@ def main():
     dev = torch.device("cuda", local)
     rl.load()
     comm = None
-    if world > 1:
+    if world > 1 or args.config == "vocabpar":
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
-        comm = rl.Comm.from_torch()
-    cfg = synth.get_config("single")
-    V = cfg.vocab
-    T = cfg.seq_len
+        if world > 1:
+            dist.init_process_group("nccl", device_id=dev)
+            comm = rl.Comm.from_torch()
+        else:
+            import ctypes
+            buf = (ctypes.c_uint8 * 128)()
+            lib = rl.load()
+            assert lib.rl_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)) == 0
+            h = ctypes.c_void_p()
+            assert lib.rl_comm_init(ctypes.byref(h), bytes(buf), 1, 0) == 0
+            comm = rl.Comm(h.value, 1, 0)
     MB = args.minibatch_tokens
-    N = N_MINIBATCH * MB                # 524,288 tokens per rank at the default MB
-    assert MB % T == 0 and N <= cfg.n_tokens
-    S_mb = MB // T
-    S = N // T                          # 256 sequences per rank at the default MB
-    G = S // cfg.group
-    lay = synth.seq_layout(cfg, seed=cfg.seed + 1000 * rank)
-
-    # --- resident inputs: 2 distinct mini-batch logits buffers + targets / old logp
-    POOL = 2
-    pool, pool_y, pool_old = [], [], []
-    for b in range(POOL):
-        x = torch.empty((MB, V), dtype=torch.bfloat16, device=dev)
-        y = torch.empty(MB, dtype=torch.int32, device=dev)
-        synth.device_logits(x, V, row0=(rank * POOL + b) * MB, seed=cfg.seed, targets_out=y)
-        # behaviour log-probs: log-softmax via torch (input synthesis only) + seeded drift
-        old = torch.empty(MB, dtype=torch.float32, device=dev)
-        g = torch.Generator(device=dev)
-        g.manual_seed(77 + b + 10 * rank)
-        for c0 in range(0, MB, 4096):
-            blk = x[c0:c0 + 4096].float()
-            lp = blk.gather(1, y[c0:c0 + 4096, None].long())[:, 0] - torch.logsumexp(blk, dim=1)
-            old[c0:c0 + 4096] = lp + 0.02 * torch.randn(lp.shape, generator=g, device=dev)
-            del blk
-        pool.append(x)
-        pool_y.append(y)
-        pool_old.append(old)
-    dlogits = torch.empty((MB, V), dtype=torch.bfloat16, device=dev)
+    scaling = "weak"
+    kern = os.environ.get("RL_LOSS_KERNEL", "cluster")
+    parallelism = f"dp{world} (token-parallel)"
+    if args.config == "single":
+        cfg = synth.get_config("single")
+        cfg = synth.get_config("single", seed=cfg.seed + 1000 * rank)   # each rank its own batch (DP)
+        n_calls = N_MINIBATCH
+        S = n_calls * MB // cfg.seq_len
+        wl = TokenParallelWorkload(rl, torch, np, synth, dev, comm, cfg, (0, S), MB, n_calls, rank, -1)
+        # each rank's own batch: restrict advantages to its sequences
+        wl.rewards, wl.cu_groups = wl.rewards[:S], wl.cu_groups[:S // cfg.group + 1]
+        wl.adv, wl.zero_var = wl.adv[:S], wl.zero_var[:S // cfg.group]
+        wl.seq_active = wl.seq_active[:S]
+        kname = f"rl_policy_loss_fwd_bwd ({kern})"
+    elif args.config == "long":
+        cfg = synth.get_config("long")
+        sh = shard_sequences(np.arange(cfg.n_seq + 1) * cfg.seq_len, world, rank)
+        n_calls = sh.n_tokens // MB
+        wl = TokenParallelWorkload(rl, torch, np, synth, dev, comm, cfg, (sh.seq_begin, sh.seq_end), MB, n_calls,
+                                   rank, -1)
+        scaling = "strong"
+        kname = f"rl_policy_loss_fwd_bwd ({kern})"
+    elif args.config == "multi":
+        half = max(1, world // 2)
+        policy = 0 if world == 1 else rank // half
+        cfgs = [synth.get_config("multi_a"), synth.get_config("multi_b")]
+        sub = comm.split(policy, rank) if comm is not None else None
+        ranks_pp = half if world > 1 else 1
+        prank = rank % half if world > 1 else 0
+        cfg = cfgs[policy]
+        sh = shard_sequences(np.arange(cfg.n_seq + 1) * cfg.seq_len, ranks_pp, prank)
+        n_calls = sh.n_tokens // MB
+        if world == 1:   # one GPU: both policies' batches in turn (one logits buffer each, shared dlogits)
+            shared = torch.empty(MB * max(c.vocab for c in cfgs), dtype=torch.bfloat16, device=dev)
+            wl = [TokenParallelWorkload(rl, torch, np, synth, dev, None, c, (0, c.n_seq), MB,
+                                        c.n_tokens // MB, rank, c.max_staleness, n_pool=1, dlogits_buf=shared)
+                  for c in cfgs]
+        else:
+            wl = TokenParallelWorkload(rl, torch, np, synth, dev, sub, cfg, (sh.seq_begin, sh.seq_end), MB,
+                                       n_calls, prank, cfg.max_staleness)
+        scaling = "strong"
+        parallelism = f"2 policy groups x {ranks_pp} GPU (token-parallel within a group)"
+        kname = f"rl_policy_loss_fwd_bwd ({kern})"
+    elif args.config == "vocabpar":
+        cfg = synth.get_config("vocabpar")
+        wl = VocabParallelWorkload(rl, torch, np, synth, dev, comm, cfg, world, rank)
+        scaling = "strong"
+        parallelism = f"vocab-parallel over {world} GPU (NCCL all-gather of per-row max/sum-exp/target logit)"
+        kname = "rl_vocab_parallel_logprob (vp_stats + NCCL all-gather + vp_finish)"
+    else:
+        raise SystemExit(f"unknown config {args.config}")
+    wls = wl if isinstance(wl, list) else [wl]
     torch.cuda.synchronize()
 
-    rewards = torch.from_numpy(lay["rewards"][:S]).to(dev)
-    cu_groups = torch.from_numpy(lay["cu_groups"][:G + 1]).to(dev)
-    seq_version = torch.from_numpy(lay["seq_version"][:S]).to(dev)
-    mask = torch.from_numpy(lay["loss_mask"][:N]).to(dev)
-    cu_mb = torch.from_numpy((np.arange(S_mb + 1) * T).astype(np.int32)).to(dev)
-    token_seq = torch.empty((N_MINIBATCH, MB), dtype=torch.int32, device=dev)
-    seq_active = torch.empty(S, dtype=torch.int32, device=dev)
-    counts = torch.zeros((N_MINIBATCH, 20), dtype=torch.float64, device=dev)
-    adv = torch.empty(S, dtype=torch.float32, device=dev)
-    zero_var = torch.empty(G, dtype=torch.uint8, device=dev)
-    ws_adv = torch.empty(rl.group_advantage_workspace_size(S), dtype=torch.uint8, device=dev)
-    stats = torch.zeros((N_MINIBATCH, 10), dtype=torch.float64, device=dev)
-    ws = torch.empty(rl.policy_loss_workspace_size(MB, V), dtype=torch.uint8, device=dev)
-    logp = torch.empty((N_MINIBATCH, MB), dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream()
-    ev_loss = []          # (start, end) CUDA events around every loss launch in the timed region
-    launches = [0]
-
-    def step(record: bool):
-        for j in range(N_MINIBATCH):
-            rl.seq_bookkeeping(cu_mb, pool_y[j % POOL], V, token_seq[j], seq_active[j * S_mb:(j + 1) * S_mb],
-                               loss_mask=mask[j * MB:(j + 1) * MB],
-                               seq_version=seq_version[j * S_mb:(j + 1) * S_mb],
-                               trainer_version=lay["trainer_version"], max_staleness=-1,
-                               counts_out=counts[j])
-            launches[0] += 2
-            if comm is not None:
-                comm.allreduce_f64(counts[j])
-        rl.group_advantage(rewards, cu_groups, adv, zero_var, batch_norm=True, seq_weight=seq_active,
-                           workspace=ws_adv)
-        launches[0] += 1
-        for j in range(N_MINIBATCH):
-            p = rl.LossParams(trainer_version=lay["trainer_version"], active_tokens_dev=counts[j, 0:1])
-            if record:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            rl.policy_loss_fwd_bwd(pool[j % POOL], pool_y[j % POOL], pool_old[j % POOL], token_seq[j],
-                                   adv[j * S_mb:(j + 1) * S_mb], p, dlogits, stats[j], ws,
-                                   loss_mask=mask[j * MB:(j + 1) * MB],
-                                   seq_version=seq_version[j * S_mb:(j + 1) * S_mb],
-                                   logp_out=logp[j])
-            if record:
-                e1 = torch.cuda.Event(enable_timing=True)
-                e1.record(stream)
-                ev_loss.append((e0, e1))
-            launches[0] += 2
-            if comm is not None:
-                comm.allreduce_f64(stats[j])
+    def step(record):
+        for w in wls:
+            w.step(record)
 
     for _ in range(args.warmup):
         step(False)
@@ -308,7 +497,10 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches[0] = 0
+    for w in wls:
+        w.launches = 0
+        w.ev = []
+    stream = torch.cuda.current_stream()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -320,69 +512,74 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     elapsed_ms = t0.elapsed_time(t1)
-    gpu_launches = launches[0]
+    gpu_launches = sum(w.launches for w in wls)
     if world > 1:
         tt = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         elapsed_ms = tt.item()
-    loss_ms = [a.elapsed_time(b) for a, b in ev_loss]
-    avg_loss_ms = sum(loss_ms) / len(loss_ms)
-    tokens_total = world * N * args.steps
-    value = tokens_total / (elapsed_ms / 1e3)
+    tokens_rank = sum(w.tokens_per_step for w in wls)
+    tok_all = torch.tensor([float(tokens_rank)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tok_all)
+    tokens_step = tok_all.item() if args.config != "vocabpar" else float(wls[0].tokens_per_step)
+    value = tokens_step * args.steps / (elapsed_ms / 1e3)
 
-    # --- roofline of the dominant kernel (fused loss): algorithmic bytes / launch duration
-    bytes_per_token = 2 * V * 2 + SIDE_BYTES
-    alg_bytes = MB * bytes_per_token
-    achieved = alg_bytes / (avg_loss_ms / 1e3) / 1e9
+    # roofline of the dominant kernel: algorithmic bytes per launch / its average launch duration
+    w0 = wls[0]
+    launch_tokens = w0.MB if hasattr(w0, "MB") else w0.N
+    alg_bytes = launch_tokens * w0.bytes_per_token
+    avg_ms = w0.kernel_ms()
+    achieved = alg_bytes / (avg_ms / 1e3) / 1e9
     peak, peak_src = measured_peak_hbm()
-    kern = os.environ.get("RL_LOSS_KERNEL", "cluster")
-    traffic = ncu_traffic(kern)
+    traffic = ncu_traffic(kern) if args.config in ("single", "long", "multi") else None
 
-    # --- e2e: the host-buffer C-ABI entry point, pinned host logits, H2D inside the timed region
-    e2e = None
-    if not args.no_e2e:
-        e2e = measure_e2e(rl, torch, dev, pool[0], pool_y[0], pool_old[0], token_seq[0], adv[:S_mb],
-                          mask[:MB], seq_version[:S_mb], lay, V, args)
-        if world > 1:
-            tt = torch.tensor([e2e["seconds"]], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e["value"] = world * e2e["tokens"] / tt.item()
-        e2e = {k: e2e[k] for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step", "sample")}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        x16 = pool[0][:64].view(torch.int16).cpu().numpy().view(np.uint16)
-        yy = pool_y[0][:64].cpu().numpy()
-        oo = pool_old[0][:64].cpu().numpy()
-        workers = host_cores()
-        rate, secs, done = time_oracle(x16, yy, oo, 8192, workers)
-        cpu = {"value": rate, "unit": "tokens/s", "cores": workers, "kind": "oracle",
-               "sample": f"{done} token rows (64 distinct rows of mini-batch 0) x V=151936 fwd+bwd "
-                         f"in {secs:.1f} s wall over {workers} processes"}
+    e2e, cpu = None, None
+    if args.config == "single":
+        if not args.no_e2e:
+            S_mb = MB // 2048
+            e2e = measure_e2e(rl, torch, dev, w0.pool[0], w0.pool_y[0], w0.pool_old[0], w0.calls[0]["tok"],
+                              w0.adv[:S_mb], w0.calls[0]["mask"], w0.seq_version[:S_mb],
+                              {"trainer_version": w0.trainer_version}, w0.V, args)
+            if world > 1:
+                tt = torch.tensor([e2e["seconds"]], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                e2e["value"] = world * e2e["tokens"] / tt.item()
+            e2e = {k: e2e[k] for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step", "sample")}
+        if rank == 0 and world == 1 and not args.no_cpu:
+            x16 = w0.pool[0][:64].view(torch.int16).cpu().numpy().view(np.uint16)
+            yy = w0.pool_y[0][:64].cpu().numpy()
+            oo = w0.pool_old[0][:64].cpu().numpy()
+            workers = host_cores()
+            rate, secs, done = time_oracle(x16, yy, oo, 8192, workers)
+            cpu = {"value": rate, "unit": "tokens/s", "cores": workers, "kind": "oracle",
+                   "sample": f"{done} token rows (64 distinct rows of mini-batch 0) x V=151936 fwd+bwd "
+                             f"in {secs:.1f} s wall over {workers} processes"}
 
     if rank == 0:
+        workload = CONFIG_WORKLOADS[args.config]
+        if MB != 131072:
+            workload = f"PROFILING ONLY ({MB}-token calls): " + workload
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD if MB == 131072 else f"PROFILING ONLY: {N} tokens/step",
-                       "tokens_per_rank_per_step": N,
-                       "minibatches_per_step": N_MINIBATCH, "minibatch_tokens": MB, "vocab": V,
-                       "global_batch_tokens": world * N, "parallelism": f"dp{world} (token-parallel)",
-                       "loss_kernel": kern, "l2": "no flush: each call streams a distinct 39.8 GB "
-                       "buffer (pool of 2) >> 126 MB L2", "agg": "token_mean", "batch_norm": True},
+            "config": {"workload": workload, "config": args.config, "tokens_per_step": tokens_step,
+                       "tokens_per_rank_per_step": tokens_rank, "call_tokens": launch_tokens,
+                       "vocab": w0.V, "parallelism": parallelism, "loss_kernel": kern,
+                       "l2": "no flush: every loss call streams a distinct >= 2.5 GB logits buffer >> 126 MB L2",
+                       "agg": "token_mean", "batch_norm": True},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": f"rl_policy_loss_fwd_bwd ({kern})",
-                         "algorithmic_bytes_per_launch": alg_bytes,
-                         "bytes_per_token": bytes_per_token, "avg_launch_ms": avg_loss_ms,
+                         "kernel": kname, "algorithmic_bytes_per_launch": alg_bytes,
+                         "bytes_per_token": w0.bytes_per_token, "avg_launch_ms": avg_ms,
                          "frac_of_8TBs": achieved / 8000.0},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.destroy()
+    if world > 1:
         dist.destroy_process_group()
 
 
