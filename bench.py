@@ -474,9 +474,13 @@ def main():
     elif args.config == "vocabpar":
         cfg = synth.get_config("vocabpar")
         wl = VocabParallelWorkload(rl, torch, np, synth, dev, comm, cfg, world, rank)
+        fused_vp = os.environ.get("RL_VP_PATH", "peer") == "peer" and comm.enable_peer_exchange(cfg.n_tokens)
         scaling = "strong"
-        parallelism = f"vocab-parallel over {world} GPU (NCCL all-gather of per-row max/sum-exp/target logit)"
-        kname = "rl_vocab_parallel_logprob (vp_stats + NCCL all-gather + vp_finish)"
+        parallelism = (f"vocab-parallel over {world} GPU: " + (
+            "one fused kernel per rank, per-row (max, sum-exp, target logit) exchanged by NVLink peer stores"
+            if fused_vp else "vp_stats + NCCL all-gather + vp_finish"))
+        kname = "rl_vocab_parallel_logprob (" + ("vp_fused_kernel, in-kernel peer exchange" if fused_vp
+                                                 else "vp_stats + NCCL all-gather + vp_finish") + ")"
     else:
         raise SystemExit(f"unknown config {args.config}")
     wls = wl if isinstance(wl, list) else [wl]

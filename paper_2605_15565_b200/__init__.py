@@ -72,6 +72,7 @@ _SIGS = {
     "rl_comm_destroy": (i32, [vp]),
     "rl_comm_size": (i32, [vp, vp, vp]),
     "rl_comm_allreduce_f64": (i32, [vp, vp, sz, vp]),
+    "rl_comm_enable_peer_exchange": (i32, [vp, i64]),
     "rl_vocab_parallel_workspace_size": (sz, [i64, i32]),
     "rl_vocab_parallel_logprob": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, f32, vp, vp, vp, vp,
                                         vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
@@ -317,6 +318,15 @@ class Comm:
         n, r = i32(), i32()
         _check(lib.rl_comm_size(h.value, C.byref(n), C.byref(r)), "rl_comm_size")
         return Comm(h.value, n.value, r.value)
+
+    def enable_peer_exchange(self, max_tokens: int) -> bool:
+        """Collective: map every rank's exchange buffer (CUDA IPC over NVLink) so the fused
+        vocab-parallel loss runs as one kernel per rank.  Returns False if P2P is unavailable."""
+        st = load().rl_comm_enable_peer_exchange(self.handle, int(max_tokens))
+        if st == 3:   # RL_ERR_UNSUPPORTED: keep the NCCL path
+            return False
+        _check(st, "rl_comm_enable_peer_exchange")
+        return True
 
     def allreduce_f64(self, buf, stream=None):
         _check(load().rl_comm_allreduce_f64(self.handle, _dev(buf, "buf"), buf.numel(),

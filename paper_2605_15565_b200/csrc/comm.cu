@@ -12,6 +12,11 @@ struct rl_comm {
   ncclComm_t nccl;
   int32_t nranks;
   int32_t rank;
+  // peer exchange (rl_comm_enable_peer_exchange): this rank's buffer and every rank's mapping
+  void* xbuf = nullptr;
+  void* peers[8] = {};
+  int64_t max_tokens = 0;
+  uint32_t epoch = 0;
 };
 
 namespace rl {
@@ -21,6 +26,21 @@ static rl_status nccl_fail(ncclResult_t r, const char* what) {
 ncclComm_t comm_nccl(rl_comm* c) { return c->nccl; }
 int32_t comm_rank(const rl_comm* c) { return c->rank; }
 int32_t comm_size(const rl_comm* c) { return c->nranks; }
+// peer exchange layout (per rank buffer): records float4[P][max_tokens], flags uint32[P][max_tokens]
+bool comm_peer_exchange(rl_comm* c, int64_t n_tokens, void** peers, int64_t* max_tokens, uint32_t* epoch) {
+  if (!c->xbuf || n_tokens > c->max_tokens) return false;
+  for (int r = 0; r < c->nranks; ++r) peers[r] = c->peers[r];
+  *max_tokens = c->max_tokens;
+  *epoch = ++c->epoch;
+  return true;
+}
+static void release_peer_exchange(rl_comm* c) {
+  for (int r = 0; r < c->nranks; ++r)
+    if (c->peers[r] && c->peers[r] != c->xbuf) cudaIpcCloseMemHandle(c->peers[r]);
+  if (c->xbuf) cudaFree(c->xbuf);
+  c->xbuf = nullptr;
+  for (auto& p : c->peers) p = nullptr;
+}
 }  // namespace rl
 
 static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
@@ -48,6 +68,57 @@ extern "C" rl_status rl_comm_init(rl_comm** out, const void* unique_id_host, int
   return RL_OK;
 }
 
+extern "C" rl_status rl_comm_enable_peer_exchange(rl_comm* c, int64_t max_tokens) {
+  using namespace rl;
+  if (!c || max_tokens < 1) return fail(RL_ERR_INVALID_ARGUMENT, "NULL comm or max_tokens < 1");
+  if (c->nranks > 8) return fail(RL_ERR_UNSUPPORTED, "peer exchange supports <= 8 ranks");
+  release_peer_exchange(c);
+  const size_t bytes = (size_t)c->nranks * max_tokens * (16 + 4);
+  if (cudaMalloc(&c->xbuf, bytes) != cudaSuccess) return check_launch("cudaMalloc(peer exchange)");
+  if (cudaMemset(c->xbuf, 0, bytes) != cudaSuccess) return check_launch("cudaMemset(peer exchange)");
+  cudaIpcMemHandle_t mine;
+  if (cudaIpcGetMemHandle(&mine, c->xbuf) != cudaSuccess) {
+    release_peer_exchange(c);
+    return check_launch("cudaIpcGetMemHandle");
+  }
+  char* dh = nullptr;
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  if (cudaMalloc(&dh, hb * (c->nranks + 1)) != cudaSuccess) return check_launch("cudaMalloc(handles)");
+  cudaMemcpy(dh + hb * c->nranks, &mine, hb, cudaMemcpyHostToDevice);
+  ncclResult_t r = ncclAllGather(dh + hb * c->nranks, dh, hb, ncclChar, c->nccl, 0);
+  if (r != ncclSuccess) {
+    cudaFree(dh);
+    release_peer_exchange(c);
+    return nccl_fail(r, "ncclAllGather(ipc handles)");
+  }
+  cudaIpcMemHandle_t* all = new cudaIpcMemHandle_t[c->nranks];
+  cudaDeviceSynchronize();
+  cudaMemcpy(all, dh, hb * c->nranks, cudaMemcpyDeviceToHost);
+  cudaFree(dh);
+  rl_status st = RL_OK;
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) {
+      c->peers[q] = c->xbuf;
+      continue;
+    }
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      st = fail(RL_ERR_UNSUPPORTED, "cudaIpcOpenMemHandle failed for rank %d (no P2P?)", q);
+      break;
+    }
+    c->peers[q] = p;
+  }
+  delete[] all;
+  if (st != RL_OK) {
+    release_peer_exchange(c);
+    return st;
+  }
+  c->max_tokens = max_tokens;
+  c->epoch = 0;
+  return RL_OK;
+}
+
 extern "C" rl_status rl_comm_split(rl_comm* parent, int32_t color, int32_t key, rl_comm** out) {
   if (!parent || !out) return rl::fail(RL_ERR_INVALID_ARGUMENT, "NULL parent/out");
   ncclComm_t c = nullptr;
@@ -66,6 +137,7 @@ extern "C" rl_status rl_comm_split(rl_comm* parent, int32_t color, int32_t key, 
 
 extern "C" rl_status rl_comm_destroy(rl_comm* c) {
   if (!c) return RL_OK;
+  rl::release_peer_exchange(c);
   ncclResult_t r = ncclCommDestroy(c->nccl);
   delete c;
   if (r != ncclSuccess) return rl::nccl_fail(r, "ncclCommDestroy");

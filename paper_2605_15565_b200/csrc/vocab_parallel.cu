@@ -14,12 +14,14 @@
 
 #include "loss_common.cuh"
 #include "rowstats.cuh"
+#include "sm100.cuh"
 
 namespace rl {
 
 ncclComm_t comm_nccl(rl_comm* c);
 int32_t comm_rank(const rl_comm* c);
 int32_t comm_size(const rl_comm* c);
+bool comm_peer_exchange(rl_comm* c, int64_t n_tokens, void** peers, int64_t* max_tokens, uint32_t* epoch);
 rl_status launch_stats_reduce(const double* partials, int n_ctas, rl_loss_stats* stats,
                               bool accumulate, cudaStream_t s);
 
@@ -147,6 +149,184 @@ __global__ void __launch_bounds__(kVpThreads) vp_finish_kernel(
     for (int i = 0; i < RL_LOSS_STATS_N; ++i) partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = acc.v[i];
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Fused vocab-parallel loss with in-kernel peer exchange (rl_comm_enable_peer_exchange).
+// One CTA per SM; each CTA walks its rows (row = blockIdx.x + k * gridDim.x, the same on every
+// rank).  A 4-deep ring of row slices in shared memory (TMA bulk loads): the statistics of row
+// k+1 are computed and published to every rank (NVLink stores of a 16-B record + a flag carrying
+// the call's epoch) BEFORE the kernel waits for the peers' records of row k, so the exchange
+// latency hides behind the next row's pass; then row k is combined (M, S, lse, logp, loss
+// epilogue) and its dlogits slice written from shared memory.  Logits read once, dlogits once.
+constexpr int kVfThreads = 512;
+constexpr int kVfBufs = 4;
+
+struct VfArgs {
+  const void* logits;
+  void* dlogits;
+  int64_t n, Vr, off, Vtot, ld, max_tokens;
+  const int32_t* targets;
+  const float* old_logp;
+  const uint8_t* mask;
+  const int32_t* token_seq;
+  const float* seq_adv;
+  const int32_t* seq_version;
+  const int32_t* seq_active;
+  float* logp_out;
+  float* lse_out;
+  double* partials;
+  Knobs kn;
+  int32_t count_stats, P, me, nb;  // nb: shared-memory row buffers (2..4)
+  uint32_t epoch;
+  float4* rec[8];     // rank q's record array  [P][max_tokens]
+  uint32_t* flag[8];  // rank q's flag array    [P][max_tokens]
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kVfThreads, 1) vp_fused_kernel(const VfArgs a) {
+  constexpr int EPV = VecTraits<T>::EPV;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  float* red = reinterpret_cast<float*>(smem + 64);                 // 64 floats
+  float4* rsc = reinterpret_cast<float4*>(smem + 64 + 256);         // per buffer (st, c2, dy, ycol)
+  unsigned char* bufs = smem + 1024;
+  const int64_t nvec = a.Vr / EPV;                                  // whole 16-B vectors per slice
+  const int64_t slice_bytes = (a.Vr * elem_bytes<T>() + 15) / 16 * 16;
+  const int64_t row_bytes = a.ld * elem_bytes<T>();
+  const int tid = threadIdx.x;
+  const float k = a.kn.inv_t * RL_LOG2E;
+  const int64_t nk = blockIdx.x < a.n ? (a.n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const double inv_tm = token_mean_inv(a.kn);
+  Acc acc;
+  acc.zero();
+  if (tid == 0) {
+    for (int i = 0; i < kVfBufs; ++i) sm100::mbar_init(&full[i], 1);
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
+  auto row_of = [&](int64_t kk) { return (int64_t)blockIdx.x + kk * gridDim.x; };
+  const int nb = a.nb;
+  auto issue = [&](int64_t kk) {
+    if (tid == 0 && kk < nk) {
+      const int b = (int)(kk % nb);
+      sm100::mbar_arrive_expect_tx(&full[b], (uint32_t)slice_bytes);
+      sm100::bulk_g2s_nohint(bufs + (size_t)b * slice_bytes,
+                             reinterpret_cast<const char*>(a.logits) + row_of(kk) * row_bytes, (uint32_t)slice_bytes,
+                             &full[b]);
+    }
+  };
+  // statistics of row kk (buffer kk % 4) -> record published to every rank
+  auto stats_publish = [&](int64_t kk) {
+    const int b = (int)(kk % nb);
+    sm100::mbar_wait(&full[b], (uint32_t)((kk / nb) & 1));
+    const unsigned char* rowp = bufs + (size_t)b * slice_bytes;
+    const uint4* vrow = reinterpret_cast<const uint4*>(rowp);
+    MS st{-INFINITY, 0.f};
+    int64_t i = tid;
+    for (; i + kVfThreads < nvec; i += 2 * kVfThreads) {  // two shared-memory vectors per step
+      float f[2 * EPV];
+      VecTraits<T>::unpack(vrow[i], f);
+      VecTraits<T>::unpack(vrow[i + kVfThreads], f + EPV);
+      ms_update<2 * EPV>(st, f, k);
+    }
+    for (; i < nvec; i += kVfThreads) {
+      float f[EPV];
+      VecTraits<T>::unpack(vrow[i], f);
+      ms_update<EPV>(st, f, k);
+    }
+    st = block_reduce_ms<kVfThreads>(st, red);
+    if (tid == 0) {
+      const int64_t row = row_of(kk);
+      const int32_t y = a.targets[row];
+      const int64_t yl = (int64_t)y - a.off;
+      // columns past the whole vectors (Vr % EPV) live in the same smem row
+      MS tail{-INFINITY, 0.f};
+      for (int64_t c = nvec * EPV; c < a.Vr; ++c) {
+        float f[1] = {VecTraits<T>::load1(rowp, c)};
+        ms_update<1>(tail, f, k);
+      }
+      st = ms_combine(st, tail);
+      const bool owned = y >= 0 && yl >= 0 && yl < a.Vr;
+      const float zy = owned ? VecTraits<T>::load1(rowp, yl) * a.kn.inv_t : 0.f;
+      const float4 rec = make_float4(st.m, st.s, zy, owned ? 1.f : 0.f);
+      for (int q = 0; q < a.P; ++q) a.rec[q][(int64_t)a.me * a.max_tokens + row] = rec;
+      __threadfence_system();
+      for (int q = 0; q < a.P; ++q)
+        *reinterpret_cast<volatile uint32_t*>(&a.flag[q][(int64_t)a.me * a.max_tokens + row]) = a.epoch;
+    }
+  };
+  for (int q = 0; q < nb - 1; ++q) issue(q);
+  if (nk > 0) stats_publish(0);
+  for (int64_t kk = 0; kk < nk; ++kk) {
+    issue(kk + nb - 1);                   // buffer (kk+nb-1)%nb == (kk-1)%nb, freed at the end of kk-1
+    if (kk + 1 < nk) stats_publish(kk + 1);
+    const int b = (int)(kk % nb);
+    const int64_t row = row_of(kk);
+    if (tid == 0) {  // wait for every rank's record of this row, then combine + loss epilogue
+      for (int q = 0; q < a.P; ++q) {
+        const volatile uint32_t* f = &a.flag[a.me][(int64_t)q * a.max_tokens + row];
+        while (*f != a.epoch) {
+        }
+      }
+      __threadfence_system();
+      float M = -INFINITY;
+      for (int q = 0; q < a.P; ++q) M = fmaxf(M, a.rec[a.me][(int64_t)q * a.max_tokens + row].x);
+      float S = 0.f, zy = 0.f;
+      for (int q = 0; q < a.P; ++q) {
+        const float4 e = a.rec[a.me][(int64_t)q * a.max_tokens + row];
+        if (e.x != -INFINITY) S += e.y * fast_exp2(e.x - M);
+        zy += e.z;
+      }
+      const float c2 = M + fast_log2(S);
+      const RowMeta mt = row_meta(row, a.Vtot, a.targets, a.mask, a.token_seq, a.seq_version,
+                                  a.kn.trainer_version, a.kn.max_staleness);
+      const float lp = logp_from(mt, zy, c2);
+      if (a.logp_out) a.logp_out[row] = lp;
+      if (a.lse_out) a.lse_out[row] = c2 * RL_LN2;
+      const float A = mt.valid ? a.seq_adv[mt.seq] : 0.f;
+      const float old = mt.valid ? a.old_logp[row] : 0.f;
+      Acc tmp;
+      tmp.zero();
+      const float s = token_epilogue(mt, lp, old, A, a.seq_active, inv_tm, a.kn, tmp, nullptr);
+      if (a.count_stats)
+        for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
+      const int64_t yl = (int64_t)mt.y - a.off;
+      const int ycol = (mt.in_range && yl >= 0 && yl < a.Vr) ? (int)yl : -1;
+      rsc[b] = make_float4(s, c2, s * (fast_exp2(zy * RL_LOG2E - c2) - 1.f), __int_as_float(ycol));
+    }
+    __syncthreads();
+    const float4 sc = rsc[b];
+    const float s = sc.x, c2 = sc.y, dy = sc.z;
+    const int ycol = __float_as_int(sc.w);
+    const unsigned char* rowp = bufs + (size_t)b * slice_bytes;
+    char* dp = reinterpret_cast<char*>(a.dlogits) + row * row_bytes;
+    const uint4* vin = reinterpret_cast<const uint4*>(rowp);
+    uint4* vout = reinterpret_cast<uint4*>(dp);
+    for (int64_t i = tid; i < nvec; i += kVfThreads) {
+      float f[EPV];
+      if (s == 0.f) {
+#pragma unroll
+        for (int j = 0; j < EPV; ++j) f[j] = 0.f;
+      } else {
+        VecTraits<T>::unpack(vin[i], f);
+#pragma unroll
+        for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
+        const int64_t c0 = i * EPV;
+        if (ycol >= c0 && ycol < c0 + EPV) f[ycol - c0] = dy;
+      }
+      st_stream_v4(vout + i, VecTraits<T>::pack(f));
+    }
+    for (int64_t c = nvec * EPV + tid; c < a.Vr; c += kVfThreads) {
+      float v = (s == 0.f) ? 0.f : s * fast_exp2(fmaf(VecTraits<T>::load1(rowp, c), k, -c2));
+      if (s != 0.f && c == ycol) v = dy;
+      VecTraits<T>::store1(dp, c, v);
+    }
+    __syncthreads();  // buffer b free for the load of row kk + nb
+  }
+  if (tid == 0)
+    for (int i = 0; i < RL_LOSS_STATS_N; ++i) a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = acc.v[i];
+}
+
 static int vp_grid(int64_t n) {
   static int ctas = 0;
   if (!ctas) {
@@ -205,6 +385,58 @@ extern "C" rl_status rl_vocab_parallel_logprob(
   if (n_tokens == 0) {
     if (with_loss && !(p->flags & RL_F_STATS_ACCUMULATE)) cudaMemsetAsync(stats, 0, sizeof(rl_loss_stats), s);
     return check_launch("vp empty");
+  }
+  void* peers[8];
+  int64_t max_tok = 0;
+  uint32_t epoch = 0;
+  const int64_t slice_bytes = (vocab_shard * eb + 15) / 16 * 16;
+  const int nbuf = (int)std::min<int64_t>(kVfBufs, (232448 - 1024) / std::max<int64_t>(slice_bytes, 16));
+  const size_t vf_smem = 1024 + (size_t)nbuf * slice_bytes;
+  if (with_loss && nbuf >= 2 && comm_peer_exchange(comm, n_tokens, peers, &max_tok, &epoch)) {
+    VfArgs v;
+    v.logits = logits_shard;
+    v.dlogits = dlogits_shard;
+    v.n = n_tokens;
+    v.Vr = vocab_shard;
+    v.off = vocab_offset;
+    v.Vtot = vocab_total;
+    v.ld = ld;
+    v.max_tokens = max_tok;
+    v.targets = targets;
+    v.old_logp = old_logp;
+    v.mask = loss_mask;
+    v.token_seq = token_seq;
+    v.seq_adv = seq_adv;
+    v.seq_version = seq_version;
+    v.seq_active = seq_active;
+    v.logp_out = logp_out;
+    v.lse_out = lse_out;
+    v.partials = partials;
+    v.kn = make_knobs(p);
+    v.count_stats = comm_rank(comm) == 0;
+    v.P = P;
+    v.me = comm_rank(comm);
+    v.epoch = epoch;
+    v.nb = nbuf;
+    for (int q = 0; q < 8; ++q) {
+      v.rec[q] = q < P ? reinterpret_cast<float4*>(peers[q]) : nullptr;
+      v.flag[q] = q < P ? reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(peers[q]) + (size_t)P * max_tok * 16)
+                        : nullptr;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int vgrid = (int)std::min<int64_t>(n_tokens, std::min(sms, kMaxStatCtas));
+    if (dtype == RL_BF16) {
+      cudaFuncSetAttribute(vp_fused_kernel<bf16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vf_smem);
+      vp_fused_kernel<bf16_t><<<vgrid, kVfThreads, vf_smem, s>>>(v);
+    } else {
+      cudaFuncSetAttribute(vp_fused_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vf_smem);
+      vp_fused_kernel<float><<<vgrid, kVfThreads, vf_smem, s>>>(v);
+    }
+    rl_status st0 = check_launch("vp_fused_kernel");
+    if (st0 != RL_OK) return st0;
+    return launch_stats_reduce(partials, vgrid, stats, (p->flags & RL_F_STATS_ACCUMULATE) != 0, s);
   }
   const int grid = vp_grid(n_tokens);
   if (dtype == RL_BF16)

@@ -87,44 +87,50 @@ def main():
             fails.append(f"tp row {t0 + i} dlogits")
 
     # ------------------------------------------------------------------ vocab parallel
-    vs = shard_vocab(V, world, rank)
-    N = len(case["targets"])
-    ld_s = max(8, (vs.size + 7) // 8 * 8)
-    shard = np.zeros((N, ld_s), dtype=np.uint16)
-    shard[:, :vs.size] = case["logits"][:, vs.offset:vs.offset + vs.size]
-    shard_t = d(shard)
-    dls = torch.empty_like(shard_t)
-    logp = torch.empty(N, dtype=torch.float32, device=dev)
-    lse = torch.empty(N, dtype=torch.float32, device=dev)
-    stats_v = torch.zeros(10, dtype=torch.float64, device=dev)
-    ws_v = torch.empty(rl.vocab_parallel_workspace_size(N, world), dtype=torch.uint8, device=dev)
-    p_v = rl.LossParams(trainer_version=case["trainer_version"], max_staleness=case["max_staleness"],
-                        global_active_tokens=float(ref["bk"]["active_tokens"]))
-    tok_full = d(ref["bk"]["token_seq"])
-    rl.vocab_parallel_logprob(shard_t, d(case["targets"]), vs.offset, V, comm, logp, ws_v, lse_out=lse,
-                              vocab_shard=vs.size, old_logp=d(case["old_logp"]),
-                              loss_mask=d(case["loss_mask"]), token_seq=tok_full, seq_adv=adv,
-                              seq_version=d(case["seq_version"]), params=p_v, dlogits_shard=dls,
-                              stats=stats_v)
-    comm.allreduce_f64(stats_v)
-    torch.cuda.synchronize()
-    lp = logp.cpu().numpy()
-    y = case["targets"]
-    ok = (y >= 0) & (y < V)
-    if np.abs(lp[ok] - out_ref["logp"][ok]).max() > 2e-3:
-        fails.append(f"vp logp max err {np.abs(lp[ok] - out_ref['logp'][ok]).max()}")
-    sv = stats_v.cpu().numpy()
-    if abs(sv[0] - out_ref["loss"]) > 1e-4 * scale or sv[1] != out_ref["stats"]["active_tokens"]:
-        fails.append(f"vp loss {sv[0]} vs {out_ref['loss']} active {sv[1]}")
-    gv = oracle.decode_bf16(dls.view(torch.int16).cpu().numpy().view(np.uint16))[:, :vs.size]
-    s_all = out_ref["scale"]
-    for i in range(N):
-        refrow = out_ref["dlogits"][i, vs.offset:vs.offset + vs.size]
-        if s_all[i] == 0:
-            if np.any(gv[i] != 0):
-                fails.append(f"vp row {i} not zero")
-        elif vs.size and np.abs(gv[i] - refrow).max() > 1e-2 * abs(s_all[i]):
-            fails.append(f"vp row {i} dlogits")
+    # twice: the NCCL all-gather path, then the fused in-kernel peer-exchange path
+    for mode in ("nccl", "peer"):
+      if mode == "peer":
+        if not comm.enable_peer_exchange(len(case["targets"])):
+            fails.append("peer exchange unavailable")
+            break
+      vs = shard_vocab(V, world, rank)
+      N = len(case["targets"])
+      ld_s = max(8, (vs.size + 7) // 8 * 8)
+      shard = np.zeros((N, ld_s), dtype=np.uint16)
+      shard[:, :vs.size] = case["logits"][:, vs.offset:vs.offset + vs.size]
+      shard_t = d(shard)
+      dls = torch.empty_like(shard_t)
+      logp = torch.empty(N, dtype=torch.float32, device=dev)
+      lse = torch.empty(N, dtype=torch.float32, device=dev)
+      stats_v = torch.zeros(10, dtype=torch.float64, device=dev)
+      ws_v = torch.empty(rl.vocab_parallel_workspace_size(N, world), dtype=torch.uint8, device=dev)
+      p_v = rl.LossParams(trainer_version=case["trainer_version"], max_staleness=case["max_staleness"],
+                          global_active_tokens=float(ref["bk"]["active_tokens"]))
+      tok_full = d(ref["bk"]["token_seq"])
+      rl.vocab_parallel_logprob(shard_t, d(case["targets"]), vs.offset, V, comm, logp, ws_v, lse_out=lse,
+                                vocab_shard=vs.size, old_logp=d(case["old_logp"]),
+                                loss_mask=d(case["loss_mask"]), token_seq=tok_full, seq_adv=adv,
+                                seq_version=d(case["seq_version"]), params=p_v, dlogits_shard=dls,
+                                stats=stats_v)
+      comm.allreduce_f64(stats_v)
+      torch.cuda.synchronize()
+      lp = logp.cpu().numpy()
+      y = case["targets"]
+      ok = (y >= 0) & (y < V)
+      if np.abs(lp[ok] - out_ref["logp"][ok]).max() > 2e-3:
+          fails.append(f"{mode} vp logp max err {np.abs(lp[ok] - out_ref['logp'][ok]).max()}")
+      sv = stats_v.cpu().numpy()
+      if abs(sv[0] - out_ref["loss"]) > 1e-4 * scale or sv[1] != out_ref["stats"]["active_tokens"]:
+          fails.append(f"{mode} vp loss {sv[0]} vs {out_ref['loss']} active {sv[1]}")
+      gv = oracle.decode_bf16(dls.view(torch.int16).cpu().numpy().view(np.uint16))[:, :vs.size]
+      s_all = out_ref["scale"]
+      for i in range(N):
+          refrow = out_ref["dlogits"][i, vs.offset:vs.offset + vs.size]
+          if s_all[i] == 0:
+              if np.any(gv[i] != 0):
+                  fails.append(f"{mode} vp row {i} not zero")
+          elif vs.size and np.abs(gv[i] - refrow).max() > 1e-2 * abs(s_all[i]):
+              fails.append(f"{mode} vp row {i} dlogits")
 
     # ------------------------------------------------------------------ comm split
     sub = comm.split(rank % 2, rank)

@@ -344,6 +344,24 @@ def test_vocab_parallel_single_rank(cuda_lib):
     lp = logp.cpu().numpy()
     ok = case["targets"] >= 0
     assert np.all(np.abs(lp[ok] - g["logp"][ok]) <= 1e-4)
+    # fused loss through the in-kernel peer exchange (P = 1: the rank exchanges with itself)
+    assert comm.enable_peer_exchange(N)
+    bk = oracle.seq_bookkeeping(case["cu_seqlens"], case["loss_mask"], case["targets"], 2048,
+                                case["seq_version"], case["trainer_version"], case["max_staleness"])
+    p = rl.LossParams(trainer_version=case["trainer_version"], max_staleness=case["max_staleness"],
+                      global_active_tokens=float(bk["active_tokens"]))
+    dl = t.empty_like(dev(case["logits"]))
+    stats = t.zeros(10, dtype=t.float64, device="cuda")
+    rl.vocab_parallel_logprob(dev(case["logits"]), dev(case["targets"]), 0, 2048, comm, logp, ws,
+                              old_logp=dev(case["old_logp"]), loss_mask=dev(case["loss_mask"]),
+                              token_seq=dev(bk["token_seq"]), seq_adv=dev(g["adv"]),
+                              seq_version=dev(case["seq_version"]), params=p, dlogits_shard=dl, stats=stats)
+    t.cuda.synchronize()
+    assert np.all(np.abs(logp.cpu().numpy()[ok] - g["logp"][ok]) <= 1e-4)
+    st = stats.cpu().numpy()
+    assert st[1] == g["stats"][1] and abs(st[0] - g["stats"][0]) <= 1e-5 * max(1e-30, abs(g["stats"][0]) + 1e-6)
+    d = host_logits(dl)[:, :2048]
+    assert np.abs(d - g["dlogits"]).max() <= 1e-2 * max(1e-30, np.abs(g["dlogits"]).max())
     comm.destroy()
 
 
