@@ -474,7 +474,7 @@ def main():
     elif args.config == "vocabpar":
         cfg = synth.get_config("vocabpar")
         wl = VocabParallelWorkload(rl, torch, np, synth, dev, comm, cfg, world, rank)
-        fused_vp = os.environ.get("RL_VP_PATH", "peer") == "peer" and comm.enable_peer_exchange(cfg.n_tokens)
+        fused_vp = os.environ.get("RL_VP_PATH", "nccl") == "peer" and comm.enable_peer_exchange(cfg.n_tokens)
         scaling = "strong"
         parallelism = (f"vocab-parallel over {world} GPU: " + (
             "one fused kernel per rank, per-row (max, sum-exp, target logit) exchanged by NVLink peer stores"

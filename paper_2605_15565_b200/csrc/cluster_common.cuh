@@ -41,6 +41,7 @@ struct ClArgs {
   int32_t nslots;
   int32_t prefetch_chunks;  // L2 lookahead in chunks beyond a full ring (RL_L2_PREFETCH_CHUNKS)
   int32_t debug;            // development only (RL_CLUSTER_DEBUG): 1 = no dlogits stores, 2 = no exp2
+  int32_t inflight_cap;     // max chunk loads in flight per CTA (0 = ring-limited), RL_INFLIGHT_CAP
 };
 
 // ------------------------------------------------------------------ packed fp32x2 helpers
@@ -123,6 +124,36 @@ struct ClVec<bf16_t> {
   __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t q2) {
     return make_uint4(f2_to_bf2(fmul2(h2_to_f2(c.x), q2)), f2_to_bf2(fmul2(h2_to_f2(c.y), q2)),
                       f2_to_bf2(fmul2(h2_to_f2(c.z), q2)), f2_to_bf2(fmul2(h2_to_f2(c.w), q2)));
+  }
+  // bf16-cache variant: e' cached as bf16 (F2FP.BF16), pass C is one packed bf16 multiply
+  // (HMUL2.BF16) per pair: 4 instructions per vector instead of 16, at the cost of two extra
+  // bf16 roundings (e' and q): <= ~0.6 % relative per element (reading Z21)
+  __device__ static __forceinline__ uint64_t exp_cache_bf(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
+                                                          uint4& c) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t t = ffma2(f2pack(bf16_lo(w[i]), bf16_hi(w[i])), k2, mn2);
+      float a, b;
+      f2unpack(t, a, b);
+      a = fast_exp2(a);
+      b = fast_exp2(b);
+      acc = fadd2(acc, f2pack(a, b));
+      o[i] = pack_bf16x2(a, b);
+    }
+    c = make_uint4(o[0], o[1], o[2], o[3]);
+    return acc;
+  }
+  __device__ static __forceinline__ uint4 grad_bf(const uint4& c, uint32_t qb2) {
+    const __nv_bfloat162 q = *reinterpret_cast<const __nv_bfloat162*>(&qb2);
+    uint4 o;
+    __nv_bfloat162 r;
+    r = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&c.x), q); o.x = *reinterpret_cast<uint32_t*>(&r);
+    r = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&c.y), q); o.y = *reinterpret_cast<uint32_t*>(&r);
+    r = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&c.z), q); o.z = *reinterpret_cast<uint32_t*>(&r);
+    r = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&c.w), q); o.w = *reinterpret_cast<uint32_t*>(&r);
+    return o;
   }
 };
 

@@ -65,7 +65,25 @@ struct __align__(16) ClShared {
 // Warp roles: warps 0..14 consume (passes A/B/C); warp 15 is the service warp: lane 0 issues the
 // TMA bulk copies, lane 1 runs the per-row epilogue (DSMEM exchange with the peer CTA(s),
 // combine, ratio/clip/scale, statistics) off the consumers' critical path.
-template <typename T, int CL, int NCH, bool EXACT, int H, bool TRACE = false>
+// cache operations: fp16 e' + fp32 multiply (default) or bf16 e' + packed bf16 multiply (BFC)
+template <typename T, bool BFC>
+struct CacheOps {
+  __device__ static __forceinline__ uint64_t exp(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc, uint4& c) {
+    return ClVec<T>::exp_cache(v, k2, mn2, acc, c);
+  }
+  __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t q2, uint32_t) { return ClVec<T>::grad(c, q2); }
+};
+template <>
+struct CacheOps<bf16_t, true> {
+  __device__ static __forceinline__ uint64_t exp(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc, uint4& c) {
+    return ClVec<bf16_t>::exp_cache_bf(v, k2, mn2, acc, c);
+  }
+  __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t, uint32_t qb2) {
+    return ClVec<bf16_t>::grad_bf(c, qb2);
+  }
+};
+
+template <typename T, int CL, int NCH, bool EXACT, int H, bool TRACE = false, bool BFC = false>
 __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArgs a) {
   static_assert(H >= 1 && H <= 8, "chunk groups per row");
   constexpr int EPV = ClVec<T>::EPV;
@@ -326,7 +344,7 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
           if (RL_PRESENT(j)) {
             if (live) {
               const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off);
-              const uint64_t nacc = ClVec<T>::exp_cache(v, k2, mn2, acc2, cache[j]);
+              const uint64_t nacc = CacheOps<T, BFC>::exp(v, k2, mn2, acc2, cache[j]);
               acc2 = RL_MINE(j) ? nacc : acc2;
             }
             sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
@@ -373,6 +391,7 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
         const float q = (st == 0.f || Rc == -INFINITY) ? 0.f : st * fast_exp2(Rc - kCacheShift - c2);
         q_last = q;
         const uint64_t q2 = f2pack(q, q);
+        const uint32_t qb2 = pack_bf16x2(q, q);
         const bool zero = q == 0.f;
         const bool live = has_next && Rg != -INFINITY;
         const uint64_t mn2 = f2pack(kCacheShift - Rg, kCacheShift - Rg);
@@ -381,11 +400,11 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
         for (int j = g * GS; j < (g + 1) * GS && j < NCH; ++j) {
           if (RL_PRESENT(j)) {
             if (RL_MINE(j) && (!TRACE || a.debug != 1))
-              st_stream_v4(out + j * kChunkVec, zero ? make_uint4(0, 0, 0, 0) : ClVec<T>::grad(cache[j], q2));
+              st_stream_v4(out + j * kChunkVec, zero ? make_uint4(0, 0, 0, 0) : CacheOps<T, BFC>::grad(cache[j], q2, qb2));
             if (has_next) {
               if (live && (!TRACE || a.debug != 2)) {
                 const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)kChunkBytes + my_off);
-                const uint64_t nacc = ClVec<T>::exp_cache(v, k2, mn2, acc2, cache[j]);
+                const uint64_t nacc = CacheOps<T, BFC>::exp(v, k2, mn2, acc2, cache[j]);
                 acc2 = RL_MINE(j) ? nacc : acc2;
               }
               sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
@@ -428,10 +447,11 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
   sm100::cluster_sync();  // no CTA leaves while a peer may still arrive on / write its smem
 }
 
-template <typename T, int CL, int NCH, bool EXACT = false, int H = 1, bool TRACE = false>
+template <typename T, int CL, int NCH, bool EXACT = false, int H = 1, bool TRACE = false,
+          bool BFC = std::is_same<T, bf16_t>::value>
 static rl_status launch_cl(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_ctas) {
   ClArgs a = a0;
-  auto kern = loss_cluster_kernel<T, CL, NCH, EXACT, H, TRACE>;
+  auto kern = loss_cluster_kernel<T, CL, NCH, EXACT, H, TRACE, BFC>;
   const size_t head = (sizeof(ClShared) + 127) & ~(size_t)127;
   int nslots = (int)((kSmemMax - head - 256) / (kChunkBytes + 16));
   const int nch = (int)((a.h_vec + kChunkVec - 1) / kChunkVec);
@@ -529,7 +549,10 @@ rl_status launch_loss_cluster(const void* logits, int32_t dtype, int64_t n, int6
   if (bf && nch2 == 20) {  // V = 151936: 4 chunk groups (RL_CLUSTER_GROUPS = 1, 2, 4, 5)
     static int groups = -1;
     if (groups < 0) groups = getenv("RL_CLUSTER_GROUPS") ? atoi(getenv("RL_CLUSTER_GROUPS")) : 1;
-    if (getenv("RL_TRACE")) return launch_cl<bf16_t, 2, 20, true, 1, true>(a, n, s, n_ctas);
+    if (getenv("RL_TRACE")) return launch_cl<bf16_t, 2, 20, true, 1, true, true>(a, n, s, n_ctas);
+    static int f16c = -1;  // RL_CACHE=fp16: fp16 row cache + fp32 multiply in pass C (comparison)
+    if (f16c < 0) f16c = (getenv("RL_CACHE") && strcmp(getenv("RL_CACHE"), "fp16") == 0) ? 1 : 0;
+    if (groups == 1 && f16c) return launch_cl<bf16_t, 2, 20, true, 1, false, false>(a, n, s, n_ctas);
     if (groups == 1) return launch_cl<bf16_t, 2, 20, true, 1>(a, n, s, n_ctas);
     if (groups == 2) return launch_cl<bf16_t, 2, 20, true, 2>(a, n, s, n_ctas);
     if (groups == 5) return launch_cl<bf16_t, 2, 20, true, 5>(a, n, s, n_ctas);

@@ -483,6 +483,7 @@ rl_status launch_loss_stream(const void* logits, int32_t dtype, int64_t n, int64
   a.nslots = 0;
   a.prefetch_chunks = 0;
   a.debug = 0;
+  a.inflight_cap = 0;
   a.h_vec = (a.nvec + 1) / 2;
   const int64_t c = (a.h_vec + kChunkVec - 1) / kChunkVec;
   const bool bf = dtype == RL_BF16;

@@ -40,6 +40,7 @@ constexpr int kWarps = 15, kThreads = kWarps * 32 + 32, kChunkVec = kWarps * 32,
 // Each CTA streams rows rowsPerCta apart (row = blockIdx.x + t * gridDim.x), columns [0, V) of bf16.
 // mode 0: consumers LDS + STG.cs ; mode 1: one thread issues a TMA bulk store of the chunk.
 __device__ int g_inflight_cap = 0;
+__device__ int g_pace = 0;
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) tma_copy(const char* in, char* out, int64_t nrows, int64_t row_bytes,
                                                         int nslots) {
@@ -96,7 +97,8 @@ __global__ void __launch_bounds__(kThreads, 1) tma_copy(const char* in, char* ou
     return;
   }
   uint32_t slot = 0, ph = 0;
-  if (MODE == 2) {  // whole row resident before it is processed (the loss kernel's pass A constraint)
+  if (MODE == 2 || MODE == 6) {  // whole row resident before it is processed (pass A constraint); 6: paced
+    const int pace = g_pace;  // ns of busy work per chunk in the copy-out (MODE 6)
     for (int64_t t = 0; t < my_rows; ++t) {
       uint32_t s2 = slot, p2 = ph;
       for (int j = 0; j < nch; ++j) {
@@ -116,6 +118,15 @@ __global__ void __launch_bounds__(kThreads, 1) tma_copy(const char* in, char* ou
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[slot])) : "memory");
         if (++slot == (uint32_t)nslots) { slot = 0; ph ^= 1; }
+        if (MODE == 6 && pace > 0) {
+          unsigned long long t0;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          for (;;) {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 >= (unsigned long long)pace) break;
+          }
+        }
       }
     }
     return;
@@ -184,6 +195,25 @@ int main(int argc, char** argv) {
         cudaEventElapsedTime(&ms, a, b);
         char nm[64];
         snprintf(nm, 64, "%s slots=%d cap=%d", m == 0 ? "tma_stg" : "burst", nslots, cap);
+        if (rep) report(nm, ms);
+      }
+    return 0;
+  }
+  if (!strcmp(mode, "paced")) {
+    for (int rep = 0; rep < 2; ++rep)
+      for (int pace : {0, 100, 200, 250, 300}) {
+        CK(cudaMemcpyToSymbol(g_pace, &pace, sizeof(int)));
+        const int nslots = 28;
+        const int smem = ((16 * nslots + 127) & ~127) + nslots * kChunkBytes;
+        CK(cudaFuncSetAttribute(tma_copy<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cudaEventRecord(a);
+        tma_copy<6><<<sms, kThreads, smem>>>(in, out, 2 * N, row_bytes / 2, nslots);
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        char nm[64];
+        snprintf(nm, 64, "burst paced %d ns/chunk", pace);
         if (rep) report(nm, ms);
       }
     return 0;
