@@ -4,6 +4,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "loss_common.cuh"
 #include "rowstats.cuh"
 #include "sm100.cuh"
@@ -42,6 +44,7 @@ struct ClArgs {
   int32_t prefetch_chunks;  // L2 lookahead in chunks beyond a full ring (RL_L2_PREFETCH_CHUNKS)
   int32_t debug;            // development only (RL_CLUSTER_DEBUG): 1 = no dlogits stores, 2 = no exp2
   int32_t inflight_cap;     // max chunk loads in flight per CTA (0 = ring-limited), RL_INFLIGHT_CAP
+  uint8_t* redo;            // SV kernel: per-row flag, 1 = row left to the two-pass fixup
 };
 
 // ------------------------------------------------------------------ packed fp32x2 helpers
@@ -145,6 +148,11 @@ struct ClVec<bf16_t> {
     c = make_uint4(o[0], o[1], o[2], o[3]);
     return acc;
   }
+  // single-visit kernel (policy_loss_sv.cu): bf16 cache of e' = 2^(x k - R + 15), R = target
+  __device__ static __forceinline__ uint64_t exp_sv(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc, uint4& c) {
+    return exp_cache_bf(v, k2, mn2, acc, c);
+  }
+  __device__ static __forceinline__ uint4 grad_sv(const uint4& c, uint32_t qb2, float) { return grad_bf(c, qb2); }
   __device__ static __forceinline__ uint4 grad_bf(const uint4& c, uint32_t qb2) {
     const __nv_bfloat162 q = *reinterpret_cast<const __nv_bfloat162*>(&qb2);
     uint4 o;
@@ -186,6 +194,29 @@ struct ClVec<float> {
     c.y = o[1];
     return acc;
   }
+  // single-visit kernel: fp32 cache (e' may exceed the fp16 range once R is not the max)
+  __device__ static __forceinline__ uint64_t exp_sv(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc, uint4& c) {
+    const uint64_t t0 = ffma2(f2pack(__uint_as_float(v.x), __uint_as_float(v.y)), k2, mn2);
+    const uint64_t t1 = ffma2(f2pack(__uint_as_float(v.z), __uint_as_float(v.w)), k2, mn2);
+    float a, b, d, e;
+    f2unpack(t0, a, b);
+    f2unpack(t1, d, e);
+    a = fast_exp2(a);
+    b = fast_exp2(b);
+    d = fast_exp2(d);
+    e = fast_exp2(e);
+    acc = fadd2(acc, f2pack(a, b));
+    acc = fadd2(acc, f2pack(d, e));
+    c = make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(d), __float_as_uint(e));
+    return acc;
+  }
+  __device__ static __forceinline__ uint4 grad_sv(const uint4& c, uint32_t, float q) {
+    const uint64_t q2 = f2pack(q, q);
+    float a, b, d, e;
+    f2unpack(fmul2(f2pack(__uint_as_float(c.x), __uint_as_float(c.y)), q2), a, b);
+    f2unpack(fmul2(f2pack(__uint_as_float(c.z), __uint_as_float(c.w)), q2), d, e);
+    return make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(d), __float_as_uint(e));
+  }
   __device__ static __forceinline__ uint4 grad(const uint4& c, uint64_t q2) {
     float a, b, d, e;
     f2unpack(fmul2(h2_to_f2(c.x), q2), a, b);
@@ -203,6 +234,16 @@ __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Compile-time loop: f(integral_constant<int, i>) for i in [B, E) — register-array indices and
+// phase boundaries stay static in the fully unrolled row loops.
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
 }
 
 // Ring position of the first chunk of a row (slot index + phase parity), advanced per row.

@@ -27,17 +27,18 @@ __global__ void __launch_bounds__(kL2Threads) loss_two_pass_kernel(
     const uint8_t* __restrict__ loss_mask, const int32_t* __restrict__ token_seq,
     const float* __restrict__ seq_adv, const int32_t* __restrict__ seq_version,
     const int32_t* __restrict__ seq_active, Knobs kn, void* dlogits, float* __restrict__ logp_out,
-    uint8_t* __restrict__ clipped_out, double* __restrict__ partials) {
+    uint8_t* __restrict__ clipped_out, double* __restrict__ partials, const uint8_t* __restrict__ only) {
   constexpr int EPV = VecTraits<T>::EPV;
   __shared__ float red[64];
   __shared__ float s_row[3];  // s_t, c2, (unused)
+  __shared__ uint32_t sel[kL2Threads / 32];
   const float k = kn.inv_t * RL_LOG2E;
   const uint64_t keep = policy_evict_last();
   const int64_t row_bytes = ld * elem_bytes<T>();
   const double inv_tm = token_mean_inv(kn);
   Acc acc;
   acc.zero();
-  for (int64_t row = blockIdx.x; row < n_tokens; row += gridDim.x) {
+  auto process = [&](int64_t row) {
     const char* rp = reinterpret_cast<const char*>(logits) + row * row_bytes;
     char* dp = reinterpret_cast<char*>(dlogits) + row * row_bytes;
     const RowMeta mt = row_meta(row, V, targets, loss_mask, token_seq, seq_version,
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(kL2Threads) loss_two_pass_kernel(
     if (s == 0.f) {
       for (int64_t i = threadIdx.x; i < nvec; i += kL2Threads) st_stream_v4(vout + i, make_uint4(0, 0, 0, 0));
       for (int64_t c = nvec * EPV + threadIdx.x; c < V; c += kL2Threads) VecTraits<T>::store1(dp, c, 0.f);
-      continue;
+      return;
     }
     const uint64_t drop = policy_evict_first();
     const int32_t y = mt.y;
@@ -86,6 +87,28 @@ __global__ void __launch_bounds__(kL2Threads) loss_two_pass_kernel(
       float v = s * fast_exp2(fmaf(VecTraits<T>::load1(rp, c), k, -c2));
       if (c == y) v -= s;
       VecTraits<T>::store1(dp, c, v);
+    }
+  };
+  if (!only) {
+    for (int64_t row = blockIdx.x; row < n_tokens; row += gridDim.x) process(row);
+  } else {
+    // fixup launch after the single-visit kernel: only the rows it flagged, found 512 candidate
+    // rows at a time by ballot and visited in ascending order (deterministic partial sums)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t base = 0; blockIdx.x + base * gridDim.x < n_tokens; base += kL2Threads) {
+      const int64_t cand = blockIdx.x + (base + threadIdx.x) * gridDim.x;
+      const uint32_t m = __ballot_sync(0xffffffffu, cand < n_tokens && only[cand] != 0);
+      if (lane == 0) sel[warp] = m;
+      __syncthreads();
+      for (int w = 0; w < kL2Threads / 32; ++w) {
+        uint32_t mw = sel[w];
+        while (mw) {
+          const int bit = __ffs(mw) - 1;
+          mw &= mw - 1;
+          process(blockIdx.x + (base + w * 32 + bit) * gridDim.x);
+        }
+      }
+      __syncthreads();  // sel reusable
     }
   }
   if (threadIdx.x == 0) {
@@ -129,17 +152,18 @@ rl_status launch_loss_two_pass(const void* logits, int32_t dtype, int64_t n, int
                                const int32_t* token_seq, const float* seq_adv,
                                const int32_t* seq_version, const int32_t* seq_active,
                                const Knobs& kn, void* dlogits, float* logp_out, uint8_t* clipped_out,
-                               double* partials, int* n_ctas, cudaStream_t s) {
-  const int grid = two_pass_grid(n);
+                               double* partials, int* n_ctas, cudaStream_t s, const uint8_t* only = nullptr) {
+  // fixup launch (only != NULL): a fixed small grid, scanned rows are rare
+  const int grid = only ? (int)std::min<int64_t>(n, 148) : two_pass_grid(n);
   *n_ctas = grid;
   if (dtype == RL_BF16)
     loss_two_pass_kernel<bf16_t><<<grid, kL2Threads, 0, s>>>(
         logits, n, V, ld, targets, old_logp, mask, token_seq, seq_adv, seq_version, seq_active, kn,
-        dlogits, logp_out, clipped_out, partials);
+        dlogits, logp_out, clipped_out, partials, only);
   else
     loss_two_pass_kernel<float><<<grid, kL2Threads, 0, s>>>(
         logits, n, V, ld, targets, old_logp, mask, token_seq, seq_adv, seq_version, seq_active, kn,
-        dlogits, logp_out, clipped_out, partials);
+        dlogits, logp_out, clipped_out, partials, only);
   return check_launch("loss_two_pass_kernel");
 }
 
@@ -159,14 +183,25 @@ rl_status launch_loss_stream(const void* logits, int32_t dtype, int64_t n, int64
                              const int32_t* seq_active, const Knobs& kn, void* dlogits, float* logp_out,
                              uint8_t* clipped_out, double* partials, int* n_ctas, cudaStream_t s);
 
-// Kernel choice: "cluster" (default), "stream" or "two_pass", overridable with RL_LOSS_KERNEL.
+// Single-visit cluster kernel (policy_loss_sv.cu); rows it flags in `redo` are left to a
+// two-pass fixup launch.
+rl_status launch_loss_sv(const void* logits, int32_t dtype, int64_t n, int64_t V, int64_t ld,
+                         const int32_t* targets, const float* old_logp, const uint8_t* mask,
+                         const int32_t* token_seq, const float* seq_adv, const int32_t* seq_version,
+                         const int32_t* seq_active, const Knobs& kn, void* dlogits, float* logp_out,
+                         uint8_t* clipped_out, double* partials, uint8_t* redo, int* n_ctas,
+                         cudaStream_t s);
+
+// Kernel choice: "sv" (default), "cluster", "stream" or "two_pass" (RL_LOSS_KERNEL).
+enum { K_SV = 0, K_TWO_PASS = 1, K_STREAM = 2, K_CLUSTER = 3 };
 static int loss_kernel_choice() {
   static int choice = -1;
   if (choice < 0) {
-    choice = 0;
+    choice = K_SV;
     if (const char* e = getenv("RL_LOSS_KERNEL")) {
-      if (strcmp(e, "two_pass") == 0) choice = 1;
-      if (strcmp(e, "stream") == 0) choice = 2;
+      if (strcmp(e, "two_pass") == 0) choice = K_TWO_PASS;
+      if (strcmp(e, "stream") == 0) choice = K_STREAM;
+      if (strcmp(e, "cluster") == 0) choice = K_CLUSTER;
     }
   }
   return choice;
@@ -174,9 +209,11 @@ static int loss_kernel_choice() {
 
 }  // namespace rl
 
+// per-CTA statistics partials (fast kernel + fixup) | per-row redo flags of the SV kernel
 extern "C" size_t rl_policy_loss_workspace_size(int64_t n_tokens, int64_t vocab, int32_t dtype) {
-  (void)n_tokens; (void)vocab; (void)dtype;
-  return (size_t)rl::kMaxStatCtas * RL_LOSS_STATS_N * sizeof(double);
+  (void)vocab; (void)dtype;
+  const size_t flags = n_tokens > 0 ? ((size_t)n_tokens + 255) & ~(size_t)255 : 0;
+  return (size_t)rl::kMaxStatCtas * RL_LOSS_STATS_N * sizeof(double) + flags;
 }
 
 extern "C" rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, int64_t n_tokens,
@@ -227,15 +264,35 @@ extern "C" rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, i
   double* partials = (double*)workspace;
   int n_ctas = 0;
   rl_status st = RL_ERR_UNSUPPORTED;
-  if (loss_kernel_choice() == 2)
+  const int choice = loss_kernel_choice();
+  const char* which = "two_pass";
+  if (choice == K_SV) {
+    uint8_t* redo = (uint8_t*)workspace + (size_t)kMaxStatCtas * RL_LOSS_STATS_N * sizeof(double);
+    st = launch_loss_sv(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask, token_seq,
+                        seq_adv, seq_version, seq_active, kn, dlogits, logp_out, clipped_out, partials,
+                        redo, &n_ctas, s);
+    if (st == RL_OK) {  // rows the fast path flagged: exact two-pass, own partial slots
+      which = "sv";
+      int n_fix = 0;
+      st = launch_loss_two_pass(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask, token_seq, seq_adv, seq_version,
+                                seq_active, kn, dlogits, logp_out, clipped_out,
+                                partials + (size_t)n_ctas * RL_LOSS_STATS_N, &n_fix, s, redo);
+      if (st != RL_OK) return st;
+      n_ctas += n_fix;
+    }
+  }
+  if (choice == K_STREAM) {
     st = launch_loss_stream(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
                             token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,
                             clipped_out, partials, &n_ctas, s);
-  if (loss_kernel_choice() == 0)
+    if (st == RL_OK) which = "stream";
+  }
+  if (choice == K_CLUSTER) {
     st = launch_loss_cluster(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
                              token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,
                              clipped_out, partials, &n_ctas, s);
-  const char* which = st == RL_OK ? (loss_kernel_choice() == 2 ? "stream" : "cluster") : "two_pass";
+    if (st == RL_OK) which = "cluster";
+  }
   if (st == RL_ERR_UNSUPPORTED)
     st = launch_loss_two_pass(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
                               token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,

@@ -94,8 +94,10 @@ def check_against_oracle(case, g, params, **adv_kw):
     y = case["targets"]
     V = case["vocab"]
     inr = (y >= 0) & (y < V)
-    assert np.all(np.abs(g["logp"][inr] - out["logp"][inr]) <= LOGP_ATOL), \
-        np.abs(g["logp"][inr] - out["logp"][inr]).max()
+    a, b = g["logp"][inr], out["logp"][inr]
+    same = (a == b) | (np.isnan(a) & np.isnan(b))          # -inf / NaN rows (special values)
+    with np.errstate(invalid="ignore"):
+        assert np.all(same | (np.abs(a - b) <= LOGP_ATOL)), np.abs(a - b)[~same].max()
     assert np.all(g["logp"][y < 0] == 0)
     assert np.all(np.isnan(g["logp"][y >= V]))
     # --- clip decisions: exact outside the tie band (Z23); inside, adopt the GPU's decision
@@ -286,6 +288,48 @@ def test_all_masked_batch_and_determinism(cuda_lib):
     b = run_gpu_chain(cuda_lib, case, {})
     assert a["stats"].tobytes() == b["stats"].tobytes()
     assert a["dlogits"].tobytes() == b["dlogits"].tobytes() and a["logp"].tobytes() == b["logp"].tobytes()
+
+
+def set_logits(case, row, cols, value):
+    """Overwrite logits[row, cols] in both the device input (bf16 bits / fp32) and the oracle's copy."""
+    v = np.float32(value)
+    if case["dtype"] == "bf16":
+        bits = synth.bf16_round_bits(np.array([v]))[0]
+        case["logits"][row, cols] = bits
+        case["x64"][row, cols] = oracle.decode_bf16(np.array([bits], dtype=np.uint16))[0]
+    else:
+        case["logits"][row, cols] = v
+        case["x64"][row, cols] = float(v)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_extreme_rows(cuda_lib, dtype):
+    """Rows far from the synthetic distribution: the single-visit kernel's exponent reference is
+    the target logit, so a target ~100 nats below the row max (or a -inf target, or inf / NaN
+    logits) takes the exact two-pass fixup; a 60-nat gap stays on the fast path (e' ~ 2^101)."""
+    case = small_case(vocab=5003, ld=5008, dtype=dtype, seed=21, mask_mode="all", ignore_frac=0.0,
+                      n_prompts=2, group=4, seq_len=16)
+    y = case["targets"]
+    adv = oracle_chain(case, oracle.LossParams())["adv"]
+    live = [s for s in range(len(adv)) if adv[s] != 0]          # sequences with a gradient
+    ra, rb, rc, rd = (live[i] * 16 + 3 for i in range(4))        # rows in distinct live sequences
+    other = lambda r: (int(y[r]) + 1 + 7 * r) % case["vocab"]  # a column that is not the target
+    set_logits(case, ra, y[ra], -40.0); set_logits(case, ra, other(ra), 60.0)  # gap 100: redo
+    set_logits(case, rb, y[rb], -20.0); set_logits(case, rb, other(rb), 40.0)  # gap 60: fast
+    rn, ri, rt = (s * 16 + 9 for s in range(3))
+    set_logits(case, rn, other(rn), np.nan); case["loss_mask"][rn] = 0         # NaN, masked
+    set_logits(case, ri, other(ri), np.inf); case["loss_mask"][ri] = 0         # +inf, masked
+    set_logits(case, rt, y[rt], -np.inf)                                       # -inf target
+    set_logits(case, rc, slice(None), -np.inf); set_logits(case, rc, y[rc], 1.5)  # one finite
+    set_logits(case, rd, slice(None), 3.0)                                      # constant row
+    lp, _ = oracle.token_logprob(case["x64"], y)
+    for r in (ra, rb, rc, rd):  # behaviour log-probs near the new values: unclipped gradients
+        case["old_logp"][r] = lp[r] + 0.01
+    g = run_gpu_chain(cuda_lib, case, {})
+    out = check_against_oracle(case, g, {})
+    assert np.isnan(g["logp"][rn]) and np.isnan(g["logp"][ri]) and g["logp"][rt] == -np.inf
+    assert abs(g["logp"][rc]) <= 1e-6 and abs(g["logp"][rd] + math.log(case["vocab"])) <= LOGP_ATOL
+    assert out["scale"][ra] != 0 and out["scale"][rb] != 0 and out["scale"][rc] != 0
 
 
 def test_rows_sum_to_zero_bf16(cuda_lib):

@@ -7,6 +7,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #define CK(x)                                                                 \
   do {                                                                        \
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1) tma_copy(const char* in, char* ou
     }
     return;
   }
+  uint32_t sink = 0;
   for (int64_t g = 0; g < total; ++g) {
     const int64_t t = g / nch;
     const int j = (int)(g - t * nch);
@@ -140,7 +142,14 @@ __global__ void __launch_bounds__(kThreads, 1) tma_copy(const char* in, char* ou
     while (!ok)
       asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
                    : "=r"(ok) : "r"(smem_u32(&full[slot])), "r"(ph) : "memory");
-    if (MODE == 0 || MODE >= 3) {
+    if (MODE == 7) {  // read only: fold the data into one word per thread
+      if ((uint32_t)tid * 16 < bytes) {
+        uint4 v = *reinterpret_cast<const uint4*>(ring + (size_t)slot * kChunkBytes + tid * 16);
+        sink ^= v.x ^ v.y ^ v.z ^ v.w;
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[slot])) : "memory");
+    } else if (MODE == 0 || MODE >= 3) {
       if ((uint32_t)tid * 16 < bytes) {
         uint4 v = *reinterpret_cast<const uint4*>(ring + (size_t)slot * kChunkBytes + tid * 16);
         if (MODE == 0 || MODE == 5)
@@ -163,6 +172,172 @@ __global__ void __launch_bounds__(kThreads, 1) tma_copy(const char* in, char* ou
     }
     if (++slot == (uint32_t)nslots) { slot = 0; ph ^= 1; }
   }
+  if (MODE == 7 && sink == 0x12345678u) out[tid] = 1;
+}
+
+// LDG read only: 4 independent 16-B loads in flight per thread, folded into one word.
+__global__ void ldg_read(const uint4* __restrict__ in, uint32_t* out, int64_t n) {
+  uint32_t sink = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x * 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int64_t j = i + (int64_t)u * gridDim.x * blockDim.x;
+      v[u] = make_uint4(0, 0, 0, 0);
+      if (j < n) asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w) : "l"(in + j));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sink ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+  }
+  if (sink == 0x12345678u) out[threadIdx.x] = 1;
+}
+
+// Per-thread cp.async (LDGSTS) ring: every consumer thread streams ITS OWN 16-B vectors of the
+// CTA's rows D chunks ahead into its own smem slots (no producer warp, no mbarriers); COPY =
+// also store them (st.global.cs), else read only.
+template <int D, bool COPY>
+__global__ void __launch_bounds__(kWarps * 32, 1) ldgsts_stream(const char* in, char* out, int64_t nrows, int64_t row_bytes) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int tid = threadIdx.x;
+  const int nch = (int)((row_bytes + kChunkBytes - 1) / kChunkBytes);
+  const int64_t my_rows = blockIdx.x < nrows ? (nrows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = my_rows * nch;
+  auto src = [&](int64_t g, uint32_t& ok) -> int64_t {
+    const int64_t t = g / nch;
+    const int j = (int)(g - t * nch);
+    const int64_t o = (int64_t)j * kChunkBytes + tid * 16;
+    ok = g < total && o < row_bytes;
+    return (blockIdx.x + t * gridDim.x) * row_bytes + o;
+  };
+  const uint32_t my = smem_u32(sm) + tid * 16;
+  for (int d = 0; d < D; ++d) {
+    uint32_t ok;
+    const int64_t o = src(d, ok);
+    if (ok) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(my + d * kChunkBytes), "l"(in + o) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  uint32_t sink = 0;
+  int slot = 0;
+  for (int64_t g = 0; g < total; ++g) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+    uint32_t ok;
+    const int64_t o = src(g, ok);
+    if (ok) {
+      uint4 v;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(my + slot * kChunkBytes));
+      if (COPY) asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(out + o), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+      else sink ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    uint32_t ok2;
+    const int64_t o2 = src(g + D, ok2);
+    if (ok2) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(my + slot * kChunkBytes), "l"(in + o2) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (++slot == D) slot = 0;
+  }
+  if (!COPY && sink == 0x12345678u) out[tid] = 1;
+}
+
+__global__ void fill_hash(uint32_t* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)i * 0x9E3779B9u ^ (uint32_t)(i >> 32);
+    x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+    p[i] = x & 0xBFFFBFFFu;  // finite bf16 pairs
+  }
+}
+
+// Row streams: each CTA reads whole rows (row = blockIdx.x + t * gridDim.x), U loads in flight
+// per thread — the access pattern of the token_logprob kernel.  STREAMS rows per CTA at a time
+// (interleaved) when STREAMS > 1.
+template <int THREADS, int U, int STREAMS>
+__global__ void __launch_bounds__(THREADS) ldg_rows(const char* in, uint32_t* out, int64_t nrows, int64_t row_bytes) {
+  uint32_t sink = 0;
+  const int64_t nvec = row_bytes / 16;
+  for (int64_t r0 = blockIdx.x * STREAMS; r0 < nrows; r0 += (int64_t)gridDim.x * STREAMS) {
+    for (int64_t i = threadIdx.x; i < nvec; i += (int64_t)U * THREADS) {
+      uint4 v[STREAMS][U];
+#pragma unroll
+      for (int st = 0; st < STREAMS; ++st)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t j = i + u * THREADS;
+          v[st][u] = make_uint4(0, 0, 0, 0);
+          if (j < nvec && r0 + st < nrows)
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v[st][u].x), "=r"(v[st][u].y), "=r"(v[st][u].z), "=r"(v[st][u].w) : "l"(in + (r0 + st) * row_bytes + j * 16));
+        }
+#pragma unroll
+      for (int st = 0; st < STREAMS; ++st)
+#pragma unroll
+        for (int u = 0; u < U; ++u) sink ^= v[st][u].x ^ v[st][u].y ^ v[st][u].z ^ v[st][u].w;
+    }
+  }
+  if (sink == 0x12345678u) out[threadIdx.x] = 1;
+}
+
+// TMA read (COPY: + STG) with VPT 16-B vectors per consumer thread per slot, i.e. one bulk copy
+// of VPT * 7.5 KB per slot: does a larger bulk transfer raise the per-SM TMA read rate?
+template <int VPT, bool COPY>
+__global__ void __launch_bounds__(kThreads, 1) tma_sz(const char* in, char* out, int64_t nrows, int64_t row_bytes, int nslots) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  constexpr int SB = VPT * kChunkBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + nslots;
+  unsigned char* ring = sm + ((16 * nslots + 127) & ~127);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nch = (int)((row_bytes + SB - 1) / SB);
+  if (tid == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[i])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[i])), "r"(kWarps));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t my_rows = blockIdx.x < nrows ? (nrows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = my_rows * nch;
+  if (warp == kWarps) {
+    if (lane == 0) {
+      uint32_t slot = 0, ph = 0;
+      for (int64_t g = 0; g < total; ++g) {
+        uint32_t ok = 0;
+        while (!ok)
+          asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                       : "=r"(ok) : "r"(smem_u32(&empty[slot])), "r"(ph ^ 1) : "memory");
+        const int64_t t = g / nch;
+        const int j = (int)(g - t * nch);
+        const int64_t off = (blockIdx.x + t * gridDim.x) * row_bytes + (int64_t)j * SB;
+        const uint32_t bytes = (uint32_t)min((int64_t)SB, row_bytes - (int64_t)j * SB);
+        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[slot])), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(ring + (size_t)slot * SB)), "l"(in + off), "r"(bytes), "r"(smem_u32(&full[slot])) : "memory");
+        if (++slot == (uint32_t)nslots) { slot = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+  uint32_t slot = 0, ph = 0, sink = 0;
+  for (int64_t g = 0; g < total; ++g) {
+    const int64_t t = g / nch;
+    const int j = (int)(g - t * nch);
+    const int64_t off = (blockIdx.x + t * gridDim.x) * row_bytes + (int64_t)j * SB;
+    const uint32_t bytes = (uint32_t)min((int64_t)SB, row_bytes - (int64_t)j * SB);
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                   : "=r"(ok) : "r"(smem_u32(&full[slot])), "r"(ph) : "memory");
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const uint32_t o = (uint32_t)(u * kChunkVec + tid) * 16;
+      if (o < bytes) {
+        uint4 v = *reinterpret_cast<const uint4*>(ring + (size_t)slot * SB + o);
+        if (COPY) asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(out + off + o), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+        else sink ^= v.x ^ v.y ^ v.z ^ v.w;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[slot])) : "memory");
+    if (++slot == (uint32_t)nslots) { slot = 0; ph ^= 1; }
+  }
+  if (!COPY && sink == 0x12345678u) out[tid] = 1;
 }
 
 int main(int argc, char** argv) {
@@ -172,7 +347,9 @@ int main(int argc, char** argv) {
   char *in, *out;
   CK(cudaMalloc(&in, bytes));
   CK(cudaMalloc(&out, bytes));
-  CK(cudaMemset(in, 1, bytes));
+  if (getenv("PROBE_MEMSET")) CK(cudaMemset(in, 1, bytes));
+  else fill_hash<<<1184, 256>>>((uint32_t*)in, (int64_t)(bytes / 4));
+  CK(cudaDeviceSynchronize());
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -197,6 +374,137 @@ int main(int argc, char** argv) {
         snprintf(nm, 64, "%s slots=%d cap=%d", m == 0 ? "tma_stg" : "burst", nslots, cap);
         if (rep) report(nm, ms);
       }
+    return 0;
+  }
+  if (!strcmp(mode, "read")) {
+    auto rreport = [&](const char* name, float ms, double mult) { printf("%-28s %8.3f ms  %8.1f GB/s (%s)\n", name, ms, mult * bytes / ms / 1e6, mult > 1 ? "R+W" : "read"); };
+    for (int rep = 0; rep < 2; ++rep) {
+      float ms;
+      for (int per : {2, 4}) {
+        cudaEventRecord(a);
+        ldg_read<<<sms * per, 512>>>((const uint4*)in, (uint32_t*)out, (int64_t)(bytes / 16));
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        cudaEventElapsedTime(&ms, a, b);
+        char nm[64];
+        snprintf(nm, 64, "ldg read %d CTA/SM", per);
+        if (rep) rreport(nm, ms, 1);
+      }
+      for (int nslots : {10, 28}) {
+        const int smem = ((16 * nslots + 127) & ~127) + nslots * kChunkBytes;
+        CK(cudaFuncSetAttribute(tma_copy<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cudaEventRecord(a);
+        tma_copy<7><<<sms, kThreads, smem>>>(in, out, N, row_bytes, nslots);
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        cudaEventElapsedTime(&ms, a, b);
+        char nm[64];
+        snprintf(nm, 64, "tma read nslots=%d", nslots);
+        if (rep) rreport(nm, ms, 1);
+        CK(cudaFuncSetAttribute(tma_copy<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cudaEventRecord(a);
+        tma_copy<0><<<sms, kThreads, smem>>>(in, out, N, row_bytes, nslots);
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        cudaEventElapsedTime(&ms, a, b);
+        snprintf(nm, 64, "tma copy nslots=%d", nslots);
+        if (rep) rreport(nm, ms, 2);
+      }
+#define LDGSTS_RUN(D)                                                                                     \
+      {                                                                                                   \
+        const int smem = (D) * kChunkBytes;                                                               \
+        CK(cudaFuncSetAttribute(ldgsts_stream<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+        CK(cudaFuncSetAttribute(ldgsts_stream<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));  \
+        cudaEventRecord(a);                                                                               \
+        ldgsts_stream<D, false><<<sms, kWarps * 32, smem>>>(in, out, N, row_bytes);                       \
+        cudaEventRecord(b);                                                                               \
+        CK(cudaEventSynchronize(b));                                                                      \
+        CK(cudaGetLastError());                                                                           \
+        cudaEventElapsedTime(&ms, a, b);                                                                  \
+        char nm[64];                                                                                      \
+        snprintf(nm, 64, "ldgsts read D=%d", D);                                                          \
+        if (rep) rreport(nm, ms, 1);                                                                      \
+        cudaEventRecord(a);                                                                               \
+        ldgsts_stream<D, true><<<sms, kWarps * 32, smem>>>(in, out, N, row_bytes);                        \
+        cudaEventRecord(b);                                                                               \
+        CK(cudaEventSynchronize(b));                                                                      \
+        cudaEventElapsedTime(&ms, a, b);                                                                  \
+        snprintf(nm, 64, "ldgsts copy D=%d", D);                                                          \
+        if (rep) rreport(nm, ms, 2);                                                                      \
+      }
+      LDGSTS_RUN(4) LDGSTS_RUN(8) LDGSTS_RUN(16) LDGSTS_RUN(28)
+#define ROWS_RUN(TH, U, ST, PER)                                                           \
+      {                                                                                    \
+        cudaEventRecord(a);                                                                \
+        ldg_rows<TH, U, ST><<<sms * PER, TH>>>(in, (uint32_t*)out, N, row_bytes);          \
+        cudaEventRecord(b);                                                                \
+        CK(cudaEventSynchronize(b));                                                       \
+        CK(cudaGetLastError());                                                            \
+        cudaEventElapsedTime(&ms, a, b);                                                   \
+        char nm[64];                                                                       \
+        snprintf(nm, 64, "rows th=%d U=%d st=%d x%d/SM", TH, U, ST, PER);                   \
+        if (rep) rreport(nm, ms, 1);                                                       \
+      }
+      ROWS_RUN(256, 4, 1, 8) ROWS_RUN(256, 4, 1, 4) ROWS_RUN(256, 4, 1, 1) ROWS_RUN(512, 4, 1, 1)
+      ROWS_RUN(512, 8, 1, 1) ROWS_RUN(512, 2, 4, 1) ROWS_RUN(512, 4, 2, 1) ROWS_RUN(256, 4, 1, 2)
+    }
+    return 0;
+  }
+  if (!strcmp(mode, "cluster")) {  // the same TMA copy, plain vs cluster launches
+    for (int rep = 0; rep < 2; ++rep)
+      for (int cl : {1, 2, 4})
+        for (int half : {0, 1}) {
+          const int nslots = 10;
+          const int smem = ((16 * nslots + 127) & ~127) + nslots * kChunkBytes;
+          CK(cudaFuncSetAttribute(tma_copy<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          if (cl > 1) CK(cudaFuncSetAttribute(tma_copy<0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+          cudaLaunchConfig_t cfg = {};
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = cl;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.gridDim = dim3(sms / cl * cl);
+          if (cl == 4) cfg.gridDim = dim3(132);
+          cfg.blockDim = dim3(kThreads);
+          cfg.dynamicSmemBytes = smem;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          cudaEventRecord(a);
+          if (half) CK(cudaLaunchKernelEx(&cfg, tma_copy<0>, (const char*)in, out, 2 * N, row_bytes / 2, nslots));
+          else CK(cudaLaunchKernelEx(&cfg, tma_copy<0>, (const char*)in, out, N, row_bytes, nslots));
+          cudaEventRecord(b);
+          CK(cudaEventSynchronize(b));
+          float ms;
+          cudaEventElapsedTime(&ms, a, b);
+          char nm[64];
+          snprintf(nm, 64, "tma copy cluster=%d %s grid=%d", cl, half ? "half-rows" : "rows", cfg.gridDim.x);
+          if (rep) report(nm, ms);
+        }
+    return 0;
+  }
+  if (!strcmp(mode, "tmasize")) {
+    auto rreport = [&](const char* name, float ms, double mult) { printf("%-28s %8.3f ms  %8.1f GB/s (%s)\n", name, ms, mult * bytes / ms / 1e6, mult > 1 ? "R+W" : "read"); };
+#define SZ_RUN(VPT, COPY, NS)                                                                      \
+    {                                                                                            \
+      const int smem = ((16 * (NS) + 127) & ~127) + (NS) * (VPT) * kChunkBytes;                  \
+      CK(cudaFuncSetAttribute(tma_sz<VPT, COPY>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+      cudaEventRecord(a);                                                                        \
+      tma_sz<VPT, COPY><<<sms, kThreads, smem>>>(in, out, N, row_bytes, NS);                     \
+      cudaEventRecord(b);                                                                        \
+      CK(cudaEventSynchronize(b));                                                               \
+      CK(cudaGetLastError());                                                                    \
+      float ms;                                                                                  \
+      cudaEventElapsedTime(&ms, a, b);                                                           \
+      char nm[64];                                                                               \
+      snprintf(nm, 64, "tma %s %dKB x %d slots", COPY ? "copy" : "read", (VPT) * 15 / 2, NS);    \
+      if (rep) rreport(nm, ms, COPY ? 2 : 1);                                                    \
+    }
+    for (int rep = 0; rep < 2; ++rep) {
+      SZ_RUN(1, false, 10) SZ_RUN(1, false, 28) SZ_RUN(2, false, 6) SZ_RUN(2, false, 14) SZ_RUN(4, false, 3)
+      SZ_RUN(4, false, 7) SZ_RUN(8, false, 3) SZ_RUN(1, true, 10) SZ_RUN(2, true, 6) SZ_RUN(4, true, 3)
+      SZ_RUN(4, true, 7) SZ_RUN(8, true, 3)
+    }
     return 0;
   }
   if (!strcmp(mode, "paced")) {

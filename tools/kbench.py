@@ -52,7 +52,7 @@ def main():
     t, avg = timeit(lambda: rl.token_logprob(x, y, logp))
     print(f"token_logprob   : {t:8.3f} ms  {nbytes / t / 1e6:8.1f} GB/s read (avg {avg:.3f})")
     p = rl.LossParams(agg=rl.AGG_SUM)
-    kern = os.environ.get("RL_LOSS_KERNEL", "cluster")  # latched by the library on first use
+    kern = os.environ.get("RL_LOSS_KERNEL", "sv")  # latched by the library on first use
     t, avg = timeit(lambda: rl.policy_loss_fwd_bwd(x, y, old, tseq, adv, p, dl, stats, ws, logp_out=logp))
     print(f"loss ({kern:8s}): {t:8.3f} ms  {2 * nbytes / t / 1e6:8.1f} GB/s R+W (avg {avg:.3f})")
     t, avg = timeit(lambda: rl.policy_loss_fwd_bwd(x, y, old, tseq, adv, p, x, stats, ws, logp_out=logp))

@@ -1,5 +1,5 @@
-"""Phase timeline of the cluster loss kernel (RL_TRACE=1; development tool).
-    RL_TRACE=1 python tools/trace_cluster.py [--rows 131072]"""
+"""Phase timeline of the cluster loss kernels (RL_TRACE=1; development tool).
+    RL_TRACE=1 [RL_LOSS_KERNEL=cluster] python tools/trace_cluster.py [--rows 131072]"""
 import ctypes
 import os
 import sys
@@ -31,23 +31,41 @@ def main():
         rl.policy_loss_fwd_bwd(x, y, old, tseq, adv, p, dl, stats, ws)
     torch.cuda.synchronize()
     buf = np.zeros((256, 64, 8), dtype=np.uint64)
-    lib.rl_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-    assert lib.rl_debug_trace(buf.ctypes.data, buf.nbytes) == 0
+    sv = os.environ.get("RL_LOSS_KERNEL", "sv") == "sv"
+    fn = lib.rl_debug_trace_sv if sv else lib.rl_debug_trace
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    assert fn(buf.ctypes.data, buf.nbytes) == 0
     b = buf[:148].astype(np.float64)
     rows = slice(8, 60)
     d = lambda i, j: (b[:, rows, j] - b[:, rows, i])
     per_row = (b[:, 9:61, 0] - b[:, 8:60, 0])
     print(f"row period (consumer T0->T0 next)  : {np.median(per_row):8.0f} ns  (p10 {np.percentile(per_row,10):.0f}, p90 {np.percentile(per_row,90):.0f})")
-    for name, i, j in [("passA(next) T0->T1", 0, 1), ("scale wait T1->T2", 1, 2), ("fused C+B T2->T3", 2, 3),
-                       ("epi: wait sumbar E4->E5", 4, 5), ("epi: peer wait E5->E6", 5, 6), ("epi: compute E6->E7", 6, 7)]:
+    if sv:
+        phases = [("pub wait T0->T1", 0, 1), ("chunk loop T1->T2", 1, 2), ("epi: fetch->sums E3->E4", 3, 4),
+                  ("epi: peer wait E4->E5", 4, 5), ("epi: compute+publish E5->E6", 5, 6)]
+    else:
+        phases = [("passA(next) T0->T1", 0, 1), ("scale wait T1->T2", 1, 2), ("fused C+B T2->T3", 2, 3),
+                  ("epi: wait sumbar E4->E5", 4, 5), ("epi: peer wait E5->E6", 5, 6), ("epi: compute E6->E7", 6, 7)]
+    for name, i, j in phases:
         v = d(i, j)
         print(f"{name:36s}: {np.median(v):8.0f} ns  (p10 {np.percentile(v,10):.0f}, p90 {np.percentile(v,90):.0f})")
+    if sv:
+        v = b[:, rows, 4] - b[:, rows, 2]
+        print(f"{'loop done -> epi sees sums':36s}: {np.median(v):8.0f} ns")
+        v = b[:, 9:61, 1] - b[:, 8:60, 6]
+        print(f"{'publish -> consumer past wait':36s}: {np.median(v):8.0f} ns")
+        v = b[:, rows, 4] - b[:, rows, 3]
+        print(f"{'epi idle before sums':36s}: {np.median(v):8.0f} ns")
+        v = b[:, rows, 1] - b[:, rows, 7]
+        print(f"{'chunk 0 issued -> loop start':36s}: {np.median(v):8.0f} ns  (p10 {np.percentile(v,10):.0f}, p90 {np.percentile(v,90):.0f})")
+        v = b[:, 9:61, 7] - b[:, 8:60, 7]
+        print(f"{'producer row period':36s}: {np.median(v):8.0f} ns")
+        return
     # sumbar completes at E5: relative to the consumer's T3 of the previous row (send_sum)
     v = b[:, 9:61, 5] - b[:, 8:60, 3]
     print(f"{'send(i) -> epi sees sums':36s}: {np.median(v):8.0f} ns")
     v = b[:, 9:61, 2] - b[:, 9:61, 7]
     print(f"{'publish(i) -> consumer past scale':36s}: {np.median(v):8.0f} ns")
-
 
 if __name__ == "__main__":
     main()
