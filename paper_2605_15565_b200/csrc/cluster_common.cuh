@@ -1,4 +1,4 @@
-// Shared pieces of the row-resident loss kernels (policy_loss_cluster.cu, policy_loss_stream.cu):
+// Shared pieces of the cluster loss kernels (policy_loss_sv.cu, policy_loss_cluster.cu):
 // launch geometry, kernel arguments, packed fp32x2 / fp16 / bf16 helpers, per-vector math.
 #pragma once
 #include <cuda_bf16.h>
@@ -42,8 +42,7 @@ struct ClArgs {
   Knobs kn;
   int32_t nslots;
   int32_t prefetch_chunks;  // L2 lookahead in chunks beyond a full ring (RL_L2_PREFETCH_CHUNKS)
-  int32_t debug;            // development only (RL_CLUSTER_DEBUG): 1 = no dlogits stores, 2 = no exp2
-  int32_t inflight_cap;     // max chunk loads in flight per CTA (0 = ring-limited), RL_INFLIGHT_CAP
+  int32_t debug;            // development only (RL_CLUSTER_DEBUG / RL_SV_DEBUG timing experiments)
   uint8_t* redo;            // SV kernel: per-row flag, 1 = row left to the two-pass fixup
 };
 

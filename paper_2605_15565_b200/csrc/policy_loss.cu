@@ -176,13 +176,6 @@ rl_status launch_loss_cluster(const void* logits, int32_t dtype, int64_t n, int6
                               const Knobs& kn, void* dlogits, float* logp_out, uint8_t* clipped_out,
                               double* partials, int* n_ctas, cudaStream_t s);
 
-// Streaming two-cache variant (policy_loss_stream.cu); same contract as launch_loss_cluster.
-rl_status launch_loss_stream(const void* logits, int32_t dtype, int64_t n, int64_t V, int64_t ld,
-                             const int32_t* targets, const float* old_logp, const uint8_t* mask,
-                             const int32_t* token_seq, const float* seq_adv, const int32_t* seq_version,
-                             const int32_t* seq_active, const Knobs& kn, void* dlogits, float* logp_out,
-                             uint8_t* clipped_out, double* partials, int* n_ctas, cudaStream_t s);
-
 // Single-visit cluster kernel (policy_loss_sv.cu); rows it flags in `redo` are left to a
 // two-pass fixup launch.
 rl_status launch_loss_sv(const void* logits, int32_t dtype, int64_t n, int64_t V, int64_t ld,
@@ -192,15 +185,14 @@ rl_status launch_loss_sv(const void* logits, int32_t dtype, int64_t n, int64_t V
                          uint8_t* clipped_out, double* partials, uint8_t* redo, int* n_ctas,
                          cudaStream_t s);
 
-// Kernel choice: "sv" (default), "cluster", "stream" or "two_pass" (RL_LOSS_KERNEL).
-enum { K_SV = 0, K_TWO_PASS = 1, K_STREAM = 2, K_CLUSTER = 3 };
+// Kernel choice: "sv" (default), "cluster" or "two_pass" (RL_LOSS_KERNEL).
+enum { K_SV = 0, K_TWO_PASS = 1, K_CLUSTER = 3 };
 static int loss_kernel_choice() {
   static int choice = -1;
   if (choice < 0) {
     choice = K_SV;
     if (const char* e = getenv("RL_LOSS_KERNEL")) {
       if (strcmp(e, "two_pass") == 0) choice = K_TWO_PASS;
-      if (strcmp(e, "stream") == 0) choice = K_STREAM;
       if (strcmp(e, "cluster") == 0) choice = K_CLUSTER;
     }
   }
@@ -280,12 +272,6 @@ extern "C" rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, i
       if (st != RL_OK) return st;
       n_ctas += n_fix;
     }
-  }
-  if (choice == K_STREAM) {
-    st = launch_loss_stream(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
-                            token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,
-                            clipped_out, partials, &n_ctas, s);
-    if (st == RL_OK) which = "stream";
   }
   if (choice == K_CLUSTER) {
     st = launch_loss_cluster(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,

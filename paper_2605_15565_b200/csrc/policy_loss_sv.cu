@@ -21,7 +21,10 @@
 //     dlogits_v = (s_t / S') e'_v  (bf16 x bf16 HMUL2),  target column s_t (p_y - 1).
 //
 // Per CTA: warps 0..14 consume; warp 15 lane 0 issues the TMA bulk copies of this CTA's column
-// slice into a ring of 7.5 KB smem slots (mbarrier full/empty); lane 1 is the row epilogue.
+// slice into a ring of smem slots (mbarrier full/empty); lane 1 is the row epilogue.  A slot
+// holds VPT x 7.5 KB (VPT 16-B vectors per consumer thread; default 4 -> 30 KB, 7 slots): the
+// copy probe (tools/copy_probe.cu) reads 3.6-4.5 TB/s from 7.5 KB bulk copies but
+// 7.5 TB/s from 15-30 KB ones, so the copy size, not the ring depth, bounds the read side.
 // Consumer iteration p: wait publication p (reference of row p, grad scale of row p-1), then one
 // loop over the chunks: store dlogits chunk j of row p-1 from cache[j], refill cache[j] with
 // row p's chunk j as it lands.  The epilogue meanwhile prefetches row p+1's metadata, waits for
@@ -328,387 +331,6 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
   sm100::cluster_sync();  // no CTA leaves while a peer may still arrive on / write its smem
 }
 
-// ----------------------------------------------------------------------------------------------
-// SVX: the single-visit kernel with the cross-CTA exchange hidden.  In SV every row ends with a
-// cluster-wide sync (sums -> peer -> scale, ~2 us of 8) during which the consumers idle.  SVX
-// double-buffers the e' cache — row p in registers, row p+1 in shared memory, alternating — so
-// the dlogits pass C(p-1) can lag the exp pass S(p):
-//   phase 1: S(p) chunks [0, K)                 (row p-1's exchange in flight)
-//   phase 2: S(p) chunks [K, NCH) + C(p-1) chunks [0, NCH-K)   -> row p's sums sent
-//   phase 3: C(p-1) chunks [NCH-K, NCH)         (row p's exchange in flight)
-// The shared-memory cache (NCH x 7.5 KB) leaves ~10 TMA ring slots, enough read slack once
-// nothing waits on the exchange.  Row references are published two rows ahead, separately from
-// the row scales.
-struct __align__(16) SvxShared {
-  float4 xch[2][8];     // [row parity][cluster rank]: (S'_c, -, -, -)
-  float red_sum[2][kNcw];
-  float4 ref[2];        // row p: (15 - R_p, need_p, -, -)
-  float4 sc[2];         // row p: (q, dy, target column or -1, mode)
-  uint32_t scb[2];      // row p: q as bf16x2
-  uint64_t xbar[2], sumbar[2], refbar[2], scbar[2];
-};
-
-template <typename T, int CL, int NCH, bool EXACT, int K, bool TRACE = false, int VPT = 1>
-__global__ void __launch_bounds__(kSvThreads, 1) loss_svx_kernel(const ClArgs a) {
-  static_assert(K >= 1 && K < NCH, "phase split");
-  constexpr int EPV = ClVec<T>::EPV;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  SvxShared& sh = *reinterpret_cast<SvxShared*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + sizeof(SvxShared));
-  uint64_t* empty = full + a.nslots;
-  const size_t ring_off = (sizeof(SvxShared) + 2 * sizeof(uint64_t) * a.nslots + 127) & ~(size_t)127;
-  const int nslots = a.nslots;
-  const uint32_t full_s = sm100::smem_u32(full), empty_s = sm100::smem_u32(empty);
-  uint4* ring = reinterpret_cast<uint4*>(smem_raw + ring_off);
-  const uint32_t ring_s = sm100::smem_u32(ring);
-  const uint32_t cache_s = ring_s + (uint32_t)nslots * (VPT * kChunkBytes);  // [NCH][kCons] uint4
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const uint32_t crank = sm100::cluster_ctarank();
-  const int64_t cid = sm100::cluster_id_x();
-  const int64_t ncl = sm100::nclusters_x();
-  const int64_t v0 = (int64_t)crank * a.h_vec;
-  const int64_t v1 = min(a.nvec, v0 + a.h_vec);
-  const int my_nv = (int)max((int64_t)0, v1 - v0);
-  const int nfull = my_nv / kChunkVec;
-  const int last_nv = my_nv - nfull * kChunkVec;
-  const int nch = nfull + (last_nv > 0);
-  const bool tail_owner = crank == CL - 1;
-  const int n_tail = (int)(a.V - a.nvec * EPV);
-  const int64_t row_bytes = a.ld * elem_bytes<T>();
-  const bool skip_masked = (a.kn.flags & RL_F_SKIP_MASKED_READS) != 0;
-  const float k = a.kn.inv_t * RL_LOG2E;
-
-  if (tid == 0) {
-    for (int i = 0; i < nslots; ++i) {
-      sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&empty[i], kNcw);
-    }
-    for (int i = 0; i < 2; ++i) {
-      sm100::mbar_init(&sh.xbar[i], CL - 1);
-      sm100::mbar_init(&sh.sumbar[i], kNcw);
-      sm100::mbar_init(&sh.refbar[i], 1);
-      sm100::mbar_init(&sh.scbar[i], 1);
-    }
-    sm100::fence_mbar_init();
-  }
-  sm100::cluster_sync();
-
-  if (warp == kNcw) {
-    if (lane == 0 && nch > 0) {
-      // ---------------------------------------------------------- TMA producer (lane 0)
-      auto need_of = [&](int64_t row) -> bool {
-        const RowMeta mt = row_meta(row, a.V, a.targets, a.mask, a.token_seq, a.seq_version,
-                                    a.kn.trainer_version, a.kn.max_staleness);
-        return mt.in_range && !(skip_masked && !mt.valid);
-      };
-      RingPos rp{0, 0};
-      bool need = cid < a.n_tokens && need_of(cid);
-      uint32_t pp = 0;
-      for (int64_t row = cid; row < a.n_tokens; row += ncl, ++pp) {
-        const int64_t nx = row + ncl;
-        const int32_t y_nx = nx < a.n_tokens ? a.targets[nx] : -1;
-        if (need) {
-          const char* src = reinterpret_cast<const char*>(a.logits) + row * row_bytes + v0 * 16;
-          for (int c = 0; c * VPT < nch; ++c) {  // one bulk copy of VPT x 7.5 KB per ring slot
-            sm100::mbar_wait_a(empty_s + rp.slot * 8, rp.phase ^ 1);
-            if (c == 0) RL_SV_EV(pp, 7);
-            const uint32_t bytes = (uint32_t)min(VPT * kChunkVec, my_nv - c * VPT * kChunkVec) * 16u;
-            sm100::mbar_arrive_expect_tx(&full[rp.slot], bytes);
-            sm100::bulk_g2s_nohint(ring + (size_t)rp.slot * (VPT * kChunkVec), src + (size_t)c * VPT * kChunkBytes,
-                                   bytes, &full[rp.slot]);
-            rp.advance(1, nslots);
-          }
-        }
-        need = nx < a.n_tokens && (skip_masked ? need_of(nx) : (y_nx >= 0 && (int64_t)y_nx < a.V));
-      }
-    } else if (lane == 1) {
-      // ---------------------------------------------------------- row epilogue (lane 1)
-      const double inv_tm = token_mean_inv(a.kn);
-      Acc acc;
-      acc.zero();
-      struct Pre {
-        RowMeta mt;
-        float xk, A, old;
-        bool need, owned;
-      };
-      auto fetch = [&](int64_t row) {
-        Pre r;
-        r.mt = row_meta(row, a.V, a.targets, a.mask, a.token_seq, a.seq_version, a.kn.trainer_version,
-                        a.kn.max_staleness);
-        r.need = r.mt.in_range && !(skip_masked && !r.mt.valid);
-        r.xk = 0.f;
-        r.owned = false;
-        if (r.need) {
-          r.xk = VecTraits<T>::load1(reinterpret_cast<const char*>(a.logits) + row * row_bytes, r.mt.y) * k;
-          const int64_t vy = r.mt.y / EPV;
-          r.owned = (vy >= v0 && vy < v1) || (tail_owner && vy >= a.nvec);
-        }
-        r.A = r.mt.valid ? a.seq_adv[r.mt.seq] : 0.f;
-        r.old = r.mt.valid ? a.old_logp[row] : 0.f;
-        return r;
-      };
-      auto publish_ref = [&](uint32_t p, const Pre& r) {
-        sh.ref[p & 1] = make_float4(kCacheShift - r.xk, r.need ? 1.f : 0.f, 0.f, 0.f);
-        sm100::mbar_arrive(&sh.refbar[p & 1]);
-      };
-      if (cid < a.n_tokens) {
-        Pre cur = fetch(cid), nxt;
-        publish_ref(0, cur);
-        if (cid + ncl < a.n_tokens) {
-          nxt = fetch(cid + ncl);
-          publish_ref(1, nxt);
-        }
-        uint32_t p = 0;
-        for (int64_t row = cid; row < a.n_tokens; row += ncl, ++p) {
-          const uint32_t b = p & 1, ph = (p >> 1) & 1;
-          RL_SV_EV(p, 3);
-          sm100::mbar_wait_polite(&sh.sumbar[b], ph, false);
-          RL_SV_EV(p, 4);
-          float s = 0.f;
-#pragma unroll
-          for (int w = 0; w < kNcw; ++w) s += sh.red_sum[b][w];
-          const float4 rec = make_float4(s, 0.f, 0.f, 0.f);
-          sh.xch[b][crank] = rec;
-#pragma unroll
-          for (int r = 0; r < CL; ++r)
-            if (r != (int)crank) {
-              sm100::st_remote_v4(&sh.xch[b][crank], r, rec.x, rec.y, rec.z, rec.w);
-              sm100::mbar_arrive_remote(&sh.xbar[b], r);
-            }
-          if (CL > 1) sm100::mbar_wait_polite(&sh.xbar[b], ph, true);
-          RL_SV_EV(p, 5);
-          float S = 0.f;
-#pragma unroll
-          for (int r = 0; r < CL; ++r) S += sh.xch[b][r].x;
-          const RowMeta& mt = cur.mt;
-          const bool redo = cur.need && !(S < kSvRedo);
-          uint32_t mode = SV_NONE;
-          float q = 0.f, dy = 0.f;
-          if (!redo) {
-            float lp;
-            if (cur.need) lp = (kCacheShift - fast_log2(S)) * RL_LN2;
-            else lp = mt.in_range ? 0.f : logp_from(mt, 0.f, 0.f);
-            uint8_t cl = 0;
-            Acc tmp;
-            tmp.zero();
-            const float st = token_epilogue(mt, lp, cur.old, cur.A, a.seq_active, inv_tm, a.kn, tmp, &cl);
-            if (crank == 0) {
-#pragma unroll
-              for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
-              if (a.logp_out) a.logp_out[row] = lp;
-              if (a.clipped_out) a.clipped_out[row] = cl;
-            }
-            mode = st == 0.f ? SV_ZERO : SV_GRAD;
-            const float inv_s = 1.f / S;
-            q = st * inv_s;
-            dy = st * (32768.f * inv_s - 1.f);
-          }
-          if (crank == 0) a.redo[row] = redo ? 1 : 0;
-          sh.sc[b] = make_float4(q, dy, __int_as_float(cur.owned ? mt.y : -1), __uint_as_float(mode));
-          sh.scb[b] = pack_bf16x2(q, q);
-          sm100::mbar_arrive(&sh.scbar[b]);
-          RL_SV_EV(p, 6);
-          // rotate the metadata pipeline: row p+2's reference is published now (two ahead)
-          const int64_t n2 = row + 2 * ncl;
-          cur = nxt;
-          if (n2 < a.n_tokens) {
-            nxt = fetch(n2);
-            publish_ref(p + 2, nxt);
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < RL_LOSS_STATS_N; ++i)
-        a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = crank == 0 ? acc.v[i] : 0.0;
-    }
-    __syncwarp();
-  } else {
-    // ------------------------------------------------------------ consumer warps
-    const uint64_t k2 = f2pack(k, k);
-    const uint32_t my_off = (uint32_t)tid * 16u;
-    const uint32_t my_cache = cache_s + my_off;
-    const bool last_mine = tid < last_nv;
-    const bool tail_mine = tail_owner && tid < n_tail;
-    uint4 cache[NCH];  // register half of the double-buffered e' cache
-#pragma unroll
-    for (int j = 0; j < NCH; ++j) cache[j] = make_uint4(0, 0, 0, 0);
-    uint32_t slot = 0, rph = 0;
-    float xt_reg = 0.f, xt_smem = 0.f;  // tail-column e' of the register / shared-memory row
-#define RL_PRESENT(j) (EXACT ? true : ((j) < nch))
-#define RL_PARTIAL(j) (EXACT ? ((j) == NCH - 1 && last_nv > 0) : ((j) == nfull))
-#define RL_MINE(j) (!RL_PARTIAL(j) || last_mine)
-#define RL_CHUNK_END(j) ((j) % VPT == VPT - 1 || (EXACT ? (j) == NCH - 1 : (j) == nch - 1))
-    int64_t row = cid;
-    // one row iteration; S_SMEM: this row's e' go to shared memory (and row p-1's come from
-    // the registers), else the other way round
-    auto iter = [&](auto s_smem_tag, uint32_t p, bool has_row) {
-      constexpr bool S_SMEM = decltype(s_smem_tag)::value;
-      const bool has_prev = p > 0;
-      bool need = false;
-      uint64_t mn2 = 0;
-      float mn = 0.f;
-      if (has_row) {
-        if (tid == 0) RL_SV_EV(p, 0);
-        sm100::mbar_wait(&sh.refbar[p & 1], (p >> 1) & 1);
-        const float4 rf = sh.ref[p & 1];
-        need = rf.y != 0.f;
-        mn = rf.x;
-        mn2 = f2pack(mn, mn);
-      }
-      float x_tail = -INFINITY;
-      if (need && tail_mine)
-        x_tail = VecTraits<T>::load1(reinterpret_cast<const char*>(a.logits) + row * row_bytes, a.nvec * EPV + tid);
-      uint64_t acc2 = f2pack(0.f, 0.f);
-      auto s_op = [&](auto jt) {
-        constexpr int j = decltype(jt)::value;
-        if (RL_PRESENT(j) && need) {
-          if (j % VPT == 0) sm100::mbar_wait_a(full_s + slot * 8, rph);
-          const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)(VPT * kChunkBytes) + (j % VPT) * kChunkBytes + my_off);
-          if (RL_CHUNK_END(j)) sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
-          uint4 c;
-          const uint64_t nacc = ClVec<T>::exp_sv(v, k2, mn2, acc2, c);
-          acc2 = RL_MINE(j) ? nacc : acc2;
-          if (S_SMEM) sm100::sts128(my_cache + j * (uint32_t)kChunkBytes, c);
-          else cache[j] = c;
-          if (RL_CHUNK_END(j) && ++slot == (uint32_t)nslots) {
-            slot = 0;
-            rph ^= 1u;
-          }
-        }
-      };
-      // row p-1's scale (after phase 1)
-      bool stores = false, zero = false;
-      uint32_t qb2 = 0;
-      float q = 0.f, dy = 0.f;
-      int ycol = -1;
-      uint32_t pmode = SV_NONE;
-      char* dp = reinterpret_cast<char*>(a.dlogits) + (row - ncl) * row_bytes;  // row p-1
-      uint4* out = reinterpret_cast<uint4*>(dp) + v0 + tid;
-      auto c_op = [&](auto jt) {
-        constexpr int j = decltype(jt)::value;
-        if (RL_PRESENT(j) && stores && RL_MINE(j)) {
-          const uint4 c = S_SMEM ? cache[j] : sm100::lds128_a(my_cache + j * (uint32_t)kChunkBytes);
-          st_stream_v4(out + j * kChunkVec, zero ? make_uint4(0, 0, 0, 0) : ClVec<T>::grad_sv(c, qb2, q));
-        }
-      };
-      // ---- phase 1
-      static_for<0, K>([&](auto jt) { s_op(jt); });
-      if (tid == 0) RL_SV_EV(p, 1);
-      if (has_prev) {
-        const uint32_t pb = (p - 1) & 1;
-        sm100::mbar_wait(&sh.scbar[pb], ((p - 1) >> 1) & 1);
-        const float4 sc = sh.sc[pb];
-        qb2 = sh.scb[pb];
-        q = sc.x;
-        dy = sc.y;
-        ycol = __float_as_int(sc.z);
-        pmode = __float_as_uint(sc.w);
-        stores = pmode != SV_NONE;
-        zero = pmode == SV_ZERO;
-      }
-      // ---- phase 2
-      static_for<K, NCH>([&](auto jt) {
-        s_op(jt);
-        c_op(std::integral_constant<int, decltype(jt)::value - K>{});
-      });
-      if (has_row) {
-        if (need && tail_mine) {
-          const float e = fast_exp2(fmaf(x_tail, k, mn));
-          acc2 = fadd2(acc2, f2pack(e, 0.f));
-          if (S_SMEM) xt_smem = e;
-          else xt_reg = e;
-        }
-        float s0, s1;
-        f2unpack(acc2, s0, s1);
-        const float sum = warp_sum(s0 + s1);
-        if (lane == 0) {
-          sh.red_sum[p & 1][warp] = sum;
-          sm100::mbar_arrive(&sh.sumbar[p & 1]);
-        }
-      }
-      if (tid == 0) RL_SV_EV(p, 2);
-      // ---- phase 3
-      static_for<NCH - K, NCH>([&](auto jt) { c_op(jt); });
-      if (tail_mine && stores) {
-        const float e = S_SMEM ? xt_reg : xt_smem;
-        VecTraits<T>::store1(dp, a.nvec * EPV + tid, zero ? 0.f : e * q);
-      }
-      if (pmode == SV_GRAD && ycol >= 0) {
-        const bool in_tail = ycol >= a.nvec * EPV;
-        const int owner = in_tail ? (int)(ycol - a.nvec * EPV) : (int)((ycol / EPV - v0) % kChunkVec);
-        if (tid == owner) VecTraits<T>::store1(dp, ycol, dy);
-      }
-    };
-    for (uint32_t p = 0;; ++p, row += ncl) {
-      const bool has_row = row < a.n_tokens;
-      if (!has_row && p == 0) break;
-      if (p & 1) iter(std::false_type{}, p, has_row);
-      else iter(std::true_type{}, p, has_row);
-      if (!has_row) break;
-    }
-#undef RL_PRESENT
-#undef RL_PARTIAL
-#undef RL_MINE
-#undef RL_CHUNK_END
-  }
-  __syncwarp();
-  sm100::cluster_sync();
-}
-
-template <typename T, int CL, int NCH, bool EXACT = false, int K = 5, bool TRACE = false, int VPT = 1>
-static rl_status launch_svx(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_ctas) {
-  ClArgs a = a0;
-  auto kern = loss_svx_kernel<T, CL, NCH, EXACT, (K < NCH ? K : NCH - 1), TRACE, VPT>;
-  const size_t head = (sizeof(SvxShared) + 127) & ~(size_t)127;
-  const size_t cache_bytes = (size_t)NCH * kChunkBytes;
-  constexpr size_t slot_bytes = (size_t)VPT * kChunkBytes;
-  if (kSmemMax < head + cache_bytes + 2 * (slot_bytes + 16) + 256) return RL_ERR_UNSUPPORTED;
-  int nslots = (int)((kSmemMax - head - cache_bytes - 256) / (slot_bytes + 16));
-  static int slots_cap = -1;
-  if (slots_cap < 0) slots_cap = getenv("RL_SV_SLOTS") ? atoi(getenv("RL_SV_SLOTS")) : 0;
-  if (slots_cap > 0) nslots = std::min(nslots, std::max(slots_cap, 2));
-  const int nch = (int)((a.h_vec + kChunkVec - 1) / kChunkVec);
-  if (nch > NCH || (EXACT && nch != NCH)) return RL_ERR_UNSUPPORTED;
-  a.nslots = nslots;
-  const size_t smem = ((sizeof(SvxShared) + 2 * sizeof(uint64_t) * nslots + 127) & ~(size_t)127) +
-                      (size_t)nslots * slot_bytes + cache_bytes;
-  static bool attr_done = false;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return check_launch("cudaFuncSetAttribute(max dynamic smem)");
-    attr_done = true;
-  }
-  static int max_clusters = 0;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(kSvThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (!max_clusters) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cfg.gridDim = dim3(sms / CL * CL);
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
-      cudaGetLastError();
-      max_clusters = sms / CL;
-    }
-  }
-  const int64_t ncl = std::min<int64_t>(std::min<int64_t>(n, max_clusters), kMaxStatCtas / 2 / CL);
-  cfg.gridDim = dim3((unsigned)(ncl * CL));
-  *n_ctas = (int)(ncl * CL);
-  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return check_launch("loss_svx_kernel");
-  return check_launch("loss_svx_kernel");
-}
-
 template <typename T, int CL, int NCH, bool EXACT = false, bool TRACE = false, int VPT = 1>
 static rl_status launch_sv(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_ctas) {
   ClArgs a = a0;
@@ -792,30 +414,12 @@ rl_status launch_loss_sv(const void* logits, int32_t dtype, int64_t n, int64_t V
   static int dbg = -1;
   if (dbg < 0) dbg = getenv("RL_SV_DEBUG") ? atoi(getenv("RL_SV_DEBUG")) : 0;
   a.debug = dbg;
-  a.inflight_cap = 0;
   auto nchunks = [&](int64_t h) { return (h + kChunkVec - 1) / kChunkVec; };
   a.h_vec = (a.nvec + 1) / 2;
   const int64_t nch2 = nchunks(a.h_vec);
-  static int variant = -1;  // RL_SV_VARIANT: 0 = SV (default), 1 = SVX (exchange hidden)
-  if (variant < 0) variant = getenv("RL_SV_VARIANT") ? atoi(getenv("RL_SV_VARIANT")) : 0;
   static int vpt = -1;  // RL_SV_VPT: 16-B vectors per thread per TMA bulk copy (1, 2, 4, 5, 8)
   if (vpt < 0) vpt = getenv("RL_SV_VPT") ? atoi(getenv("RL_SV_VPT")) : 4;
   const bool trace = getenv("RL_TRACE") != nullptr;
-  if (variant == 1) {
-    if (bf && nch2 == 20) {  // V = 151936
-      if (trace) return launch_svx<bf16_t, 2, 20, true, 6, true, 2>(a, n, s, n_ctas);
-      if (vpt == 1) return launch_svx<bf16_t, 2, 20, true, 5, false, 1>(a, n, s, n_ctas);
-      if (vpt == 4) return launch_svx<bf16_t, 2, 20, true, 4, false, 4>(a, n, s, n_ctas);
-      return launch_svx<bf16_t, 2, 20, true, 6, false, 2>(a, n, s, n_ctas);
-    }
-    if (bf && nch2 == 17) return launch_svx<bf16_t, 2, 17, true, 6, false, 2>(a, n, s, n_ctas);  // V = 128256
-    if (nch2 <= 2) return bf ? launch_svx<bf16_t, 2, 2>(a, n, s, n_ctas) : launch_svx<float, 2, 2>(a, n, s, n_ctas);
-    if (nch2 <= 5) return bf ? launch_svx<bf16_t, 2, 5>(a, n, s, n_ctas) : launch_svx<float, 2, 5>(a, n, s, n_ctas);
-    if (nch2 <= 10) return bf ? launch_svx<bf16_t, 2, 10>(a, n, s, n_ctas) : launch_svx<float, 2, 10>(a, n, s, n_ctas);
-    if (nch2 <= 20) return bf ? launch_svx<bf16_t, 2, 20>(a, n, s, n_ctas) : launch_svx<float, 2, 20>(a, n, s, n_ctas);
-    a.h_vec = (a.nvec + 3) / 4;
-    return bf ? launch_svx<bf16_t, 4, 20>(a, n, s, n_ctas) : launch_svx<float, 4, 20>(a, n, s, n_ctas);
-  }
   if (bf && nch2 == 20) {
     if (trace) return launch_sv<bf16_t, 2, 20, true, true, 4>(a, n, s, n_ctas);
     if (vpt == 1) return launch_sv<bf16_t, 2, 20, true, false, 1>(a, n, s, n_ctas);
