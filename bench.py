@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default=None, choices=[None, "cluster", "two_pass"])
+    ap.add_argument("--kernel", default=None, choices=[None, "sv", "cluster", "two_pass"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
@@ -296,7 +296,8 @@ class TokenParallelWorkload:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
                 self.ev.append((e0, e1))
-            self.launches += 2
+            # sv: loss_sv_kernel + two-pass fixup + stats reduce; cluster / two_pass: kernel + reduce
+            self.launches += 3 if os.environ.get("RL_LOSS_KERNEL", "sv") == "sv" else 2
             if self.comm is not None:
                 self.comm.allreduce_f64(cl["stats"])
 
@@ -429,7 +430,7 @@ def main():
             comm = rl.Comm(h.value, 1, 0)
     MB = args.minibatch_tokens
     scaling = "weak"
-    kern = os.environ.get("RL_LOSS_KERNEL", "cluster")
+    kern = os.environ.get("RL_LOSS_KERNEL", "sv")
     parallelism = f"dp{world} (token-parallel)"
     if args.config == "single":
         cfg = synth.get_config("single")

@@ -13,7 +13,7 @@ timeout 600 python bench.py $ARGS > gpurun_out/bench_short.log 2>&1 && \
     --log-file gpurun_out/launches_bench.csv python bench.py $ARGS > gpurun_out/ncu_launch.log 2>&1
 echo "launch list rc=$?"
 timeout 300 python tools/kbench.py --rows 16384 --reps 2 > gpurun_out/kb_small.log 2>&1 && \
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:loss_cluster -s 1 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:loss_sv_kernel -s 1 -c 1 \
     -o gpurun_out/prof_loss python tools/kbench.py --rows 16384 --reps 2 > gpurun_out/ncu_loss.log 2>&1
 echo "ncu loss rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:token_logprob -s 1 -c 1 \

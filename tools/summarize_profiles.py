@@ -51,7 +51,7 @@ def main():
     summary = [f"# ncu evidence, round {tag}", "", "## Launch list of bench.py (our kernels)", "```",
                launches(tag), "```", ""]
     traffic = {}
-    for name, rep, rows in (("cluster", "prof_loss.ncu-rep", 16384), ("logprob", "prof_logprob.ncu-rep", 16384)):
+    for name, rep, rows in (("sv", "prof_loss.ncu-rep", 16384), ("logprob", "prof_logprob.ncu-rep", 16384)):
         p = os.path.join(OUT, rep)
         if not os.path.exists(p):
             continue
@@ -80,7 +80,7 @@ def main():
                   "sm__ctas_launched.sum"]:
             if k in d:
                 summary.append(f"{k:60s} {d[k]} {units.get(k, '')}")
-        alg = 2 * 151936 * 2 + 17 if name == "cluster" else 151936 * 2 + 12
+        alg = 2 * 151936 * 2 + 17 if name in ("sv", "cluster") else 151936 * 2 + 12
         summary.append(f"{'algorithmic bytes per token':60s} {alg}")
         summary.append(f"{'dram bytes per token (measured)':60s} {per_tok:.0f}")
         st = sorted(((k, g(k)) for k in d if k.startswith("smsp__pcsamp_warps_issue_stalled")
