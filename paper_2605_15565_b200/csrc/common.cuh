@@ -74,6 +74,13 @@ __device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
                : "memory");
 }
 
+// predicated form (no branch around it in unrolled loops)
+__device__ __forceinline__ void st_stream_v4_if(void* p, uint4 v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\n\t}" ::"l"(p),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"((uint32_t)pred)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- (max, sum) in log2 domain
 // A partial softmax state over a set of columns: m = max t, s = sum 2^(t - m), t = x*k.
 struct MS {

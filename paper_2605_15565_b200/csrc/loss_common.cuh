@@ -50,11 +50,44 @@ __device__ __forceinline__ double token_mean_inv(const Knobs& kn) {
   return d > 0.0 ? 1.0 / d : 0.0;
 }
 
+// Per-token ratio / clip decision (c4, c5) and gradient scale (c7).  Shared by token_epilogue
+// and the SV kernel's consumer threads, so the statistics and the written gradient take the
+// same decisions from the same float operations.
+//   D = logp - old; Dc = clamp(D, +-c); r = exp(Dc); clipped: A>0 && r>hi -> 2, A<0 && r<lo -> 1
+struct TokRatio {
+  float r;
+  uint8_t cl;
+  bool clamp;
+};
+__device__ __forceinline__ TokRatio token_ratio(float logp, float old, float A, const Knobs& kn) {
+  const float D = logp - old;
+  const float Dc = fminf(fmaxf(D, -kn.clamp_c), kn.clamp_c);
+  TokRatio t;
+  t.clamp = Dc != D;
+  t.r = expf(Dc);
+  t.cl = 0;
+  if (A > 0.f && t.r > kn.hi_b) t.cl = 2;
+  else if (A < 0.f && t.r < kn.lo_b) t.cl = 1;
+  return t;
+}
+// s = w A r inv_T grad_scale if unclipped and unclamped (wf = (float) w)
+__device__ __forceinline__ float token_scale(const TokRatio& t, float wf, float A, const Knobs& kn) {
+  return (t.cl != 0 || t.clamp) ? 0.f : wf * A * t.r * kn.inv_t * kn.grad_scale;
+}
+// w = 1/N | 1/(S L_i) | 1 (c6)
+__device__ __forceinline__ double token_weight(const RowMeta& mt, const int32_t* seq_active, double inv_tm,
+                                               const Knobs& kn) {
+  if (kn.agg == RL_AGG_TOKEN_MEAN) return inv_tm;
+  if (kn.agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN) {
+    const int32_t Li = seq_active ? seq_active[mt.seq] : 0;
+    return (Li > 0 && kn.global_num_seqs > 0) ? 1.0 / ((double)kn.global_num_seqs * (double)Li) : 0.0;
+  }
+  return 1.0;
+}
+
 // Per-token epilogue.  Returns the gradient scale s_t (0 for invalid / clipped / clamped
 // tokens) and adds the token's contribution to `acc`.  `inv_tm` = token_mean_inv(kn).
-//   D = logp - old; Dc = clamp(D, +-c); r = exp(Dc)
-//   L = -min(r A, clip(r, lo, hi) A); clipped: A>0 && r>hi -> 2, A<0 && r<lo -> 1
-//   w = 1/N | 1/(S L_i) | 1;  s = w A r inv_T grad_scale if unclipped and unclamped
+//   L = -min(r A, clip(r, lo, hi) A)
 __device__ __forceinline__ float token_epilogue(const RowMeta& mt, float logp, float old, float A,
                                                 const int32_t* seq_active, double inv_tm,
                                                 const Knobs& kn, Acc& acc, uint8_t* clipped_out) {
@@ -65,35 +98,20 @@ __device__ __forceinline__ float token_epilogue(const RowMeta& mt, float logp, f
     if (clipped_out) *clipped_out = 0;
     return 0.f;
   }
-  const float D = logp - old;
-  const float Dc = fminf(fmaxf(D, -kn.clamp_c), kn.clamp_c);
-  const bool clamp_active = Dc != D;
-  const float r = expf(Dc);
-  const float u = r * A;
-  const float kk = fminf(fmaxf(r, kn.lo_b), kn.hi_b) * A;
+  const TokRatio t = token_ratio(logp, old, A, kn);
+  const float u = t.r * A;
+  const float kk = fminf(fmaxf(t.r, kn.lo_b), kn.hi_b) * A;
   const float L = -fminf(u, kk);
-  uint8_t cl = 0;
-  if (A > 0.f && r > kn.hi_b) cl = 2;
-  else if (A < 0.f && r < kn.lo_b) cl = 1;
-  double w;
-  if (kn.agg == RL_AGG_TOKEN_MEAN) {
-    w = inv_tm;
-  } else if (kn.agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN) {
-    const int32_t Li = seq_active ? seq_active[mt.seq] : 0;
-    w = (Li > 0 && kn.global_num_seqs > 0) ? 1.0 / ((double)kn.global_num_seqs * (double)Li) : 0.0;
-  } else {
-    w = 1.0;
-  }
+  const double w = token_weight(mt, seq_active, inv_tm, kn);
   acc.v[ST_LOSS] += w * (double)L;
   acc.v[ST_ACTIVE] += 1.0;
   acc.v[ST_WSUM] += w;
-  acc.v[ST_RSUM] += (double)r;
-  acc.v[ST_CLO] += cl == 1 ? 1.0 : 0.0;
-  acc.v[ST_CHI] += cl == 2 ? 1.0 : 0.0;
-  acc.v[ST_CLAMP] += clamp_active ? 1.0 : 0.0;
-  if (clipped_out) *clipped_out = cl;
-  if (cl != 0 || clamp_active) return 0.f;
-  return (float)w * A * r * kn.inv_t * kn.grad_scale;
+  acc.v[ST_RSUM] += (double)t.r;
+  acc.v[ST_CLO] += t.cl == 1 ? 1.0 : 0.0;
+  acc.v[ST_CHI] += t.cl == 2 ? 1.0 : 0.0;
+  acc.v[ST_CLAMP] += t.clamp ? 1.0 : 0.0;
+  if (clipped_out) *clipped_out = t.cl;
+  return token_scale(t, (float)w, A, kn);
 }
 
 // log-prob from the log2-domain statistics: c2 = M + log2 S; logp = z_y - c2 ln2

@@ -21,14 +21,17 @@
 //     dlogits_v = (s_t / S') e'_v  (bf16 x bf16 HMUL2),  target column s_t (p_y - 1).
 //
 // Per CTA: warps 0..14 consume; warp 15 lane 0 issues the TMA bulk copies of this CTA's column
-// slice into a ring of smem slots (mbarrier full/empty); lane 1 is the row epilogue.  A slot
+// slice into a ring of smem slots (mbarrier full/empty); lane 1 is the service lane.  A slot
 // holds VPT x 7.5 KB (VPT 16-B vectors per consumer thread; default 4 -> 30 KB, 7 slots): the
 // copy probe (tools/copy_probe.cu) reads 3.6-4.5 TB/s from 7.5 KB bulk copies but
 // 7.5 TB/s from 15-30 KB ones, so the copy size, not the ring depth, bounds the read side.
-// Consumer iteration p: wait publication p (reference of row p, grad scale of row p-1), then one
-// loop over the chunks: store dlogits chunk j of row p-1 from cache[j], refill cache[j] with
-// row p's chunk j as it lands.  The epilogue meanwhile prefetches row p+1's metadata, waits for
-// row p's partial sums, exchanges them with the peer CTA over DSMEM and publishes p+1.
+// Consumer iteration p: wait ref(p) (reference and metadata of row p, published two rows ahead by
+// the service lane), then one loop over the chunks: store dlogits chunk j of row p-1 from
+// cache[j], refill cache[j] with row p's chunk j as it lands; then the row exchange, done by the
+// consumers themselves to keep it short: warp sums -> named barrier -> CTA sum -> thread 0
+// st.async's it to the peer (no release fence) -> every thread combines and computes the row's
+// scale (token_ratio / token_scale, the statistics' own functions).  Thread 0 posts (S', logp) and
+// the service lane writes logp, clip flag, redo flag and the statistics off the critical path.
 #include <cuda_bf16.h>
 
 #include "cluster_common.cuh"
@@ -36,21 +39,22 @@
 namespace rl {
 
 struct __align__(16) SvShared {
-  float4 xch[2][8];    // [row parity][cluster rank]: (S'_c, -, -, -)
+  float4 xch[2][8];    // [row parity][cluster rank]: (S'_c, -, -, -), written by the peers' st.async
   float red_sum[2][kNcw];
-  float4 pub[2];       // publication p: (15 - R_p, q_{p-1}, dy_{p-1}, target column of p-1 or -1)
-  uint4 pubi[2];       // (need_p, mode_{p-1}, q_{p-1} as bf16x2, -)
-  uint64_t xbar[2];    // peer records landed (CL - 1 remote arrivals)
-  uint64_t sumbar[2];  // consumers finished row p (kNcw arrivals)
-  uint64_t pubbar[2];  // epilogue published p (1 arrival)
+  float4 refa[2];      // row p: (15 - R_p, A, old_logp, (float) w)
+  int4 refb[2];        // row p: (need | valid << 1, target column if in this CTA's slice else -1, -, -)
+  float4 res[2];       // row p: (S', logp, -, -) from consumer thread 0 for the statistics lane
+  uint64_t xbar[2];    // peer records landed (thread 0's expect_tx arrive + 16 B st.async per peer)
+  uint64_t refbar[2];  // service lane published ref(p) (1 arrival)
+  uint64_t resbar[2];  // consumer thread 0 posted res(p) (1 arrival)
 };
 enum : uint32_t { SV_NONE = 0, SV_ZERO = 1, SV_GRAD = 2 };  // how row p-1's dlogits are written
 constexpr float kSvRedo = 0x1p115f;                         // S' bound of the fast path
 static_assert(kCacheShift == 15.f, "p_y = 2^15 / S' below");
 
 // Development trace (RL_TRACE=1): per CTA, the first 64 rows' phase times (globaltimer ns):
-// 0 consumer iteration start, 1 publication received, 2 chunk loop done; epilogue: 3 next-row
-// metadata fetched, 4 partial sums in, 5 peer record in, 6 published; 7 producer issues chunk 0.
+// consumers 0 iteration start, 1 ref(p) received, 2 chunk loop done, 3 exchange done; service lane
+// 4 res(p) seen, 5 statistics written, 6 ref(p+2) published; 7 producer issues row p's first copy.
 constexpr int kSvTraceRows = 64, kSvTraceEv = 8, kSvTraceCtas = 256;
 __device__ unsigned long long g_trace_sv[kSvTraceCtas][kSvTraceRows][kSvTraceEv];
 #define RL_SV_EV(p, ev)                                                                              \
@@ -100,9 +104,9 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       sm100::mbar_init(&empty[i], kNcw);
     }
     for (int i = 0; i < 2; ++i) {
-      sm100::mbar_init(&sh.xbar[i], CL - 1);
-      sm100::mbar_init(&sh.sumbar[i], kNcw);
-      sm100::mbar_init(&sh.pubbar[i], 1);
+      sm100::mbar_init(&sh.xbar[i], 1);
+      sm100::mbar_init(&sh.refbar[i], 1);
+      sm100::mbar_init(&sh.resbar[i], 1);
     }
     sm100::fence_mbar_init();
   }
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
     if (lane == 0 && nch > 0) {
       // ---------------------------------------------------------- TMA producer (lane 0)
       // a row is read iff it has an in-range target (and, under SKIP_MASKED_READS, is valid):
-      // the same predicate the epilogue publishes as need_p.
+      // the same predicate the service lane publishes as need_p.
       auto need_of = [&](int64_t row) -> bool {
         const RowMeta mt = row_meta(row, a.V, a.targets, a.mask, a.token_seq, a.seq_version,
                                     a.kn.trainer_version, a.kn.max_staleness);
@@ -139,13 +143,16 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
         need = nx < a.n_tokens && (skip_masked ? need_of(nx) : (y_nx >= 0 && (int64_t)y_nx < a.V));
       }
     } else if (lane == 1) {
-      // ---------------------------------------------------------- row epilogue (lane 1)
+      // ---------------------------------------------------------- service lane (lane 1)
+      // Row metadata two rows ahead (ref), and — off the consumers' critical path — each row's
+      // statistics, logp, clip flag and redo flag from the record consumer thread 0 posts.
       const double inv_tm = token_mean_inv(a.kn);
       Acc acc;
       acc.zero();
       struct Pre {
         RowMeta mt;
         float xk, A, old;
+        double w;
         bool need, owned;
       };
       auto fetch = [&](int64_t row) {
@@ -162,75 +169,48 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
         }
         r.A = r.mt.valid ? a.seq_adv[r.mt.seq] : 0.f;
         r.old = r.mt.valid ? a.old_logp[row] : 0.f;
+        r.w = r.mt.valid ? token_weight(r.mt, a.seq_active, inv_tm, a.kn) : 0.0;
         return r;
       };
-      auto publish = [&](uint32_t p, const Pre* nxt, uint32_t mode, float q, float dy, int ycol) {
-        const uint32_t b = p & 1;
-        sh.pub[b] = make_float4(nxt ? kCacheShift - nxt->xk : 0.f, q, dy, __int_as_float(ycol));
-        sh.pubi[b] = make_uint4(nxt && nxt->need ? 1u : 0u, mode, pack_bf16x2(q, q), 0u);
-        sm100::mbar_arrive(&sh.pubbar[b]);
+      auto publish_ref = [&](uint32_t p, const Pre& r) {
+        sh.refa[p & 1] = make_float4(kCacheShift - r.xk, r.A, r.old, (float)r.w);
+        sh.refb[p & 1] = make_int4((r.need ? 1 : 0) | (r.mt.valid ? 2 : 0), r.owned ? r.mt.y : -1, 0, 0);
+        sm100::mbar_arrive(&sh.refbar[p & 1]);
       };
       if (cid < a.n_tokens) {
-        Pre cur = fetch(cid);
-        publish(0, &cur, SV_NONE, 0.f, 0.f, -1);
+        Pre cur = fetch(cid), nxt;
+        publish_ref(0, cur);
+        if (cid + ncl < a.n_tokens) {
+          nxt = fetch(cid + ncl);
+          publish_ref(1, nxt);
+        }
         uint32_t p = 0;
         for (int64_t row = cid; row < a.n_tokens; row += ncl, ++p) {
-          const int64_t nx = row + ncl;
-          const bool has_next = nx < a.n_tokens;
-          Pre nxt;
-          if (has_next) nxt = fetch(nx);  // loads overlap the wait below
-          if (TRACE && has_next) (void)*(volatile float*)&nxt.xk;
-          RL_SV_EV(p, 3);
-          const uint32_t b = p & 1, ph = (p >> 1) & 1;
-          if (a.debug & 4) sm100::mbar_wait(&sh.sumbar[b], ph);
-          else sm100::mbar_wait_polite(&sh.sumbar[b], ph, false);
+          sm100::mbar_wait_polite(&sh.resbar[p & 1], (p >> 1) & 1, false);
           RL_SV_EV(p, 4);
-          float s = 0.f;
-#pragma unroll
-          for (int w = 0; w < kNcw; ++w) s += sh.red_sum[b][w];
-          const float4 rec = make_float4(s, 0.f, 0.f, 0.f);
-          sh.xch[b][crank] = rec;
-#pragma unroll
-          for (int r = 0; r < CL; ++r)
-            if (r != (int)crank) {
-              sm100::st_remote_v4(&sh.xch[b][crank], r, rec.x, rec.y, rec.z, rec.w);
-              sm100::mbar_arrive_remote(&sh.xbar[b], r);
-            }
-          if (CL > 1) {
-            if (a.debug & 4) sm100::mbar_wait_cluster(&sh.xbar[b], ph);
-            else sm100::mbar_wait_polite(&sh.xbar[b], ph, true);
-          }
-          RL_SV_EV(p, 5);
-          float S = 0.f;  // rank order: bitwise identical in every CTA of the cluster
-#pragma unroll
-          for (int r = 0; r < CL; ++r) S += sh.xch[b][r].x;
+          const float4 rs = sh.res[p & 1];
+          const float S = rs.x;
           const RowMeta& mt = cur.mt;
           const bool redo = cur.need && !(S < kSvRedo);
-          uint32_t mode = SV_NONE;
-          float q = 0.f, dy = 0.f;
-          if (!redo) {
-            float lp;
-            if (cur.need) lp = (kCacheShift - fast_log2(S)) * RL_LN2;  // z_y - lse = ln(2^15 / S')
-            else lp = mt.in_range ? 0.f : logp_from(mt, 0.f, 0.f);    // skipped masked row: 0
-            uint8_t cl = 0;
-            Acc tmp;
-            tmp.zero();
-            const float st = token_epilogue(mt, lp, cur.old, cur.A, a.seq_active, inv_tm, a.kn, tmp, &cl);
-            if (crank == 0) {
-#pragma unroll
-              for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
+          if (crank == 0) {
+            a.redo[row] = redo ? 1 : 0;
+            if (!redo) {
+              const float lp = cur.need ? rs.y : (mt.in_range ? 0.f : logp_from(mt, 0.f, 0.f));
+              uint8_t cl = 0;
+              token_epilogue(mt, lp, cur.old, cur.A, a.seq_active, inv_tm, a.kn, acc, &cl);
               if (a.logp_out) a.logp_out[row] = lp;
               if (a.clipped_out) a.clipped_out[row] = cl;
             }
-            mode = st == 0.f ? SV_ZERO : SV_GRAD;
-            const float inv_s = 1.f / S;
-            q = st * inv_s;
-            dy = st * (32768.f * inv_s - 1.f);  // p_y = e'_y / S' = 2^15 / S'
           }
-          if (crank == 0) a.redo[row] = redo ? 1 : 0;
-          publish(p + 1, has_next ? &nxt : nullptr, mode, q, dy, cur.owned ? mt.y : -1);
+          RL_SV_EV(p, 5);
+          // ref(p) has been consumed (res(p) is posted after it): reuse its buffer for ref(p+2)
+          const int64_t n2 = row + 2 * ncl;
+          cur = nxt;
+          if (n2 < a.n_tokens) {
+            nxt = fetch(n2);
+            publish_ref(p + 2, nxt);
+          }
           RL_SV_EV(p, 6);
-          if (has_next) cur = nxt;
         }
       }
 #pragma unroll
@@ -249,6 +229,10 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
     for (int j = 0; j < NCH; ++j) cache[j] = make_uint4(0, 0, 0, 0);
     uint32_t slot = 0, rph = 0;
     float xt = 0.f;  // e' of this thread's scalar tail column (V % EPV != 0)
+    // row p-1's gradient (set by the exchange at the end of iteration p-1)
+    uint32_t mode = SV_NONE, qb2 = 0;
+    float q = 0.f, dy = 0.f;
+    int ycol = -1;
 #define RL_PRESENT(j) (EXACT ? true : ((j) < nch))
 #define RL_PARTIAL(j) (EXACT ? ((j) == NCH - 1 && last_nv > 0) : ((j) == nfull))
 #define RL_MINE(j) (!RL_PARTIAL(j) || last_mine)
@@ -259,67 +243,112 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       if (!has_row && p == 0) break;
       const uint32_t b = p & 1;
       if (tid == 0) RL_SV_EV(p, 0);
-      sm100::mbar_wait(&sh.pubbar[b], (p >> 1) & 1);
+      bool need = false;
+      float mn = 0.f;
+      if (has_row) {
+        sm100::mbar_wait(&sh.refbar[b], (p >> 1) & 1);
+        need = (sh.refb[b].x & 1) != 0;
+        mn = sh.refa[b].x;
+      }
       if (tid == 0) RL_SV_EV(p, 1);
-      const float4 pf = sh.pub[b];
-      const uint4 pi = sh.pubi[b];
-      const bool need = has_row && pi.x != 0;
-      const uint32_t mode = p == 0 ? SV_NONE : pi.y;
-      const bool stores = mode != SV_NONE, zero = mode == SV_ZERO;
-      const uint32_t qb2 = pi.z;
-      const uint64_t mn2 = f2pack(pf.x, pf.x);
+      const uint64_t mn2 = f2pack(mn, mn);
+      const bool stores = mode != SV_NONE;
       char* dp = reinterpret_cast<char*>(a.dlogits) + (row - ncl) * row_bytes;  // row p-1
       uint4* out = reinterpret_cast<uint4*>(dp) + v0 + tid;
       float x_tail = -INFINITY;
       if (need && tail_mine)
         x_tail = VecTraits<T>::load1(reinterpret_cast<const char*>(a.logits) + row * row_bytes, a.nvec * EPV + tid);
       uint64_t acc2 = f2pack(0.f, 0.f);
+      // one pass over the chunks: dlogits of row p-1 out of cache[j] (predicated store; a row
+      // with s = 0 has q = 0 and a finite cache -> exact zeros), row p's chunk j into cache[j]
+      auto chunk_loop = [&](auto need_c) {
+        const bool NEED = decltype(need_c)::value == 2 ? need : decltype(need_c)::value == 1;
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        if (RL_PRESENT(j)) {
-          if (stores && RL_MINE(j) && (!TRACE || !(a.debug & 1)))
-            st_stream_v4(out + j * kChunkVec, zero ? make_uint4(0, 0, 0, 0) : ClVec<T>::grad_sv(cache[j], qb2, pf.y));
-          if (need) {
-            if (j % VPT == 0) sm100::mbar_wait_a(full_s + slot * 8, rph);
-            const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)(VPT * kChunkBytes) + (j % VPT) * kChunkBytes + my_off);
-            if (RL_CHUNK_END(j)) sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
-            if (TRACE && (a.debug & 2)) {
-              cache[j] = v;
-              acc2 = fadd2(acc2, f2pack(__uint_as_float(v.x & 0x7fff), 1.f));
+        for (int j = 0; j < NCH; ++j) {
+          if (RL_PRESENT(j)) {
+            st_stream_v4_if(out + j * kChunkVec, ClVec<T>::grad_sv(cache[j], qb2, q),
+                            stores && RL_MINE(j) && (!TRACE || !(a.debug & 1)));
+            if (NEED) {
+              if (j % VPT == 0) sm100::mbar_wait_a(full_s + slot * 8, rph);
+              const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)(VPT * kChunkBytes) + (j % VPT) * kChunkBytes + my_off);
+              if (RL_CHUNK_END(j)) sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+              if (TRACE && (a.debug & 2)) {
+                cache[j] = v;
+                acc2 = fadd2(acc2, f2pack(__uint_as_float(v.x & 0x7fff), 1.f));
+              } else if (EXACT && j < NCH - 1) {
+                acc2 = ClVec<T>::exp_sv(v, k2, mn2, acc2, cache[j]);
+              } else {
+                const uint64_t nacc = ClVec<T>::exp_sv(v, k2, mn2, acc2, cache[j]);
+                acc2 = RL_MINE(j) ? nacc : acc2;
+              }
+              if (RL_CHUNK_END(j) && ++slot == (uint32_t)nslots) {
+                slot = 0;
+                rph ^= 1u;
+              }
             } else {
-              const uint64_t nacc = ClVec<T>::exp_sv(v, k2, mn2, acc2, cache[j]);
-              acc2 = RL_MINE(j) ? nacc : acc2;
-            }
-            if (RL_CHUNK_END(j) && ++slot == (uint32_t)nslots) {
-              slot = 0;
-              rph ^= 1u;
+              cache[j] = make_uint4(0, 0, 0, 0);  // an unread row writes zeros next iteration
             }
           }
         }
-      }
+      };
+      chunk_loop(std::integral_constant<int, 2>{});  // runtime need (one loop body: no spills)
       if (tail_mine) {
-        if (stores) VecTraits<T>::store1(dp, a.nvec * EPV + tid, zero ? 0.f : xt * pf.y);
+        if (stores) VecTraits<T>::store1(dp, a.nvec * EPV + tid, xt * q);
+        xt = 0.f;
         if (need) {
-          xt = fast_exp2(fmaf(x_tail, k, pf.x));
+          xt = fast_exp2(fmaf(x_tail, k, mn));
           acc2 = fadd2(acc2, f2pack(xt, 0.f));
         }
       }
       // target column of row p-1: rewritten by the thread that stored its vector (or tail
       // column) above — same-thread program order to the same address.
-      const int ycol = __float_as_int(pf.w);
       if (mode == SV_GRAD && ycol >= 0) {
         const bool in_tail = ycol >= a.nvec * EPV;
         const int owner = in_tail ? (int)(ycol - a.nvec * EPV) : (int)((ycol / EPV - v0) % kChunkVec);
-        if (tid == owner) VecTraits<T>::store1(dp, ycol, pf.z);
+        if (tid == owner) VecTraits<T>::store1(dp, ycol, dy);
       }
       if (tid == 0) RL_SV_EV(p, 2);
       if (!has_row) break;
-      float s0, s1;
-      f2unpack(acc2, s0, s1);
-      const float sum = warp_sum(s0 + s1);
-      if (lane == 0) {
-        sh.red_sum[b][warp] = sum;
-        sm100::mbar_arrive(&sh.sumbar[b]);
+      // ---- exchange of row p: CTA sum (named barrier), cluster sum (st.async), row scale
+      {
+        float s0, s1;
+        f2unpack(acc2, s0, s1);
+        const float ws = warp_sum(s0 + s1);
+        if (lane == 0) sh.red_sum[b][warp] = ws;
+      }
+      sm100::named_bar_sync(1, kCons);
+      float Sc = 0.f;
+#pragma unroll
+      for (int w = 0; w < kNcw; ++w) Sc += sh.red_sum[b][w];
+      if (CL > 1) {
+        if (tid == 0) {
+          sm100::mbar_arrive_expect_tx(&sh.xbar[b], 16u * (CL - 1));
+#pragma unroll
+          for (int r = 0; r < CL; ++r)
+            if (r != (int)crank) sm100::st_async_v4(&sh.xch[b][crank], &sh.xbar[b], r, Sc, 0.f, 0.f, 0.f);
+        }
+        sm100::mbar_wait_cluster(&sh.xbar[b], (p >> 1) & 1);
+      }
+      float S = 0.f;  // rank order: bitwise identical in every CTA of the cluster
+#pragma unroll
+      for (int r = 0; r < CL; ++r) S += r == (int)crank ? Sc : sh.xch[b][r].x;
+      if (tid == 0) RL_SV_EV(p, 3);
+      const float4 ra = sh.refa[b];
+      const int4 rb = sh.refb[b];
+      const bool valid = (rb.x & 2) != 0;
+      const bool redo = need && !(S < kSvRedo);
+      const float lp = need ? (kCacheShift - fast_log2(S)) * RL_LN2 : 0.f;  // ln(2^15 / S')
+      float st = 0.f;
+      if (valid && !redo) st = token_scale(token_ratio(lp, ra.z, ra.y, a.kn), ra.w, ra.y, a.kn);
+      mode = redo ? SV_NONE : (st == 0.f ? SV_ZERO : SV_GRAD);
+      const float inv_s = 1.f / S;
+      q = st == 0.f ? 0.f : st * inv_s;  // (an unread row has S' = 0)
+      dy = st == 0.f ? 0.f : st * (32768.f * inv_s - 1.f);  // p_y = e'_y / S' = 2^15 / S'
+      qb2 = pack_bf16x2(q, q);
+      ycol = rb.y;
+      if (tid == 0) {
+        sh.res[b] = make_float4(S, lp, 0.f, 0.f);
+        sm100::mbar_arrive(&sh.resbar[b]);
       }
     }
 #undef RL_PRESENT
@@ -328,7 +357,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
 #undef RL_CHUNK_END
   }
   __syncwarp();
-  sm100::cluster_sync();  // no CTA leaves while a peer may still arrive on / write its smem
+  sm100::cluster_sync();  // no CTA leaves while a peer may still write its smem
 }
 
 template <typename T, int CL, int NCH, bool EXACT = false, bool TRACE = false, int VPT = 1>

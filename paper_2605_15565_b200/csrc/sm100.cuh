@@ -102,6 +102,19 @@ __device__ __forceinline__ void st_remote_v4(void* local_addr, uint32_t rank, fl
                : "memory");
 }
 
+// 16-B store into the same smem offset of cluster CTA `rank`, completing 16 tx bytes on that CTA's
+// mbarrier at the offset of `bar` (st.async: no release fence, so the sender does not wait for its
+// own earlier global stores — the receiver arms its barrier with mbar_arrive_expect_tx).
+__device__ __forceinline__ void st_async_v4(void* local_addr, uint64_t* bar, uint32_t rank, float a, float b,
+                                            float c, float d) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local_addr)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(ra),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(rb)
+               : "memory");
+}
+
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }

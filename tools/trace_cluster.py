@@ -41,23 +41,20 @@ def main():
     per_row = (b[:, 9:61, 0] - b[:, 8:60, 0])
     print(f"row period (consumer T0->T0 next)  : {np.median(per_row):8.0f} ns  (p10 {np.percentile(per_row,10):.0f}, p90 {np.percentile(per_row,90):.0f})")
     if sv:
-        phases = [("pub wait T0->T1", 0, 1), ("chunk loop T1->T2", 1, 2), ("epi: fetch->sums E3->E4", 3, 4),
-                  ("epi: peer wait E4->E5", 4, 5), ("epi: compute+publish E5->E6", 5, 6)]
+        phases = [("ref wait T0->T1", 0, 1), ("chunk loop T1->T2", 1, 2), ("exchange T2->T3", 2, 3),
+                  ("scale + next start T3->T0'", None, None), ("service: res seen -> stats E4->E5", 4, 5)]
     else:
         phases = [("passA(next) T0->T1", 0, 1), ("scale wait T1->T2", 1, 2), ("fused C+B T2->T3", 2, 3),
                   ("epi: wait sumbar E4->E5", 4, 5), ("epi: peer wait E5->E6", 5, 6), ("epi: compute E6->E7", 6, 7)]
     for name, i, j in phases:
-        v = d(i, j)
+        if i is None:
+            v = b[:, 9:61, 0] - b[:, 8:60, 3]
+        else:
+            v = d(i, j)
         print(f"{name:36s}: {np.median(v):8.0f} ns  (p10 {np.percentile(v,10):.0f}, p90 {np.percentile(v,90):.0f})")
     if sv:
-        v = b[:, rows, 4] - b[:, rows, 2]
-        print(f"{'loop done -> epi sees sums':36s}: {np.median(v):8.0f} ns")
-        v = b[:, 9:61, 1] - b[:, 8:60, 6]
-        print(f"{'publish -> consumer past wait':36s}: {np.median(v):8.0f} ns")
-        v = b[:, rows, 4] - b[:, rows, 3]
-        print(f"{'epi idle before sums':36s}: {np.median(v):8.0f} ns")
         v = b[:, rows, 1] - b[:, rows, 7]
-        print(f"{'chunk 0 issued -> loop start':36s}: {np.median(v):8.0f} ns  (p10 {np.percentile(v,10):.0f}, p90 {np.percentile(v,90):.0f})")
+        print(f"{'first copy issued -> ref received':36s}: {np.median(v):8.0f} ns  (p10 {np.percentile(v,10):.0f}, p90 {np.percentile(v,90):.0f})")
         v = b[:, 9:61, 7] - b[:, 8:60, 7]
         print(f"{'producer row period':36s}: {np.median(v):8.0f} ns")
         return
