@@ -396,6 +396,9 @@ CONFIG_WORKLOADS = {
 
 def main():
     args = parse()
+    # the image sets NCCL_DEBUG=VERSION, whose banner NCCL writes to stdout: send NCCL's log to
+    # stderr so stdout stays the single JSON line (an explicit NCCL_DEBUG_FILE is respected)
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.impl == "reference":
         return run_reference(args)
     if args.kernel:
