@@ -147,6 +147,17 @@ struct ClVec<bf16_t> {
     c = make_uint4(o[0], o[1], o[2], o[3]);
     return acc;
   }
+  // read-only sum of 2^(x k + c) (logprob_warp_kernel)
+  __device__ static __forceinline__ uint64_t exp_sum(const uint4& v, uint64_t k2, uint64_t c2, uint64_t acc) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float a, b;
+      f2unpack(ffma2(f2pack(bf16_lo(w[i]), bf16_hi(w[i])), k2, c2), a, b);
+      acc = fadd2(acc, f2pack(fast_exp2(a), fast_exp2(b)));
+    }
+    return acc;
+  }
   // single-visit kernel (policy_loss_sv.cu): bf16 cache of e' = 2^(x k - R + 15), R = target
   __device__ static __forceinline__ uint64_t exp_sv(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc, uint4& c) {
     return exp_cache_bf(v, k2, mn2, acc, c);
@@ -192,6 +203,13 @@ struct ClVec<float> {
     c.x = o[0];
     c.y = o[1];
     return acc;
+  }
+  __device__ static __forceinline__ uint64_t exp_sum(const uint4& v, uint64_t k2, uint64_t c2, uint64_t acc) {
+    float a, b, d, e;
+    f2unpack(ffma2(f2pack(__uint_as_float(v.x), __uint_as_float(v.y)), k2, c2), a, b);
+    f2unpack(ffma2(f2pack(__uint_as_float(v.z), __uint_as_float(v.w)), k2, c2), d, e);
+    acc = fadd2(acc, f2pack(fast_exp2(a), fast_exp2(b)));
+    return fadd2(acc, f2pack(fast_exp2(d), fast_exp2(e)));
   }
   // single-visit kernel: fp32 cache (e' may exceed the fp16 range once R is not the max)
   __device__ static __forceinline__ uint64_t exp_sv(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc, uint4& c) {

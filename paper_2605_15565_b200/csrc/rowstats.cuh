@@ -86,13 +86,16 @@ __device__ __forceinline__ MS block_reduce_ms(MS v, float* smem) {
 
 // Per-thread pass over a row: vectors tid, tid+THREADS, ... (U in flight), then the
 // scalar tail [nvec*EPV, V).  `pol` is an L2 cache policy (evict_last for a re-read).
+// (t = this thread's index among the THREADS sharing the row; threadIdx.x by default)
 template <typename T, int THREADS, int U>
-__device__ __forceinline__ MS row_stats_thread(const void* row, int64_t V, float k, uint64_t pol) {
+__device__ __forceinline__ MS row_stats_thread(const void* row, int64_t V, float k, uint64_t pol,
+                                               int t = -1) {
   constexpr int EPV = VecTraits<T>::EPV;
   const uint4* vrow = reinterpret_cast<const uint4*>(row);
   const int64_t nvec = V / EPV;
+  if (t < 0) t = threadIdx.x;
   MS st{-INFINITY, 0.f};
-  int64_t i = threadIdx.x;
+  int64_t i = t;
   for (; i + (int64_t)(U - 1) * THREADS < nvec; i += (int64_t)U * THREADS) {
     uint4 v[U];
 #pragma unroll
@@ -107,7 +110,7 @@ __device__ __forceinline__ MS row_stats_thread(const void* row, int64_t V, float
     VecTraits<T>::unpack(ld_hint_v4(vrow + i, pol), f);
     ms_update<EPV>(st, f, k);
   }
-  for (int64_t c = nvec * EPV + threadIdx.x; c < V; c += THREADS) {
+  for (int64_t c = nvec * EPV + t; c < V; c += THREADS) {
     float f[1] = {VecTraits<T>::load1(row, c)};
     ms_update<1>(st, f, k);
   }

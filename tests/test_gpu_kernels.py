@@ -1,5 +1,5 @@
-"""The non-default fused-loss kernels (selected per process with RL_LOSS_KERNEL, latched on
-first use) against the same oracle parity tests as the default single-visit kernel."""
+"""The non-default kernels (selected per process with RL_LOSS_KERNEL / RL_LOGPROB_KERNEL, latched
+on first use) against the same oracle parity tests as the default ones."""
 import os
 import subprocess
 import sys
@@ -10,11 +10,14 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("kernel", ["cluster", "two_pass"])
-def test_alternate_loss_kernels(kernel):
-    env = dict(os.environ, RL_LOSS_KERNEL=kernel)
+@pytest.mark.parametrize("var,kernel,select", [
+    ("RL_LOSS_KERNEL", "cluster", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero"),
+    ("RL_LOSS_KERNEL", "two_pass", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero"),
+    ("RL_LOGPROB_KERNEL", "block", "token_logprob"),
+])
+def test_alternate_kernels(var, kernel, select):
+    env = dict(os.environ, **{var: kernel})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(ROOT, "tests", "test_gpu_parity.py"),
-                        "-k", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero"],
+                        os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-k", select],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
