@@ -396,9 +396,10 @@ CONFIG_WORKLOADS = {
 
 def main():
     args = parse()
-    # the image sets NCCL_DEBUG=VERSION, whose banner NCCL writes to stdout: send NCCL's log to
-    # stderr so stdout stays the single JSON line (an explicit NCCL_DEBUG_FILE is respected)
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    # the image sets NCCL_DEBUG=VERSION, whose only output is a banner NCCL prints on stdout: keep
+    # stdout to the single JSON line (an explicit WARN / INFO setting is left alone)
+    if os.environ.get("NCCL_DEBUG") == "VERSION":
+        os.environ["NCCL_DEBUG"] = "NONE"
     if args.impl == "reference":
         return run_reference(args)
     if args.kernel:

@@ -11,6 +11,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "loss_common.cuh"
 #include "rowstats.cuh"
@@ -149,6 +151,132 @@ __global__ void __launch_bounds__(kVpThreads) vp_finish_kernel(
     for (int i = 0; i < RL_LOSS_STATS_N; ++i) partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = acc.v[i];
 }
 
+
+// Warp-per-row forms of the two NCCL-path passes (default; the CTA-per-row kernels above are
+// kept for RL_VP_KERNEL=block): a warp streams one row slice with 4 x 16-B loads in flight per
+// lane and no block barriers (the layout of logprob_warp_kernel, 7 TB/s read).
+constexpr int kVwThreads = 256;
+constexpr int kVwWarps = kVwThreads / 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kVwThreads) vp_stats_warp_kernel(
+    const void* __restrict__ logits, int64_t n_tokens, int64_t Vr, int64_t offset, int64_t ld,
+    const int32_t* __restrict__ targets, float inv_t, float4* __restrict__ rec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float k = inv_t * RL_LOG2E;
+  const uint64_t pol = policy_evict_first();
+  const int64_t row_bytes = ld * elem_bytes<T>();
+  for (int64_t row = gw; row < n_tokens; row += nw) {
+    const char* rp = reinterpret_cast<const char*>(logits) + row * row_bytes;
+    MS st = row_stats_thread<T, 32, 4>(rp, Vr, k, pol, lane);
+    st = warp_reduce_ms(st);
+    if (lane == 0) {
+      const int32_t y = targets[row];
+      const int64_t yl = (int64_t)y - offset;
+      const bool owned = y >= 0 && yl >= 0 && yl < Vr;
+      const float zy = owned ? VecTraits<T>::load1(rp, yl) * inv_t : 0.f;
+      rec[row] = make_float4(st.m, st.s, zy, owned ? 1.f : 0.f);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kVwThreads) vp_finish_warp_kernel(
+    const void* __restrict__ logits, int64_t n_tokens, int64_t Vr, int64_t offset,
+    int64_t vocab_total, int64_t ld, const float4* __restrict__ all, int P,
+    const int32_t* __restrict__ targets, const float* __restrict__ old_logp,
+    const uint8_t* __restrict__ loss_mask, const int32_t* __restrict__ token_seq,
+    const float* __restrict__ seq_adv, const int32_t* __restrict__ seq_version,
+    const int32_t* __restrict__ seq_active, Knobs kn, int count_stats, void* dlogits,
+    float* __restrict__ logp_out, float* __restrict__ lse_out, double* __restrict__ partials) {
+  constexpr int EPV = VecTraits<T>::EPV;
+  __shared__ double wacc[kVwWarps][RL_LOSS_STATS_N];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float k = kn.inv_t * RL_LOG2E;
+  const uint64_t pol = policy_evict_first();
+  const int64_t row_bytes = ld * elem_bytes<T>();
+  const int64_t nvec = Vr / EPV;
+  const double inv_tm = token_mean_inv(kn);
+  Acc acc;  // lane 0's
+  acc.zero();
+  for (int64_t row = gw; row < n_tokens; row += nw) {
+    float s = 0.f, c2 = 0.f, dy = 0.f;
+    int64_t yl = -1;
+    if (lane == 0) {
+      const RowMeta mt = row_meta(row, vocab_total, targets, loss_mask, token_seq, seq_version,
+                                  kn.trainer_version, kn.max_staleness);
+      float zy;
+      c2 = vp_combine(all, n_tokens, P, row, &zy);
+      const float lp = logp_from(mt, zy, c2);
+      if (logp_out) logp_out[row] = lp;
+      if (lse_out) lse_out[row] = c2 * RL_LN2;
+      const float A = mt.valid ? seq_adv[mt.seq] : 0.f;
+      const float old = mt.valid ? old_logp[row] : 0.f;
+      Acc tmp;
+      tmp.zero();
+      s = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr);
+      if (count_stats)
+        for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
+      yl = (int64_t)mt.y - offset;
+      if (!(mt.in_range && yl >= 0 && yl < Vr)) yl = -1;
+    }
+    s = __shfl_sync(0xffffffffu, s, 0);
+    c2 = __shfl_sync(0xffffffffu, c2, 0);
+    yl = __shfl_sync(0xffffffffu, yl, 0);
+    const char* rp = reinterpret_cast<const char*>(logits) + row * row_bytes;
+    char* dp = reinterpret_cast<char*>(dlogits) + row * row_bytes;
+    const uint4* vrow = reinterpret_cast<const uint4*>(rp);
+    uint4* vout = reinterpret_cast<uint4*>(dp);
+    if (s == 0.f) {
+      for (int64_t i = lane; i < nvec; i += 32) st_stream_v4(vout + i, make_uint4(0, 0, 0, 0));
+      for (int64_t c = nvec * EPV + lane; c < Vr; c += 32) VecTraits<T>::store1(dp, c, 0.f);
+      continue;
+    }
+    int64_t i = lane;
+    for (; i + 3 * 32 < nvec; i += 4 * 32) {  // 4 vectors in flight per lane
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ld_hint_v4(vrow + i + u * 32, pol);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float f[EPV];
+        VecTraits<T>::unpack(v[u], f);
+#pragma unroll
+        for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
+        const int64_t c0 = (i + u * 32) * EPV;
+        if (yl >= c0 && yl < c0 + EPV) f[yl - c0] -= s;
+        st_stream_v4(vout + i + u * 32, VecTraits<T>::pack(f));
+      }
+    }
+    for (; i < nvec; i += 32) {
+      float f[EPV];
+      VecTraits<T>::unpack(ld_hint_v4(vrow + i, pol), f);
+#pragma unroll
+      for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
+      const int64_t c0 = i * EPV;
+      if (yl >= c0 && yl < c0 + EPV) f[yl - c0] -= s;
+      st_stream_v4(vout + i, VecTraits<T>::pack(f));
+    }
+    for (int64_t c = nvec * EPV + lane; c < Vr; c += 32) {
+      float v = s * fast_exp2(fmaf(VecTraits<T>::load1(rp, c), k, -c2));
+      if (c == yl) v -= s;
+      VecTraits<T>::store1(dp, c, v);
+    }
+  }
+  // per-CTA partials: the warps' accumulators summed in warp order (deterministic)
+  if (lane == 0)
+    for (int i = 0; i < RL_LOSS_STATS_N; ++i) wacc[warp][i] = acc.v[i];
+  __syncthreads();
+  if (threadIdx.x < RL_LOSS_STATS_N) {
+    double t = 0.0;
+    for (int w = 0; w < kVwWarps; ++w) t += wacc[w][threadIdx.x];
+    partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + threadIdx.x] = t;
+  }
+}
 
 // ---------------------------------------------------------------------------------------
 // Fused vocab-parallel loss with in-kernel peer exchange (rl_comm_enable_peer_exchange).
@@ -438,8 +566,27 @@ extern "C" rl_status rl_vocab_parallel_logprob(
     if (st0 != RL_OK) return st0;
     return launch_stats_reduce(partials, vgrid, stats, (p->flags & RL_F_STATS_ACCUMULATE) != 0, s);
   }
-  const int grid = vp_grid(n_tokens);
-  if (dtype == RL_BF16)
+  static int block_kernels = -1;  // RL_VP_KERNEL=block: the CTA-per-row passes
+  if (block_kernels < 0)
+    block_kernels = (getenv("RL_VP_KERNEL") && strcmp(getenv("RL_VP_KERNEL"), "block") == 0) ? 1 : 0;
+  int grid = vp_grid(n_tokens);
+  if (!block_kernels) {
+    static int wctas = 0;
+    if (!wctas) {
+      int dev = 0, sms = 148, occ = 4;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vp_finish_warp_kernel<bf16_t>, kVwThreads, 0);
+      wctas = std::min(sms * std::max(occ, 1), kMaxStatCtas);
+    }
+    grid = (int)std::min<int64_t>((n_tokens + kVwWarps - 1) / kVwWarps, wctas);
+    if (dtype == RL_BF16)
+      vp_stats_warp_kernel<bf16_t><<<grid, kVwThreads, 0, s>>>(logits_shard, n_tokens, vocab_shard,
+                                                               vocab_offset, ld, targets, inv_temperature, send);
+    else
+      vp_stats_warp_kernel<float><<<grid, kVwThreads, 0, s>>>(logits_shard, n_tokens, vocab_shard,
+                                                              vocab_offset, ld, targets, inv_temperature, send);
+  } else if (dtype == RL_BF16)
     vp_stats_kernel<bf16_t><<<grid, kVpThreads, 0, s>>>(logits_shard, n_tokens, vocab_shard,
                                                         vocab_offset, ld, targets, inv_temperature, send);
   else
@@ -456,7 +603,18 @@ extern "C" rl_status rl_vocab_parallel_logprob(
   }
   const Knobs kn = make_knobs(p);
   const int count = comm_rank(comm) == 0;
-  if (dtype == RL_BF16)
+  if (!block_kernels) {
+    if (dtype == RL_BF16)
+      vp_finish_warp_kernel<bf16_t><<<grid, kVwThreads, 0, s>>>(
+          logits_shard, n_tokens, vocab_shard, vocab_offset, vocab_total, ld, recv, P, targets,
+          old_logp, loss_mask, token_seq, seq_adv, seq_version, seq_active, kn, count, dlogits_shard,
+          logp_out, lse_out, partials);
+    else
+      vp_finish_warp_kernel<float><<<grid, kVwThreads, 0, s>>>(
+          logits_shard, n_tokens, vocab_shard, vocab_offset, vocab_total, ld, recv, P, targets,
+          old_logp, loss_mask, token_seq, seq_adv, seq_version, seq_active, kn, count, dlogits_shard,
+          logp_out, lse_out, partials);
+  } else if (dtype == RL_BF16)
     vp_finish_kernel<bf16_t><<<grid, kVpThreads, 0, s>>>(
         logits_shard, n_tokens, vocab_shard, vocab_offset, vocab_total, ld, recv, P, targets,
         old_logp, loss_mask, token_seq, seq_adv, seq_version, seq_active, kn, count, dlogits_shard,

@@ -1,4 +1,4 @@
-"""The non-default kernels (selected per process with RL_LOSS_KERNEL / RL_LOGPROB_KERNEL, latched
+"""The non-default kernels (selected per process with RL_LOSS_KERNEL / RL_LOGPROB_KERNEL / RL_VP_KERNEL, latched
 on first use) against the same oracle parity tests as the default ones."""
 import os
 import subprocess
@@ -14,6 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     ("RL_LOSS_KERNEL", "cluster", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero"),
     ("RL_LOSS_KERNEL", "two_pass", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero"),
     ("RL_LOGPROB_KERNEL", "block", "token_logprob"),
+    ("RL_VP_KERNEL", "block", "vocab_parallel"),
 ])
 def test_alternate_kernels(var, kernel, select):
     env = dict(os.environ, **{var: kernel})
