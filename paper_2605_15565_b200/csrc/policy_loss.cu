@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kL2Threads) loss_two_pass_kernel(
 #pragma unroll
       for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
       const int64_t c0 = i * EPV;
-      if (y >= c0 && y < c0 + EPV) f[y - c0] -= s;
+      onehot_sub(f, y - c0, s);  // static indices: f stays in registers
       st_stream_v4(vout + i, VecTraits<T>::pack(f));
     }
     for (int64_t c = nvec * EPV + threadIdx.x; c < V; c += kL2Threads) {

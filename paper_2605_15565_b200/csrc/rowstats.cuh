@@ -47,6 +47,19 @@ struct VecTraits<bf16_t> {
   }
 };
 
+// f[j] -= s (resp. = v) for the one j == d in [0, N), if any — compile-time indices only, so the
+// array is never placed in local memory (a runtime index f[d] would put it there)
+template <int N>
+__device__ __forceinline__ void onehot_sub(float (&f)[N], int64_t d, float s) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) f[j] = (d == j) ? f[j] - s : f[j];
+}
+template <int N>
+__device__ __forceinline__ void onehot_set(float (&f)[N], int64_t d, float v) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) f[j] = (d == j) ? v : f[j];
+}
+
 template <typename T>
 __device__ __forceinline__ int64_t elem_bytes() {
   return VecTraits<T>::EPV == 8 ? 2 : 4;

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "cluster_common.cuh"
 #include "loss_common.cuh"
 #include "rowstats.cuh"
 #include "sm100.cuh"
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kVpThreads) vp_finish_kernel(
 #pragma unroll
       for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
       const int64_t c0 = i * EPV;
-      if (yl >= c0 && yl < c0 + EPV) f[yl - c0] -= s;
+      onehot_sub(f, yl - c0, s);  // static indices: f stays in registers
       st_stream_v4(vout + i, VecTraits<T>::pack(f));
     }
     for (int64_t c = nvec * EPV + threadIdx.x; c < Vr; c += kVpThreads) {
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(kVwThreads) vp_stats_warp_kernel(
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kVwThreads) vp_finish_warp_kernel(
+__global__ void __launch_bounds__(kVwThreads, 4) vp_finish_warp_kernel(
     const void* __restrict__ logits, int64_t n_tokens, int64_t Vr, int64_t offset,
     int64_t vocab_total, int64_t ld, const float4* __restrict__ all, int P,
     const int32_t* __restrict__ targets, const float* __restrict__ old_logp,
@@ -201,10 +202,10 @@ __global__ void __launch_bounds__(kVwThreads) vp_finish_warp_kernel(
   const int64_t row_bytes = ld * elem_bytes<T>();
   const int64_t nvec = Vr / EPV;
   const double inv_tm = token_mean_inv(kn);
-  Acc acc;  // lane 0's
-  acc.zero();
+  if (lane == 0)  // the warp's statistics live in shared memory (no fp64 registers in the loop)
+    for (int i = 0; i < RL_LOSS_STATS_N; ++i) wacc[warp][i] = 0.0;
   for (int64_t row = gw; row < n_tokens; row += nw) {
-    float s = 0.f, c2 = 0.f, dy = 0.f;
+    float s = 0.f, c2 = 0.f;
     int64_t yl = -1;
     if (lane == 0) {
       const RowMeta mt = row_meta(row, vocab_total, targets, loss_mask, token_seq, seq_version,
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kVwThreads) vp_finish_warp_kernel(
       tmp.zero();
       s = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr);
       if (count_stats)
-        for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
+        for (int i = 0; i < RL_LOSS_STATS_N; ++i) wacc[warp][i] += tmp.v[i];
       yl = (int64_t)mt.y - offset;
       if (!(mt.in_range && yl >= 0 && yl < Vr)) yl = -1;
     }
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kVwThreads) vp_finish_warp_kernel(
 #pragma unroll
         for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
         const int64_t c0 = (i + u * 32) * EPV;
-        if (yl >= c0 && yl < c0 + EPV) f[yl - c0] -= s;
+        onehot_sub(f, yl - c0, s);  // static indices: f stays in registers
         st_stream_v4(vout + i + u * 32, VecTraits<T>::pack(f));
       }
     }
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(kVwThreads) vp_finish_warp_kernel(
 #pragma unroll
       for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
       const int64_t c0 = i * EPV;
-      if (yl >= c0 && yl < c0 + EPV) f[yl - c0] -= s;
+      onehot_sub(f, yl - c0, s);  // static indices: f stays in registers
       st_stream_v4(vout + i, VecTraits<T>::pack(f));
     }
     for (int64_t c = nvec * EPV + lane; c < Vr; c += 32) {
@@ -268,13 +269,151 @@ __global__ void __launch_bounds__(kVwThreads) vp_finish_warp_kernel(
     }
   }
   // per-CTA partials: the warps' accumulators summed in warp order (deterministic)
-  if (lane == 0)
-    for (int i = 0; i < RL_LOSS_STATS_N; ++i) wacc[warp][i] = acc.v[i];
   __syncthreads();
   if (threadIdx.x < RL_LOSS_STATS_N) {
     double t = 0.0;
     for (int w = 0; w < kVwWarps; ++w) t += wacc[w][threadIdx.x];
     partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + threadIdx.x] = t;
+  }
+}
+
+// Finish pass, TMA-streamed (default): one CTA per SM walks rows blockIdx.x + k * gridDim.x.
+// Warp 15 streams the row slices through a ring of 30 KB shared-memory slots (TMA bulk
+// copies — the copy size that reads at full rate); warp 16 combines the
+// ranks' records, runs the loss epilogue and publishes (s, c2, target column) one row ahead;
+// warps 0..14 turn each landed chunk into dlogits (one MUFU.EX2 per element) with 128-bit
+// streaming stores.
+constexpr int kVtCons = 480, kVtThreads = 544, kVtVpt = 4;  // 15 consumer warps + producer + service
+constexpr int kVtSlot = kVtVpt * kVtCons * 16;  // 30 KB
+constexpr int kVtScale = 8;                     // rows of scales published ahead
+
+template <typename T>
+__global__ void __launch_bounds__(kVtThreads, 1) vp_finish_tma_kernel(
+    const void* __restrict__ logits, int64_t n_tokens, int64_t Vr, int64_t offset,
+    int64_t vocab_total, int64_t ld, const float4* __restrict__ all, int P,
+    const int32_t* __restrict__ targets, const float* __restrict__ old_logp,
+    const uint8_t* __restrict__ loss_mask, const int32_t* __restrict__ token_seq,
+    const float* __restrict__ seq_adv, const int32_t* __restrict__ seq_version,
+    const int32_t* __restrict__ seq_active, Knobs kn, int count_stats, void* dlogits,
+    float* __restrict__ logp_out, float* __restrict__ lse_out, double* __restrict__ partials,
+    int nslots) {
+  constexpr int EPV = VecTraits<T>::EPV;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + nslots;
+  uint64_t* scbar = empty + nslots;          // [kVtScale] service warp published row k's scale
+  uint64_t* donebar = scbar + kVtScale;      // [kVtScale] consumers finished row k (15 arrivals)
+  float4* sc = reinterpret_cast<float4*>(smem + 8 * (2 * nslots + 2 * kVtScale) + 64);  // [kVtScale]
+  unsigned char* ring = smem + ((8 * (2 * nslots + 2 * kVtScale) + 64 + 16 * kVtScale + 127) & ~127);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t nvec = Vr / EPV;
+  const int64_t row_bytes = ld * elem_bytes<T>();
+  const int64_t slice_bytes = nvec * 16;
+  const int nch = (int)((slice_bytes + kVtSlot - 1) / kVtSlot);
+  const int64_t nk = blockIdx.x < n_tokens ? (n_tokens - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const float k = kn.inv_t * RL_LOG2E;
+  if (tid == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], 15);
+    }
+    for (int i = 0; i < kVtScale; ++i) {
+      sm100::mbar_init(&scbar[i], 1);
+      sm100::mbar_init(&donebar[i], 15);
+    }
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t full_s = sm100::smem_u32(full), empty_s = sm100::smem_u32(empty);
+  const uint32_t ring_s = sm100::smem_u32(ring);
+  if (warp >= 15) {
+    if (warp == 15 && lane == 0 && nch > 0) {  // ---- TMA producer (its own warp)
+      RingPos rp{0, 0};
+      for (int64_t kk = 0; kk < nk; ++kk) {
+        const char* src = reinterpret_cast<const char*>(logits) + ((int64_t)blockIdx.x + kk * gridDim.x) * row_bytes;
+        for (int c = 0; c < nch; ++c) {
+          sm100::mbar_wait_a(empty_s + rp.slot * 8, rp.phase ^ 1);
+          const uint32_t bytes = (uint32_t)min((int64_t)kVtSlot, slice_bytes - (int64_t)c * kVtSlot);
+          sm100::mbar_arrive_expect_tx(&full[rp.slot], bytes);
+          sm100::bulk_g2s_nohint(ring + (size_t)rp.slot * kVtSlot, src + (size_t)c * kVtSlot, bytes, &full[rp.slot]);
+          rp.advance(1, nslots);
+        }
+      }
+    } else if (warp == 16 && lane == 0) {  // ---- service warp: combine + loss epilogue, rows ahead
+      const double inv_tm = token_mean_inv(kn);
+      Acc acc;
+      acc.zero();
+      for (int64_t kk = 0; kk < nk; ++kk) {
+        const int64_t row = (int64_t)blockIdx.x + kk * gridDim.x;
+        const RowMeta mt = row_meta(row, vocab_total, targets, loss_mask, token_seq, seq_version,
+                                    kn.trainer_version, kn.max_staleness);
+        float zy;
+        const float c2 = vp_combine(all, n_tokens, P, row, &zy);
+        const float lp = logp_from(mt, zy, c2);
+        if (logp_out) logp_out[row] = lp;
+        if (lse_out) lse_out[row] = c2 * RL_LN2;
+        const float A = mt.valid ? seq_adv[mt.seq] : 0.f;
+        const float old = mt.valid ? old_logp[row] : 0.f;
+        Acc tmp;
+        tmp.zero();
+        const float st = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr);
+        if (count_stats)
+          for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
+        const int64_t yl = (int64_t)mt.y - offset;
+        const int ycol = (mt.in_range && yl >= 0 && yl < Vr) ? (int)yl : -1;
+        const int q = (int)(kk % kVtScale);
+        if (kk >= kVtScale) sm100::mbar_wait_polite(&donebar[q], (uint32_t)(((kk - kVtScale) / kVtScale) & 1), false);
+        sc[q] = make_float4(st, c2, 0.f, __int_as_float(ycol));
+        sm100::mbar_arrive(&scbar[q]);
+      }
+      for (int i = 0; i < RL_LOSS_STATS_N; ++i) partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = acc.v[i];
+    }
+    return;
+  }
+  // ---- consumers
+  uint32_t slot = 0, rph = 0;
+  const uint32_t my_off = (uint32_t)tid * 16u;
+  for (int64_t kk = 0; kk < nk; ++kk) {
+    const int64_t row = (int64_t)blockIdx.x + kk * gridDim.x;
+    const int q = (int)(kk % kVtScale);
+    sm100::mbar_wait(&scbar[q], (uint32_t)((kk / kVtScale) & 1));
+    const float4 r = sc[q];
+    const float s = r.x, c2 = r.y;
+    const int64_t yl = __float_as_int(r.w);
+    char* dp = reinterpret_cast<char*>(dlogits) + row * row_bytes;
+    uint4* vout = reinterpret_cast<uint4*>(dp);
+    for (int c = 0; c < nch; ++c) {
+      sm100::mbar_wait_a(full_s + slot * 8, rph);
+#pragma unroll
+      for (int u = 0; u < kVtVpt; ++u) {
+        const int64_t i = ((int64_t)c * kVtVpt + u) * kVtCons + tid;  // vector index in the slice
+        if (i < nvec) {
+          uint4 o = make_uint4(0, 0, 0, 0);
+          if (s != 0.f) {
+            float f[EPV];
+            VecTraits<T>::unpack(sm100::lds128_a(ring_s + slot * (uint32_t)kVtSlot + u * (kVtCons * 16) + my_off), f);
+#pragma unroll
+            for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
+            const int64_t c0 = i * EPV;
+            onehot_sub(f, yl - c0, s);  // static indices: f stays in registers
+            o = VecTraits<T>::pack(f);
+          }
+          st_stream_v4(vout + i, o);
+        }
+      }
+      sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+      if (++slot == (uint32_t)nslots) {
+        slot = 0;
+        rph ^= 1u;
+      }
+    }
+    const char* rp = reinterpret_cast<const char*>(logits) + row * row_bytes;
+    for (int64_t cc = nvec * EPV + tid; cc < Vr; cc += kVtCons) {  // scalar tail columns
+      float v = (s == 0.f) ? 0.f : s * fast_exp2(fmaf(VecTraits<T>::load1(rp, cc), k, -c2));
+      if (s != 0.f && cc == yl) v -= s;
+      VecTraits<T>::store1(dp, cc, v);
+    }
+    sm100::mbar_arrive_lane0(sm100::smem_u32(&donebar[q]), lane);
   }
 }
 
@@ -440,7 +579,7 @@ __global__ void __launch_bounds__(kVfThreads, 1) vp_fused_kernel(const VfArgs a)
 #pragma unroll
         for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
         const int64_t c0 = i * EPV;
-        if (ycol >= c0 && ycol < c0 + EPV) f[ycol - c0] = dy;
+        onehot_set(f, ycol - c0, dy);
       }
       st_stream_v4(vout + i, VecTraits<T>::pack(f));
     }
@@ -603,7 +742,24 @@ extern "C" rl_status rl_vocab_parallel_logprob(
   }
   const Knobs kn = make_knobs(p);
   const int count = comm_rank(comm) == 0;
-  if (!block_kernels) {
+  static int finish_warp = -1;  // RL_VP_FINISH=warp: the warp-per-row finish pass
+  if (finish_warp < 0)
+    finish_warp = (getenv("RL_VP_FINISH") && strcmp(getenv("RL_VP_FINISH"), "warp") == 0) ? 1 : 0;
+  if (!block_kernels && !finish_warp) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tgrid = (int)std::min<int64_t>(n_tokens, std::min(sms, kMaxStatCtas));
+    const int nslots = 7;
+    const size_t smem = ((8 * (2 * nslots + 2 * kVtScale) + 64 + 16 * kVtScale + 127) & ~(size_t)127) +
+                        (size_t)nslots * kVtSlot;
+    auto kern = dtype == RL_BF16 ? vp_finish_tma_kernel<bf16_t> : vp_finish_tma_kernel<float>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<tgrid, kVtThreads, smem, s>>>(logits_shard, n_tokens, vocab_shard, vocab_offset, vocab_total, ld, recv,
+                                         P, targets, old_logp, loss_mask, token_seq, seq_adv, seq_version,
+                                         seq_active, kn, count, dlogits_shard, logp_out, lse_out, partials, nslots);
+    grid = tgrid;
+  } else if (!block_kernels) {
     if (dtype == RL_BF16)
       vp_finish_warp_kernel<bf16_t><<<grid, kVwThreads, 0, s>>>(
           logits_shard, n_tokens, vocab_shard, vocab_offset, vocab_total, ld, recv, P, targets,
