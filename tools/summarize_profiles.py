@@ -51,7 +51,8 @@ def main():
     summary = [f"# ncu evidence, round {tag}", "", "## Launch list of bench.py (our kernels)", "```",
                launches(tag), "```", ""]
     traffic = {}
-    for name, rep, rows in (("sv", "prof_loss.ncu-rep", 16384), ("logprob", "prof_logprob.ncu-rep", 16384)):
+    for name, rep, rows in (("sv", "prof_loss.ncu-rep", 16384), ("logprob", "prof_logprob.ncu-rep", 16384),
+                            ("vp_finish", "prof_vpfin.ncu-rep", 16384)):
         p = os.path.join(OUT, rep)
         if not os.path.exists(p):
             continue
@@ -65,11 +66,13 @@ def main():
         wr = g("dram__bytes_write.sum") * UNITS[units["dram__bytes_write.sum"]]
         unit = 1.0
         per_tok = (rd + wr) / rows
-        traffic[name] = {"dram_bytes_per_launch": per_tok * 131072, "dram_bytes_per_token": per_tok,
+        launch_rows = 65536 if name == "vp_finish" else 131072  # the bench's launch of that kernel
+        traffic[name] = {"dram_bytes_per_launch": per_tok * launch_rows, "dram_bytes_per_token": per_tok,
                          "captured_rows": rows, "read_bytes": rd * unit, "write_bytes": wr * unit,
-                         "note": "ncu --set full of a 16,384-row launch (V=151936 bf16); per-launch figure scaled "
-                                 "to the bench's 131,072-row launch"}
-        summary += [f"## ncu --set full: {name} kernel ({rows} rows x V=151936 bf16)", "```"]
+                         "note": f"ncu --set full of a {rows}-row launch; per-launch figure scaled to the "
+                                 f"bench's {launch_rows}-row launch"}
+        cols = 37984 if name == "vp_finish" else 151936
+        summary += [f"## ncu --set full: {name} kernel ({rows} rows x {cols} bf16 columns)", "```"]
         for k in ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
                   "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
                   "sm__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -80,7 +83,7 @@ def main():
                   "sm__ctas_launched.sum"]:
             if k in d:
                 summary.append(f"{k:60s} {d[k]} {units.get(k, '')}")
-        alg = 2 * 151936 * 2 + 17 if name in ("sv", "cluster") else 151936 * 2 + 12
+        alg = {"sv": 2 * 151936 * 2 + 17, "logprob": 151936 * 2 + 12, "vp_finish": 2 * 37984 * 2 + 17}[name]
         summary.append(f"{'algorithmic bytes per token':60s} {alg}")
         summary.append(f"{'dram bytes per token (measured)':60s} {per_tok:.0f}")
         st = sorted(((k, g(k)) for k in d if k.startswith("smsp__pcsamp_warps_issue_stalled")
