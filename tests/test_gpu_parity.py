@@ -410,13 +410,18 @@ def test_vocab_parallel_single_rank(cuda_lib):
 
 
 @pytest.mark.slow
-def test_full_size_single_policy_sampled(cuda_lib):
-    """BASELINE.json configs[1] at full width (V = 151936 bf16) in the bench's launch
-    configuration (one 131,072-token PPO mini-batch): sampled rows against the
-    oracle, plus the row-sum invariant over every row."""
+@pytest.mark.parametrize("name,N,in_place", [
+    ("single", 131072, False),   # configs[1]: the bench's 131,072-token mini-batch, V = 151936
+    ("long", 65536, True),       # configs[2]: multi-turn tool masks (~50 % masked rows), in place
+    ("multi_b", 32768, False),   # configs[4] policy B: V = 128256, prompt masks, staleness 8
+])
+def test_full_size_sampled(cuda_lib, name, N, in_place):
+    """Full vocabulary width in the bench's launch configuration: sampled rows against the
+    oracle (masks, staleness and versions of the config), plus the row-sum invariant over
+    every row.  V = 151936 and V = 128256 are the two compile-time fast paths of the kernel."""
     rl, t = cuda_lib, torch()
-    cfg = synth.get_config("single")
-    N, V = 131072, cfg.vocab
+    cfg = synth.get_config(name)
+    V = cfg.vocab
     lay = synth.seq_layout(cfg)
     logits = t.empty((N, V), dtype=t.bfloat16, device="cuda")
     y = t.empty(N, dtype=t.int32, device="cuda")
@@ -428,22 +433,27 @@ def test_full_size_single_policy_sampled(cuda_lib):
     ref_lp, _ = oracle.token_logprob(xs, yh[rows])
     old = np.zeros(N, dtype=np.float32)
     old[rows] = ref_lp + np.random.default_rng(1).normal(size=len(rows)) * 0.05
-    S = N // cfg.seq_len
-    tseq = np.repeat(np.arange(S), cfg.seq_len).astype(np.int32)
+    tseq = (np.arange(N) // cfg.seq_len).astype(np.int32)
+    S = int(tseq[-1]) + 1
     adv = np.random.default_rng(2).normal(size=S).astype(np.float32)
-    p = rl.LossParams(agg=rl.AGG_SUM)
-    dl = t.empty_like(logits)
+    mask = np.ascontiguousarray(lay["loss_mask"][:N]).astype(np.uint8)
+    ver = np.ascontiguousarray(lay["seq_version"][:S]).astype(np.int32)
+    tv, ms = int(lay["trainer_version"]), int(cfg.max_staleness)
+    p = rl.LossParams(agg=rl.AGG_SUM, trainer_version=tv, max_staleness=ms)
+    dl = logits if in_place else t.empty_like(logits)
     stats = t.zeros(10, dtype=t.float64, device="cuda")
     ws = t.empty(rl.policy_loss_workspace_size(N, V), dtype=t.uint8, device="cuda")
     logp = t.empty(N, device="cuda")
-    rl.policy_loss_fwd_bwd(logits, y, dev(old), dev(tseq), dev(adv), p, dl, stats, ws, logp_out=logp)
+    rl.policy_loss_fwd_bwd(logits, y, dev(old), dev(tseq), dev(adv), p, dl, stats, ws, logp_out=logp,
+                           loss_mask=dev(mask), seq_version=dev(ver))
     t.cuda.synchronize()
-    out = oracle.policy_loss_fwd_bwd(xs, yh[rows], old[rows], np.ones(len(rows)), tseq[rows], adv,
-                                     None, None, oracle.LossParams(agg=oracle.AGG_SUM))
+    out = oracle.policy_loss_fwd_bwd(xs, yh[rows], old[rows], mask[rows], tseq[rows], adv, ver, None,
+                                     oracle.LossParams(agg=oracle.AGG_SUM, trainer_version=tv, max_staleness=ms))
     g_lp = logp.cpu().numpy()[rows]
     assert np.all(np.abs(g_lp - out["logp"]) <= LOGP_ATOL)
     d = oracle.decode_bf16(dl[t.from_numpy(rows).cuda()].view(t.int16).cpu().numpy().view(np.uint16))
     s = out["scale"]
+    assert (s != 0).any() and (s == 0).any() or name == "single"
     for k in range(len(rows)):
         if s[k] == 0:
             assert np.all(d[k] == 0)
