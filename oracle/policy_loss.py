@@ -222,11 +222,13 @@ class LossParams:
     trainer_version: int = 0
     max_staleness: int = -1
     grad_scale: float = 1.0
+    kl_coef: float = 0.0   # NEXT 2: beta of the k3 KL term vs ref_logp (1e-3); reading N1
 
 
 def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_seq,
                         seq_adv, seq_version, seq_active, p: LossParams,
-                        clip_override=None, want_dlogits: bool = True):
+                        clip_override=None, want_dlogits: bool = True,
+                        ref_logp=None, prox_logp=None, want_entropy: bool = False):
     """c4–c7 for the token rows given (any subset of a batch; the global
     normalisers come from ``p``).
 
@@ -242,6 +244,18 @@ def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_
       loss = fsum_t valid_t * w_t * L_t
     ``clip_override`` (optional int array) replaces the clipped_t decision — used only
     inside the tie band of reading Z23, where either decision is correct.
+
+    NEXT 2 extensions (the paper names the KL coefficient, and
+    the staleness-aware setting, but no formulas — readings N1-N3):
+      prox_logp (decoupled ratio, N2): r = exp(clamp(logp - prox)) is the clipped ratio and the
+        surrogate is weighted by the behaviour correction rho = exp(clamp(prox - old)), no
+        gradient through rho:  L_t = -rho * min(r A, clip(r) A).  prox_logp=None -> rho = 1,
+        r vs old (the standard surrogate).
+      ref_logp + p.kl_coef (k3 KL penalty, N1): Dk = clamp(ref - logp); KL_t = exp(Dk) - Dk - 1;
+        L_t += kl_coef * KL_t;  dKL/dlogp = 1 - exp(Dk) (0 when the clamp is active).
+      s_t = w * (rho A r [unclipped, unclamped] - kl_coef (1 - exp(Dk)) [KL unclamped]) inv_T grad_scale
+      want_entropy (N3): H_t = lse_t - sum_v p_v z_v for valid tokens (reported, no gradient);
+        stats entropy_sum = fsum valid H_t;  kl_sum = fsum valid w KL_t.
     """
     x = np.asarray(logits, dtype=np.float64)
     n, V = x.shape
@@ -256,8 +270,15 @@ def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_
     c = float(p.log_ratio_clamp)
     lo_b, hi_b = 1.0 - float(p.clip_eps_low), 1.0 + float(p.clip_eps_high)
 
+    prox = None if prox_logp is None else np.asarray(prox_logp, dtype=np.float64)
+    ref = None if ref_logp is None else np.asarray(ref_logp, dtype=np.float64)
+    beta = float(p.kl_coef)
+    if beta != 0.0 and ref is None:
+        raise ValueError("kl_coef != 0 needs ref_logp")
     logp, lse = token_logprob(x, y, invT)
     dl = np.zeros((n, V), dtype=np.float64) if want_dlogits else None
+    entropy = np.zeros(n, dtype=np.float64)
+    kl_terms, ent_terms = [], []
     loss_terms = []
     valid = np.zeros(n, dtype=np.uint8)
     clipped = np.zeros(n, dtype=np.uint8)
@@ -284,13 +305,24 @@ def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_
             continue
         valid[t] = 1
         A = float(adv[i])
-        D = logp[t] - old[t]
+        base = old[t] if prox is None else prox[t]          # the clipped ratio's denominator
+        rho = 1.0
+        if prox is not None:
+            rho = math.exp(min(max(prox[t] - old[t], -c), c))  # behaviour correction, no gradient
+        D = logp[t] - base
         Dc = min(max(D, -c), c)
         clamp_active = Dc != D
         r = math.exp(Dc)
         u = r * A
         k = min(max(r, lo_b), hi_b) * A
-        L = -min(u, k)
+        L = -rho * min(u, k)
+        kl, dkl = 0.0, 0.0
+        if beta != 0.0:
+            Dk = ref[t] - logp[t]
+            Dkc = min(max(Dk, -c), c)
+            kl = math.exp(Dkc) - Dkc - 1.0
+            dkl = (1.0 - math.exp(Dkc)) if Dkc == Dk else 0.0
+            L += beta * kl
         if A > 0 and r > hi_b:
             cl = 2
         elif A < 0 and r < lo_b:
@@ -308,9 +340,9 @@ def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_
             w = 1.0
         else:
             raise ValueError("bad agg")
-        s = 0.0
-        if cl == 0 and not clamp_active:
-            s = w * A * r * invT * float(p.grad_scale)
+        g = (rho * A * r) if (cl == 0 and not clamp_active) else 0.0   # -dL_sur/dlogp
+        g -= beta * dkl                                                  # -dL_kl/dlogp
+        s = w * g * invT * float(p.grad_scale)
         clipped[t] = cl
         scale[t] = s
         ratio[t] = r
@@ -318,6 +350,11 @@ def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_
         wl[t] = w * L
         ratio_terms.append(r)
         weight_terms.append(w)
+        kl_terms.append(w * kl)
+        if want_entropy:
+            prob = np.exp(x[t] * invT - lse[t])
+            entropy[t] = lse[t] - float(np.sum(prob * (x[t] * invT)))
+            ent_terms.append(entropy[t])
         st["active_tokens"] += 1
         st["clipped_low"] += cl == 1
         st["clipped_high"] += cl == 2
@@ -329,9 +366,11 @@ def policy_loss_fwd_bwd(logits: np.ndarray, targets, old_logp, loss_mask, token_
             dl[t] = row
     st["ratio_sum"] = math.fsum(ratio_terms)
     st["weight_sum"] = math.fsum(weight_terms)
+    st["kl_sum"] = math.fsum(kl_terms)
+    st["entropy_sum"] = math.fsum(ent_terms)
     loss = math.fsum(loss_terms)
     return dict(loss=loss, dlogits=dl, logp=logp, lse=lse, valid=valid, clipped=clipped,
-                scale=scale, ratio=ratio, token_loss=wl, stats=st)
+                scale=scale, ratio=ratio, token_loss=wl, stats=st, entropy=entropy)
 
 
 # ----------------------------------------------------------------------------- c8

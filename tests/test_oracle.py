@@ -435,3 +435,111 @@ def test_parity_case_builder_runs_on_cpu():
                       max_staleness=8, big_delta_frac=0.2)
     ref = oracle_chain(case, LossParams())
     assert ref["loss"]["stats"]["stale_masked"] > 0
+
+
+# ----------------------------------------------------------------------------- NEXT 2 (N1-N3)
+def _softmax(z):
+    e = np.exp(z - z.max())
+    return e / e.sum()
+
+
+def test_k3_kl_is_unbiased_for_the_exact_kl():
+    """N1 pin: the per-token k3 estimator KL_t = e^{ref-logp} - (ref-logp) - 1, averaged over
+    targets drawn from pi (exact expectation over all V targets of one row), equals the closed-form
+    KL(pi || pi_ref) = sum p log(p / p_ref) of the two distributions."""
+    rng = np.random.default_rng(21)
+    V = 7
+    z, zr = rng.normal(size=V) * 1.5, rng.normal(size=V) * 1.5
+    p, pr = _softmax(z), _softmax(zr)
+    x = np.tile(z, (V, 1))
+    y = np.arange(V)
+    logp = np.log(p)
+    ref = np.log(pr)
+    out = oracle.policy_loss_fwd_bwd(x, y, logp, np.ones(V), np.zeros(V, dtype=int), [0.0], None, None,
+                                     LossParams(agg=oracle.AGG_SUM, kl_coef=1.0), ref_logp=ref)
+    per_token = out["token_loss"]   # A = 0: the surrogate is 0, L_t = KL_t (w = 1)
+    assert abs(float(np.sum(p * per_token)) - float(np.sum(p * np.log(p / pr)))) < 1e-12
+    assert np.all(per_token >= 0)
+    assert abs(out["stats"]["kl_sum"] - float(np.sum(per_token))) < 1e-12
+
+
+def test_kl_vanishes_at_the_reference_and_is_linear_in_beta():
+    x, y, old, tseq, adv = _random_case(22)
+    logp, _ = oracle.token_logprob(x, y)
+    p0 = LossParams(global_active_tokens=len(y))
+    base = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(len(y)), tseq, adv, None, None, p0)
+    same = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(len(y)), tseq, adv, None, None,
+                                      LossParams(global_active_tokens=len(y), kl_coef=0.5), ref_logp=logp)
+    assert same["loss"] == base["loss"] and np.array_equal(same["dlogits"], base["dlogits"])
+    ref = logp + np.random.default_rng(3).normal(size=len(y)) * 0.3
+    b1 = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(len(y)), tseq, adv, None, None,
+                                    LossParams(global_active_tokens=len(y), kl_coef=1e-3), ref_logp=ref)
+    b2 = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(len(y)), tseq, adv, None, None,
+                                    LossParams(global_active_tokens=len(y), kl_coef=2e-3), ref_logp=ref)
+    assert abs((b2["loss"] - base["loss"]) - 2 * (b1["loss"] - base["loss"])) < 1e-14
+    assert np.allclose(b2["dlogits"] - base["dlogits"], 2 * (b1["dlogits"] - base["dlogits"]), atol=1e-16)
+
+
+def test_decoupled_ratio_reduces_to_the_standard_surrogate():
+    """N2 pins: prox = old is the standard surrogate exactly; without clipping, rho * r =
+    (pi_prox / pi_behav)(pi / pi_prox) = pi / pi_behav for ANY proximal policy, so loss and gradient
+    equal the standard unclipped ones."""
+    x, y, old, tseq, adv = _random_case(23)
+    n = len(y)
+    p = LossParams(global_active_tokens=n)
+    std = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(n), tseq, adv, None, None, p)
+    same = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(n), tseq, adv, None, None, p, prox_logp=old)
+    assert same["loss"] == std["loss"] and np.array_equal(same["dlogits"], std["dlogits"])
+    noclip = LossParams(global_active_tokens=n, clip_eps_low=1e9, clip_eps_high=1e9)
+    prox = old + np.random.default_rng(4).normal(size=n) * 0.4
+    a = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(n), tseq, adv, None, None, noclip)
+    b = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(n), tseq, adv, None, None, noclip, prox_logp=prox)
+    assert abs(a["loss"] - b["loss"]) < 1e-12
+    assert np.allclose(a["dlogits"], b["dlogits"], atol=1e-14)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_extended_objective_finite_differences(seed):
+    """Gradient of the full objective (clipped decoupled surrogate + k3 KL) against central
+    differences of the oracle's own loss."""
+    x, y, old, tseq, adv = _random_case(30 + seed)
+    n = len(y)
+    rng = np.random.default_rng(40 + seed)
+    logp, _ = oracle.token_logprob(x, y)
+    prox = old + rng.normal(size=n) * 0.2
+    ref = logp + rng.normal(size=n) * 0.5
+    p = LossParams(global_active_tokens=n, kl_coef=0.3, inv_temperature=0.8)
+    out = oracle.policy_loss_fwd_bwd(x, y, old, np.ones(n), tseq, adv, None, None, p, ref_logp=ref,
+                                     prox_logp=prox)
+    r = out["ratio"]
+    near = (np.abs(r - 0.8) < 1e-4) | (np.abs(r - 1.2) < 1e-4)
+    f = lambda xx: oracle.policy_loss_fwd_bwd(xx, y, old, np.ones(n), tseq, adv, None, None, p,
+                                              clip_override=out["clipped"], want_dlogits=False,
+                                              ref_logp=ref, prox_logp=prox)["loss"]
+    h = 1e-6
+    num = np.zeros_like(x)
+    for t in range(n):
+        if near[t]:
+            continue
+        for v in range(x.shape[1]):
+            xp = x.copy(); xp[t, v] += h
+            xm = x.copy(); xm[t, v] -= h
+            num[t, v] = (f(xp) - f(xm)) / (2 * h)
+    assert np.allclose(num[~near], out["dlogits"][~near], atol=1e-8)
+
+
+def test_entropy_closed_forms_and_scipy():
+    """N3 pins: a constant row has entropy ln V; random rows match scipy.stats.entropy of the
+    softmax (natural log)."""
+    scipy_stats = pytest.importorskip("scipy.stats")
+    rng = np.random.default_rng(24)
+    V = 50
+    x = rng.normal(size=(6, V)) * 2
+    x[0] = 3.0
+    y = rng.integers(0, V, size=6)
+    out = oracle.policy_loss_fwd_bwd(x, y, oracle.token_logprob(x, y)[0], np.ones(6), np.zeros(6, dtype=int),
+                                     [1.0], None, None, LossParams(agg=oracle.AGG_SUM), want_entropy=True)
+    assert abs(out["entropy"][0] - math.log(V)) < 1e-12
+    for t in range(1, 6):
+        assert abs(out["entropy"][t] - scipy_stats.entropy(_softmax(x[t]))) < 1e-12
+    assert abs(out["stats"]["entropy_sum"] - math.fsum(out["entropy"])) < 1e-12
