@@ -256,7 +256,7 @@ class TokenParallelWorkload:
                 mask=torch.from_numpy(mask_all[t0:t0 + MB]).to(dev), sa=sa, sb=sb,
                 tok=torch.empty(MB, dtype=torch.int32, device=dev),
                 counts=torch.zeros(20, dtype=torch.float64, device=dev),
-                stats=torch.zeros(10, dtype=torch.float64, device=dev),
+                stats=torch.zeros(12, dtype=torch.float64, device=dev),
                 logp=torch.empty(MB, dtype=torch.float32, device=dev)))
         self.total_counts = torch.zeros(20, dtype=torch.float64, device=dev)
         self.ws = torch.empty(rl.policy_loss_workspace_size(MB, V), dtype=torch.uint8, device=dev)
@@ -346,7 +346,7 @@ class VocabParallelWorkload:
         self.seq_version = torch.from_numpy(lay["seq_version"]).to(dev)
         self.adv = torch.empty(S, dtype=torch.float32, device=dev)
         self.ws_adv = torch.empty(rl.group_advantage_workspace_size(S), dtype=torch.uint8, device=dev)
-        self.stats = torch.zeros(10, dtype=torch.float64, device=dev)
+        self.stats = torch.zeros(12, dtype=torch.float64, device=dev)
         self.ws = torch.empty(rl.vocab_parallel_workspace_size(N, world), dtype=torch.uint8, device=dev)
         self.V, self.N = V, N
         self.tokens_per_step = N

@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define RL_POLICY_ABI_VERSION 1
+#define RL_POLICY_ABI_VERSION 2
 
 typedef void* rl_stream; /* cudaStream_t */
 
@@ -75,6 +75,8 @@ typedef enum { RL_AGG_TOKEN_MEAN = 0, RL_AGG_SEQ_MEAN_TOKEN_MEAN = 1, RL_AGG_SUM
 /* rl_loss_params.flags */
 #define RL_F_STATS_ACCUMULATE 0x1u /* add into *stats instead of overwriting it */
 #define RL_F_SKIP_MASKED_READS 0x2u /* masked rows: do not read logits (logp_out = 0), only write zeros */
+#define RL_F_ENTROPY 0x4u /* also sum the per-token entropy H_t = lse - sum_v p_v z_v of valid tokens into
+                             stats->entropy_sum (rl_policy_loss_fwd_bwd; reading N3) */
 
 #define RL_STALE_HIST_BINS 16
 
@@ -100,8 +102,10 @@ typedef struct {
   double stale_masked;  /* tokens (mask=1, 0<=y<V) dropped because staleness > max_staleness */
   double bad_targets;   /* tokens with y >= vocab */
   double neg_staleness; /* TOKENS whose sequence has negative staleness */
+  double kl_sum;        /* sum_t valid_t * w_t * KL_t (k3 vs ref_logp; 0 unless kl_coef != 0), reading N1 */
+  double entropy_sum;   /* sum_t valid_t * H_t (only with RL_F_ENTROPY), reading N3 */
 } rl_loss_stats;
-#define RL_LOSS_STATS_N 10
+#define RL_LOSS_STATS_N 12
 
 typedef struct {
   float clip_eps_low;    /* default 0.2 (reading Z9) */
@@ -118,6 +122,13 @@ typedef struct {
                                       used iff active_tokens_dev == NULL */
   const double* active_tokens_dev; /* device pointer to the same count (e.g. &counts->active_tokens
                                       after rl_comm_allreduce_f64); NULL -> use the host value */
+  /* NEXT-2 terms (readings N1, N2), default off: */
+  float kl_coef;                   /* beta: L_t += beta * KL_t, KL_t = e^{ref-logp} - (ref-logp) - 1 (k3);
+                                      PAPER.md:572 "fixed KL penalty coefficient of 10^-3" */
+  const float* ref_logp;           /* device [n_tokens] reference-policy log-probs; required iff kl_coef != 0 */
+  const float* prox_logp;          /* device [n_tokens] proximal-policy log-probs or NULL: the clipped ratio is
+                                      pi/pi_prox and the surrogate is weighted by pi_prox/pi_behav (old_logp),
+                                      no gradient through that weight (decoupled ratio) */
 } rl_loss_params;
 
 /* ---------------------------------------------------------------- misc */

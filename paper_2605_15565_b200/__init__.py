@@ -18,7 +18,7 @@ from typing import Optional
 __all__ = [
     "load", "lib_path", "RLError", "LossParams", "STATS_FIELDS", "COUNTS_FIELDS",
     "STD_UNBIASED", "STD_BIASED", "STD_NONE", "AGG_TOKEN_MEAN", "AGG_SEQ_MEAN_TOKEN_MEAN",
-    "AGG_SUM", "F_STATS_ACCUMULATE", "F_SKIP_MASKED_READS", "F32", "BF16",
+    "AGG_SUM", "F_STATS_ACCUMULATE", "F_SKIP_MASKED_READS", "F_ENTROPY", "F32", "BF16",
     "group_advantage", "group_advantage_workspace_size", "seq_bookkeeping", "token_logprob",
     "policy_loss_fwd_bwd", "policy_loss_workspace_size", "policy_loss_fwd_bwd_host",
     "policy_loss_host_workspace_size", "vocab_parallel_logprob",
@@ -28,10 +28,11 @@ __all__ = [
 F32, BF16 = 0, 1
 STD_UNBIASED, STD_BIASED, STD_NONE = 0, 1, 2
 AGG_TOKEN_MEAN, AGG_SEQ_MEAN_TOKEN_MEAN, AGG_SUM = 0, 1, 2
-F_STATS_ACCUMULATE, F_SKIP_MASKED_READS = 0x1, 0x2
+F_STATS_ACCUMULATE, F_SKIP_MASKED_READS, F_ENTROPY = 0x1, 0x2, 0x4
 STALE_HIST_BINS = 16
 STATS_FIELDS = ("loss_sum", "active_tokens", "weight_sum", "ratio_sum", "clipped_low",
-                "clipped_high", "clamped", "stale_masked", "bad_targets", "neg_staleness")
+                "clipped_high", "clamped", "stale_masked", "bad_targets", "neg_staleness",
+                "kl_sum", "entropy_sum")
 COUNTS_FIELDS = ("active_tokens", "stale_masked", "neg_staleness", "bad_targets")
 N_COUNTS = len(COUNTS_FIELDS) + STALE_HIST_BINS
 
@@ -46,7 +47,8 @@ class _Params(C.Structure):
     _fields_ = [("clip_eps_low", f32), ("clip_eps_high", f32), ("inv_temperature", f32),
                 ("log_ratio_clamp", f32), ("grad_scale", f32), ("agg", i32),
                 ("trainer_version", i32), ("max_staleness", i32), ("global_num_seqs", i32),
-                ("flags", u32), ("global_active_tokens", f64), ("active_tokens_dev", vp)]
+                ("flags", u32), ("global_active_tokens", f64), ("active_tokens_dev", vp),
+                ("kl_coef", f32), ("ref_logp", vp), ("prox_logp", vp)]
 
 
 # name -> (restype, argtypes)
@@ -158,12 +160,18 @@ class LossParams:
     flags: int = 0
     global_active_tokens: float = 0.0
     active_tokens_dev: object = None   # CUDA tensor (float64 scalar view) or int pointer
+    kl_coef: float = 0.0               # beta of the k3 KL term (reading N1)
+    ref_logp: object = None            # CUDA float32 [n_tokens] (required iff kl_coef != 0)
+    prox_logp: object = None           # CUDA float32 [n_tokens] or None (decoupled ratio, N2)
 
     def _c(self) -> _Params:
         p = _Params()
         for f, _ in _Params._fields_:
-            if f == "active_tokens_dev":
-                p.active_tokens_dev = _ptr(self.active_tokens_dev)
+            if f in ("active_tokens_dev", "ref_logp", "prox_logp"):
+                v = getattr(self, f)
+                if v is not None and hasattr(v, "is_cuda") and not v.is_cuda:
+                    raise RLError(f"{f} must be a CUDA tensor")
+                setattr(p, f, _ptr(v))
             else:
                 setattr(p, f, getattr(self, f))
         return p
@@ -234,7 +242,7 @@ def policy_loss_fwd_bwd(logits, targets, old_logp, token_seq, seq_adv, params: L
                         dlogits, stats, workspace, loss_mask=None, seq_version=None,
                         seq_active=None, logp_out=None, clipped_out=None, vocab=None,
                         stream=None):
-    """stats: CUDA float64 tensor with >= 10 elements (rl_loss_stats, STATS_FIELDS order).
+    """stats: CUDA float64 tensor with >= 12 elements (rl_loss_stats, STATS_FIELDS order).
     dlogits may be ``logits`` itself (in place)."""
     lib = load()
     n, ld = logits.shape
@@ -243,7 +251,7 @@ def policy_loss_fwd_bwd(logits, targets, old_logp, token_seq, seq_adv, params: L
             dlogits.stride() != logits.stride() or dlogits.dtype != logits.dtype:
         raise RLError("logits/dlogits must be contiguous [n_tokens, ld] tensors of one dtype")
     if stats.numel() < len(STATS_FIELDS):
-        raise RLError("stats needs 10 float64 elements")
+        raise RLError(f"stats needs {len(STATS_FIELDS)} float64 elements")
     p = params._c()
     _check(lib.rl_policy_loss_fwd_bwd(
         _dev(logits, "logits"), _dtype_code(logits), n, V, ld, _dev(targets, "targets"),

@@ -62,4 +62,7 @@ extern "C" void rl_loss_params_default(rl_loss_params* p) {
   p->flags = 0;
   p->global_active_tokens = 0.0;
   p->active_tokens_dev = nullptr;
+  p->kl_coef = 0.f;
+  p->ref_logp = nullptr;
+  p->prox_logp = nullptr;
 }

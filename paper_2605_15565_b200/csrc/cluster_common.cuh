@@ -163,6 +163,26 @@ struct ClVec<bf16_t> {
     return exp_cache_bf(v, k2, mn2, acc, c);
   }
   __device__ static __forceinline__ uint4 grad_sv(const uint4& c, uint32_t qb2, float) { return grad_bf(c, qb2); }
+  // exp_sv + the entropy moment accx += e' * x (fp32 pairs)
+  __device__ static __forceinline__ uint64_t exp_sv_ent(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
+                                                        uint64_t& accx, uint4& c) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t x2 = f2pack(bf16_lo(w[i]), bf16_hi(w[i]));
+      float a, b;
+      f2unpack(ffma2(x2, k2, mn2), a, b);
+      a = fast_exp2(a);
+      b = fast_exp2(b);
+      const uint64_t e2 = f2pack(a, b);
+      acc = fadd2(acc, e2);
+      accx = ffma2(e2, x2, accx);
+      o[i] = pack_bf16x2(a, b);
+    }
+    c = make_uint4(o[0], o[1], o[2], o[3]);
+    return acc;
+  }
   __device__ static __forceinline__ uint4 grad_bf(const uint4& c, uint32_t qb2) {
     const __nv_bfloat162 q = *reinterpret_cast<const __nv_bfloat162*>(&qb2);
     uint4 o;
@@ -227,6 +247,22 @@ struct ClVec<float> {
     c = make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(d), __float_as_uint(e));
     return acc;
   }
+  __device__ static __forceinline__ uint64_t exp_sv_ent(const uint4& v, uint64_t k2, uint64_t mn2, uint64_t acc,
+                                                        uint64_t& accx, uint4& c) {
+    const uint64_t x0 = f2pack(__uint_as_float(v.x), __uint_as_float(v.y));
+    const uint64_t x1 = f2pack(__uint_as_float(v.z), __uint_as_float(v.w));
+    float a, b, d, e;
+    f2unpack(ffma2(x0, k2, mn2), a, b);
+    f2unpack(ffma2(x1, k2, mn2), d, e);
+    const uint64_t e0 = f2pack(fast_exp2(a), fast_exp2(b)), e1 = f2pack(fast_exp2(d), fast_exp2(e));
+    acc = fadd2(fadd2(acc, e0), e1);
+    accx = ffma2(e1, x1, ffma2(e0, x0, accx));
+    float p, q, r, t;
+    f2unpack(e0, p, q);
+    f2unpack(e1, r, t);
+    c = make_uint4(__float_as_uint(p), __float_as_uint(q), __float_as_uint(r), __float_as_uint(t));
+    return acc;
+  }
   __device__ static __forceinline__ uint4 grad_sv(const uint4& c, uint32_t, float q) {
     const uint64_t q2 = f2pack(q, q);
     float a, b, d, e;
@@ -241,17 +277,6 @@ struct ClVec<float> {
     return make_uint4(__float_as_uint(a), __float_as_uint(b), __float_as_uint(d), __float_as_uint(e));
   }
 };
-
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 // Compile-time loop: f(integral_constant<int, i>) for i in [B, E) — register-array indices and
 // phase boundaries stay static in the fully unrolled row loops.

@@ -81,6 +81,17 @@ __device__ __forceinline__ void st_stream_v4_if(void* p, uint4 v, bool pred) {
                : "memory");
 }
 
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // ---------------------------------------------------------------- (max, sum) in log2 domain
 // A partial softmax state over a set of columns: m = max t, s = sum 2^(t - m), t = x*k.
 struct MS {

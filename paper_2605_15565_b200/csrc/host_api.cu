@@ -76,6 +76,8 @@ extern "C" rl_status rl_policy_loss_fwd_bwd_host(
     size_t workspace_bytes, rl_stream stream) {
   using namespace rl;
   if (!p || !stats_host) return fail(RL_ERR_INVALID_ARGUMENT, "NULL params/stats_host");
+  if (p->kl_coef != 0.f || p->prox_logp)  // per-token device arrays do not fit the host staging
+    return fail(RL_ERR_UNSUPPORTED, "kl_coef / prox_logp are device-buffer options (rl_policy_loss_fwd_bwd)");
   if (n_tokens < 0 || vocab < 1 || ld < vocab || n_seq < 0 || chunk_tokens < 1)
     return fail(RL_ERR_INVALID_ARGUMENT, "bad sizes");
   if (dtype != RL_F32 && dtype != RL_BF16) return fail(RL_ERR_INVALID_ARGUMENT, "bad dtype %d", dtype);

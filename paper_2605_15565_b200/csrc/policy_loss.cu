@@ -55,38 +55,61 @@ __global__ void __launch_bounds__(kL2Threads) loss_two_pass_kernel(
       if (logp_out) logp_out[row] = lp;
       const float A = mt.valid ? seq_adv[mt.seq] : 0.f;
       const float old = mt.valid ? old_logp[row] : 0.f;
+      float prox_, ref_;
+      token_extra(kn, row, old, prox_, ref_);
       const float s = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, acc,
-                                     clipped_out ? clipped_out + row : nullptr);
+                                     clipped_out ? clipped_out + row : nullptr, prox_, ref_);
       s_row[0] = s;
       s_row[1] = c2;
     }
     __syncthreads();
     const float s = s_row[0], c2 = s_row[1];
     __syncthreads();  // s_row reusable by the next row
+    // entropy (reading N3): H = lse - sum_v p_v z_v over the row, for valid tokens
+    const bool ent = (kn.flags & RL_F_ENTROPY) && mt.valid;
     // pass 2: dlogits = s*(2^(t - c2) - [v == y]); exact zeros when s == 0
     const uint4* vrow = reinterpret_cast<const uint4*>(rp);
     uint4* vout = reinterpret_cast<uint4*>(dp);
     const int64_t nvec = V / EPV;
-    if (s == 0.f) {
+    if (s == 0.f && !ent) {
       for (int64_t i = threadIdx.x; i < nvec; i += kL2Threads) st_stream_v4(vout + i, make_uint4(0, 0, 0, 0));
       for (int64_t c = nvec * EPV + threadIdx.x; c < V; c += kL2Threads) VecTraits<T>::store1(dp, c, 0.f);
       return;
     }
     const uint64_t drop = policy_evict_first();
     const int32_t y = mt.y;
+    float pz = 0.f;  // this thread's sum p_v x_v
     for (int64_t i = threadIdx.x; i < nvec; i += kL2Threads) {
       float f[EPV];
       VecTraits<T>::unpack(ld_hint_v4(vrow + i, drop), f);
 #pragma unroll
-      for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
+      for (int j = 0; j < EPV; ++j) {
+        const float pv = fast_exp2(fmaf(f[j], k, -c2));
+        if (ent) pz = fmaf(pv, f[j], pz);
+        f[j] = s * pv;
+      }
       const int64_t c0 = i * EPV;
       onehot_sub(f, y - c0, s);  // static indices: f stays in registers
       st_stream_v4(vout + i, VecTraits<T>::pack(f));
     }
     for (int64_t c = nvec * EPV + threadIdx.x; c < V; c += kL2Threads) {
-      float v = s * fast_exp2(fmaf(VecTraits<T>::load1(rp, c), k, -c2));
+      const float x = VecTraits<T>::load1(rp, c);
+      const float pv = fast_exp2(fmaf(x, k, -c2));
+      if (ent) pz = fmaf(pv, x, pz);
+      float v = s * pv;
       if (c == y) v -= s;
       VecTraits<T>::store1(dp, c, v);
+    }
+    if (ent) {  // block sum, then thread 0: H = c2 ln2 - inv_T sum p x
+      pz = warp_sum(pz);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pz;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < kL2Threads / 32; ++w) t += red[w];
+        acc.v[ST_ENT] += (double)(c2 * RL_LN2 - kn.inv_t * t);
+      }
+      __syncthreads();  // red reusable
     }
   };
   if (!only) {
@@ -230,6 +253,8 @@ extern "C" rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, i
   if (p->agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN && !seq_active)
     return fail(RL_ERR_INVALID_ARGUMENT, "SEQ_MEAN_TOKEN_MEAN needs seq_active");
   if (!stats) return fail(RL_ERR_INVALID_ARGUMENT, "NULL stats");
+  if (p->kl_coef != 0.f && !p->ref_logp) return fail(RL_ERR_INVALID_ARGUMENT, "kl_coef != 0 needs ref_logp");
+  if (!(p->kl_coef == p->kl_coef)) return fail(RL_ERR_INVALID_ARGUMENT, "kl_coef is NaN");
   if (!workspace || workspace_bytes < rl_policy_loss_workspace_size(n_tokens, vocab, dtype))
     return fail(RL_ERR_WORKSPACE, "workspace must be >= %zu bytes",
                 rl_policy_loss_workspace_size(n_tokens, vocab, dtype));

@@ -226,7 +226,9 @@ __global__ void __launch_bounds__(kClThreads, 1) loss_cluster_kernel(const ClArg
         uint8_t cl = 0;
         Acc tmp;
         tmp.zero();
-        const float st = token_epilogue(mt, lp, old, A, a.seq_active, inv_tm, a.kn, tmp, &cl);
+        float prox_, ref_;
+        token_extra(a.kn, row, old, prox_, ref_);
+        const float st = token_epilogue(mt, lp, old, A, a.seq_active, inv_tm, a.kn, tmp, &cl, prox_, ref_);
         if (crank == 0) {
 #pragma unroll
           for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
@@ -503,7 +505,8 @@ rl_status launch_loss_cluster(const void* logits, int32_t dtype, int64_t n, int6
                               const int32_t* seq_version, const int32_t* seq_active,
                               const Knobs& kn, void* dlogits, float* logp_out, uint8_t* clipped_out,
                               double* partials, int* n_ctas, cudaStream_t s) {
-  if (kn.flags & RL_F_SKIP_MASKED_READS) return RL_ERR_UNSUPPORTED;
+  // masked-row skipping and the entropy moment are not in this kernel: the two-pass kernel runs
+  if (kn.flags & (RL_F_SKIP_MASKED_READS | RL_F_ENTROPY)) return RL_ERR_UNSUPPORTED;
   ClArgs a;
   a.logits = logits;
   a.dlogits = dlogits;

@@ -41,11 +41,16 @@ namespace rl {
 struct __align__(16) SvShared {
   float4 xch[2][8];    // [row parity][cluster rank]: (S'_c, -, -, -), written by the peers' st.async
   float red_sum[2][kNcw];
-  float4 refa[2];      // row p: (15 - R_p, A, old_logp, (float) w)
-  int4 refb[2];        // row p: (need | valid << 1, target column if in this CTA's slice else -1, -, -)
-  float4 res[2];       // row p: (S', logp, -, -) from consumer thread 0 for the statistics lane
+  float red_ent[2][kNcw];  // RL_F_ENTROPY: per-warp sum e' x
+  // row p's metadata in slot p % 4: published two rows ahead and read by the consumers up to the
+  // end of row p's exchange, so the slot of ref(p+2) must differ from row p's (a 2-deep ring let a
+  // slow consumer warp read row p+2's values)
+  float4 refa[4];      // row p: (15 - R_p, A, old_logp, (float) w)
+  float4 refc[4];      // row p: (prox_logp, ref_logp, -, -)
+  int4 refb[4];        // row p: (need | valid << 1, target column if in this CTA's slice else -1, -, -)
+  float4 res[2];       // row p: (S', logp, sum e' x, -) from consumer thread 0 for the statistics lane
   uint64_t xbar[2];    // peer records landed (thread 0's expect_tx arrive + 16 B st.async per peer)
-  uint64_t refbar[2];  // service lane published ref(p) (1 arrival)
+  uint64_t refbar[4];  // service lane published ref(p) (1 arrival)
   uint64_t resbar[2];  // consumer thread 0 posted res(p) (1 arrival)
 };
 enum : uint32_t { SV_NONE = 0, SV_ZERO = 1, SV_GRAD = 2 };  // how row p-1's dlogits are written
@@ -68,7 +73,7 @@ __device__ unsigned long long g_trace_sv[kSvTraceCtas][kSvTraceRows][kSvTraceEv]
 
 constexpr int kSvThreads = kClThreads;  // 15 consumer warps + 1 service warp (128 registers)
 
-template <typename T, int CL, int NCH, bool EXACT, bool TRACE = false, int VPT = 1>
+template <typename T, int CL, int NCH, bool EXACT, bool TRACE = false, int VPT = 1, bool ENT = false>
 __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) {
   constexpr int EPV = ClVec<T>::EPV;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -105,9 +110,9 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&sh.xbar[i], 1);
-      sm100::mbar_init(&sh.refbar[i], 1);
       sm100::mbar_init(&sh.resbar[i], 1);
     }
+    for (int i = 0; i < 4; ++i) sm100::mbar_init(&sh.refbar[i], 1);
     sm100::fence_mbar_init();
   }
   sm100::cluster_sync();
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       acc.zero();
       struct Pre {
         RowMeta mt;
-        float xk, A, old;
+        float xk, A, old, prox, ref;
         double w;
         bool need, owned;
       };
@@ -170,12 +175,14 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
         r.A = r.mt.valid ? a.seq_adv[r.mt.seq] : 0.f;
         r.old = r.mt.valid ? a.old_logp[row] : 0.f;
         r.w = r.mt.valid ? token_weight(r.mt, a.seq_active, inv_tm, a.kn) : 0.0;
+        token_extra(a.kn, row, r.old, r.prox, r.ref);
         return r;
       };
       auto publish_ref = [&](uint32_t p, const Pre& r) {
-        sh.refa[p & 1] = make_float4(kCacheShift - r.xk, r.A, r.old, (float)r.w);
-        sh.refb[p & 1] = make_int4((r.need ? 1 : 0) | (r.mt.valid ? 2 : 0), r.owned ? r.mt.y : -1, 0, 0);
-        sm100::mbar_arrive(&sh.refbar[p & 1]);
+        sh.refa[p & 3] = make_float4(kCacheShift - r.xk, r.A, r.old, (float)r.w);
+        sh.refc[p & 3] = make_float4(r.prox, r.ref, 0.f, 0.f);
+        sh.refb[p & 3] = make_int4((r.need ? 1 : 0) | (r.mt.valid ? 2 : 0), r.owned ? r.mt.y : -1, 0, 0);
+        sm100::mbar_arrive(&sh.refbar[p & 3]);
       };
       if (cid < a.n_tokens) {
         Pre cur = fetch(cid), nxt;
@@ -197,13 +204,15 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
             if (!redo) {
               const float lp = cur.need ? rs.y : (mt.in_range ? 0.f : logp_from(mt, 0.f, 0.f));
               uint8_t cl = 0;
-              token_epilogue(mt, lp, cur.old, cur.A, a.seq_active, inv_tm, a.kn, acc, &cl);
+              token_epilogue(mt, lp, cur.old, cur.A, a.seq_active, inv_tm, a.kn, acc, &cl, cur.prox, cur.ref);
+              if (ENT && cur.need && mt.valid)  // H = lse - sum p z,  lse = z_y + (log2 S' - 15) ln2
+                acc.v[ST_ENT] += (double)((cur.xk + fast_log2(S) - kCacheShift) * RL_LN2 - rs.z * a.kn.inv_t / S);
               if (a.logp_out) a.logp_out[row] = lp;
               if (a.clipped_out) a.clipped_out[row] = cl;
             }
           }
           RL_SV_EV(p, 5);
-          // ref(p) has been consumed (res(p) is posted after it): reuse its buffer for ref(p+2)
+          // ref(p+2) goes to slot (p+2) % 4: row p's slot stays intact for its late readers
           const int64_t n2 = row + 2 * ncl;
           cur = nxt;
           if (n2 < a.n_tokens) {
@@ -245,10 +254,11 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       if (tid == 0) RL_SV_EV(p, 0);
       bool need = false;
       float mn = 0.f;
+      const uint32_t q4 = p & 3;
       if (has_row) {
-        sm100::mbar_wait(&sh.refbar[b], (p >> 1) & 1);
-        need = (sh.refb[b].x & 1) != 0;
-        mn = sh.refa[b].x;
+        sm100::mbar_wait(&sh.refbar[q4], (p >> 2) & 1);
+        need = (sh.refb[q4].x & 1) != 0;
+        mn = sh.refa[q4].x;
       }
       if (tid == 0) RL_SV_EV(p, 1);
       const uint64_t mn2 = f2pack(mn, mn);
@@ -258,7 +268,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       float x_tail = -INFINITY;
       if (need && tail_mine)
         x_tail = VecTraits<T>::load1(reinterpret_cast<const char*>(a.logits) + row * row_bytes, a.nvec * EPV + tid);
-      uint64_t acc2 = f2pack(0.f, 0.f);
+      uint64_t acc2 = f2pack(0.f, 0.f), accx = f2pack(0.f, 0.f);
       // one pass over the chunks: dlogits of row p-1 out of cache[j] (predicated store; a row
       // with s = 0 has q = 0 and a finite cache -> exact zeros), row p's chunk j into cache[j]
       auto chunk_loop = [&](auto need_c) {
@@ -275,6 +285,11 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
               if (TRACE && (a.debug & 2)) {
                 cache[j] = v;
                 acc2 = fadd2(acc2, f2pack(__uint_as_float(v.x & 0x7fff), 1.f));
+              } else if (ENT) {
+                uint64_t nx = accx;
+                const uint64_t nacc = ClVec<T>::exp_sv_ent(v, k2, mn2, acc2, nx, cache[j]);
+                acc2 = RL_MINE(j) ? nacc : acc2;
+                accx = RL_MINE(j) ? nx : accx;
               } else if (EXACT && j < NCH - 1) {
                 acc2 = ClVec<T>::exp_sv(v, k2, mn2, acc2, cache[j]);
               } else {
@@ -298,6 +313,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
         if (need) {
           xt = fast_exp2(fmaf(x_tail, k, mn));
           acc2 = fadd2(acc2, f2pack(xt, 0.f));
+          if (ENT) accx = fadd2(accx, f2pack(xt * x_tail, 0.f));
         }
       }
       // target column of row p-1: rewritten by the thread that stored its vector (or tail
@@ -315,31 +331,41 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
         f2unpack(acc2, s0, s1);
         const float ws = warp_sum(s0 + s1);
         if (lane == 0) sh.red_sum[b][warp] = ws;
+        if (ENT) {
+          f2unpack(accx, s0, s1);
+          const float wx = warp_sum(s0 + s1);
+          if (lane == 0) sh.red_ent[b][warp] = wx;
+        }
       }
       sm100::named_bar_sync(1, kCons);
-      float Sc = 0.f;
+      float Sc = 0.f, Tc = 0.f;
 #pragma unroll
       for (int w = 0; w < kNcw; ++w) Sc += sh.red_sum[b][w];
+      if (ENT && tid == 0)
+        for (int w = 0; w < kNcw; ++w) Tc += sh.red_ent[b][w];
       if (CL > 1) {
         if (tid == 0) {
           sm100::mbar_arrive_expect_tx(&sh.xbar[b], 16u * (CL - 1));
 #pragma unroll
           for (int r = 0; r < CL; ++r)
-            if (r != (int)crank) sm100::st_async_v4(&sh.xch[b][crank], &sh.xbar[b], r, Sc, 0.f, 0.f, 0.f);
+            if (r != (int)crank) sm100::st_async_v4(&sh.xch[b][crank], &sh.xbar[b], r, Sc, Tc, 0.f, 0.f);
         }
         sm100::mbar_wait_cluster(&sh.xbar[b], (p >> 1) & 1);
       }
-      float S = 0.f;  // rank order: bitwise identical in every CTA of the cluster
+      float S = 0.f, Tx = 0.f;  // rank order: bitwise identical in every CTA of the cluster
 #pragma unroll
       for (int r = 0; r < CL; ++r) S += r == (int)crank ? Sc : sh.xch[b][r].x;
+      if (ENT && tid == 0)
+        for (int r = 0; r < CL; ++r) Tx += r == (int)crank ? Tc : sh.xch[b][r].y;
       if (tid == 0) RL_SV_EV(p, 3);
-      const float4 ra = sh.refa[b];
-      const int4 rb = sh.refb[b];
+      const float4 ra = sh.refa[q4];
+      const float4 rc = sh.refc[q4];
+      const int4 rb = sh.refb[q4];
       const bool valid = (rb.x & 2) != 0;
       const bool redo = need && !(S < kSvRedo);
       const float lp = need ? (kCacheShift - fast_log2(S)) * RL_LN2 : 0.f;  // ln(2^15 / S')
       float st = 0.f;
-      if (valid && !redo) st = token_scale(token_ratio(lp, ra.z, ra.y, a.kn), ra.w, ra.y, a.kn);
+      if (valid && !redo) st = token_scale(token_ratio(lp, ra.z, rc.x, rc.y, ra.y, a.kn), ra.w, ra.y, a.kn);
       mode = redo ? SV_NONE : (st == 0.f ? SV_ZERO : SV_GRAD);
       const float inv_s = 1.f / S;
       q = st == 0.f ? 0.f : st * inv_s;  // (an unread row has S' = 0)
@@ -347,7 +373,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       qb2 = pack_bf16x2(q, q);
       ycol = rb.y;
       if (tid == 0) {
-        sh.res[b] = make_float4(S, lp, 0.f, 0.f);
+        sh.res[b] = make_float4(S, lp, Tx, 0.f);
         sm100::mbar_arrive(&sh.resbar[b]);
       }
     }
@@ -360,10 +386,10 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
   sm100::cluster_sync();  // no CTA leaves while a peer may still write its smem
 }
 
-template <typename T, int CL, int NCH, bool EXACT = false, bool TRACE = false, int VPT = 1>
+template <typename T, int CL, int NCH, bool EXACT = false, bool TRACE = false, int VPT = 1, bool ENT = false>
 static rl_status launch_sv(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_ctas) {
   ClArgs a = a0;
-  auto kern = loss_sv_kernel<T, CL, NCH, EXACT, TRACE, VPT>;
+  auto kern = loss_sv_kernel<T, CL, NCH, EXACT, TRACE, VPT, ENT>;
   const size_t head = (sizeof(SvShared) + 127) & ~(size_t)127;
   constexpr size_t slot_bytes = (size_t)VPT * kChunkBytes;
   int nslots = (int)((kSmemMax - head - 256) / (slot_bytes + 16));
@@ -449,6 +475,14 @@ rl_status launch_loss_sv(const void* logits, int32_t dtype, int64_t n, int64_t V
   static int vpt = -1;  // RL_SV_VPT: 16-B vectors per thread per TMA bulk copy (1, 2, 4, 5, 8)
   if (vpt < 0) vpt = getenv("RL_SV_VPT") ? atoi(getenv("RL_SV_VPT")) : 4;
   const bool trace = getenv("RL_TRACE") != nullptr;
+  if (kn.flags & RL_F_ENTROPY) {  // entropy moment in the exp pass (reading N3)
+    if (bf && nch2 == 20) return launch_sv<bf16_t, 2, 20, true, false, 4, true>(a, n, s, n_ctas);
+    if (bf && nch2 == 17) return launch_sv<bf16_t, 2, 17, true, false, 4, true>(a, n, s, n_ctas);
+    if (nch2 <= 20)
+      return bf ? launch_sv<bf16_t, 2, 20, false, false, 4, true>(a, n, s, n_ctas)
+                : launch_sv<float, 2, 20, false, false, 4, true>(a, n, s, n_ctas);
+    return RL_ERR_UNSUPPORTED;  // very wide rows: the two-pass kernel computes it
+  }
   if (bf && nch2 == 20) {
     if (trace) return launch_sv<bf16_t, 2, 20, true, true, 4>(a, n, s, n_ctas);
     if (vpt == 1) return launch_sv<bf16_t, 2, 20, true, false, 1>(a, n, s, n_ctas);

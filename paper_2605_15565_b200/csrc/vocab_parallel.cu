@@ -113,7 +113,9 @@ __global__ void __launch_bounds__(kVpThreads) vp_finish_kernel(
       const float old = mt.valid ? old_logp[row] : 0.f;
       Acc tmp;
       tmp.zero();
-      const float s = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr);
+      float prox_, ref_;
+      token_extra(kn, row, old, prox_, ref_);
+      const float s = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr, prox_, ref_);
       if (count_stats)
         for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
       s_row[0] = s;
@@ -219,7 +221,9 @@ __global__ void __launch_bounds__(kVwThreads, 4) vp_finish_warp_kernel(
       const float old = mt.valid ? old_logp[row] : 0.f;
       Acc tmp;
       tmp.zero();
-      s = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr);
+      float prox_, ref_;
+      token_extra(kn, row, old, prox_, ref_);
+      s = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr, prox_, ref_);
       if (count_stats)
         for (int i = 0; i < RL_LOSS_STATS_N; ++i) wacc[warp][i] += tmp.v[i];
       yl = (int64_t)mt.y - offset;
@@ -356,7 +360,9 @@ __global__ void __launch_bounds__(kVtThreads, 1) vp_finish_tma_kernel(
         const float old = mt.valid ? old_logp[row] : 0.f;
         Acc tmp;
         tmp.zero();
-        const float st = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr);
+        float prox_, ref_;
+        token_extra(kn, row, old, prox_, ref_);
+        const float st = token_epilogue(mt, lp, old, A, seq_active, inv_tm, kn, tmp, nullptr, prox_, ref_);
         if (count_stats)
           for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
         const int64_t yl = (int64_t)mt.y - offset;
@@ -554,7 +560,9 @@ __global__ void __launch_bounds__(kVfThreads, 1) vp_fused_kernel(const VfArgs a)
       const float old = mt.valid ? a.old_logp[row] : 0.f;
       Acc tmp;
       tmp.zero();
-      const float s = token_epilogue(mt, lp, old, A, a.seq_active, inv_tm, a.kn, tmp, nullptr);
+      float prox_, ref_;
+      token_extra(a.kn, row, old, prox_, ref_);
+      const float s = token_epilogue(mt, lp, old, A, a.seq_active, inv_tm, a.kn, tmp, nullptr, prox_, ref_);
       if (a.count_stats)
         for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
       const int64_t yl = (int64_t)mt.y - a.off;
@@ -641,6 +649,9 @@ extern "C" rl_status rl_vocab_parallel_logprob(
       return fail(RL_ERR_INVALID_ARGUMENT, "fused loss needs p, token_seq, seq_adv, stats, dlogits_shard");
     if (p->agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN && !seq_active)
       return fail(RL_ERR_INVALID_ARGUMENT, "SEQ_MEAN_TOKEN_MEAN needs seq_active");
+    if (p->kl_coef != 0.f && !p->ref_logp) return fail(RL_ERR_INVALID_ARGUMENT, "kl_coef != 0 needs ref_logp");
+    if (p->flags & RL_F_ENTROPY)
+      return fail(RL_ERR_UNSUPPORTED, "RL_F_ENTROPY is not available on the vocab-parallel path");
   }
   const int64_t eb = dtype == RL_BF16 ? 2 : 4;
   if (((uintptr_t)logits_shard & 15) || ((uintptr_t)dlogits_shard & 15) || (ld * eb) % 16)

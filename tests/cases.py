@@ -41,7 +41,8 @@ def small_case(n_prompts=2, group=4, seq_len=64, vocab=1024, dtype="f32", seed=1
 
 
 def oracle_chain(case, params: oracle.LossParams, std_mode=oracle.STD_UNBIASED, eps=1e-6,
-                 batch_norm=False, bn_eps=1e-6, rows=None):
+                 batch_norm=False, bn_eps=1e-6, rows=None, ref_logp=None, prox_logp=None,
+                 want_entropy=False):
     """Advantages -> bookkeeping -> loss, all in the oracle (optionally on a row subset; the
     global normalisers always come from the full batch)."""
     bk = oracle.seq_bookkeeping(case["cu_seqlens"], case["loss_mask"], case["targets"],
@@ -58,7 +59,10 @@ def oracle_chain(case, params: oracle.LossParams, std_mode=oracle.STD_UNBIASED, 
     sel = np.arange(len(case["targets"])) if rows is None else np.asarray(rows)
     out = oracle.policy_loss_fwd_bwd(case["x64"][sel], case["targets"][sel], case["old_logp"][sel],
                                      case["loss_mask"][sel], bk["token_seq"][sel], adv,
-                                     case["seq_version"], bk["seq_active"], p)
+                                     case["seq_version"], bk["seq_active"], p,
+                                     ref_logp=None if ref_logp is None else np.asarray(ref_logp)[sel],
+                                     prox_logp=None if prox_logp is None else np.asarray(prox_logp)[sel],
+                                     want_entropy=want_entropy)
     return dict(bk=bk, adv=adv, zero_var=zv, loss=out, params=p, rows=sel)
 
 

@@ -62,7 +62,7 @@ def main():
     comm.allreduce_f64(counts)                        # N_active over all ranks
     logits = d(case["logits"][t0:t1])
     dl = torch.empty_like(logits)
-    stats = torch.zeros(10, dtype=torch.float64, device=dev)
+    stats = torch.zeros(12, dtype=torch.float64, device=dev)
     ws = torch.empty(rl.policy_loss_workspace_size(n, V), dtype=torch.uint8, device=dev)
     p = rl.LossParams(trainer_version=case["trainer_version"], max_staleness=case["max_staleness"],
                       active_tokens_dev=counts[0:1])
@@ -102,7 +102,7 @@ def main():
       dls = torch.empty_like(shard_t)
       logp = torch.empty(N, dtype=torch.float32, device=dev)
       lse = torch.empty(N, dtype=torch.float32, device=dev)
-      stats_v = torch.zeros(10, dtype=torch.float64, device=dev)
+      stats_v = torch.zeros(12, dtype=torch.float64, device=dev)
       ws_v = torch.empty(rl.vocab_parallel_workspace_size(N, world), dtype=torch.uint8, device=dev)
       p_v = rl.LossParams(trainer_version=case["trainer_version"], max_staleness=case["max_staleness"],
                           global_active_tokens=float(ref["bk"]["active_tokens"]))

@@ -46,7 +46,7 @@ def test_sm100a_cubin_only(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert lib.rl_abi_version() == 1
+    assert lib.rl_abi_version() == 2
     assert lib.rl_status_string(0) == b"ok"
     assert lib.rl_status_string(1) == b"invalid-argument"
     assert lib.rl_status_string(6) == b"nccl-error"
@@ -58,6 +58,25 @@ def test_params_default(lib):
     assert abs(p.clip_eps_low - 0.2) < 1e-7 and abs(p.clip_eps_high - 0.2) < 1e-7
     assert p.inv_temperature == 1.0 and p.log_ratio_clamp == 20.0 and p.max_staleness == -1
     assert p.agg == rl.AGG_TOKEN_MEAN and p.active_tokens_dev is None
+    assert p.kl_coef == 0.0 and p.ref_logp is None and p.prox_logp is None
+    # the ctypes mirror matches the C layout (size and every field offset), compiled from the header
+    import shutil
+    import subprocess
+    import tempfile
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    fields = [f for f, _ in rl._Params._fields_]
+    src = "#include <stdio.h>\n#include <stddef.h>\n#include \"rl_policy.h\"\nint main(void){printf(\"%zu\", sizeof(rl_loss_params));"
+    src += "".join(f'printf(" %zu", offsetof(rl_loss_params, {f}));' for f in fields) + "return 0;}\n"
+    with tempfile.TemporaryDirectory() as d:
+        with open(os.path.join(d, "t.c"), "w") as fh:
+            fh.write(src)
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", os.path.join(d, "t"),
+                        os.path.join(d, "t.c")], check=True)
+        vals = [int(v) for v in subprocess.run([os.path.join(d, "t")], capture_output=True, text=True,
+                                               check=True).stdout.split()]
+    assert vals[0] == C.sizeof(rl._Params)
+    assert vals[1:] == [getattr(rl._Params, f).offset for f in fields]
 
 
 def test_host_validation_rejects_before_launch(lib):
@@ -76,6 +95,12 @@ def test_host_validation_rejects_before_launch(lib):
     # workspace too small
     assert lib.rl_policy_loss_fwd_bwd(fake, rl.BF16, 4, 96, 96, fake, fake, None, fake, fake, None,
                                       None, C.byref(p), fake, None, None, fake, fake, 8, None) == 4
+    # kl_coef without ref_logp
+    p.kl_coef = 1e-3
+    assert lib.rl_policy_loss_fwd_bwd(fake, rl.BF16, 4, 96, 96, fake, fake, None, fake, fake, None,
+                                      None, C.byref(p), fake, None, None, fake, fake, 1 << 20, None) == 1
+    assert b"ref_logp" in lib.rl_last_error()
+    p.kl_coef = 0.0
     # SEQ_MEAN without seq_active
     p.agg = rl.AGG_SEQ_MEAN_TOKEN_MEAN
     ws = lib.rl_policy_loss_workspace_size(4, 96, rl.BF16)

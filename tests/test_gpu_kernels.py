@@ -11,8 +11,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("var,kernel,select", [
-    ("RL_LOSS_KERNEL", "cluster", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero"),
-    ("RL_LOSS_KERNEL", "two_pass", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero"),
+    ("RL_LOSS_KERNEL", "cluster", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero or objective"),
+    ("RL_LOSS_KERNEL", "two_pass", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero or objective"),
     ("RL_LOGPROB_KERNEL", "block", "token_logprob"),
     ("RL_VP_KERNEL", "block", "vocab_parallel"),
 ])

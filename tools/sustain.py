@@ -28,7 +28,7 @@ def main():
     old = torch.zeros(N, dtype=torch.float32, device="cuda")
     tseq = torch.zeros(N, dtype=torch.int32, device="cuda")
     adv = torch.ones(1, dtype=torch.float32, device="cuda")
-    stats = torch.zeros(10, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(12, dtype=torch.float64, device="cuda")
     ws = torch.empty(rl.policy_loss_workspace_size(N, V), dtype=torch.uint8, device="cuda")
     logp = torch.empty(N, device="cuda")
     p = rl.LossParams(agg=rl.AGG_SUM)

@@ -33,7 +33,7 @@ def main():
     old = torch.zeros(N, device="cuda")
     tseq = torch.zeros(N, dtype=torch.int32, device="cuda")
     adv = torch.zeros(1, device="cuda") if "--adv0" in sys.argv else torch.ones(1, device="cuda")
-    stats = torch.zeros(10, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(12, dtype=torch.float64, device="cuda")
     ws = torch.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=torch.uint8, device="cuda")
     p = rl.LossParams(agg=rl.AGG_SUM)
     call = lambda: rl.vocab_parallel_logprob(x, y, 0, Vr, comm, logp, ws, vocab_shard=Vr, old_logp=old,
