@@ -35,6 +35,7 @@ METRIC = "policy-loss fwd+bwd tokens/s @V=151936; % of HBM roofline; 1/2/4/8 GPU
 WORKLOAD = "single-policy GRPO batch (BASELINE.json configs[1]): 32 prompts x 8 responses x 2048 tokens, V=151936, bf16 logits"
 N_MINIBATCH = 4          # PAPER.md:574 "4 PPO mini-batches per iteration"
 SIDE_BYTES = 17          # target 4 + old_logp 4 + mask 1 + logp out 4 + token_seq 4
+OBJECTIVE = "clip"       # --objective
 
 
 def parse():
@@ -47,6 +48,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
+    ap.add_argument("--objective", default="clip", choices=["clip", "full"],
+                    help="clip: the north_star's clipped surrogate (default); full: + decoupled proximal "
+                         "ratio, k3 KL penalty (beta 1e-3, PAPER.md:572) and entropy (NEXT 2)")
     ap.add_argument("--config", default="single", choices=["single", "long", "vocabpar", "multi"],
                     help="BASELINE.json config (single = the headline metric's workload, the default)")
     return ap.parse_args()
@@ -230,6 +234,12 @@ class TokenParallelWorkload:
         s0, s1 = seqs                     # this rank's sequences [s0, s1) of the policy batch
         self.trainer_version, self.max_staleness = lay["trainer_version"], max_staleness
         self.pool, self.pool_y, self.pool_old = make_pool(torch, synth, dev, n_pool, MB, V, cfg.seed, rank)
+        self.full = OBJECTIVE == "full"
+        if self.full:  # reference / proximal log-probs: behaviour log-probs + seeded drift (input synthesis)
+            g = torch.Generator(device=dev)
+            g.manual_seed(991 + rank)
+            self.pool_ref = [o + 0.2 * torch.randn(o.shape, generator=g, device=dev) for o in self.pool_old]
+            self.pool_prox = [o + 0.02 * torch.randn(o.shape, generator=g, device=dev) for o in self.pool_old]
         if dlogits_buf is not None:  # shared [MB * V_max] bf16 buffer viewed as [MB, V]
             self.dlogits = dlogits_buf[:MB * V].view(MB, V)
         else:
@@ -261,7 +271,7 @@ class TokenParallelWorkload:
         self.total_counts = torch.zeros(20, dtype=torch.float64, device=dev)
         self.ws = torch.empty(rl.policy_loss_workspace_size(MB, V), dtype=torch.uint8, device=dev)
         self.tokens_per_step = n_calls * MB
-        self.bytes_per_token = 2 * V * 2 + SIDE_BYTES
+        self.bytes_per_token = 2 * V * 2 + SIDE_BYTES + (8 if self.full else 0)  # + ref, prox reads
         self.launches = 0
         self.ev = []
 
@@ -285,6 +295,9 @@ class TokenParallelWorkload:
         for c, cl in enumerate(self.calls):
             p = rl.LossParams(trainer_version=self.trainer_version, max_staleness=self.max_staleness,
                               active_tokens_dev=self.total_counts[0:1])
+            if self.full:
+                p.kl_coef, p.ref_logp, p.prox_logp = 1e-3, self.pool_ref[c % P], self.pool_prox[c % P]
+                p.flags |= rl.F_ENTROPY
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -395,7 +408,9 @@ CONFIG_WORKLOADS = {
 
 
 def main():
+    global OBJECTIVE
     args = parse()
+    OBJECTIVE = args.objective
     # the image sets NCCL_DEBUG=VERSION, whose only output is a banner NCCL prints on stdout: keep
     # stdout to the single JSON line (an explicit WARN / INFO setting is left alone)
     if os.environ.get("NCCL_DEBUG") == "VERSION":
@@ -577,7 +592,9 @@ def main():
                        "tokens_per_rank_per_step": tokens_rank, "call_tokens": launch_tokens,
                        "vocab": w0.V, "parallelism": parallelism, "loss_kernel": kern,
                        "l2": "no flush: every loss call streams a distinct >= 2.5 GB logits buffer >> 126 MB L2",
-                       "agg": "token_mean", "batch_norm": True},
+                       "agg": "token_mean", "batch_norm": True,
+                       "objective": ("clipped decoupled surrogate + k3 KL (beta 1e-3) + entropy"
+                                     if args.objective == "full" else "clipped surrogate")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": kname, "algorithmic_bytes_per_launch": alg_bytes,
