@@ -87,7 +87,8 @@ class RLError(RuntimeError):
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "librlpolicy.so")
+    # RL_LIB_PATH: development A/B of another build of the same library (tools/); default in-tree
+    return os.environ.get("RL_LIB_PATH") or os.path.join(_HERE, "librlpolicy.so")
 
 
 def load():

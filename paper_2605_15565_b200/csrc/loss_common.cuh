@@ -97,6 +97,24 @@ __device__ __forceinline__ float token_scale(const TokRatio& t, float wf, float 
   const float g = ((t.cl != 0 || t.clamp) ? 0.f : t.rho * A * t.r) - kn.kl_coef * t.dkl;
   return wf * g * kn.inv_t * kn.grad_scale;
 }
+// the clipped surrogate alone (no proximal ratio, no KL): the default path's per-token math
+__device__ __forceinline__ TokRatio token_ratio_basic(float logp, float old, float A, const Knobs& kn) {
+  TokRatio t;
+  const float D = logp - old;
+  const float Dc = fminf(fmaxf(D, -kn.clamp_c), kn.clamp_c);
+  t.clamp = Dc != D;
+  t.r = expf(Dc);
+  t.rho = 1.f;
+  t.kl = 0.f;
+  t.dkl = 0.f;
+  t.cl = 0;
+  if (A > 0.f && t.r > kn.hi_b) t.cl = 2;
+  else if (A < 0.f && t.r < kn.lo_b) t.cl = 1;
+  return t;
+}
+__device__ __forceinline__ float token_scale_basic(const TokRatio& t, float wf, float A, const Knobs& kn) {
+  return (t.cl != 0 || t.clamp) ? 0.f : wf * A * t.r * kn.inv_t * kn.grad_scale;
+}
 // w = 1/N | 1/(S L_i) | 1 (c6)
 __device__ __forceinline__ double token_weight(const RowMeta& mt, const int32_t* seq_active, double inv_tm,
                                                const Knobs& kn) {
@@ -142,6 +160,33 @@ __device__ __forceinline__ float token_epilogue(const RowMeta& mt, float logp, f
   acc.v[ST_KL] += w * (double)t.kl;
   if (clipped_out) *clipped_out = t.cl;
   return token_scale(t, (float)w, A, kn);
+}
+
+// token_epilogue of the clipped surrogate alone (token_ratio_basic / token_scale_basic)
+__device__ __forceinline__ float token_epilogue_basic(const RowMeta& mt, float logp, float old, float A,
+                                                      const int32_t* seq_active, double inv_tm,
+                                                      const Knobs& kn, Acc& acc, uint8_t* clipped_out) {
+  acc.v[ST_BAD] += mt.bad ? 1.0 : 0.0;
+  acc.v[ST_NEG] += mt.neg_stale ? 1.0 : 0.0;
+  acc.v[ST_STALE] += mt.stale_drop ? 1.0 : 0.0;
+  if (!mt.valid) {
+    if (clipped_out) *clipped_out = 0;
+    return 0.f;
+  }
+  const TokRatio t = token_ratio_basic(logp, old, A, kn);
+  const float u = t.r * A;
+  const float kk = fminf(fmaxf(t.r, kn.lo_b), kn.hi_b) * A;
+  const float L = -fminf(u, kk);
+  const double w = token_weight(mt, seq_active, inv_tm, kn);
+  acc.v[ST_LOSS] += w * (double)L;
+  acc.v[ST_ACTIVE] += 1.0;
+  acc.v[ST_WSUM] += w;
+  acc.v[ST_RSUM] += (double)t.r;
+  acc.v[ST_CLO] += t.cl == 1 ? 1.0 : 0.0;
+  acc.v[ST_CHI] += t.cl == 2 ? 1.0 : 0.0;
+  acc.v[ST_CLAMP] += t.clamp ? 1.0 : 0.0;
+  if (clipped_out) *clipped_out = t.cl;
+  return token_scale_basic(t, (float)w, A, kn);
 }
 
 // log-prob from the log2-domain statistics: c2 = M + log2 S; logp = z_y - c2 ln2

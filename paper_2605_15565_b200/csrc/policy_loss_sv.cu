@@ -73,9 +73,12 @@ __device__ unsigned long long g_trace_sv[kSvTraceCtas][kSvTraceRows][kSvTraceEv]
 
 constexpr int kSvThreads = kClThreads;  // 15 consumer warps + 1 service warp (128 registers)
 
-template <typename T, int CL, int NCH, bool EXACT, bool TRACE = false, int VPT = 1, bool ENT = false>
+// XF: compile-time extensions — bit 0 the entropy moment (RL_F_ENTROPY), bit 1 the KL / proximal
+// terms (kl_coef, prox_logp); the default instantiation (XF = 0) carries neither.
+template <typename T, int CL, int NCH, bool EXACT, bool TRACE = false, int VPT = 1, int XF = 0>
 __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) {
   constexpr int EPV = ClVec<T>::EPV;
+  constexpr bool ENT = (XF & 1) != 0, EXT = (XF & 2) != 0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SvShared& sh = *reinterpret_cast<SvShared*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + sizeof(SvShared));
@@ -175,12 +178,14 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
         r.A = r.mt.valid ? a.seq_adv[r.mt.seq] : 0.f;
         r.old = r.mt.valid ? a.old_logp[row] : 0.f;
         r.w = r.mt.valid ? token_weight(r.mt, a.seq_active, inv_tm, a.kn) : 0.0;
-        token_extra(a.kn, row, r.old, r.prox, r.ref);
+        r.prox = r.old;
+        r.ref = 0.f;
+        if (EXT) token_extra(a.kn, row, r.old, r.prox, r.ref);
         return r;
       };
       auto publish_ref = [&](uint32_t p, const Pre& r) {
         sh.refa[p & 3] = make_float4(kCacheShift - r.xk, r.A, r.old, (float)r.w);
-        sh.refc[p & 3] = make_float4(r.prox, r.ref, 0.f, 0.f);
+        if (EXT) sh.refc[p & 3] = make_float4(r.prox, r.ref, 0.f, 0.f);
         sh.refb[p & 3] = make_int4((r.need ? 1 : 0) | (r.mt.valid ? 2 : 0), r.owned ? r.mt.y : -1, 0, 0);
         sm100::mbar_arrive(&sh.refbar[p & 3]);
       };
@@ -204,8 +209,9 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
             if (!redo) {
               const float lp = cur.need ? rs.y : (mt.in_range ? 0.f : logp_from(mt, 0.f, 0.f));
               uint8_t cl = 0;
-              token_epilogue(mt, lp, cur.old, cur.A, a.seq_active, inv_tm, a.kn, acc, &cl, cur.prox, cur.ref);
-              if (ENT && cur.need && mt.valid)  // H = lse - sum p z,  lse = z_y + (log2 S' - 15) ln2
+              if (EXT) token_epilogue(mt, lp, cur.old, cur.A, a.seq_active, inv_tm, a.kn, acc, &cl, cur.prox, cur.ref);
+              else token_epilogue_basic(mt, lp, cur.old, cur.A, a.seq_active, inv_tm, a.kn, acc, &cl);
+              if (ENT && (a.kn.flags & RL_F_ENTROPY) && cur.need && mt.valid)  // H = lse - sum p z
                 acc.v[ST_ENT] += (double)((cur.xk + fast_log2(S) - kCacheShift) * RL_LN2 - rs.z * a.kn.inv_t / S);
               if (a.logp_out) a.logp_out[row] = lp;
               if (a.clipped_out) a.clipped_out[row] = cl;
@@ -232,7 +238,8 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
     const uint64_t k2 = f2pack(k, k);
     const uint32_t my_off = (uint32_t)tid * 16u;
     const bool last_mine = tid < last_nv;
-    const bool tail_mine = tail_owner && tid < n_tail;
+    // EXACT shapes (V = 151936, 128256) have V % 8 == 0: no scalar tail columns
+    const bool tail_mine = !EXACT && tail_owner && tid < n_tail;
     uint4 cache[NCH];  // bf16 e' of this thread's vectors of the current row
 #pragma unroll
     for (int j = 0; j < NCH; ++j) cache[j] = make_uint4(0, 0, 0, 0);
@@ -318,6 +325,8 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       }
       // target column of row p-1: rewritten by the thread that stored its vector (or tail
       // column) above — same-thread program order to the same address.
+      // target column of row p-1: rewritten by the thread that stored its vector (or tail
+      // column) above — same-thread program order to the same address.
       if (mode == SV_GRAD && ycol >= 0) {
         const bool in_tail = ycol >= a.nvec * EPV;
         const int owner = in_tail ? (int)(ycol - a.nvec * EPV) : (int)((ycol / EPV - v0) % kChunkVec);
@@ -350,6 +359,8 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
           for (int r = 0; r < CL; ++r)
             if (r != (int)crank) sm100::st_async_v4(&sh.xch[b][crank], &sh.xbar[b], r, Sc, Tc, 0.f, 0.f);
         }
+        // the peer's st.async completes THIS CTA's barrier (async proxy, like a TMA load): a
+        // CTA-scope wait makes its bytes visible — no cluster-scope acquire (an L1 invalidate)
         sm100::mbar_wait_cluster(&sh.xbar[b], (p >> 1) & 1);
       }
       float S = 0.f, Tx = 0.f;  // rank order: bitwise identical in every CTA of the cluster
@@ -359,13 +370,16 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
         for (int r = 0; r < CL; ++r) Tx += r == (int)crank ? Tc : sh.xch[b][r].y;
       if (tid == 0) RL_SV_EV(p, 3);
       const float4 ra = sh.refa[q4];
-      const float4 rc = sh.refc[q4];
+      const float4 rc = EXT ? sh.refc[q4] : make_float4(ra.z, 0.f, 0.f, 0.f);
       const int4 rb = sh.refb[q4];
       const bool valid = (rb.x & 2) != 0;
       const bool redo = need && !(S < kSvRedo);
       const float lp = need ? (kCacheShift - fast_log2(S)) * RL_LN2 : 0.f;  // ln(2^15 / S')
       float st = 0.f;
-      if (valid && !redo) st = token_scale(token_ratio(lp, ra.z, rc.x, rc.y, ra.y, a.kn), ra.w, ra.y, a.kn);
+      if (valid && !redo) {
+        if (EXT) st = token_scale(token_ratio(lp, ra.z, rc.x, rc.y, ra.y, a.kn), ra.w, ra.y, a.kn);
+        else st = token_scale_basic(token_ratio_basic(lp, ra.z, ra.y, a.kn), ra.w, ra.y, a.kn);
+      }
       mode = redo ? SV_NONE : (st == 0.f ? SV_ZERO : SV_GRAD);
       const float inv_s = 1.f / S;
       q = st == 0.f ? 0.f : st * inv_s;  // (an unread row has S' = 0)
@@ -386,10 +400,10 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
   sm100::cluster_sync();  // no CTA leaves while a peer may still write its smem
 }
 
-template <typename T, int CL, int NCH, bool EXACT = false, bool TRACE = false, int VPT = 1, bool ENT = false>
+template <typename T, int CL, int NCH, bool EXACT = false, bool TRACE = false, int VPT = 1, int XF = 0>
 static rl_status launch_sv(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_ctas) {
   ClArgs a = a0;
-  auto kern = loss_sv_kernel<T, CL, NCH, EXACT, TRACE, VPT, ENT>;
+  auto kern = loss_sv_kernel<T, CL, NCH, EXACT, TRACE, VPT, XF>;
   const size_t head = (sizeof(SvShared) + 127) & ~(size_t)127;
   constexpr size_t slot_bytes = (size_t)VPT * kChunkBytes;
   int nslots = (int)((kSmemMax - head - 256) / (slot_bytes + 16));
@@ -475,13 +489,19 @@ rl_status launch_loss_sv(const void* logits, int32_t dtype, int64_t n, int64_t V
   static int vpt = -1;  // RL_SV_VPT: 16-B vectors per thread per TMA bulk copy (1, 2, 4, 5, 8)
   if (vpt < 0) vpt = getenv("RL_SV_VPT") ? atoi(getenv("RL_SV_VPT")) : 4;
   const bool trace = getenv("RL_TRACE") != nullptr;
-  if (kn.flags & RL_F_ENTROPY) {  // entropy moment in the exp pass (reading N3)
-    if (bf && nch2 == 20) return launch_sv<bf16_t, 2, 20, true, false, 4, true>(a, n, s, n_ctas);
-    if (bf && nch2 == 17) return launch_sv<bf16_t, 2, 17, true, false, 4, true>(a, n, s, n_ctas);
+  const int xf = ((kn.flags & RL_F_ENTROPY) ? 1 : 0) | ((kn.kl_coef != 0.f || kn.prox_logp) ? 2 : 0);
+  if (xf) {  // NEXT-2 terms: compile-time variants of the hot shapes, the general one otherwise
+#define RL_SV_XF(X)                                                                                      \
+    if (xf == X) {                                                                                       \
+      if (bf && nch2 == 20) return launch_sv<bf16_t, 2, 20, true, false, 4, X>(a, n, s, n_ctas);        \
+      if (bf && nch2 == 17) return launch_sv<bf16_t, 2, 17, true, false, 4, X>(a, n, s, n_ctas);        \
+    }
+    RL_SV_XF(1) RL_SV_XF(2) RL_SV_XF(3)
+#undef RL_SV_XF
     if (nch2 <= 20)
-      return bf ? launch_sv<bf16_t, 2, 20, false, false, 4, true>(a, n, s, n_ctas)
-                : launch_sv<float, 2, 20, false, false, 4, true>(a, n, s, n_ctas);
-    return RL_ERR_UNSUPPORTED;  // very wide rows: the two-pass kernel computes it
+      return bf ? launch_sv<bf16_t, 2, 20, false, false, 4, 3>(a, n, s, n_ctas)
+                : launch_sv<float, 2, 20, false, false, 4, 3>(a, n, s, n_ctas);
+    return RL_ERR_UNSUPPORTED;  // very wide rows: the two-pass kernel computes them
   }
   if (bf && nch2 == 20) {
     if (trace) return launch_sv<bf16_t, 2, 20, true, true, 4>(a, n, s, n_ctas);
