@@ -17,6 +17,9 @@ definitions in DESIGN.md §3 (which restate SURVEY.md §8(c) c1–c9):
 * ``policy_loss_fwd_bwd`` – c4–c7, clipped importance-ratio surrogate against the
   behaviour log-probs, token-mean weighting and dL/dlogits = scale·(softmax − onehot).
 * ``vocab_shard_stats`` / ``vocab_combine`` – c8, vocab-parallel log-softmax combine.
+* NEXT rows: ``policy_loss_fwd_bwd``'s ref_logp / prox_logp / want_entropy
+  (k3 KL, decoupled ratio, entropy — readings N1-N3) and ``m2po_mask`` (M2PO second-moment
+  masking, reading M1).
 
 Parity status of every function is listed in DESIGN.md §4 ("pins").
 """
@@ -26,6 +29,7 @@ from .policy_loss import (  # noqa: F401
     AGG_TOKEN_MEAN, AGG_SEQ_MEAN_TOKEN_MEAN, AGG_SUM,
     LossParams,
     decode_bf16,
+    m2po_mask,
     group_advantage,
     seq_bookkeeping,
     token_logprob,

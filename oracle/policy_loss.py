@@ -404,3 +404,42 @@ def vocab_combine(ms, ss, xys):
     with np.errstate(invalid="ignore"):
         S = np.sum(s * np.exp(m - M[None, :]), axis=0)
     return M + np.log(S), np.sum(np.stack(xys), axis=0)
+
+
+# ----------------------------------------------------------------------------- NEXT 1: M2PO
+def m2po_mask(logp, old_logp, valid, tau: float):
+    """M2PO second-moment trust masking (reading M1; "M2PO ... with
+    m²-threshold 0.01" — the paper gives no formula, so this follows the M2PO definition it cites):
+
+      delta_t = logp_t - old_t,  m_t = delta_t^2           for valid tokens (fp32, the kernel's
+                                                            precision: the mask is a decision)
+      order the valid tokens by m descending, ties by token index ascending;
+      k* = the smallest k >= 0 such that the mean of m over the remaining n_valid - k tokens is
+           <= tau (sums in fp64, left to right over the sorted order); k* = n_valid if none
+      mask_t = 1 for the kept valid tokens, 0 for masked and invalid tokens.
+
+    Returns (mask u8[N], k_star, m2_before, m2_after) with m2 = mean of m over the tokens kept."""
+    lp = np.asarray(logp, dtype=np.float32)
+    old = np.asarray(old_logp, dtype=np.float32)
+    val = np.asarray(valid) != 0
+    n = len(lp)
+    d = (lp - old).astype(np.float32)
+    m = (d * d).astype(np.float32)
+    idx = [t for t in range(n) if val[t]]
+    idx.sort(key=lambda t: (-float(m[t]), t))
+    nv = len(idx)
+    # suffix sums S_k = sum of m over sorted positions k..nv-1 (fp64, sequential from the end)
+    suffix = [0.0] * (nv + 1)
+    for i in range(nv - 1, -1, -1):
+        suffix[i] = suffix[i + 1] + float(m[idx[i]])
+    k_star = nv
+    for k in range(nv):
+        if suffix[k] / (nv - k) <= tau:
+            k_star = k
+            break
+    mask = np.zeros(n, dtype=np.uint8)
+    for i in range(k_star, nv):
+        mask[idx[i]] = 1
+    m2_before = suffix[0] / nv if nv else 0.0
+    m2_after = suffix[k_star] / (nv - k_star) if nv > k_star else 0.0
+    return mask, k_star, m2_before, m2_after

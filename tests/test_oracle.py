@@ -543,3 +543,48 @@ def test_entropy_closed_forms_and_scipy():
     for t in range(1, 6):
         assert abs(out["entropy"][t] - scipy_stats.entropy(_softmax(x[t]))) < 1e-12
     assert abs(out["stats"]["entropy_sum"] - math.fsum(out["entropy"])) < 1e-12
+
+
+# ----------------------------------------------------------------------------- NEXT 1: M2PO (M1)
+def test_m2po_mask_is_the_minimal_subset_by_brute_force():
+    """M1 pin: over every subset of a tiny batch, the fewest tokens whose removal brings the kept
+    mean of (logp - old)^2 to <= tau equals the oracle's k*, and its kept set satisfies the bound."""
+    import itertools
+    rng = np.random.default_rng(50)
+    for trial in range(40):
+        n = int(rng.integers(1, 11))
+        lp = rng.normal(size=n).astype(np.float32)
+        old = (lp + rng.normal(size=n) * rng.uniform(0.05, 1.0)).astype(np.float32)
+        valid = (rng.random(n) < 0.85).astype(np.uint8)
+        tau = float(rng.uniform(0.001, 0.5))
+        mask, k, _, m2a = oracle.m2po_mask(lp, old, valid, tau)
+        m = ((lp - old).astype(np.float32) ** 2).astype(np.float64)
+        vidx = [t for t in range(n) if valid[t]]
+        best = len(vidx)
+        for r in range(len(vidx) + 1):                      # r = tokens removed
+            ok = any(np.mean([m[t] for t in vidx if t not in drop]) <= tau
+                     for drop in map(set, itertools.combinations(vidx, r)) if len(vidx) - r > 0)
+            if ok:
+                best = r
+                break
+        assert k == best, (trial, k, best)
+        kept = [t for t in range(n) if mask[t]]
+        assert all(valid[t] for t in kept) and len(kept) == len(vidx) - k
+        if kept:
+            assert np.mean([m[t] for t in kept]) <= tau and abs(m2a - np.mean([m[t] for t in kept])) < 1e-12
+
+
+def test_m2po_limits():
+    rng = np.random.default_rng(51)
+    lp = rng.normal(size=50).astype(np.float32)
+    old = (lp + rng.normal(size=50) * 0.3).astype(np.float32)
+    valid = np.ones(50, dtype=np.uint8)
+    mask, k, m2b, m2a = oracle.m2po_mask(lp, old, valid, 1e9)       # huge tau keeps everything
+    assert k == 0 and mask.sum() == 50 and m2a == m2b
+    mask, k, _, _ = oracle.m2po_mask(lp, lp, valid, 0.0)              # ratio 1: nothing to mask
+    assert k == 0 and mask.sum() == 50
+    mask, k, _, m2a = oracle.m2po_mask(lp, old, valid, 0.0)           # tau 0 keeps only m == 0 tokens
+    assert k == 50 - int(np.sum(((lp - old).astype(np.float32) ** 2) == 0)) and m2a == 0.0
+    # larger tau never masks more (monotone)
+    ks = [oracle.m2po_mask(lp, old, valid, t)[1] for t in (0.01, 0.03, 0.1, 0.3)]
+    assert ks == sorted(ks, reverse=True)
