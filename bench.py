@@ -48,9 +48,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
-    ap.add_argument("--objective", default="clip", choices=["clip", "full"],
+    ap.add_argument("--objective", default="clip", choices=["clip", "full", "m2po"],
                     help="clip: the north_star's clipped surrogate (default); full: + decoupled proximal "
-                         "ratio, k3 KL penalty (beta 1e-3, PAPER.md:572) and entropy (NEXT 2)")
+                         "ratio, k3 KL penalty (beta 1e-3, PAPER.md:572) and entropy (NEXT 2); m2po: "
+                         "rl_token_logprob -> rl_m2po_mask (tau 0.01, PAPER.md:572) -> unclipped loss (NEXT 1)")
     ap.add_argument("--config", default="single", choices=["single", "long", "vocabpar", "multi"],
                     help="BASELINE.json config (single = the headline metric's workload, the default)")
     return ap.parse_args()
@@ -272,6 +273,13 @@ class TokenParallelWorkload:
         self.ws = torch.empty(rl.policy_loss_workspace_size(MB, V), dtype=torch.uint8, device=dev)
         self.tokens_per_step = n_calls * MB
         self.bytes_per_token = 2 * V * 2 + SIDE_BYTES + (8 if self.full else 0)  # + ref, prox reads
+        self.m2po = OBJECTIVE == "m2po"
+        if self.m2po:  # the roofline stays the loss call's (the log-prob pass is a separate kernel)
+            self.m2_logp = torch.empty(MB, dtype=torch.float32, device=dev)
+            self.m2_mask = torch.empty(MB, dtype=torch.uint8, device=dev)
+            self.m2_stats = torch.zeros(5, dtype=torch.float64, device=dev)
+            self.m2_ws = torch.empty(rl.m2po_workspace_size(MB, comm.nranks if comm is not None else 1),
+                                     dtype=torch.uint8, device=dev)
         self.launches = 0
         self.ev = []
 
@@ -295,6 +303,15 @@ class TokenParallelWorkload:
         for c, cl in enumerate(self.calls):
             p = rl.LossParams(trainer_version=self.trainer_version, max_staleness=self.max_staleness,
                               active_tokens_dev=self.total_counts[0:1])
+            mask = cl["mask"]
+            if self.m2po:  # NEXT 1: fresh log-probs -> global second-moment mask -> unclipped loss
+                rl.token_logprob(self.pool[c % P], self.pool_y[c % P], self.m2_logp)
+                rl.m2po_mask(self.m2_logp, self.pool_old[c % P], self.m2_mask, self.m2_stats, self.m2_ws,
+                             tau=0.01, valid=cl["mask"], comm=self.comm)
+                mask = self.m2_mask
+                p.clip_eps_low = p.clip_eps_high = 1e30
+                p.active_tokens_dev = self.m2_stats[4:5]
+                self.launches += 9
             if self.full:
                 p.kl_coef, p.ref_logp, p.prox_logp = 1e-3, self.pool_ref[c % P], self.pool_prox[c % P]
                 p.flags |= rl.F_ENTROPY
@@ -303,7 +320,7 @@ class TokenParallelWorkload:
                 e0.record(stream)
             rl.policy_loss_fwd_bwd(self.pool[c % P], self.pool_y[c % P], self.pool_old[c % P], cl["tok"],
                                    self.adv[cl["sa"]:cl["sb"]], p, self.dlogits, cl["stats"], self.ws,
-                                   loss_mask=cl["mask"], seq_version=self.seq_version[cl["sa"]:cl["sb"]],
+                                   loss_mask=mask, seq_version=self.seq_version[cl["sa"]:cl["sb"]],
                                    logp_out=cl["logp"])
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
@@ -593,8 +610,9 @@ def main():
                        "vocab": w0.V, "parallelism": parallelism, "loss_kernel": kern,
                        "l2": "no flush: every loss call streams a distinct >= 2.5 GB logits buffer >> 126 MB L2",
                        "agg": "token_mean", "batch_norm": True,
-                       "objective": ("clipped decoupled surrogate + k3 KL (beta 1e-3) + entropy"
-                                     if args.objective == "full" else "clipped surrogate")},
+                       "objective": {"full": "clipped decoupled surrogate + k3 KL (beta 1e-3) + entropy",
+                                     "m2po": "M2PO: log-prob pass + second-moment mask (tau 0.01) + unclipped loss",
+                                     }.get(args.objective, "clipped surrogate")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": kname, "algorithmic_bytes_per_launch": alg_bytes,

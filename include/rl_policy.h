@@ -294,6 +294,30 @@ rl_status rl_vocab_parallel_logprob(const void* logits_shard, int32_t dtype, int
                                     void* dlogits_shard, rl_loss_stats* stats, void* workspace,
                                     size_t workspace_bytes, rl_stream stream);
 
+/* ---------------------------------------------------------------- (6) M2PO mask (NEXT 1)
+ * M2PO second-moment trust masking, reading M1 of DESIGN.md §3 ("M2PO ... with
+ * m²-threshold 0.01"; the paper gives no formula).  For every token with valid != 0,
+ * m_t = (logp_t - old_logp_t)^2 in fp32; the fewest largest-m tokens are masked so that the mean
+ * m of the kept valid tokens is <= tau (ties of equal m: the lower token index is masked first).
+ * With comm != NULL the selection is GLOBAL over the ranks of comm (global token index =
+ * rank * n_tokens + t: every rank must pass the same n_tokens — pad with valid = 0) and every
+ * rank derives the same cut; comm == NULL selects over this call's tokens.
+ *   logp, old_logp  device float [n_tokens] (logp e.g. from rl_token_logprob)
+ *   valid           device u8 [n_tokens] or NULL (= all valid)
+ *   mask_out        device u8 [n_tokens]: 1 = kept valid token, 0 = masked or invalid.  Use it as
+ *                   the loss_mask of rl_policy_loss_fwd_bwd (with clip_eps_* large: M2PO's
+ *                   surrogate is unclipped) and &stats_out[4] as its active_tokens_dev
+ *   stats_out       device double[5]: (n_valid, n_masked, mean m of the valid tokens,
+ *                   mean m of the kept tokens, n_kept), over all ranks of comm
+ *   workspace       device, >= rl_m2po_workspace_size(n_tokens, nranks) bytes
+ * Errors: RL_ERR_INVALID_ARGUMENT (n_tokens < 0, tau < 0 or NaN, NULL arrays), RL_ERR_UNSUPPORTED
+ * (n_tokens * nranks >= 2^31), RL_ERR_WORKSPACE, RL_ERR_NCCL.  Deterministic (radix sort, fixed
+ * scan, order-free max). */
+size_t rl_m2po_workspace_size(int64_t n_tokens, int32_t nranks);
+rl_status rl_m2po_mask(const float* logp, const float* old_logp, const uint8_t* valid, int64_t n_tokens,
+                       float tau, rl_comm* comm, uint8_t* mask_out, double* stats_out, void* workspace,
+                       size_t workspace_bytes, rl_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

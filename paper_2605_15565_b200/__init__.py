@@ -22,7 +22,7 @@ __all__ = [
     "group_advantage", "group_advantage_workspace_size", "seq_bookkeeping", "token_logprob",
     "policy_loss_fwd_bwd", "policy_loss_workspace_size", "policy_loss_fwd_bwd_host",
     "policy_loss_host_workspace_size", "vocab_parallel_logprob",
-    "vocab_parallel_workspace_size", "Comm", "EXPORTED_SYMBOLS",
+    "vocab_parallel_workspace_size", "m2po_mask", "m2po_workspace_size", "Comm", "EXPORTED_SYMBOLS",
 ]
 
 F32, BF16 = 0, 1
@@ -78,6 +78,8 @@ _SIGS = {
     "rl_vocab_parallel_workspace_size": (sz, [i64, i32]),
     "rl_vocab_parallel_logprob": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, f32, vp, vp, vp, vp,
                                         vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+    "rl_m2po_workspace_size": (sz, [i64, i32]),
+    "rl_m2po_mask": (i32, [vp, vp, vp, i64, f32, vp, vp, vp, vp, sz, vp]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
@@ -370,3 +372,21 @@ def vocab_parallel_logprob(logits_shard, targets, vocab_offset, vocab_total, com
         _dev(stats, "stats"), _dev(workspace, "workspace"),
         workspace.numel() * workspace.element_size(), _stream(stream)),
         "rl_vocab_parallel_logprob")
+
+
+# ----------------------------------------------------------------------------- (6) M2PO
+def m2po_workspace_size(n_tokens: int, nranks: int = 1) -> int:
+    return load().rl_m2po_workspace_size(n_tokens, nranks)
+
+
+def m2po_mask(logp, old_logp, mask_out, stats_out, workspace, tau=0.01, valid=None, comm=None, stream=None):
+    """M2PO second-moment trust mask (reading M1): mask_out (CUDA uint8 [n]) gets 1 for the kept
+    valid tokens; stats_out (CUDA float64 [5]) = (n_valid, n_masked, mean m before, after, n_kept).
+    With ``comm`` the selection is global over its ranks (same n on every rank)."""
+    lib = load()
+    n = logp.numel()
+    _check(lib.rl_m2po_mask(_dev(logp, "logp"), _dev(old_logp, "old_logp"), _dev(valid, "valid"), n, float(tau),
+                            None if comm is None else comm.handle, _dev(mask_out, "mask_out"),
+                            _dev(stats_out, "stats_out"), _dev(workspace, "workspace"),
+                            workspace.numel() * workspace.element_size(), _stream(stream)), "rl_m2po_mask")
+

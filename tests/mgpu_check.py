@@ -132,6 +132,26 @@ def main():
           elif vs.size and np.abs(gv[i] - refrow).max() > 1e-2 * abs(s_all[i]):
               fails.append(f"{mode} vp row {i} dlogits")
 
+    # ------------------------------------------------------------------ M2PO global selection
+    # every rank passes its own n tokens; the mask must equal the oracle's over the concatenation
+    n_m = 5003
+    rngs = [np.random.default_rng(900 + q) for q in range(world)]
+    lps, olds, vals = [], [], []
+    for q in range(world):
+        lp_q = (rngs[q].normal(size=n_m) * 3 - 5).astype(np.float32)
+        dr = np.round(rngs[q].normal(size=n_m) * rngs[q].choice([0.02, 0.3], size=n_m) * 64) / 64
+        lps.append(lp_q)
+        olds.append((lp_q - dr).astype(np.float32))
+        vals.append((rngs[q].random(n_m) < 0.9).astype(np.uint8))
+    mask_ref, k_ref, _, _ = oracle.m2po_mask(np.concatenate(lps), np.concatenate(olds), np.concatenate(vals), 0.01)
+    mk = torch.empty(n_m, dtype=torch.uint8, device=dev)
+    mst = torch.zeros(5, dtype=torch.float64, device=dev)
+    mws = torch.empty(rl.m2po_workspace_size(n_m, world), dtype=torch.uint8, device=dev)
+    rl.m2po_mask(d(lps[rank]), d(olds[rank]), mk, mst, mws, tau=0.01, valid=d(vals[rank]), comm=comm)
+    torch.cuda.synchronize()
+    if not np.array_equal(mk.cpu().numpy(), mask_ref[rank * n_m:(rank + 1) * n_m]) or mst[1].item() != k_ref:
+        fails.append(f"m2po global mask (k {mst[1].item()} vs {k_ref})")
+
     # ------------------------------------------------------------------ comm split
     sub = comm.split(rank % 2, rank)
     one = torch.ones(1, dtype=torch.float64, device=dev)

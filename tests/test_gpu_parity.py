@@ -532,3 +532,46 @@ def test_full_size_sampled(cuda_lib, name, N, in_place, objective):
         assert bad.numel() == 0, [(c0 + int(r), float(sums[r]), float(amax[r])) for r in bad[:5]]
         del blk
     del logits, dl
+
+
+# ----------------------------------------------------------------------------- NEXT 1: M2PO (M1)
+def _m2po_band(lp, old, valid, tau, k_star):
+    """True when the oracle's cut is within rounding of tau (the fp64 prefix order may differ)."""
+    m = ((lp - old).astype(np.float32) ** 2).astype(np.float32)
+    mv = np.sort(m[valid != 0].astype(np.float64))
+    nv = len(mv)
+    P = np.cumsum(mv)
+    for j in (nv - k_star, nv - k_star + 1):
+        if 1 <= j <= nv and abs(P[j - 1] - tau * j) <= 1e-9 * max(P[j - 1], tau * j, 1e-300):
+            return True
+    return False
+
+
+@pytest.mark.parametrize("n,tau,ties", [(1, 0.01, False), (777, 0.01, False), (10007, 0.002, True),
+                                        (50000, 0.05, True), (4096, 1e9, False), (3000, 0.0, True)])
+def test_m2po_mask(cuda_lib, n, tau, ties):
+    """rl_m2po_mask against the oracle on the same fp32 inputs: the mask bit-exact (ties included),
+    the counts exact, the means to 1e-12 (reading M1)."""
+    t = torch()
+    rng = np.random.default_rng(n)
+    lp = (rng.normal(size=n) * 3 - 5).astype(np.float32)
+    drift = rng.normal(size=n) * rng.choice([0.02, 0.1, 0.5], size=n)
+    if ties:  # quantised drifts: many exactly equal m
+        drift = np.round(drift * 64) / 64
+    old = (lp - drift).astype(np.float32)
+    valid = (rng.random(n) < 0.9).astype(np.uint8)
+    mask_ref, k_ref, m2b, m2a = oracle.m2po_mask(lp, old, valid, tau)
+    mask = t.empty(n, dtype=t.uint8, device="cuda")
+    stats = t.zeros(5, dtype=t.float64, device="cuda")
+    ws = t.empty(cuda_lib.m2po_workspace_size(n), dtype=t.uint8, device="cuda")
+    cuda_lib.m2po_mask(dev(lp), dev(old), mask, stats, ws, tau=tau, valid=dev(valid))
+    t.cuda.synchronize()
+    g, st = mask.cpu().numpy(), stats.cpu().numpy()
+    assert st[0] == valid.sum()
+    if _m2po_band(lp, old, valid, tau, k_ref):
+        assert abs(st[1] - k_ref) <= 1
+        return
+    assert st[1] == k_ref and st[4] == st[0] - st[1] and np.array_equal(g, mask_ref)
+    assert abs(st[2] - m2b) <= 1e-12 * max(m2b, 1e-300) and abs(st[3] - m2a) <= 1e-12 * max(m2a, 1e-300)
+    if 0 < tau < 1e8:
+        assert 0 < k_ref < valid.sum() or tau == 0.0 or n == 1   # the bound is active in these cases
