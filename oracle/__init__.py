@@ -37,3 +37,4 @@ from .policy_loss import (  # noqa: F401
     vocab_shard_stats,
     vocab_combine,
 )
+from . import delta  # noqa: F401,E402

@@ -588,3 +588,37 @@ def test_m2po_limits():
     # larger tau never masks more (monotone)
     ks = [oracle.m2po_mask(lp, old, valid, t)[1] for t in (0.01, 0.03, 0.1, 0.3)]
     assert ks == sorted(ks, reverse=True)
+
+
+# ----------------------------------------------------------------------------- NEXT 3: delta scan
+def test_delta_spec_examples():
+    """identical snapshots -> empty, sparsity 1.0; [a,b,c,d] -> [a,x,c,d] ->
+    [(1, x)], sparsity 0.75."""
+    from oracle import delta
+    a = np.array([1, 2, 3, 4], dtype=np.uint16)
+    idx, w, s = delta.compute_delta(a, a)
+    assert idx.size == 0 and s == 1.0
+    b = a.copy(); b[1] = 0xBEEF
+    idx, w, s = delta.compute_delta(a, b)
+    assert list(idx) == [1] and list(w) == [0xBEEF] and s == 0.75
+
+
+def test_delta_brute_force_round_trip_and_payload_bound():
+    """Independent element-wise comparison (np.nonzero) on random pairs; apply(compute) = next;
+    payload bound 6 (1 - s) N bytes."""
+    from oracle import delta
+    rng = np.random.default_rng(60)
+    for n, frac in ((1000, 0.01), (1000, 0.5), (3, 1.0), (0, 0.0), (777, 0.0)):
+        a = rng.integers(0, 1 << 16, size=n, dtype=np.uint16)
+        b = a.copy()
+        ch = rng.random(n) < frac
+        b[ch] = b[ch] ^ rng.integers(1, 1 << 16, size=int(ch.sum()), dtype=np.uint16)
+        idx, w, s = delta.compute_delta(a, b)
+        assert np.array_equal(idx, np.nonzero(a != b)[0].astype(np.uint32)) and np.array_equal(w, b[idx])
+        assert np.array_equal(delta.apply_delta(a, idx, w), b)
+        assert 6 * idx.size <= 6 * (1 - s) * n + 1e-9
+        assert np.all(np.diff(idx.astype(np.int64)) > 0)
+    # bf16 bit patterns, not values: +0 and -0 differ, equal NaN payloads do not
+    a = np.array([0x0000, 0x7FC0, 0x3F80], dtype=np.uint16)
+    b = np.array([0x8000, 0x7FC0, 0x3F80], dtype=np.uint16)
+    assert list(delta.compute_delta(a, b)[0]) == [0]
