@@ -1,0 +1,256 @@
+// (7) bf16 delta-sparsity scan and sparse encode / apply — NEXT 3 of SURVEY.md §8(f)
+// ("the trainer needs to ship only a tiny fraction of its weights",
+// sparsity 0.989-0.993; SPEC.md:297-313 compute_delta / apply_delta).
+//
+// encode: the indices (increasing) and new words of every position where two 16-bit snapshots
+// differ — a single-pass stream compaction: each snapshot is read once (16-B loads), the ~1 % of
+// changes written once, HBM-bound on the two reads.  Persistent CTAs take 16384-word tiles in
+// index order (static assignment); a tile's output offset comes from a decoupled look-back over the
+// per-tile status words (flag + count in one 64-bit word), so no tile waits for a full
+// grid-wide scan and the output stays sorted by index.
+// apply: base[idx[j]] = word[j] (scatter).
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace rl {
+
+constexpr int kDtThreads = 256;
+constexpr int kDtVec = 8;                                     // 16-B vectors per thread per array
+constexpr int kDtTile = kDtThreads * kDtVec * 8;              // 16384 words per tile
+constexpr uint64_t kStAgg = 1ull << 62, kStPre = 2ull << 62, kStMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// bit e of the result: word e of the 8-word vectors a, b differ
+__device__ __forceinline__ uint32_t diff8(const uint4& a, const uint4& b) {
+  const uint32_t x[4] = {a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w};
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) m |= ((x[i] & 0xFFFFu) ? 1u : 0u) << (2 * i) | ((x[i] >> 16) ? 1u : 0u) << (2 * i + 1);
+  return m;
+}
+
+__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int o) {
+  return ((uint64_t)__shfl_up_sync(0xffffffffu, (uint32_t)(v >> 32), o) << 32) |
+         __shfl_up_sync(0xffffffffu, (uint32_t)v, o);
+}
+
+// Tile layout (coalesced): thread t compares vectors u * 256 + t, u < 8, of both snapshots; the
+// tile's changes are written in index order = (u, t, word) order.  The 8 per-vector counts
+// (<= 8 each, <= 2048 per tile and vector slot) are packed in 16-bit fields of two u64 and
+// scanned once over the block.
+__device__ __forceinline__ void dt_load(const uint16_t* __restrict__ prev, const uint16_t* __restrict__ next,
+                                        int64_t wt, int64_t n, uint4 (&va)[kDtVec], uint4 (&vb)[kDtVec]) {
+  if (wt + kDtTile <= n) {
+    const uint4* pa = reinterpret_cast<const uint4*>(prev + wt) + threadIdx.x;
+    const uint4* pb = reinterpret_cast<const uint4*>(next + wt) + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kDtVec; ++u) {
+      va[u] = ld_stream_v4(pa + u * kDtThreads);
+      vb[u] = ld_stream_v4(pb + u * kDtThreads);
+    }
+  }
+}
+
+// bits of the words that differ in this thread's 8 vector slots of the tile at wt
+__device__ __forceinline__ uint64_t dt_masks(const uint16_t* __restrict__ prev, const uint16_t* __restrict__ next,
+                                             int64_t wt, int64_t n, const uint4 (&va)[kDtVec],
+                                             const uint4 (&vb)[kDtVec]) {
+  uint64_t masks = 0;
+  if (wt + kDtTile <= n) {
+#pragma unroll
+    for (int u = 0; u < kDtVec; ++u) masks |= (uint64_t)diff8(va[u], vb[u]) << (8 * u);
+  } else {  // the ragged last tile: guarded scalar reads
+#pragma unroll
+    for (int u = 0; u < kDtVec; ++u)
+      for (int e = 0; e < 8; ++e) {
+        const int64_t w = wt + 8 * ((int64_t)u * kDtThreads + threadIdx.x) + e;
+        if (w < n && prev[w] != next[w]) masks |= 1ull << (8 * u + e);
+      }
+  }
+  return masks;
+}
+
+// Tile layout (coalesced): thread t compares vectors u * 256 + t, u < 8, of both snapshots; the
+// tile's changes are written in index order = (u, t, word) order.  The 8 per-vector counts
+// (<= 8 each, <= 2048 per tile and vector slot) are packed in 16-bit fields of two u64 and
+// scanned once over the block.  Tiles are assigned statically (blockIdx.x + k * gridDim.x; the
+// grid is all-resident, so a look-back only waits on running CTAs); several CTAs per SM overlap
+// one tile's loads with another's scan, look-back and writes.
+__global__ void __launch_bounds__(kDtThreads, 4) delta_encode_kernel(
+    const uint16_t* __restrict__ prev, const uint16_t* __restrict__ next, int64_t n, int64_t n_tiles,
+    uint32_t* __restrict__ idx_out, uint16_t* __restrict__ word_out, int64_t capacity,
+    unsigned long long* __restrict__ count_out, uint64_t* __restrict__ status) {
+  __shared__ uint64_t warp_tot[2][kDtThreads / 32];
+  __shared__ int64_t s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t wt = tile * kDtTile;
+    uint4 va[kDtVec], vb[kDtVec];
+    dt_load(prev, next, wt, n, va, vb);
+    const uint64_t masks = dt_masks(prev, next, wt, n, va, vb);
+    uint64_t c0 = 0, c1 = 0;  // packed per-slot counts: slots 0..3 in c0, 4..7 in c1
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c0 |= (uint64_t)__popc((uint32_t)(masks >> (8 * u)) & 0xFFu) << (16 * u);
+      c1 |= (uint64_t)__popc((uint32_t)(masks >> (8 * (u + 4))) & 0xFFu) << (16 * u);
+    }
+    // ---- block exclusive scan of the packed counts
+    uint64_t i0 = c0, i1 = c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t v0 = shfl_up_u64(i0, o), v1 = shfl_up_u64(i1, o);
+      if (lane >= o) {
+        i0 += v0;
+        i1 += v1;
+      }
+    }
+    if (lane == 31) {
+      warp_tot[0][warp] = i0;
+      warp_tot[1][warp] = i1;
+    }
+    __syncthreads();
+    uint64_t b0 = 0, b1 = 0, t0 = 0, t1 = 0;
+#pragma unroll
+    for (int w = 0; w < kDtThreads / 32; ++w) {
+      const uint64_t x0 = warp_tot[0][w], x1 = warp_tot[1][w];
+      b0 += w < warp ? x0 : 0;
+      b1 += w < warp ? x1 : 0;
+      t0 += x0;
+      t1 += x1;
+    }
+    const uint64_t e0 = b0 + i0 - c0, e1 = b1 + i1 - c1;  // exclusive, per slot
+    uint32_t slot_base[kDtVec], total = 0;                  // slot offsets within the tile
+#pragma unroll
+    for (int u = 0; u < kDtVec; ++u) {
+      slot_base[u] = total;
+      total += (uint32_t)(((u < 4 ? t0 : t1) >> (16 * (u & 3))) & 0xFFFFu);
+    }
+    // ---- decoupled look-back (warp 0, 32 predecessors per step): this tile's output offset
+    if (warp == 0) {
+      int64_t prefix = 0;
+      if (tile == 0) {
+        if (lane == 0) st_release_u64(status + tile, kStPre | (uint64_t)total);
+      } else {
+        if (lane == 0) st_release_u64(status + tile, kStAgg | (uint64_t)total);
+        for (int64_t j = tile - 1;;) {  // window: tiles j - lane
+          const int64_t jj = j - lane;
+          const uint64_t v = jj >= 0 ? ld_acquire_u64(status + jj) : kStPre;  // before tile 0: prefix 0
+          const uint64_t fl = v & ~kStMask;
+          const uint32_t pre = __ballot_sync(0xffffffffu, fl == kStPre);
+          const uint32_t wait = __ballot_sync(0xffffffffu, fl == 0);
+          const int first = pre ? __ffs(pre) - 1 : 32;            // nearest inclusive prefix
+          const uint32_t need = first == 32 ? 0xffffffffu : (0xffffffffu >> (31 - first));
+          if (wait & need) continue;                               // a predecessor still counting
+          uint64_t x = lane <= first ? (v & kStMask) : 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          prefix += (int64_t)x;
+          if (first < 32) break;
+          j -= 32;
+        }
+        if (lane == 0) st_release_u64(status + tile, kStPre | (uint64_t)(prefix + total));
+      }
+      if (lane == 0) {
+        if (tile == n_tiles - 1) *count_out = (unsigned long long)(prefix + total);
+        s_prefix = prefix;
+      }
+    }
+    __syncthreads();
+    const int64_t prefix = s_prefix;
+#pragma unroll
+    for (int u = 0; u < kDtVec; ++u) {
+      uint32_t m = (uint32_t)(masks >> (8 * u)) & 0xFFu;
+      int64_t off = prefix + slot_base[u] + (int64_t)(((u < 4 ? e0 : e1) >> (16 * (u & 3))) & 0xFFFFu);
+      const int64_t w0 = wt + 8 * ((int64_t)u * kDtThreads + tid);
+      while (m) {  // ~1 % of the words: the new word is re-read (L2 hit)
+        const int e = __ffs(m) - 1;
+        m &= m - 1;
+        if (off < capacity) {
+          idx_out[off] = (uint32_t)(w0 + e);
+          word_out[off] = next[w0 + e];
+        }
+        ++off;
+      }
+    }
+    __syncthreads();  // warp_tot / s_prefix reusable
+  }
+}
+
+__global__ void delta_apply_kernel(uint16_t* __restrict__ base, int64_t n, const uint32_t* __restrict__ idx,
+                                   const uint16_t* __restrict__ words, const unsigned long long* __restrict__ count,
+                                   int64_t capacity, unsigned long long* __restrict__ bad) {
+  const int64_t k = (int64_t)min((unsigned long long)capacity, *count);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx[j];
+    if (i < n) base[i] = words[j];
+    else atomicAdd(bad, 1ull);
+  }
+}
+
+static int64_t dt_tiles(int64_t n) { return (n + kDtTile - 1) / kDtTile; }
+
+}  // namespace rl
+
+extern "C" size_t rl_bf16_delta_workspace_size(int64_t n_words) {
+  if (n_words < 0) return 0;
+  return (size_t)(rl::dt_tiles(n_words) + 2) * sizeof(uint64_t);
+}
+
+extern "C" rl_status rl_bf16_delta_encode(const void* prev, const void* next, int64_t n_words, uint32_t* idx_out,
+                                          uint16_t* word_out, int64_t capacity, unsigned long long* count_out,
+                                          void* workspace, size_t workspace_bytes, rl_stream stream) {
+  using namespace rl;
+  if (n_words < 0 || n_words > (int64_t)0xFFFFFFFFll) return fail(RL_ERR_INVALID_ARGUMENT, "n_words must be in [0, 2^32)");
+  if (capacity < 0) return fail(RL_ERR_INVALID_ARGUMENT, "capacity < 0");
+  if (!count_out) return fail(RL_ERR_INVALID_ARGUMENT, "NULL count_out");
+  if (n_words > 0 && (!prev || !next)) return fail(RL_ERR_INVALID_ARGUMENT, "NULL prev/next");
+  if (capacity > 0 && (!idx_out || !word_out)) return fail(RL_ERR_INVALID_ARGUMENT, "NULL idx_out/word_out");
+  if (((uintptr_t)prev & 15) || ((uintptr_t)next & 15)) return fail(RL_ERR_ALIGNMENT, "prev/next must be 16-B aligned");
+  if (!workspace || workspace_bytes < rl_bf16_delta_workspace_size(n_words))
+    return fail(RL_ERR_WORKSPACE, "workspace must be >= %zu bytes", rl_bf16_delta_workspace_size(n_words));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t tiles = dt_tiles(n_words);
+  uint64_t* status = (uint64_t*)workspace;
+  if (cudaMemsetAsync(workspace, 0, (size_t)(tiles + 2) * 8, s) != cudaSuccess) return check_launch("delta memset");
+  if (tiles == 0) {
+    if (cudaMemsetAsync(count_out, 0, 8, s) != cudaSuccess) return check_launch("delta memset");
+    return RL_OK;
+  }
+  static int ctas = 0;
+  if (!ctas) {
+    int dev = 0, sms = 148, occ = 4;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, delta_encode_kernel, kDtThreads, 0);
+    ctas = sms * std::max(occ, 1);  // all resident: a look-back only ever waits on a running tile
+  }
+  const int grid = (int)std::min<int64_t>(tiles, ctas);
+  delta_encode_kernel<<<grid, kDtThreads, 0, s>>>((const uint16_t*)prev, (const uint16_t*)next, n_words, tiles,
+                                                  idx_out, word_out, capacity, count_out, status);
+  return check_launch("delta_encode_kernel");
+}
+
+extern "C" rl_status rl_bf16_delta_apply(void* base, int64_t n_words, const uint32_t* idx, const uint16_t* words,
+                                         const unsigned long long* count, int64_t capacity,
+                                         unsigned long long* bad_index_count, rl_stream stream) {
+  using namespace rl;
+  if (n_words < 0 || capacity < 0) return fail(RL_ERR_INVALID_ARGUMENT, "n_words / capacity < 0");
+  if (!count || !bad_index_count) return fail(RL_ERR_INVALID_ARGUMENT, "NULL count / bad_index_count");
+  if ((n_words > 0 && !base) || (capacity > 0 && (!idx || !words)))
+    return fail(RL_ERR_INVALID_ARGUMENT, "NULL base/idx/words");
+  if (capacity == 0) return RL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = (int)std::min<int64_t>((capacity + 255) / 256, 148 * 8);
+  delta_apply_kernel<<<grid, 256, 0, s>>>((uint16_t*)base, n_words, idx, words, count, capacity, bad_index_count);
+  return check_launch("delta_apply_kernel");
+}
