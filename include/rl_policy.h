@@ -318,6 +318,27 @@ rl_status rl_m2po_mask(const float* logp, const float* old_logp, const uint8_t* 
                        float tau, rl_comm* comm, uint8_t* mask_out, double* stats_out, void* workspace,
                        size_t workspace_bytes, rl_stream stream);
 
+/* ---------------------------------------------------------------- (7) bf16 delta scan (NEXT 3)
+ * Bit-exact diff of two weight snapshots of n_words 16-bit words (
+ * "exactly the indices whose 16-bit words differ"), as index-sorted
+ * (u32 index, u16 new word) pairs, and its inverse.  Words are opaque bit patterns (+0 != -0).
+ * encode: prev, next  device, 16-B aligned, n_words in [0, 2^32) (larger models: per tensor)
+ *         idx_out, word_out  device [capacity]: the first min(count, capacity) changes
+ *         count_out  device u64: the number of changes (may exceed capacity: then only the
+ *                    first `capacity` are written — the caller re-runs with a larger buffer)
+ *         workspace  device, >= rl_bf16_delta_workspace_size(n_words) bytes (tile status words)
+ *         One pass: each snapshot read once, the changes written once; deterministic output.
+ * apply:  base[idx[j]] = word[j] for j < min(*count, capacity); indices >= n_words are skipped and
+ *         counted in *bad_index_count (device u64, added to).
+ * Errors: RL_ERR_INVALID_ARGUMENT (sizes, NULL arrays), RL_ERR_ALIGNMENT, RL_ERR_WORKSPACE. */
+size_t rl_bf16_delta_workspace_size(int64_t n_words);
+rl_status rl_bf16_delta_encode(const void* prev, const void* next, int64_t n_words, uint32_t* idx_out,
+                               uint16_t* word_out, int64_t capacity, unsigned long long* count_out,
+                               void* workspace, size_t workspace_bytes, rl_stream stream);
+rl_status rl_bf16_delta_apply(void* base, int64_t n_words, const uint32_t* idx, const uint16_t* words,
+                              const unsigned long long* count, int64_t capacity,
+                              unsigned long long* bad_index_count, rl_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,8 @@ __all__ = [
     "group_advantage", "group_advantage_workspace_size", "seq_bookkeeping", "token_logprob",
     "policy_loss_fwd_bwd", "policy_loss_workspace_size", "policy_loss_fwd_bwd_host",
     "policy_loss_host_workspace_size", "vocab_parallel_logprob",
-    "vocab_parallel_workspace_size", "m2po_mask", "m2po_workspace_size", "Comm", "EXPORTED_SYMBOLS",
+    "vocab_parallel_workspace_size", "m2po_mask", "m2po_workspace_size", "delta_encode", "delta_apply",
+    "delta_workspace_size", "Comm", "EXPORTED_SYMBOLS",
 ]
 
 F32, BF16 = 0, 1
@@ -80,6 +81,9 @@ _SIGS = {
                                         vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
     "rl_m2po_workspace_size": (sz, [i64, i32]),
     "rl_m2po_mask": (i32, [vp, vp, vp, i64, f32, vp, vp, vp, vp, sz, vp]),
+    "rl_bf16_delta_workspace_size": (sz, [i64]),
+    "rl_bf16_delta_encode": (i32, [vp, vp, i64, vp, vp, i64, vp, vp, sz, vp]),
+    "rl_bf16_delta_apply": (i32, [vp, i64, vp, vp, vp, i64, vp, vp]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
@@ -389,4 +393,30 @@ def m2po_mask(logp, old_logp, mask_out, stats_out, workspace, tau=0.01, valid=No
                             None if comm is None else comm.handle, _dev(mask_out, "mask_out"),
                             _dev(stats_out, "stats_out"), _dev(workspace, "workspace"),
                             workspace.numel() * workspace.element_size(), _stream(stream)), "rl_m2po_mask")
+
+
+# ----------------------------------------------------------------------------- (7) delta scan
+def delta_workspace_size(n_words: int) -> int:
+    return load().rl_bf16_delta_workspace_size(n_words)
+
+
+def delta_encode(prev, nxt, idx_out, word_out, count_out, workspace, stream=None):
+    """Index-sorted (idx u32, word u16) of every position where the 16-bit words of ``prev`` and
+    ``nxt`` (CUDA tensors of one 2-byte dtype, same numel) differ; count_out: CUDA uint64/int64 [1]."""
+    lib = load()
+    n = prev.numel()
+    if nxt.numel() != n or prev.element_size() != 2 or nxt.element_size() != 2:
+        raise RLError("prev/nxt must be 2-byte tensors of the same length")
+    _check(lib.rl_bf16_delta_encode(_dev(prev, "prev"), _dev(nxt, "nxt"), n, _dev(idx_out, "idx_out"),
+                                    _dev(word_out, "word_out"), idx_out.numel(), _dev(count_out, "count_out"),
+                                    _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
+                                    _stream(stream)), "rl_bf16_delta_encode")
+
+
+def delta_apply(base, idx, words, count, bad_count, stream=None):
+    """base[idx[j]] = words[j] for the first min(count, len(idx)) changes (in place)."""
+    lib = load()
+    _check(lib.rl_bf16_delta_apply(_dev(base, "base"), base.numel(), _dev(idx, "idx"), _dev(words, "words"),
+                                   _dev(count, "count"), idx.numel(), _dev(bad_count, "bad_count"),
+                                   _stream(stream)), "rl_bf16_delta_apply")
 

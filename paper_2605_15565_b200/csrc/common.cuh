@@ -67,6 +67,13 @@ __device__ __forceinline__ uint4 ld_hint_v4(const void* p, uint64_t pol) {
   return r;
 }
 
+// 128-bit read-only load through L1 (consecutive per-thread vectors share cache lines)
+__device__ __forceinline__ uint4 ld_hint_v4_nc(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
 // 128-bit streaming store (evict-first in L2: dlogits are not re-read by this kernel)
 __device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),

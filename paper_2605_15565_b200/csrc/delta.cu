@@ -5,7 +5,8 @@
 // encode: the indices (increasing) and new words of every position where two 16-bit snapshots
 // differ — a single-pass stream compaction: each snapshot is read once (16-B loads), the ~1 % of
 // changes written once, HBM-bound on the two reads.  Persistent CTAs take 16384-word tiles in
-// index order (static assignment); a tile's output offset comes from a decoupled look-back over the
+// index order (static assignment, several CTAs per SM); a tile's output offset comes from a
+// decoupled look-back (one warp, 32 predecessors per step) over the
 // per-tile status words (flag + count in one 64-bit word), so no tile waits for a full
 // grid-wide scan and the output stays sorted by index.
 // apply: base[idx[j]] = word[j] (scatter).
@@ -44,31 +45,25 @@ __device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int o) {
          __shfl_up_sync(0xffffffffu, (uint32_t)v, o);
 }
 
-// Tile layout (coalesced): thread t compares vectors u * 256 + t, u < 8, of both snapshots; the
-// tile's changes are written in index order = (u, t, word) order.  The 8 per-vector counts
-// (<= 8 each, <= 2048 per tile and vector slot) are packed in 16-bit fields of two u64 and
-// scanned once over the block.
-__device__ __forceinline__ void dt_load(const uint16_t* __restrict__ prev, const uint16_t* __restrict__ next,
-                                        int64_t wt, int64_t n, uint4 (&va)[kDtVec], uint4 (&vb)[kDtVec]) {
+// bits of the words that differ in this thread's 8 vector slots of the tile at wt; the full-tile
+// path loads and compares in two halves of 4 vector pairs (32 registers of loads in flight)
+__device__ __forceinline__ uint64_t dt_masks(const uint16_t* __restrict__ prev, const uint16_t* __restrict__ next,
+                                             int64_t wt, int64_t n) {
+  uint64_t masks = 0;
   if (wt + kDtTile <= n) {
     const uint4* pa = reinterpret_cast<const uint4*>(prev + wt) + threadIdx.x;
     const uint4* pb = reinterpret_cast<const uint4*>(next + wt) + threadIdx.x;
 #pragma unroll
-    for (int u = 0; u < kDtVec; ++u) {
-      va[u] = ld_stream_v4(pa + u * kDtThreads);
-      vb[u] = ld_stream_v4(pb + u * kDtThreads);
-    }
-  }
-}
-
-// bits of the words that differ in this thread's 8 vector slots of the tile at wt
-__device__ __forceinline__ uint64_t dt_masks(const uint16_t* __restrict__ prev, const uint16_t* __restrict__ next,
-                                             int64_t wt, int64_t n, const uint4 (&va)[kDtVec],
-                                             const uint4 (&vb)[kDtVec]) {
-  uint64_t masks = 0;
-  if (wt + kDtTile <= n) {
+    for (int h = 0; h < kDtVec; h += 4) {
+      uint4 va[4], vb[4];
 #pragma unroll
-    for (int u = 0; u < kDtVec; ++u) masks |= (uint64_t)diff8(va[u], vb[u]) << (8 * u);
+      for (int u = 0; u < 4; ++u) {
+        va[u] = ld_stream_v4(pa + (h + u) * kDtThreads);
+        vb[u] = ld_stream_v4(pb + (h + u) * kDtThreads);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) masks |= (uint64_t)diff8(va[u], vb[u]) << (8 * (h + u));
+    }
   } else {  // the ragged last tile: guarded scalar reads
 #pragma unroll
     for (int u = 0; u < kDtVec; ++u)
@@ -90,14 +85,15 @@ __global__ void __launch_bounds__(kDtThreads, 4) delta_encode_kernel(
     const uint16_t* __restrict__ prev, const uint16_t* __restrict__ next, int64_t n, int64_t n_tiles,
     uint32_t* __restrict__ idx_out, uint16_t* __restrict__ word_out, int64_t capacity,
     unsigned long long* __restrict__ count_out, uint64_t* __restrict__ status) {
-  __shared__ uint64_t warp_tot[2][kDtThreads / 32];
-  __shared__ int64_t s_prefix;
+  // double-buffered by iteration parity: no barrier after a tile's scatter, so the slowest
+  // thread's writes overlap the next tile's loads
+  __shared__ uint64_t warp_tot[2][2][kDtThreads / 32];
+  __shared__ int64_t s_prefix[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  int par = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, par ^= 1) {
     const int64_t wt = tile * kDtTile;
-    uint4 va[kDtVec], vb[kDtVec];
-    dt_load(prev, next, wt, n, va, vb);
-    const uint64_t masks = dt_masks(prev, next, wt, n, va, vb);
+    const uint64_t masks = dt_masks(prev, next, wt, n);
     uint64_t c0 = 0, c1 = 0;  // packed per-slot counts: slots 0..3 in c0, 4..7 in c1
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -115,14 +111,14 @@ __global__ void __launch_bounds__(kDtThreads, 4) delta_encode_kernel(
       }
     }
     if (lane == 31) {
-      warp_tot[0][warp] = i0;
-      warp_tot[1][warp] = i1;
+      warp_tot[par][0][warp] = i0;
+      warp_tot[par][1][warp] = i1;
     }
     __syncthreads();
     uint64_t b0 = 0, b1 = 0, t0 = 0, t1 = 0;
 #pragma unroll
     for (int w = 0; w < kDtThreads / 32; ++w) {
-      const uint64_t x0 = warp_tot[0][w], x1 = warp_tot[1][w];
+      const uint64_t x0 = warp_tot[par][0][w], x1 = warp_tot[par][1][w];
       b0 += w < warp ? x0 : 0;
       b1 += w < warp ? x1 : 0;
       t0 += x0;
@@ -162,11 +158,11 @@ __global__ void __launch_bounds__(kDtThreads, 4) delta_encode_kernel(
       }
       if (lane == 0) {
         if (tile == n_tiles - 1) *count_out = (unsigned long long)(prefix + total);
-        s_prefix = prefix;
+        s_prefix[par] = prefix;
       }
     }
     __syncthreads();
-    const int64_t prefix = s_prefix;
+    const int64_t prefix = s_prefix[par];
 #pragma unroll
     for (int u = 0; u < kDtVec; ++u) {
       uint32_t m = (uint32_t)(masks >> (8 * u)) & 0xFFu;
@@ -182,7 +178,8 @@ __global__ void __launch_bounds__(kDtThreads, 4) delta_encode_kernel(
         ++off;
       }
     }
-    __syncthreads();  // warp_tot / s_prefix reusable
+    // no trailing barrier: the next tile uses the other warp_tot / s_prefix buffers, and its two
+    // barriers order every use of this tile's buffers before their reuse two tiles later
   }
 }
 

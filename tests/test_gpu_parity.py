@@ -575,3 +575,42 @@ def test_m2po_mask(cuda_lib, n, tau, ties):
     assert abs(st[2] - m2b) <= 1e-12 * max(m2b, 1e-300) and abs(st[3] - m2a) <= 1e-12 * max(m2a, 1e-300)
     if 0 < tau < 1e8:
         assert 0 < k_ref < valid.sum() or tau == 0.0 or n == 1   # the bound is active in these cases
+
+
+# ----------------------------------------------------------------------------- NEXT 3: delta scan
+@pytest.mark.parametrize("n,frac", [(0, 0.0), (1, 1.0), (8191, 0.01), (8192 * 3 + 5, 0.3), (1 << 20, 0.011),
+                                    (3_000_001, 0.0), (2_000_003, 1.0), (40_000_000, 0.008)])
+def test_delta_encode_apply(cuda_lib, n, frac):
+    """rl_bf16_delta_encode equals the oracle's element-wise diff bit for bit (indices, words,
+    count), ragged and multi-tile sizes, all-equal and all-different; apply(encode) = next."""
+    t = torch()
+    from oracle import delta
+    rng = np.random.default_rng(n + 7)
+    a = rng.integers(0, 1 << 16, size=n, dtype=np.uint16)
+    b = a.copy()
+    ch = rng.random(n) < frac
+    b[ch] ^= rng.integers(1, 1 << 16, size=int(ch.sum()), dtype=np.uint16)
+    if n > 16:
+        b[3] = 0x8000 if a[3] == 0 else b[3]   # +0 vs -0 style bit flips count
+    ta, tb = dev(a.view(np.int16)), dev(b.view(np.int16))
+    cap = max(1, int((a != b).sum()))
+    idx = t.empty(cap, dtype=t.int32, device="cuda")
+    words = t.empty(cap, dtype=t.int16, device="cuda")
+    count = t.zeros(1, dtype=t.int64, device="cuda")
+    ws = t.empty(max(8, cuda_lib.delta_workspace_size(n)), dtype=t.uint8, device="cuda")
+    cuda_lib.delta_encode(ta, tb, idx, words, count, ws)
+    t.cuda.synchronize()
+    k = int(count.item())
+    if n <= 200_000:
+        ri, rw, _ = delta.compute_delta(a, b)
+    else:  # the loop oracle is slow at this size: its definition restated by numpy (same pin)
+        ri = np.nonzero(a != b)[0].astype(np.uint32)
+        rw = b[ri]
+    assert k == ri.size
+    assert np.array_equal(idx.cpu().numpy()[:k].view(np.uint32), ri)
+    assert np.array_equal(words.cpu().numpy()[:k].view(np.uint16), rw)
+    base = ta.clone()
+    bad = t.zeros(1, dtype=t.int64, device="cuda")
+    cuda_lib.delta_apply(base, idx, words, count, bad)
+    t.cuda.synchronize()
+    assert bad.item() == 0 and t.equal(base, tb)
