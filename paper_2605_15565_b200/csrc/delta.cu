@@ -12,6 +12,10 @@
 // apply: base[idx[j]] = word[j] (scatter).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
+#include <cub/cub.cuh>
 
 #include "common.cuh"
 
@@ -183,6 +187,115 @@ __global__ void __launch_bounds__(kDtThreads, 4) delta_encode_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Two-stage encode (default): (1) a pure streaming pass writes the change bitmask (1 bit per word)
+// and each tile's change count — 16-B loads, no cross-CTA dependency; (2) an exclusive scan of the
+// tile counts (CUB, tiny); (3) a pass over the bitmask (1/32 of the input) that writes every
+// change at its sorted position, the new word gathered from `next`.  ~1.08x the one-pass traffic
+// but every pass streams at full rate.
+constexpr int kD2Tile = kDtTile;  // 16384 words: 512 u32 mask words, 256 threads x 8 vectors
+
+__global__ void __launch_bounds__(kDtThreads) delta_mask_kernel(const uint16_t* __restrict__ prev,
+                                                                  const uint16_t* __restrict__ next, int64_t n,
+                                                                  int64_t n_tiles, uint32_t* __restrict__ bits,
+                                                                  uint64_t* __restrict__ tile_count) {
+  __shared__ uint32_t wsum[kDtThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t wt = tile * kD2Tile;
+    // thread t: vectors u * 256 + t -> 8 mask bits each; written as u32 words of 4 vectors:
+    // mask word index (within the tile) = vector index / 4
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int h = 0; h < kDtVec; h += 4) {
+      uint32_t m[4];
+      if (wt + kD2Tile <= n) {
+        const uint4* pa = reinterpret_cast<const uint4*>(prev + wt) + tid;
+        const uint4* pb = reinterpret_cast<const uint4*>(next + wt) + tid;
+        uint4 va[4], vb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          va[u] = ld_stream_v4(pa + (h + u) * kDtThreads);
+          vb[u] = ld_stream_v4(pb + (h + u) * kDtThreads);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) m[u] = diff8(va[u], vb[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          m[u] = 0;
+          for (int e = 0; e < 8; ++e) {
+            const int64_t w = wt + 8 * ((int64_t)(h + u) * kDtThreads + tid) + e;
+            if (w < n && prev[w] != next[w]) m[u] |= 1u << e;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cnt += __popc(m[u]);
+        // vector v = (h+u)*256 + tid holds words [8v, 8v+8): its byte in the tile's bitmask is v
+        reinterpret_cast<uint8_t*>(bits)[(size_t)tile * (kD2Tile / 8) + (size_t)(h + u) * kDtThreads + tid] =
+            (uint8_t)m[u];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) wsum[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < kDtThreads / 32; ++w) t += wsum[w];
+      tile_count[tile] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// pass 3: thread t of a tile owns mask words [t*2, t*2+2) (64 words of the snapshot), ranks its
+// changes with a block scan and writes them at tile_offset + rank (index order = word order)
+__global__ void __launch_bounds__(kDtThreads) delta_scatter_kernel(const uint16_t* __restrict__ next, int64_t n,
+                                                                     int64_t n_tiles, const uint32_t* __restrict__ bits,
+                                                                     const uint64_t* __restrict__ tile_off,
+                                                                     uint32_t* __restrict__ idx_out,
+                                                                     uint16_t* __restrict__ word_out, int64_t capacity,
+                                                                     unsigned long long* __restrict__ count_out) {
+  __shared__ uint32_t wsum[kDtThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint2 mw = reinterpret_cast<const uint2*>(bits + (size_t)tile * (kD2Tile / 32))[tid];
+    const uint32_t c = __popc(mw.x) + __popc(mw.y);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+#pragma unroll
+    for (int w = 0; w < kDtThreads / 32; ++w) before += w < warp ? wsum[w] : 0;
+    int64_t off = (int64_t)tile_off[tile] + before + incl - c;
+    const int64_t w0 = tile * kD2Tile + (int64_t)tid * 64;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t m = half ? mw.y : mw.x;
+      while (m) {
+        const int e = __ffs(m) - 1;
+        m &= m - 1;
+        if (off < capacity) {
+          const int64_t w = w0 + half * 32 + e;
+          idx_out[off] = (uint32_t)w;
+          word_out[off] = next[w];
+        }
+        ++off;
+      }
+    }
+    if (tile == n_tiles - 1 && tid == kDtThreads - 1) *count_out = (unsigned long long)off;
+    __syncthreads();  // wsum reusable
+  }
+}
+
 __global__ void delta_apply_kernel(uint16_t* __restrict__ base, int64_t n, const uint32_t* __restrict__ idx,
                                    const uint16_t* __restrict__ words, const unsigned long long* __restrict__ count,
                                    int64_t capacity, unsigned long long* __restrict__ bad) {
@@ -198,9 +311,36 @@ static int64_t dt_tiles(int64_t n) { return (n + kDtTile - 1) / kDtTile; }
 
 }  // namespace rl
 
+namespace rl {
+// workspace: [tile status / two-stage tile counts: tiles+2 u64][tile offsets: tiles u64]
+//            [change bitmask: tiles * 2 KB][CUB scan temp]
+struct DtLayout {
+  size_t status, offs, bits, temp, temp_bytes, total;
+};
+static DtLayout dt_layout(int64_t n_words) {
+  const int64_t tiles = dt_tiles(n_words);
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)std::max<int64_t>(tiles, 1));
+  DtLayout L;
+  size_t off = 0;
+  auto al = [&](size_t b) {
+    const size_t o = off;
+    off += (b + 255) & ~(size_t)255;
+    return o;
+  };
+  L.status = al((size_t)(tiles + 2) * 8);
+  L.offs = al((size_t)tiles * 8);
+  L.bits = al((size_t)tiles * (kD2Tile / 8));
+  L.temp_bytes = scan_bytes;
+  L.temp = al(scan_bytes);
+  L.total = off;
+  return L;
+}
+}  // namespace rl
+
 extern "C" size_t rl_bf16_delta_workspace_size(int64_t n_words) {
   if (n_words < 0) return 0;
-  return (size_t)(rl::dt_tiles(n_words) + 2) * sizeof(uint64_t);
+  return rl::dt_layout(n_words).total;
 }
 
 extern "C" rl_status rl_bf16_delta_encode(const void* prev, const void* next, int64_t n_words, uint32_t* idx_out,
@@ -217,24 +357,45 @@ extern "C" rl_status rl_bf16_delta_encode(const void* prev, const void* next, in
     return fail(RL_ERR_WORKSPACE, "workspace must be >= %zu bytes", rl_bf16_delta_workspace_size(n_words));
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t tiles = dt_tiles(n_words);
-  uint64_t* status = (uint64_t*)workspace;
-  if (cudaMemsetAsync(workspace, 0, (size_t)(tiles + 2) * 8, s) != cudaSuccess) return check_launch("delta memset");
+  const DtLayout L = dt_layout(n_words);
+  char* w = (char*)workspace;
+  uint64_t* status = (uint64_t*)(w + L.status);
   if (tiles == 0) {
     if (cudaMemsetAsync(count_out, 0, 8, s) != cudaSuccess) return check_launch("delta memset");
     return RL_OK;
   }
-  static int ctas = 0;
-  if (!ctas) {
-    int dev = 0, sms = 148, occ = 4;
+  static int algo = -1;  // RL_DELTA_ALGO=onepass: the single-pass look-back kernel
+  if (algo < 0) algo = (getenv("RL_DELTA_ALGO") && strcmp(getenv("RL_DELTA_ALGO"), "onepass") == 0) ? 1 : 0;
+  static int sms = 0, ctas = 0;
+  if (!sms) {
+    int dev = 0, occ = 4;
+    sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, delta_encode_kernel, kDtThreads, 0);
     ctas = sms * std::max(occ, 1);  // all resident: a look-back only ever waits on a running tile
   }
-  const int grid = (int)std::min<int64_t>(tiles, ctas);
-  delta_encode_kernel<<<grid, kDtThreads, 0, s>>>((const uint16_t*)prev, (const uint16_t*)next, n_words, tiles,
-                                                  idx_out, word_out, capacity, count_out, status);
-  return check_launch("delta_encode_kernel");
+  if (algo == 1) {
+    if (cudaMemsetAsync(status, 0, (size_t)(tiles + 2) * 8, s) != cudaSuccess) return check_launch("delta memset");
+    const int grid = (int)std::min<int64_t>(tiles, ctas);
+    delta_encode_kernel<<<grid, kDtThreads, 0, s>>>((const uint16_t*)prev, (const uint16_t*)next, n_words, tiles,
+                                                    idx_out, word_out, capacity, count_out, status);
+    return check_launch("delta_encode_kernel");
+  }
+  uint64_t* counts = status;
+  uint64_t* offs = (uint64_t*)(w + L.offs);
+  uint32_t* bits = (uint32_t*)(w + L.bits);
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)sms * 8);
+  delta_mask_kernel<<<grid, kDtThreads, 0, s>>>((const uint16_t*)prev, (const uint16_t*)next, n_words, tiles, bits,
+                                                counts);
+  rl_status st = check_launch("delta_mask_kernel");
+  if (st != RL_OK) return st;
+  size_t tb = L.temp_bytes;
+  if (cub::DeviceScan::ExclusiveSum(w + L.temp, tb, counts, offs, (int)tiles, s) != cudaSuccess)
+    return check_launch("cub scan (delta)");
+  delta_scatter_kernel<<<grid, kDtThreads, 0, s>>>((const uint16_t*)next, n_words, tiles, bits, offs, idx_out,
+                                                   word_out, capacity, count_out);
+  return check_launch("delta_scatter_kernel");
 }
 
 extern "C" rl_status rl_bf16_delta_apply(void* base, int64_t n_words, const uint32_t* idx, const uint16_t* words,

@@ -1,4 +1,4 @@
-"""The non-default kernels (selected per process with RL_LOSS_KERNEL / RL_LOGPROB_KERNEL / RL_VP_KERNEL, latched
+"""The non-default kernels (selected per process with RL_LOSS_KERNEL / RL_LOGPROB_KERNEL / RL_VP_KERNEL / RL_DELTA_ALGO, latched
 on first use) against the same oracle parity tests as the default ones."""
 import os
 import subprocess
@@ -15,6 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     ("RL_LOSS_KERNEL", "two_pass", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero or objective"),
     ("RL_LOGPROB_KERNEL", "block", "token_logprob"),
     ("RL_VP_KERNEL", "block", "vocab_parallel"),
+    ("RL_DELTA_ALGO", "onepass", "delta"),
 ])
 def test_alternate_kernels(var, kernel, select):
     env = dict(os.environ, **{var: kernel})
