@@ -447,6 +447,61 @@ def test_vocab_parallel_single_rank(cuda_lib):
     comm.destroy()
 
 
+def test_vocab_parallel_extended_objective(cuda_lib):
+    """The vocab-parallel loss with the NEXT-2 per-token terms (k3 KL, decoupled ratio) against the
+    oracle, on the NCCL path and then on the in-kernel peer path (P = 1)."""
+    import ctypes
+    rl, t = cuda_lib, torch()
+    lib = rl.load()
+    buf = (ctypes.c_uint8 * 128)()
+    assert lib.rl_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)) == 0
+    h = ctypes.c_void_p()
+    assert lib.rl_comm_init(ctypes.byref(h), bytes(buf), 1, 0) == 0
+    comm = rl.Comm(h.value, 1, 0)
+    V = 3000
+    case = small_case(vocab=V, dtype="bf16", seed=19, sigma_delta=0.15, ld=3000)
+    y = case["targets"]
+    lp_ref, _ = oracle.token_logprob(case["x64"], y)
+    rng = np.random.default_rng(19)
+    ref = (np.where(y >= 0, lp_ref, 0.0) + rng.normal(size=len(y)) * 0.3).astype(np.float32)
+    prox = (case["old_logp"] + rng.normal(size=len(y)) * 0.05).astype(np.float32)
+    params = dict(kl_coef=0.05)
+    ref_out = oracle_chain(case, oracle.LossParams(**params), ref_logp=ref.astype(np.float64),
+                           prox_logp=prox.astype(np.float64))
+    out, bk = ref_out["loss"], ref_out["bk"]
+    N = len(y)
+    adv = dev(ref_out["adv"])   # advantages are bit-exact on the GPU (tested above); the oracle's here
+    p = rl.LossParams(trainer_version=case["trainer_version"], max_staleness=case["max_staleness"],
+                      global_active_tokens=float(bk["active_tokens"]), kl_coef=0.05,
+                      ref_logp=dev(ref), prox_logp=dev(prox))
+    ws = t.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=t.uint8, device="cuda")
+    scale = max(abs(out["loss"]), float(np.abs(out["token_loss"]).sum()))
+    for path in ("nccl", "peer"):
+        if path == "peer":
+            assert comm.enable_peer_exchange(N)
+        logp = t.empty(N, device="cuda")
+        dl = t.empty_like(dev(case["logits"]))
+        stats = t.zeros(12, dtype=t.float64, device="cuda")
+        rl.vocab_parallel_logprob(dev(case["logits"]), dev(y), 0, V, comm, logp, ws, old_logp=dev(case["old_logp"]),
+                                  loss_mask=dev(case["loss_mask"]), token_seq=dev(bk["token_seq"]), seq_adv=adv,
+                                  seq_version=dev(case["seq_version"]), params=p, dlogits_shard=dl, stats=stats)
+        t.cuda.synchronize()
+        st = stats.cpu().numpy()
+        assert abs(st[0] - out["loss"]) <= LOSS_RTOL * scale, (path, st[0], out["loss"])
+        assert abs(st[10] - out["stats"]["kl_sum"]) <= 1e-3 * abs(out["stats"]["kl_sum"]) + 1e-7
+        d = host_logits(dl)[:, :V]
+        s_ref = out["scale"]
+        band = clip_band(out["ratio"], out["valid"], 0.2, 0.2)
+        for k in range(N):
+            if band[k]:
+                continue
+            if s_ref[k] == 0:
+                assert np.all(d[k] == 0), (path, k)
+            else:
+                assert np.abs(d[k] - out["dlogits"][k]).max() <= DLOGIT_ROW_RTOL * abs(s_ref[k]), (path, k)
+    comm.destroy()
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("name,N,in_place,objective", [
     ("single", 131072, False, False),  # configs[1]: the bench's 131,072-token mini-batch, V = 151936
