@@ -516,7 +516,7 @@ def main():
         parallelism = (f"vocab-parallel over {world} GPU: " + (
             "one fused kernel per rank, per-row (max, sum-exp, target logit) exchanged by NVLink peer stores"
             if fused_vp else "vp_stats + NCCL all-gather + vp_finish"))
-        kname = "rl_vocab_parallel_logprob (" + ("vp_fused_kernel, in-kernel peer exchange" if fused_vp
+        kname = "rl_vocab_parallel_logprob (" + ("vp_fused2_kernel, in-kernel peer exchange" if fused_vp
                                                  else "vp_stats + NCCL all-gather + vp_finish") + ")"
     else:
         raise SystemExit(f"unknown config {args.config}")

@@ -602,6 +602,220 @@ __global__ void __launch_bounds__(kVfThreads, 1) vp_fused_kernel(const VfArgs a)
     for (int i = 0; i < RL_LOSS_STATS_N; ++i) a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = acc.v[i];
 }
 
+// ---------------------------------------------------------------------------------------
+// Fused vocab-parallel loss v2 (default with peer exchange): 2 HBM units per row slice.
+// Rows blockIdx.x + k * gridDim.x are processed in groups of G = 16 / WPR, one row per team of WPR
+// consumer warps (two groups of every CTA fit in L2: G * slice <= ~300 KB).  Each team runs, per
+// group g: pass 1 of its row of group g — streamed from HBM (evict_last, 8 vectors in flight per
+// thread) into the row's (max, sum 2^(t - max), target logit) record — then pass 2 of its row of
+// group g-1, re-read from L2 (evict_first) into dlogits.  Service warp 16 lane 0 (it stores no
+// dlogits, so its system fence covers only its own few stores) publishes a group's records to
+// every rank's buffer with ONE fence, waits for the peers' records of that group, combines them
+// in rank order, runs the loss epilogue and publishes the row scales — while the teams stream
+// the next group.
+constexpr int kV2Warps = 16;
+constexpr int kV2Cons = kV2Warps * 32;
+
+template <typename T, int WPR>
+__global__ void __launch_bounds__(kV2Cons + 32, 1) vp_fused2_kernel(const VfArgs a) {
+  constexpr int EPV = VecTraits<T>::EPV;
+  constexpr int G = kV2Warps / WPR;  // rows per group = teams
+  constexpr int NT = WPR * 32;       // threads per team
+  __shared__ float4 grp_rec[2][G];   // [group parity][team] this rank's records
+  __shared__ float4 grp_sc[2][G];    // (s, c2, -, target column or -1)
+  __shared__ float red_m[2][kV2Warps], red_s[2][kV2Warps];
+  __shared__ __align__(8) uint64_t stats_bar[2], scale_bar[2], done_bar[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t nk = blockIdx.x < a.n ? (a.n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t ng = (nk + G - 1) / G;
+  const int64_t row_bytes = a.ld * elem_bytes<T>();
+  const int64_t nvec = a.Vr / EPV;
+  const float k = a.kn.inv_t * RL_LOG2E;
+  auto row_of = [&](int64_t kk) { return (int64_t)blockIdx.x + kk * gridDim.x; };
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&stats_bar[i], G);
+      sm100::mbar_init(&scale_bar[i], 1);
+      sm100::mbar_init(&done_bar[i], kV2Warps);
+    }
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kV2Warps) {
+    if (lane != 0) return;
+    // ------------------------------------------------------------------ service lane
+    const double inv_tm = token_mean_inv(a.kn);
+    Acc acc;
+    acc.zero();
+    for (int64_t g = 0; g < ng; ++g) {
+      const int b = (int)(g & 1);
+      const int64_t k0 = g * G, k1 = min(nk, k0 + G);
+      sm100::mbar_wait_polite(&stats_bar[b], (uint32_t)((g >> 1) & 1), false);
+      for (int64_t kk = k0; kk < k1; ++kk) {  // records -> every rank (this rank's slot [me][row])
+        const float4 r = grp_rec[b][kk - k0];
+        const int64_t row = row_of(kk);
+        for (int q = 0; q < a.P; ++q) a.rec[q][(int64_t)a.me * a.max_tokens + row] = r;
+      }
+      __threadfence_system();
+      for (int64_t kk = k0; kk < k1; ++kk)
+        for (int q = 0; q < a.P; ++q)
+          *reinterpret_cast<volatile uint32_t*>(&a.flag[q][(int64_t)a.me * a.max_tokens + row_of(kk)]) = a.epoch;
+      // the scale slot of group g-2 must be free: its pass 2 is done
+      if (g >= 2) sm100::mbar_wait_polite(&done_bar[b], (uint32_t)(((g - 2) >> 1) & 1), false);
+      for (int64_t kk = k0; kk < k1; ++kk) {
+        const int64_t row = row_of(kk);
+        for (int q = 0; q < a.P; ++q) {
+          const volatile uint32_t* f = &a.flag[a.me][(int64_t)q * a.max_tokens + row];
+          while (*f != a.epoch) __nanosleep(20);
+        }
+      }
+      __threadfence_system();
+      for (int64_t kk = k0; kk < k1; ++kk) {
+        const int64_t row = row_of(kk);
+        float M = -INFINITY;
+        for (int q = 0; q < a.P; ++q) M = fmaxf(M, a.rec[a.me][(int64_t)q * a.max_tokens + row].x);
+        float S = 0.f, zy = 0.f;
+        for (int q = 0; q < a.P; ++q) {
+          const float4 e = a.rec[a.me][(int64_t)q * a.max_tokens + row];
+          if (e.x != -INFINITY) S += e.y * fast_exp2(e.x - M);
+          zy += e.z;
+        }
+        const float c2 = M + fast_log2(S);
+        const RowMeta mt = row_meta(row, a.Vtot, a.targets, a.mask, a.token_seq, a.seq_version,
+                                    a.kn.trainer_version, a.kn.max_staleness);
+        const float lp = logp_from(mt, zy, c2);
+        if (a.logp_out) a.logp_out[row] = lp;
+        if (a.lse_out) a.lse_out[row] = c2 * RL_LN2;
+        const float A = mt.valid ? a.seq_adv[mt.seq] : 0.f;
+        const float old = mt.valid ? a.old_logp[row] : 0.f;
+        float prox_, ref_;
+        token_extra(a.kn, row, old, prox_, ref_);
+        Acc tmp;
+        tmp.zero();
+        const float st = token_epilogue(mt, lp, old, A, a.seq_active, inv_tm, a.kn, tmp, nullptr, prox_, ref_);
+        if (a.count_stats)
+          for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
+        const int64_t yl = (int64_t)mt.y - a.off;
+        const int ycol = (mt.in_range && yl >= 0 && yl < a.Vr) ? (int)yl : -1;
+        grp_sc[b][kk - k0] = make_float4(st, c2, st * (fast_exp2(zy * RL_LOG2E - c2) - 1.f), __int_as_float(ycol));
+      }
+      sm100::mbar_arrive(&scale_bar[b]);
+    }
+    for (int i = 0; i < RL_LOSS_STATS_N; ++i) a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = acc.v[i];
+    return;
+  }
+  // -------------------------------------------------------------------- row teams
+  const int team = warp / WPR, t = tid % NT;
+  const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+  const int pf = a.nb;  // L2 prefetch distance in groups (0 = off)
+  const uint32_t slice16 = (uint32_t)((a.Vr * elem_bytes<T>() + 15) / 16 * 16);
+  if (t == 0)
+    for (int64_t gg = 0; gg < ((int64_t)pf < ng ? (int64_t)pf : ng); ++gg)
+      if (gg * G + team < nk)
+        sm100::bulk_prefetch_l2(reinterpret_cast<const char*>(a.logits) + row_of(gg * G + team) * row_bytes, slice16);
+  for (int64_t g = 0; g <= ng; ++g) {
+    if (g < ng) {  // ---- pass 1 of group g: this team's row record
+      const int b = (int)(g & 1);
+      const int64_t kk = g * G + team;
+      if (pf > 0 && t == 0 && kk + pf * G < nk)  // pull the team's row of group g + pf into L2
+        sm100::bulk_prefetch_l2(reinterpret_cast<const char*>(a.logits) + row_of(kk + pf * G) * row_bytes, slice16);
+      MS st{-INFINITY, 0.f};
+      const char* rp = nullptr;
+      if (kk < nk) {
+        rp = reinterpret_cast<const char*>(a.logits) + row_of(kk) * row_bytes;
+        st = row_stats_thread<T, NT, 8>(rp, a.Vr, k, keep, t);
+      }
+      st = warp_reduce_ms(st);
+      if (WPR > 1) {
+        if (lane == 0) {
+          red_m[b][warp] = st.m;
+          red_s[b][warp] = st.s;
+        }
+        sm100::named_bar_sync(1 + team, NT);
+      }
+      if (t == 0) {
+        if (kk < nk) {
+          MS r = st;
+          for (int w = 1; w < WPR; ++w) r = ms_combine(r, MS{red_m[b][warp + w], red_s[b][warp + w]});
+          const int32_t y = a.targets[row_of(kk)];
+          const int64_t yl = (int64_t)y - a.off;
+          const bool owned = y >= 0 && yl >= 0 && yl < a.Vr;
+          const float zy = owned ? VecTraits<T>::load1(rp, yl) * a.kn.inv_t : 0.f;
+          grp_rec[b][team] = make_float4(r.m, r.s, zy, owned ? 1.f : 0.f);
+        }
+        sm100::mbar_arrive(&stats_bar[b]);
+      }
+    }
+    if (g >= 1) {  // ---- pass 2 of group g-1: this team's row, from L2
+      const int64_t gp = g - 1;
+      const int b = (int)(gp & 1);
+      const int64_t kk = gp * G + team;
+      sm100::mbar_wait(&scale_bar[b], (uint32_t)((gp >> 1) & 1));
+      if (kk < nk) {
+        const int64_t row = row_of(kk);
+        const float4 sc = grp_sc[b][team];
+        const float s = sc.x, c2 = sc.y, dy = sc.z;
+        const int64_t yl = __float_as_int(sc.w);
+        const char* rp = reinterpret_cast<const char*>(a.logits) + row * row_bytes;
+        char* dp = reinterpret_cast<char*>(a.dlogits) + row * row_bytes;
+        const uint4* vrow = reinterpret_cast<const uint4*>(rp);
+        uint4* vout = reinterpret_cast<uint4*>(dp);
+        if (s == 0.f) {
+          for (int64_t i = t; i < nvec; i += NT) st_stream_v4(vout + i, make_uint4(0, 0, 0, 0));
+        } else {
+          constexpr int U = 4;
+          for (int64_t i0 = t; i0 < nvec; i0 += U * NT) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (i0 + u * NT < nvec) v[u] = ld_hint_v4(vrow + i0 + u * NT, drop);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int64_t i = i0 + u * NT;
+              if (i < nvec) {
+                float f[EPV];
+                VecTraits<T>::unpack(v[u], f);
+#pragma unroll
+                for (int j = 0; j < EPV; ++j) f[j] = s * fast_exp2(fmaf(f[j], k, -c2));
+                onehot_set(f, yl - i * EPV, dy);
+                st_stream_v4(vout + i, VecTraits<T>::pack(f));
+              }
+            }
+          }
+        }
+        for (int64_t c = nvec * EPV + t; c < a.Vr; c += NT) {
+          float v = (s == 0.f) ? 0.f : s * fast_exp2(fmaf(VecTraits<T>::load1(rp, c), k, -c2));
+          if (s != 0.f && c == yl) v = dy;
+          VecTraits<T>::store1(dp, c, v);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&done_bar[b]);
+    }
+  }
+}
+
+template <typename T>
+static void launch_vp_fused2(const VfArgs& v0, int64_t slice_bytes, int grid, cudaStream_t s) {
+  // rows per group G = 16 / WPR: the largest power of two with G * slice <= 300 KB
+  // (RL_VP2_WPR=1|2|4|8|16 forces the team size: tests run every instantiation at small shapes)
+  // (RL_VP2_PF = L2 prefetch distance in groups, default 1; the groups resident in L2 are then
+  //  pass 2's, pass 1's and the prefetched ones: budget 200 KB per group, 300 KB without prefetch)
+  static int forced = -1, pf = -1;
+  if (forced < 0) forced = getenv("RL_VP2_WPR") ? atoi(getenv("RL_VP2_WPR")) : 0;
+  if (pf < 0) pf = getenv("RL_VP2_PF") ? std::max(0, atoi(getenv("RL_VP2_PF"))) : 1;
+  VfArgs v = v0;
+  v.nb = pf;
+  const int64_t budget = getenv("RL_VP2_BUDGET_KB") ? (int64_t)atoi(getenv("RL_VP2_BUDGET_KB")) << 10
+                                                     : (pf > 0 ? 200 << 10 : 300 << 10);
+  if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16) slice_bytes = budget / (16 / forced);
+  if (slice_bytes * 16 <= budget) vp_fused2_kernel<T, 1><<<grid, kV2Cons + 32, 0, s>>>(v);
+  else if (slice_bytes * 8 <= budget) vp_fused2_kernel<T, 2><<<grid, kV2Cons + 32, 0, s>>>(v);
+  else if (slice_bytes * 4 <= budget) vp_fused2_kernel<T, 4><<<grid, kV2Cons + 32, 0, s>>>(v);
+  else if (slice_bytes * 2 <= budget) vp_fused2_kernel<T, 8><<<grid, kV2Cons + 32, 0, s>>>(v);
+  else vp_fused2_kernel<T, 16><<<grid, kV2Cons + 32, 0, s>>>(v);
+}
+
 static int vp_grid(int64_t n) {
   static int ctas = 0;
   if (!ctas) {
@@ -670,7 +884,9 @@ extern "C" rl_status rl_vocab_parallel_logprob(
   const int64_t slice_bytes = (vocab_shard * eb + 15) / 16 * 16;
   const int nbuf = (int)std::min<int64_t>(kVfBufs, (232448 - 1024) / std::max<int64_t>(slice_bytes, 16));
   const size_t vf_smem = 1024 + (size_t)nbuf * slice_bytes;
-  if (with_loss && nbuf >= 2 && comm_peer_exchange(comm, n_tokens, peers, &max_tok, &epoch)) {
+  static int fused_v1 = -1;  // RL_VP_FUSED=smem: the first in-kernel exchange kernel (row slices in smem)
+  if (fused_v1 < 0) fused_v1 = (getenv("RL_VP_FUSED") && strcmp(getenv("RL_VP_FUSED"), "smem") == 0) ? 1 : 0;
+  if (with_loss && (!fused_v1 || nbuf >= 2) && comm_peer_exchange(comm, n_tokens, peers, &max_tok, &epoch)) {
     VfArgs v;
     v.logits = logits_shard;
     v.dlogits = dlogits_shard;
@@ -705,7 +921,10 @@ extern "C" rl_status rl_vocab_parallel_logprob(
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int vgrid = (int)std::min<int64_t>(n_tokens, std::min(sms, kMaxStatCtas));
-    if (dtype == RL_BF16) {
+    if (!fused_v1) {
+      if (dtype == RL_BF16) launch_vp_fused2<bf16_t>(v, slice_bytes, vgrid, s);
+      else launch_vp_fused2<float>(v, slice_bytes, vgrid, s);
+    } else if (dtype == RL_BF16) {
       cudaFuncSetAttribute(vp_fused_kernel<bf16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vf_smem);
       vp_fused_kernel<bf16_t><<<vgrid, kVfThreads, vf_smem, s>>>(v);
     } else {

@@ -1,4 +1,4 @@
-"""The non-default kernels (selected per process with RL_LOSS_KERNEL / RL_LOGPROB_KERNEL / RL_VP_KERNEL / RL_DELTA_ALGO, latched
+"""The non-default kernels (selected per process with RL_LOSS_KERNEL / RL_LOGPROB_KERNEL / RL_VP_KERNEL / RL_DELTA_ALGO / RL_VP_FUSED / RL_VP2_WPR, latched
 on first use) against the same oracle parity tests as the default ones."""
 import os
 import subprocess
@@ -16,6 +16,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     ("RL_LOGPROB_KERNEL", "block", "token_logprob"),
     ("RL_VP_KERNEL", "block", "vocab_parallel"),
     ("RL_DELTA_ALGO", "onepass", "delta"),
+    ("RL_VP_FUSED", "smem", "vocab_parallel"),
+    ("RL_VP2_WPR", "4", "vocab_parallel"),
+    ("RL_VP2_WPR", "16", "vocab_parallel"),
 ])
 def test_alternate_kernels(var, kernel, select):
     env = dict(os.environ, **{var: kernel})

@@ -1,7 +1,7 @@
 """Vocab-parallel call on ONE GPU with a shard of V/P columns (development tool): times
 rl_vocab_parallel_logprob with the fused loss on a 1-rank comm, so the kernels can be profiled
 in isolation (ncu) — the all-gather of a 1-rank comm is a copy.
-    python tools/vpbench.py [--P 4] [--rows 65536] [--reps 10] [--adv0 (s = 0: zero rows)]"""
+    python tools/vpbench.py [--P 4] [--rows 65536] [--reps 10] [--adv0 (s = 0: zero rows)] [--peer]"""
 import ctypes
 import os
 import sys
@@ -36,6 +36,8 @@ def main():
     stats = torch.zeros(12, dtype=torch.float64, device="cuda")
     ws = torch.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=torch.uint8, device="cuda")
     p = rl.LossParams(agg=rl.AGG_SUM)
+    if "--peer" in sys.argv:  # in-kernel exchange (RL_VP_FUSED=smem selects the first fused kernel)
+        assert comm.enable_peer_exchange(N)
     call = lambda: rl.vocab_parallel_logprob(x, y, 0, Vr, comm, logp, ws, vocab_shard=Vr, old_logp=old,
                                              token_seq=tseq, seq_adv=adv, params=p, dlogits_shard=dl, stats=stats)
     call()
