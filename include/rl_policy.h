@@ -326,8 +326,10 @@ rl_status rl_m2po_mask(const float* logp, const float* old_logp, const uint8_t* 
  *         idx_out, word_out  device [capacity]: the first min(count, capacity) changes
  *         count_out  device u64: the number of changes (may exceed capacity: then only the
  *                    first `capacity` are written — the caller re-runs with a larger buffer)
- *         workspace  device, >= rl_bf16_delta_workspace_size(n_words) bytes (tile status words)
- *         One pass: each snapshot read once, the changes written once; deterministic output.
+ *         workspace  device, >= rl_bf16_delta_workspace_size(n_words) bytes (per 16,384-word
+ *                    tile: counts, a 2 KB change bitmask and a 4 KB staging slot; ~0.38 B/word)
+ *         Each snapshot read once; a tile's changes are staged compacted and copied to their
+ *         sorted position (dense tiles: bitmask + gather from next); deterministic output.
  * apply:  base[idx[j]] = word[j] for j < min(*count, capacity); indices >= n_words are skipped and
  *         counted in *bad_index_count (device u64, added to).
  * Errors: RL_ERR_INVALID_ARGUMENT (sizes, NULL arrays), RL_ERR_ALIGNMENT, RL_ERR_WORKSPACE. */

@@ -188,80 +188,145 @@ __global__ void __launch_bounds__(kDtThreads, 4) delta_encode_kernel(
 }
 
 // ---------------------------------------------------------------------------------------------
-// Two-stage encode (default): (1) a pure streaming pass writes the change bitmask (1 bit per word)
-// and each tile's change count — 16-B loads, no cross-CTA dependency; (2) an exclusive scan of the
-// tile counts (CUB, tiny); (3) a pass over the bitmask (1/32 of the input) that writes every
-// change at its sorted position, the new word gathered from `next`.  ~1.08x the one-pass traffic
-// but every pass streams at full rate.
-constexpr int kD2Tile = kDtTile;  // 16384 words: 512 u32 mask words, 256 threads x 8 vectors
+// Two-stage encode (default): (1) a pure streaming pass compares the snapshots tile by tile
+// (16,384 words, 16-B loads, no cross-CTA dependency), ranks the tile's changes in word order with
+// a block scan and writes them compacted into the tile's own staging slot (capacity kStageCap
+// changes: new word + 16-bit index within the tile) plus the tile's change count; a tile with more
+// changes writes its change bitmask instead (1 bit per word); (2) an exclusive scan of the tile
+// counts (CUB, tiny); (3) a copy of every tile's staged changes to its sorted output position —
+// or, for an overflowed tile, a pass over its bitmask that gathers the new words from `next`.
+// At sparsity 0.99 every tile stages (~164 changes each): the snapshots are read exactly once and
+// stage 3 touches only the changes.
+constexpr int kD2Tile = kDtTile;     // 16384 words: 512 u32 mask words, 256 threads x 8 vectors
+constexpr int kStageCap = 1024;      // staged changes per tile (6.25 % of its words)
 
-__global__ void __launch_bounds__(kDtThreads) delta_mask_kernel(const uint16_t* __restrict__ prev,
+__global__ void __launch_bounds__(kDtThreads, 3) delta_mask_kernel(const uint16_t* __restrict__ prev,
                                                                   const uint16_t* __restrict__ next, int64_t n,
                                                                   int64_t n_tiles, uint32_t* __restrict__ bits,
-                                                                  uint64_t* __restrict__ tile_count) {
-  __shared__ uint32_t wsum[kDtThreads / 32];
+                                                                  uint64_t* __restrict__ tile_count,
+                                                                  uint32_t* __restrict__ stage) {
+  __shared__ uint32_t wsum[kDtThreads / 32][kDtVec / 2];  // per warp: packed pairs of row totals
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t wt = tile * kD2Tile;
-    // thread t: vectors u * 256 + t -> 8 mask bits each; written as u32 words of 4 vectors:
-    // mask word index (within the tile) = vector index / 4
-    uint32_t cnt = 0;
+    // thread t holds vectors v = u * 256 + t (u = 0..7: "row" u of the tile), 8 words each
+    uint4 vb[kDtVec];
+    uint32_t m[kDtVec];
+    if (wt + kD2Tile <= n) {
+      const uint4* pa = reinterpret_cast<const uint4*>(prev + wt) + tid;
+      const uint4* pb = reinterpret_cast<const uint4*>(next + wt) + tid;
+      uint4 va[kDtVec];
 #pragma unroll
-    for (int h = 0; h < kDtVec; h += 4) {
-      uint32_t m[4];
-      if (wt + kD2Tile <= n) {
-        const uint4* pa = reinterpret_cast<const uint4*>(prev + wt) + tid;
-        const uint4* pb = reinterpret_cast<const uint4*>(next + wt) + tid;
-        uint4 va[4], vb[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          va[u] = ld_stream_v4(pa + (h + u) * kDtThreads);
-          vb[u] = ld_stream_v4(pb + (h + u) * kDtThreads);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) m[u] = diff8(va[u], vb[u]);
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          m[u] = 0;
-          for (int e = 0; e < 8; ++e) {
-            const int64_t w = wt + 8 * ((int64_t)(h + u) * kDtThreads + tid) + e;
-            if (w < n && prev[w] != next[w]) m[u] |= 1u << e;
-          }
-        }
+      for (int u = 0; u < kDtVec; ++u) {
+        va[u] = ld_stream_v4(pa + u * kDtThreads);
+        vb[u] = ld_stream_v4(pb + u * kDtThreads);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        cnt += __popc(m[u]);
-        // vector v = (h+u)*256 + tid holds words [8v, 8v+8): its byte in the tile's bitmask is v
-        reinterpret_cast<uint8_t*>(bits)[(size_t)tile * (kD2Tile / 8) + (size_t)(h + u) * kDtThreads + tid] =
-            (uint8_t)m[u];
+      for (int u = 0; u < kDtVec; ++u) m[u] = diff8(va[u], vb[u]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kDtVec; ++u) {
+        m[u] = 0;
+        uint16_t wv[8];
+        for (int e = 0; e < 8; ++e) {
+          const int64_t w = wt + 8 * ((int64_t)u * kDtThreads + tid) + e;
+          wv[e] = w < n ? next[w] : 0;
+          if (w < n && prev[w] != wv[e]) m[u] |= 1u << e;
+        }
+        vb[u] = make_uint4(wv[0] | (uint32_t)wv[1] << 16, wv[2] | (uint32_t)wv[3] << 16,
+                           wv[4] | (uint32_t)wv[5] << 16, wv[6] | (uint32_t)wv[7] << 16);
       }
     }
+    // word-order rank: position of (row u, thread t) = sum of rows < u + sum over threads < t of
+    // row u.  Rows are scanned in pairs packed as 16-bit halves (a row holds <= 2048 changes).
+    uint32_t incl[kDtVec / 2], cnt[kDtVec / 2];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) wsum[warp] = cnt;
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t t = 0;
-      for (int w = 0; w < kDtThreads / 32; ++w) t += wsum[w];
-      tile_count[tile] = t;
+    for (int q = 0; q < kDtVec / 2; ++q) {
+      cnt[q] = (uint32_t)__popc(m[2 * q]) | (uint32_t)__popc(m[2 * q + 1]) << 16;
+      incl[q] = cnt[q];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl[q], o);
+        if (lane >= o) incl[q] += v;
+      }
+      if (lane == 31) wsum[warp][q] = incl[q];
     }
     __syncthreads();
+    uint32_t before[kDtVec / 2], tot[kDtVec / 2];
+#pragma unroll
+    for (int q = 0; q < kDtVec / 2; ++q) {
+      before[q] = 0;
+      tot[q] = 0;
+    }
+#pragma unroll
+    for (int w = 0; w < kDtThreads / 32; ++w)
+#pragma unroll
+      for (int q = 0; q < kDtVec / 2; ++q) {
+        const uint32_t x = wsum[w][q];
+        tot[q] += x;
+        before[q] += w < warp ? x : 0u;
+      }
+    uint32_t row_base[kDtVec], T = 0;
+#pragma unroll
+    for (int u = 0; u < kDtVec; ++u) {
+      const uint32_t rt = (u & 1) ? tot[u / 2] >> 16 : tot[u / 2] & 0xFFFFu;
+      row_base[u] = T;
+      T += rt;
+    }
+    if (T <= (uint32_t)kStageCap) {
+      uint32_t* st = stage + (size_t)tile * kStageCap;
+#pragma unroll
+      for (int u = 0; u < kDtVec; ++u) {
+        const uint32_t ex = before[u / 2] + incl[u / 2] - cnt[u / 2];
+        uint32_t pos = row_base[u] + ((u & 1) ? ex >> 16 : ex & 0xFFFFu);
+        uint32_t mm = m[u];
+        const uint32_t wv[4] = {vb[u].x, vb[u].y, vb[u].z, vb[u].w};
+        while (mm) {
+          const int e = __ffs(mm) - 1;
+          mm &= mm - 1;
+          const uint32_t word = (wv[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+          const uint32_t local = (uint32_t)(8 * (u * kDtThreads + tid) + e);  // < 16384
+          st[pos++] = word << 16 | local;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kDtVec; ++u)
+        reinterpret_cast<uint8_t*>(bits)[(size_t)tile * (kD2Tile / 8) + (size_t)u * kDtThreads + tid] = (uint8_t)m[u];
+    }
+    if (tid == 0) tile_count[tile] = T;
+    __syncthreads();  // wsum reusable
   }
 }
 
-// pass 3: thread t of a tile owns mask words [t*2, t*2+2) (64 words of the snapshot), ranks its
-// changes with a block scan and writes them at tile_offset + rank (index order = word order)
+// pass 3: a staged tile is copied (thread j: changes j, j + 256, ...); an overflowed tile: thread t
+// owns mask words [t*2, t*2+2) (64 words of the snapshot), ranks its changes with a block scan and
+// writes them at tile_offset + rank, the new word gathered from `next`
 __global__ void __launch_bounds__(kDtThreads) delta_scatter_kernel(const uint16_t* __restrict__ next, int64_t n,
                                                                      int64_t n_tiles, const uint32_t* __restrict__ bits,
                                                                      const uint64_t* __restrict__ tile_off,
+                                                                     const uint64_t* __restrict__ tile_count,
+                                                                     const uint32_t* __restrict__ stage,
                                                                      uint32_t* __restrict__ idx_out,
                                                                      uint16_t* __restrict__ word_out, int64_t capacity,
                                                                      unsigned long long* __restrict__ count_out) {
   __shared__ uint32_t wsum[kDtThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t T = (int64_t)tile_count[tile], base = (int64_t)tile_off[tile];
+    if (tile == n_tiles - 1 && tid == 0) *count_out = (unsigned long long)(base + T);
+    if (T <= kStageCap) {
+      const uint32_t* st = stage + (size_t)tile * kStageCap;
+      for (int64_t j = tid; j < T; j += kDtThreads) {
+        const int64_t off = base + j;
+        if (off < capacity) {
+          const uint32_t e = st[j];
+          idx_out[off] = (uint32_t)(tile * kD2Tile + (e & 0xFFFFu));
+          word_out[off] = (uint16_t)(e >> 16);
+        }
+      }
+      continue;  // block-uniform branch: no barrier skipped by a subset of threads
+    }
     const uint2 mw = reinterpret_cast<const uint2*>(bits + (size_t)tile * (kD2Tile / 32))[tid];
     const uint32_t c = __popc(mw.x) + __popc(mw.y);
     uint32_t incl = c;
@@ -275,7 +340,7 @@ __global__ void __launch_bounds__(kDtThreads) delta_scatter_kernel(const uint16_
     uint32_t before = 0;
 #pragma unroll
     for (int w = 0; w < kDtThreads / 32; ++w) before += w < warp ? wsum[w] : 0;
-    int64_t off = (int64_t)tile_off[tile] + before + incl - c;
+    int64_t off = base + before + incl - c;
     const int64_t w0 = tile * kD2Tile + (int64_t)tid * 64;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -291,7 +356,6 @@ __global__ void __launch_bounds__(kDtThreads) delta_scatter_kernel(const uint16_
         ++off;
       }
     }
-    if (tile == n_tiles - 1 && tid == kDtThreads - 1) *count_out = (unsigned long long)off;
     __syncthreads();  // wsum reusable
   }
 }
@@ -313,9 +377,9 @@ static int64_t dt_tiles(int64_t n) { return (n + kDtTile - 1) / kDtTile; }
 
 namespace rl {
 // workspace: [tile status / two-stage tile counts: tiles+2 u64][tile offsets: tiles u64]
-//            [change bitmask: tiles * 2 KB][CUB scan temp]
+//            [change bitmask: tiles * 2 KB][staged changes: tiles * kStageCap u32][CUB scan temp]
 struct DtLayout {
-  size_t status, offs, bits, temp, temp_bytes, total;
+  size_t status, offs, bits, stage, temp, temp_bytes, total;
 };
 static DtLayout dt_layout(int64_t n_words) {
   const int64_t tiles = dt_tiles(n_words);
@@ -331,6 +395,7 @@ static DtLayout dt_layout(int64_t n_words) {
   L.status = al((size_t)(tiles + 2) * 8);
   L.offs = al((size_t)tiles * 8);
   L.bits = al((size_t)tiles * (kD2Tile / 8));
+  L.stage = al((size_t)tiles * kStageCap * 4);
   L.temp_bytes = scan_bytes;
   L.temp = al(scan_bytes);
   L.total = off;
@@ -386,15 +451,16 @@ extern "C" rl_status rl_bf16_delta_encode(const void* prev, const void* next, in
   uint64_t* offs = (uint64_t*)(w + L.offs);
   uint32_t* bits = (uint32_t*)(w + L.bits);
   const int grid = (int)std::min<int64_t>(tiles, (int64_t)sms * 8);
+  uint32_t* stage = (uint32_t*)(w + L.stage);
   delta_mask_kernel<<<grid, kDtThreads, 0, s>>>((const uint16_t*)prev, (const uint16_t*)next, n_words, tiles, bits,
-                                                counts);
+                                                counts, stage);
   rl_status st = check_launch("delta_mask_kernel");
   if (st != RL_OK) return st;
   size_t tb = L.temp_bytes;
   if (cub::DeviceScan::ExclusiveSum(w + L.temp, tb, counts, offs, (int)tiles, s) != cudaSuccess)
     return check_launch("cub scan (delta)");
-  delta_scatter_kernel<<<grid, kDtThreads, 0, s>>>((const uint16_t*)next, n_words, tiles, bits, offs, idx_out,
-                                                   word_out, capacity, count_out);
+  delta_scatter_kernel<<<grid, kDtThreads, 0, s>>>((const uint16_t*)next, n_words, tiles, bits, offs, counts, stage,
+                                                   idx_out, word_out, capacity, count_out);
   return check_launch("delta_scatter_kernel");
 }
 

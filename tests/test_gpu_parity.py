@@ -634,16 +634,28 @@ def test_m2po_mask(cuda_lib, n, tau, ties):
 
 # ----------------------------------------------------------------------------- NEXT 3: delta scan
 @pytest.mark.parametrize("n,frac", [(0, 0.0), (1, 1.0), (8191, 0.01), (8192 * 3 + 5, 0.3), (1 << 20, 0.011),
-                                    (3_000_001, 0.0), (2_000_003, 1.0), (40_000_000, 0.008)])
+                                    (3_000_001, 0.0), (2_000_003, 1.0), (40_000_000, 0.008),
+                                    (1_000_037, -1.0)])
 def test_delta_encode_apply(cuda_lib, n, frac):
     """rl_bf16_delta_encode equals the oracle's element-wise diff bit for bit (indices, words,
-    count), ragged and multi-tile sizes, all-equal and all-different; apply(encode) = next."""
+    count), ragged and multi-tile sizes, all-equal and all-different, and (frac = -1) one call
+    mixing sparse tiles (staged) with dense ones (> 1,024 changes per 16,384-word tile: bitmask
+    path) including tiles right at the staging capacity; apply(encode) = next; a short output
+    buffer holds exactly the first `capacity` changes."""
     t = torch()
     from oracle import delta
     rng = np.random.default_rng(n + 7)
     a = rng.integers(0, 1 << 16, size=n, dtype=np.uint16)
     b = a.copy()
-    ch = rng.random(n) < frac
+    if frac >= 0:
+        ch = rng.random(n) < frac
+    else:  # per-tile change rates: 0, 1/16 exactly (1,024 changes), 1,025 changes, 0.3, 0.01 ...
+        ch = np.zeros(n, dtype=bool)
+        for ti, t0 in enumerate(range(0, n, 16384)):
+            m = min(16384, n - t0)
+            kind = ti % 5
+            k = [0, 1024, 1025, int(0.3 * m), int(0.01 * m)][kind]
+            ch[t0 + rng.choice(m, size=min(k, m), replace=False)] = True
     b[ch] ^= rng.integers(1, 1 << 16, size=int(ch.sum()), dtype=np.uint16)
     if n > 16:
         b[3] = 0x8000 if a[3] == 0 else b[3]   # +0 vs -0 style bit flips count
@@ -669,3 +681,13 @@ def test_delta_encode_apply(cuda_lib, n, frac):
     cuda_lib.delta_apply(base, idx, words, count, bad)
     t.cuda.synchronize()
     assert bad.item() == 0 and t.equal(base, tb)
+    if k >= 2:  # truncated output: the first capacity changes, the full count
+        c2 = k // 2
+        idx2 = t.empty(c2, dtype=t.int32, device="cuda")
+        words2 = t.empty(c2, dtype=t.int16, device="cuda")
+        count2 = t.zeros(1, dtype=t.int64, device="cuda")
+        cuda_lib.delta_encode(ta, tb, idx2, words2, count2, ws)
+        t.cuda.synchronize()
+        assert int(count2.item()) == k
+        assert np.array_equal(idx2.cpu().numpy().view(np.uint32), ri[:c2])
+        assert np.array_equal(words2.cpu().numpy().view(np.uint16), rw[:c2])
