@@ -622,3 +622,80 @@ def test_delta_brute_force_round_trip_and_payload_bound():
     a = np.array([0x0000, 0x7FC0, 0x3F80], dtype=np.uint16)
     b = np.array([0x8000, 0x7FC0, 0x3F80], dtype=np.uint16)
     assert list(delta.compute_delta(a, b)[0]) == [0]
+
+
+# ----------------------------------------------------------------------------- NEXT 4: LM head
+def _bf16_bits(x):
+    """fp64 values that are exactly bf16 -> their bit patterns (asserts exactness)."""
+    f = np.asarray(x, dtype=np.float32)
+    b = (f.view(np.uint32) >> 16).astype(np.uint16)
+    assert np.array_equal((b.astype(np.uint32) << 16).view(np.float32), f)
+    return b
+
+
+def test_lmhead_closed_form():
+    """h = e_0, W[:, 0] = a: x = a exactly, logp_y = a_y - ln sum_v e^{a_v} (pure-Python closed
+    form) — a wrong operand order or a dropped row/column changes x."""
+    a = [0.0, 1.0, 2.0, -3.5, 0.25]
+    d = 4
+    W = np.zeros((len(a), d))
+    W[:, 0] = a
+    W[:, 1] = 7.0       # multiplied by h[1] = 0: no contribution
+    H = np.zeros((1, d))
+    H[0, 0] = 1.0
+    for y in range(len(a)):
+        lp, lse = oracle.lmhead_logprob(_bf16_bits(H), _bf16_bits(W), [y])
+        ref_lse = math.log(math.fsum(math.exp(v) for v in a))
+        assert abs(lse[0] - ref_lse) < 1e-14 and abs(lp[0] - (a[y] - ref_lse)) < 1e-14
+
+
+def test_lmhead_brute_force_rectangular():
+    """N=3, d=5, V=4 (all different): x by explicit fsum dot products, log-softmax by fsum —
+    a transposed weight (V x d vs d x V) or wrong row of h fails."""
+    rng = np.random.default_rng(3)
+    H = rng.integers(-8, 9, size=(3, 5)) / 4.0
+    W = rng.integers(-8, 9, size=(4, 5)) / 8.0
+    y = [0, 3, 1]
+    lp, lse = oracle.lmhead_logprob(_bf16_bits(H), _bf16_bits(W), y, inv_temperature=0.5)
+    for t in range(3):
+        x = [0.5 * math.fsum(H[t, k] * W[v, k] for k in range(5)) for v in range(4)]
+        m = max(x)
+        ref = m + math.log(math.fsum(math.exp(v - m) for v in x))
+        assert abs(lse[t] - ref) < 1e-13 and abs(lp[t] - (x[y[t]] - ref)) < 1e-13
+
+
+def test_lmhead_invariants():
+    """Equal weight rows -> logp = -ln V for any h; a common vector added to
+    every weight row (x_v += h.c) and a permutation of the vocabulary rows with relabelled targets
+    leave logp unchanged."""
+    rng = np.random.default_rng(5)
+    N, d, V = 6, 16, 37
+    H = np.round(rng.normal(size=(N, d)) * 8) / 8
+    W = np.round(rng.normal(size=(V, d)) * 8) / 8
+    y = rng.integers(0, V, size=N)
+    row = np.round(rng.normal(size=d) * 4) / 4
+    lp_c, _ = oracle.lmhead_logprob(_bf16_bits(H), _bf16_bits(np.tile(row, (V, 1))), y)
+    assert np.allclose(lp_c, -math.log(V), atol=1e-13, rtol=0)
+    lp, _ = oracle.lmhead_logprob(_bf16_bits(H), _bf16_bits(W), y)
+    c = np.round(rng.normal(size=d) * 2) / 2
+    lp_s, _ = oracle.lmhead_logprob(_bf16_bits(H), _bf16_bits(W + c), y)
+    assert np.allclose(lp_s, lp, atol=1e-11, rtol=0)
+    perm = rng.permutation(V)
+    inv = np.argsort(perm)
+    lp_p, _ = oracle.lmhead_logprob(_bf16_bits(H), _bf16_bits(W[perm]), inv[y])
+    assert np.allclose(lp_p, lp, atol=1e-13, rtol=0)
+
+
+def test_lmhead_torch_route():
+    """Independent library route: -cross_entropy(h @ W^T) in torch CPU fp64."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(9)
+    N, d, V = 5, 64, 300
+    hb = _bf16_bits(np.round(rng.normal(size=(N, d)) * 16) / 16)
+    wb = _bf16_bits(np.round(rng.normal(size=(V, d)) * 16) / 64)
+    y = rng.integers(0, V, size=N)
+    lp, _ = oracle.lmhead_logprob(hb, wb, y)
+    h = torch.from_numpy((hb.astype(np.uint32) << 16).view(np.float32).astype(np.float64))
+    w = torch.from_numpy((wb.astype(np.uint32) << 16).view(np.float32).astype(np.float64))
+    ref = -torch.nn.functional.cross_entropy(h @ w.T, torch.from_numpy(y), reduction="none")
+    assert np.allclose(lp, ref.numpy(), atol=1e-12, rtol=0)
