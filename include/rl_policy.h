@@ -341,6 +341,23 @@ rl_status rl_bf16_delta_apply(void* base, int64_t n_words, const uint32_t* idx, 
                               const unsigned long long* count, int64_t capacity,
                               unsigned long long* bad_index_count, rl_stream stream);
 
+/* ---------------------------------------------------------------- (8) fused LM-head log-prob (NEXT 4)
+ * SURVEY.md §8(f) NEXT 4 ("Fused LM-head GEMM + loss (tcgen05, logits never materialised) ... it
+ * takes hidden states and W"), forward half: c3 of §8(c) on x = (h W^T) * inv_T without writing
+ * the [n_tokens, vocab] logits (each 128 x 256 logits tile exists only in tensor memory).
+ *   hidden     device bf16 [n_tokens, ld_hidden] row-major (the first d columns are h), 16-B aligned
+ *   weight     device bf16 [vocab, ld_weight] row-major LM-head weight (the first d columns), 16-B aligned
+ *   ld_*       row strides in elements, >= d, multiples of 8
+ *   targets    device i32 [n_tokens]: y < 0 -> logp 0; y >= vocab -> logp NaN (as rl_token_logprob)
+ *   logp_out   device f32 [n_tokens];  lse_out  device f32 [n_tokens] or NULL (natural log)
+ * fp32 accumulation of bf16 products on the tensor cores (tcgen05.mma kind::f16), fp32 softmax.
+ * Errors: RL_ERR_INVALID_ARGUMENT (sizes, NULL, inv_temperature <= 0), RL_ERR_ALIGNMENT,
+ * RL_ERR_UNSUPPORTED (n_tokens, d or vocab >= 2^31), RL_ERR_CUDA (tensor-map encoding, launch).
+ * Deterministic: fixed K order per tile, fixed tile order per row. */
+rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                            int64_t n_tokens, int64_t d, int64_t vocab, const int32_t* targets,
+                            float inv_temperature, float* logp_out, float* lse_out, rl_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,7 @@ _SIGS = {
     "rl_bf16_delta_workspace_size": (sz, [i64]),
     "rl_bf16_delta_encode": (i32, [vp, vp, i64, vp, vp, i64, vp, vp, sz, vp]),
     "rl_bf16_delta_apply": (i32, [vp, i64, vp, vp, vp, i64, vp, vp]),
+    "rl_lmhead_logprob": (i32, [vp, i64, vp, i64, i64, i64, i64, vp, f32, vp, vp, vp]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
@@ -419,4 +420,22 @@ def delta_apply(base, idx, words, count, bad_count, stream=None):
     _check(lib.rl_bf16_delta_apply(_dev(base, "base"), base.numel(), _dev(idx, "idx"), _dev(words, "words"),
                                    _dev(count, "count"), idx.numel(), _dev(bad_count, "bad_count"),
                                    _stream(stream)), "rl_bf16_delta_apply")
+
+
+def lmhead_logprob(hidden, weight, targets, logp_out, lse_out=None, inv_temperature=1.0, stream=None):
+    """Fused LM-head log-prob (NEXT 4, forward): logp_t = log_softmax((h W^T) * inv_T)[y_t] without
+    materialising the logits.  hidden bf16 [N, d] and weight bf16 [V, d] (row strides may exceed d),
+    targets int32 [N]; logp_out / lse_out float32 [N]."""
+    lib = load()
+    if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
+        raise RLError("hidden [N, d] and weight [V, d] must share d")
+    if hidden.element_size() != 2 or weight.element_size() != 2:
+        raise RLError("hidden / weight must be bf16")
+    if hidden.stride(1) != 1 or weight.stride(1) != 1:
+        raise RLError("hidden / weight rows must be contiguous")
+    n, d = hidden.shape
+    _check(lib.rl_lmhead_logprob(_dev(hidden, "hidden"), hidden.stride(0), _dev(weight, "weight"), weight.stride(0),
+                                 n, d, weight.shape[0], _dev(targets, "targets"), float(inv_temperature),
+                                 _dev(logp_out, "logp_out"), _dev(lse_out, "lse_out") if lse_out is not None else None,
+                                 _stream(stream)), "rl_lmhead_logprob")
 

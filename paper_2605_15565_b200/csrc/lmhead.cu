@@ -1,0 +1,277 @@
+// (8) Fused LM-head log-prob — NEXT 4 of SURVEY.md §8(f), forward half ("Fused LM-head GEMM +
+// loss (tcgen05, logits never materialised) ... it takes hidden states and W").
+//
+// logp_t = x_{t,y} - lse_t with x = (h W^T) * inv_T (c3 of SURVEY.md §8(c) on the LM head's
+// output), computed without writing the [N, V] logits: the logits tile lives only in TMEM.
+//
+// Per CTA: one block of kBM = 128 token rows against every vocabulary tile of kBN = 256 rows of W.
+//   warp 0 (one lane)  TMA producer: 2-D tensor copies (128-B swizzle) of the hidden block's and
+//                      the W tile's K-slices (64 bf16 = 128 B) into a kStages-deep smem ring
+//   warp 1 (one lane)  MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M = 128, N = 256, K = 16,
+//                      bf16 x bf16 -> fp32 in TMEM; two accumulators (2 x 256 TMEM columns) so
+//                      the MMAs of vocabulary tile j+1 run while tile j is reduced
+//   warps 2..5         epilogue: tcgen05.ld 32 columns at a time (thread = token row = TMEM
+//                      lane), online (max, sum 2^(t - max)) over the row, the target logit picked
+//                      with compile-time indices; after the last tile lse and logp are written
+// The hidden block is re-read from L2 once per vocabulary tile; W streams from HBM / L2.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace rl {
+
+constexpr int kLmBM = 128, kLmBN = 256, kLmBK = 64, kLmStages = 4;
+constexpr int kLmThreads = 192;
+constexpr uint32_t kLmABytes = kLmBM * kLmBK * 2, kLmBBytes = kLmBN * kLmBK * 2;
+constexpr uint32_t kLmStageBytes = kLmABytes + kLmBBytes;  // 48 KB
+constexpr size_t kLmSmem = (size_t)kLmStages * kLmStageBytes + 1024;
+
+struct LmArgs {
+  const int32_t* targets;
+  int64_t n, V;
+  int32_t kblocks, vtiles;
+  float inv_t;
+  float* logp_out;
+  float* lse_out;
+};
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(sm100::smem_u32(bar))
+      : "memory");
+}
+// K-major operand, 128-B swizzle (8-row groups of 1024 B), descriptor version 1 (sm100)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   sm100::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// instruction descriptor, kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1),
+// both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+constexpr uint32_t kLmIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kLmBN >> 3) << 17) |
+                              ((uint32_t)(kLmBM >> 4) << 24);
+
+__global__ void __launch_bounds__(kLmThreads, 1)
+    lmhead_logprob_kernel(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ CUtensorMap tm_w,
+                          const LmArgs a) {
+  extern __shared__ uint8_t lm_smem_raw[];
+  __shared__ __align__(8) uint64_t full[kLmStages], empty[kLmStages], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t sbase = (sm100::smem_u32(lm_smem_raw) + 1023u) & ~1023u;
+  const int64_t m0 = (int64_t)blockIdx.x * kLmBM;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kLmStages; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&acc_full[i], 1);
+      sm100::mbar_init(&acc_empty[i], 4);
+    }
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     sm100::smem_u32(&tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int total = a.vtiles * a.kblocks;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      for (int it = 0; it < total; ++it) {
+        const int st = it % kLmStages;
+        const uint32_t ph = (uint32_t)(it / kLmStages) & 1u;
+        sm100::mbar_wait(&empty[st], ph ^ 1u);
+        const int j = it / a.kblocks, kb = it % a.kblocks;
+        const uint32_t sa = sbase + (uint32_t)st * kLmStageBytes, sb = sa + kLmABytes;
+        sm100::mbar_arrive_expect_tx(&full[st], kLmStageBytes);
+        tma_load_2d(sa, &tm_h, kb * kLmBK, (int32_t)m0, &full[st]);
+        tma_load_2d(sb, &tm_w, kb * kLmBK, j * kLmBN, &full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      int it = 0;
+      for (int j = 0; j < a.vtiles; ++j) {
+        const int acc = j & 1;
+        sm100::mbar_wait(&acc_empty[acc], (((uint32_t)j >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t td = tmem + (uint32_t)acc * kLmBN;
+        for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
+          const int st = it % kLmStages;
+          sm100::mbar_wait(&full[st], (uint32_t)(it / kLmStages) & 1u);
+          tc_fence_after();
+          const uint32_t sa = sbase + (uint32_t)st * kLmStageBytes, sb = sa + kLmABytes;
+          const uint64_t ad = umma_desc_sw128(sa), bd = umma_desc_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < kLmBK / 16; ++k)  // K = 16 bf16 = 32 B per MMA: start address + 2 (16-B units)
+            umma_bf16(td, ad + 2 * k, bd + 2 * k, kLmIdesc, (kb | k) != 0);
+          umma_commit(&empty[st]);  // smem slot free once these MMAs have read it
+        }
+        umma_commit(&acc_full[acc]);  // accumulator complete
+      }
+    }
+  } else {  // ---------------------------------------------------------- epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int64_t row = m0 + q * 32 + lane;
+    const bool live = row < a.n;
+    const int32_t y = live ? a.targets[row] : -1;
+    const float k = a.inv_t * RL_LOG2E;
+    float m = -INFINITY, s = 0.f, zy = 0.f;
+    for (int j = 0; j < a.vtiles; ++j) {
+      const int acc = j & 1;
+      sm100::mbar_wait(&acc_full[acc], ((uint32_t)j >> 1) & 1u);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < kLmBN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kLmBN + c * 32), v);
+        const int64_t c0 = (int64_t)j * kLmBN + c * 32;
+        if (c0 >= a.V) break;
+        const int64_t dy = (int64_t)y - c0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) zy = (dy == i) ? v[i] : zy;
+        if (c0 + 32 > a.V) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = (c0 + i < a.V) ? v[i] : -INFINITY;
+        }
+        float cm = v[0];
+#pragma unroll
+        for (int i = 1; i < 32; ++i) cm = fmaxf(cm, v[i]);
+        const float nm = fmaxf(m, cm * k);
+        float acc_s = (m == -INFINITY) ? 0.f : s * exp2f(m - nm);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc_s += exp2f(fmaf(v[i], k, -nm));
+        m = nm;
+        s = acc_s;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&acc_empty[acc]);
+    }
+    if (live) {
+      const float lse2 = m + log2f(s);
+      if (a.lse_out) a.lse_out[row] = lse2 * RL_LN2;
+      float lp = 0.f;
+      if (y >= 0 && y < a.V) lp = zy * a.inv_t - lse2 * RL_LN2;
+      else if (y >= a.V) lp = __int_as_float(0x7fc00000);
+      a.logp_out[row] = lp;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+typedef CUresult (*PfnTensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                            CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                            CUtensorMapFloatOOBfill);
+
+static PfnTensorMapEncodeTiled tensor_map_encoder() {
+  static PfnTensorMapEncodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PfnTensorMapEncodeTiled)p;
+  }
+  return fn;
+}
+
+// rows x cols bf16 matrix (row stride ld elements) as a 2-D tensor map with a {64, box_rows} box
+static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_rows) {
+  PfnTensorMapEncodeTiled enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kLmBK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace rl
+
+extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                                       int64_t n_tokens, int64_t d, int64_t vocab, const int32_t* targets,
+                                       float inv_temperature, float* logp_out, float* lse_out, rl_stream stream) {
+  using namespace rl;
+  if (n_tokens < 0 || d < 1 || vocab < 1) return fail(RL_ERR_INVALID_ARGUMENT, "need n_tokens >= 0, d >= 1, vocab >= 1");
+  if (ld_hidden < d || ld_weight < d) return fail(RL_ERR_INVALID_ARGUMENT, "ld_hidden / ld_weight < d");
+  if (n_tokens >= ((int64_t)1 << 31) || vocab >= ((int64_t)1 << 31) || d >= ((int64_t)1 << 31))
+    return fail(RL_ERR_UNSUPPORTED, "n_tokens, d and vocab must be < 2^31");
+  if (!(inv_temperature > 0.f) || !isfinite(inv_temperature))
+    return fail(RL_ERR_INVALID_ARGUMENT, "inv_temperature must be finite and > 0");
+  if (n_tokens == 0) return RL_OK;
+  if (!hidden || !weight || !targets || !logp_out) return fail(RL_ERR_INVALID_ARGUMENT, "NULL hidden/weight/targets/logp_out");
+  if (((uintptr_t)hidden & 15) || ((uintptr_t)weight & 15) || (ld_hidden % 8) || (ld_weight % 8))
+    return fail(RL_ERR_ALIGNMENT, "hidden / weight must be 16-B aligned with ld % 8 == 0");
+  CUtensorMap mh, mw;
+  if (!make_map(&mh, hidden, n_tokens, d, ld_hidden, kLmBM) || !make_map(&mw, weight, vocab, d, ld_weight, kLmBN))
+    return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  LmArgs a;
+  a.targets = targets;
+  a.n = n_tokens;
+  a.V = vocab;
+  a.kblocks = (int32_t)((d + kLmBK - 1) / kLmBK);
+  a.vtiles = (int32_t)((vocab + kLmBN - 1) / kLmBN);
+  a.inv_t = inv_temperature;
+  a.logp_out = logp_out;
+  a.lse_out = lse_out;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(lmhead_logprob_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) !=
+        cudaSuccess)
+      return check_launch("cudaFuncSetAttribute(lmhead)");
+    attr = true;
+  }
+  const unsigned grid = (unsigned)((n_tokens + kLmBM - 1) / kLmBM);
+  lmhead_logprob_kernel<<<grid, kLmThreads, kLmSmem, (cudaStream_t)stream>>>(mh, mw, a);
+  return check_launch("lmhead_logprob_kernel");
+}

@@ -691,3 +691,73 @@ def test_delta_encode_apply(cuda_lib, n, frac):
         assert int(count2.item()) == k
         assert np.array_equal(idx2.cpu().numpy().view(np.uint32), ri[:c2])
         assert np.array_equal(words2.cpu().numpy().view(np.uint16), rw[:c2])
+
+
+# ----------------------------------------------------------------------------- NEXT 4: LM head
+def _lm_inputs(N, d, V, seed, ld_h=None, ld_w=None):
+    """Seeded bf16 hidden states ~ N(0, 1) and LM-head rows ~ N(0, 9/d) (logit sd ~ 3, a few hot
+    rows per token as in the configs' logit model), as bit patterns (host) and CUDA tensors."""
+    t = torch()
+    rng = np.random.default_rng(seed)
+    ld_h, ld_w = ld_h or d, ld_w or d
+    h = rng.normal(size=(N, ld_h)).astype(np.float32)
+    w = (rng.normal(size=(V, ld_w)) * (3.0 / math.sqrt(d))).astype(np.float32)
+    if V > 4:  # hot vocabulary rows aligned with some tokens' hidden states (peaked rows)
+        for i in range(min(N, 64)):
+            w[(7 * i) % V, :d] += 0.5 * h[i, :d] / math.sqrt(d)
+    hb = (h.view(np.uint32) >> 16).astype(np.uint16)
+    wb = (w.view(np.uint32) >> 16).astype(np.uint16)
+    ht = t.from_numpy(hb.view(np.int16)).cuda().view(t.bfloat16)
+    wt = t.from_numpy(wb.view(np.int16)).cuda().view(t.bfloat16)
+    y = rng.integers(0, V, size=N).astype(np.int32)
+    y[::7] = (7 * np.arange(len(y[::7]))) % V   # some targets on the hot rows
+    if N > 3:
+        y[1], y[2] = -100, V + 3                   # ignored and out-of-range targets
+    return hb[:, :d], wb[:, :d], ht[:, :d], wt[:, :d], y
+
+
+@pytest.mark.parametrize("N,d,V,ldh,ldw", [(1, 64, 256, None, None), (300, 128, 1000, None, None),
+                                          (129, 200, 513, 208, 216), (1024, 512, 4099, None, None),
+                                          (257, 4096, 2000, None, None), (64, 16, 70000, None, None)])
+def test_lmhead_logprob(cuda_lib, N, d, V, ldh, ldw):
+    """rl_lmhead_logprob (tcgen05 GEMM + online softmax, logits never written) against the oracle
+    c3(h W^T) in fp64: logp and lse within 2e-3 absolute (SURVEY.md §8(g) logp bar); ragged N (not a
+    multiple of 128), V (not of 256), d (K tail, not of 64), padded row strides, y < 0 and y >= V."""
+    t = torch()
+    hb, wb, ht, wt, y = _lm_inputs(N, d, V, seed=N + d + V, ld_h=ldh, ld_w=ldw)
+    logp = t.empty(N, dtype=t.float32, device="cuda")
+    lse = t.empty(N, dtype=t.float32, device="cuda")
+    cuda_lib.lmhead_logprob(ht, wt, dev(y), logp, lse)
+    t.cuda.synchronize()
+    ref_lp, ref_lse = oracle.lmhead_logprob(hb, wb, y)
+    got_lp, got_lse = logp.cpu().numpy().astype(np.float64), lse.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(got_lse - ref_lse)) <= 2e-3
+    ok = ~np.isnan(ref_lp)
+    assert np.array_equal(np.isnan(got_lp), ~ok)
+    assert np.max(np.abs(got_lp[ok] - ref_lp[ok])) <= 2e-3
+    if N > 3:
+        assert got_lp[1] == 0.0 and np.isnan(got_lp[2])
+
+
+def test_lmhead_logprob_full_size_sampled(cuda_lib):
+    """Qwen3-8B-sized head (d = 4096, V = 151936) on 2,048 tokens: 24 sampled rows against the
+    oracle (its fp64 row is h W^T over all 151,936 vocabulary rows), every row finite."""
+    t = torch()
+    N, d, V = 2048, 4096, 151936
+    g = t.Generator(device="cuda").manual_seed(11)
+    ht = t.randn(N, d, device="cuda", generator=g).to(t.bfloat16)
+    wt = (t.randn(V, d, device="cuda", generator=g) * (3.0 / math.sqrt(d))).to(t.bfloat16)
+    y = t.randint(0, V, (N,), device="cuda", generator=g, dtype=t.int32)
+    logp = t.empty(N, dtype=t.float32, device="cuda")
+    lse = t.empty(N, dtype=t.float32, device="cuda")
+    cuda_lib.lmhead_logprob(ht, wt, y, logp, lse)
+    t.cuda.synchronize()
+    assert bool(t.isfinite(logp).all()) and bool(t.isfinite(lse).all())
+    rows = np.random.default_rng(0).choice(N, size=24, replace=False)
+    rows[0], rows[1] = 0, N - 1
+    wb = wt.view(t.int16).cpu().numpy().view(np.uint16)
+    hb = ht[t.from_numpy(rows).cuda()].view(t.int16).cpu().numpy().view(np.uint16)
+    yr = y.cpu().numpy()[rows]
+    ref_lp, ref_lse = oracle.lmhead_logprob(hb, wb, yr)
+    assert np.max(np.abs(logp.cpu().numpy()[rows] - ref_lp)) <= 2e-3
+    assert np.max(np.abs(lse.cpu().numpy()[rows] - ref_lse)) <= 2e-3
