@@ -30,10 +30,11 @@ constexpr size_t kLmSmem = (size_t)kLmStages * kLmStageBytes + 1024;
 struct LmArgs {
   const int32_t* targets;
   int64_t n, V;
-  int32_t kblocks, vtiles;
+  int32_t kblocks, vtiles, tiles_per_split;
   float inv_t;
   float* logp_out;
   float* lse_out;
+  float4* partial;  // [splits][n] (max2, sum, raw target logit, -) when gridDim.y > 1
 };
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
@@ -93,6 +94,10 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = (sm100::smem_u32(lm_smem_raw) + 1023u) & ~1023u;
   const int64_t m0 = (int64_t)blockIdx.x * kLmBM;
+  // this CTA's vocabulary tiles [jt0, jt1) (split blockIdx.y of gridDim.y)
+  const int jt0 = (int)blockIdx.y * a.tiles_per_split;
+  const int jt1 = min(a.vtiles, jt0 + a.tiles_per_split);
+  const int ntiles = max(0, jt1 - jt0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kLmStages; ++i) {
       sm100::mbar_init(&full[i], 1);
@@ -114,7 +119,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-  const int total = a.vtiles * a.kblocks;
+  const int total = ntiles * a.kblocks;
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
@@ -122,7 +127,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
         const int st = it % kLmStages;
         const uint32_t ph = (uint32_t)(it / kLmStages) & 1u;
         sm100::mbar_wait(&empty[st], ph ^ 1u);
-        const int j = it / a.kblocks, kb = it % a.kblocks;
+        const int j = jt0 + it / a.kblocks, kb = it % a.kblocks;
         const uint32_t sa = sbase + (uint32_t)st * kLmStageBytes, sb = sa + kLmABytes;
         sm100::mbar_arrive_expect_tx(&full[st], kLmStageBytes);
         tma_load_2d(sa, &tm_h, kb * kLmBK, (int32_t)m0, &full[st]);
@@ -132,7 +137,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       int it = 0;
-      for (int j = 0; j < a.vtiles; ++j) {
+      for (int j = 0; j < ntiles; ++j) {
         const int acc = j & 1;
         sm100::mbar_wait(&acc_empty[acc], (((uint32_t)j >> 1) & 1u) ^ 1u);
         tc_fence_after();
@@ -158,7 +163,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
     const int32_t y = live ? a.targets[row] : -1;
     const float k = a.inv_t * RL_LOG2E;
     float m = -INFINITY, s = 0.f, zy = 0.f;
-    for (int j = 0; j < a.vtiles; ++j) {
+    for (int j = 0; j < ntiles; ++j) {
       const int acc = j & 1;
       sm100::mbar_wait(&acc_full[acc], ((uint32_t)j >> 1) & 1u);
       tc_fence_after();
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       for (int c = 0; c < kLmBN / 32; ++c) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kLmBN + c * 32), v);
-        const int64_t c0 = (int64_t)j * kLmBN + c * 32;
+        const int64_t c0 = (int64_t)(jt0 + j) * kLmBN + c * 32;
         if (c0 >= a.V) break;
         const int64_t dy = (int64_t)y - c0;
 #pragma unroll
@@ -189,7 +194,9 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&acc_empty[acc]);
     }
-    if (live) {
+    if (live && gridDim.y > 1) {
+      a.partial[(int64_t)blockIdx.y * a.n + row] = make_float4(m, s, zy, 0.f);
+    } else if (live) {
       const float lse2 = m + log2f(s);
       if (a.lse_out) a.lse_out[row] = lse2 * RL_LN2;
       float lp = 0.f;
@@ -204,6 +211,52 @@ __global__ void __launch_bounds__(kLmThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+}
+
+// splits > 1: combine the per-split (max2, sum, target logit) records of each row in split order
+__global__ void lmhead_combine_kernel(const float4* __restrict__ partial, int splits, const LmArgs a) {
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.n; row += (int64_t)gridDim.x * blockDim.x) {
+    float M = -INFINITY;
+    for (int i = 0; i < splits; ++i) M = fmaxf(M, partial[(int64_t)i * a.n + row].x);
+    float S = 0.f, zy = 0.f;
+    for (int i = 0; i < splits; ++i) {
+      const float4 e = partial[(int64_t)i * a.n + row];
+      if (e.x != -INFINITY) S += e.y * exp2f(e.x - M);
+      zy += e.z;
+    }
+    const float lse2 = M + log2f(S);
+    if (a.lse_out) a.lse_out[row] = lse2 * RL_LN2;
+    const int32_t y = a.targets[row];
+    float lp = 0.f;
+    if (y >= 0 && y < a.V) lp = zy * a.inv_t - lse2 * RL_LN2;
+    else if (y >= a.V) lp = __int_as_float(0x7fc00000);
+    a.logp_out[row] = lp;
+  }
+}
+
+// vocabulary splits: minimise waves x tiles per CTA over the SMs (ties: fewer splits)
+static int lm_splits(int64_t n, int64_t vocab, int sms) {
+  const int64_t rb = (n + kLmBM - 1) / kLmBM, vt = (vocab + kLmBN - 1) / kLmBN;
+  int best = 1;
+  int64_t best_cost = INT64_MAX;
+  for (int64_t sp = 1; sp <= std::min<int64_t>(vt, 64); ++sp) {
+    const int64_t tps = (vt + sp - 1) / sp, used = (vt + tps - 1) / tps;
+    const int64_t cost = ((rb * used + sms - 1) / sms) * tps;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = (int)used;
+    }
+  }
+  return best;
+}
+static int lm_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
+  }
+  return sms;
 }
 
 typedef CUresult (*PfnTensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -238,9 +291,17 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t col
 
 }  // namespace rl
 
+extern "C" size_t rl_lmhead_workspace_size(int64_t n_tokens, int64_t vocab) {
+  using namespace rl;
+  if (n_tokens <= 0 || vocab <= 0) return 0;
+  const int sp = lm_splits(n_tokens, vocab, lm_sms());
+  return sp > 1 ? (size_t)sp * (size_t)n_tokens * sizeof(float4) : 0;
+}
+
 extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
                                        int64_t n_tokens, int64_t d, int64_t vocab, const int32_t* targets,
-                                       float inv_temperature, float* logp_out, float* lse_out, rl_stream stream) {
+                                       float inv_temperature, float* logp_out, float* lse_out, void* workspace,
+                                       size_t workspace_bytes, rl_stream stream) {
   using namespace rl;
   if (n_tokens < 0 || d < 1 || vocab < 1) return fail(RL_ERR_INVALID_ARGUMENT, "need n_tokens >= 0, d >= 1, vocab >= 1");
   if (ld_hidden < d || ld_weight < d) return fail(RL_ERR_INVALID_ARGUMENT, "ld_hidden / ld_weight < d");
@@ -261,6 +322,12 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
   a.V = vocab;
   a.kblocks = (int32_t)((d + kLmBK - 1) / kLmBK);
   a.vtiles = (int32_t)((vocab + kLmBN - 1) / kLmBN);
+  const int splits = lm_splits(n_tokens, vocab, lm_sms());
+  a.tiles_per_split = (a.vtiles + splits - 1) / splits;
+  const size_t need = splits > 1 ? (size_t)splits * (size_t)n_tokens * sizeof(float4) : 0;
+  if (need && (!workspace || workspace_bytes < need))
+    return fail(RL_ERR_WORKSPACE, "workspace must be >= %zu bytes (rl_lmhead_workspace_size)", need);
+  a.partial = (float4*)workspace;
   a.inv_t = inv_temperature;
   a.logp_out = logp_out;
   a.lse_out = lse_out;
@@ -271,7 +338,11 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
       return check_launch("cudaFuncSetAttribute(lmhead)");
     attr = true;
   }
-  const unsigned grid = (unsigned)((n_tokens + kLmBM - 1) / kLmBM);
+  const dim3 grid((unsigned)((n_tokens + kLmBM - 1) / kLmBM), (unsigned)splits);
   lmhead_logprob_kernel<<<grid, kLmThreads, kLmSmem, (cudaStream_t)stream>>>(mh, mw, a);
-  return check_launch("lmhead_logprob_kernel");
+  rl_status st = check_launch("lmhead_logprob_kernel");
+  if (st != RL_OK || splits == 1) return st;
+  const int cb = (int)std::min<int64_t>((n_tokens + 255) / 256, 148 * 4);
+  lmhead_combine_kernel<<<cb, 256, 0, (cudaStream_t)stream>>>(a.partial, splits, a);
+  return check_launch("lmhead_combine_kernel");
 }
