@@ -350,14 +350,14 @@ rl_status rl_bf16_delta_apply(void* base, int64_t n_words, const uint32_t* idx, 
  *   ld_*       row strides in elements, >= d, multiples of 8
  *   targets    device i32 [n_tokens]: y < 0 -> logp 0; y >= vocab -> logp NaN (as rl_token_logprob)
  *   logp_out   device f32 [n_tokens];  lse_out  device f32 [n_tokens] or NULL (natural log)
- *   workspace  device, >= rl_lmhead_workspace_size(n_tokens, vocab) bytes (0 when the grid of
- *              128-token blocks fills the GPU alone; else per-vocabulary-split row records)
+ *   workspace  device, >= rl_lmhead_workspace_size(n_tokens, d, vocab) bytes (per-vocabulary-split
+ *              row records, 16 B per token per split; 0 when one split is used)
  * fp32 accumulation of bf16 products on the tensor cores (tcgen05.mma kind::f16), fp32 softmax.
  * Errors: RL_ERR_INVALID_ARGUMENT (sizes, NULL, inv_temperature <= 0), RL_ERR_ALIGNMENT,
  * RL_ERR_UNSUPPORTED (n_tokens, d or vocab >= 2^31), RL_ERR_WORKSPACE, RL_ERR_CUDA (tensor-map
  * encoding, launch).
  * Deterministic: fixed K order per tile, fixed tile order per row. */
-size_t rl_lmhead_workspace_size(int64_t n_tokens, int64_t vocab);
+size_t rl_lmhead_workspace_size(int64_t n_tokens, int64_t d, int64_t vocab);
 rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
                             int64_t n_tokens, int64_t d, int64_t vocab, const int32_t* targets,
                             float inv_temperature, float* logp_out, float* lse_out, void* workspace,

@@ -85,7 +85,7 @@ _SIGS = {
     "rl_bf16_delta_encode": (i32, [vp, vp, i64, vp, vp, i64, vp, vp, sz, vp]),
     "rl_bf16_delta_apply": (i32, [vp, i64, vp, vp, vp, i64, vp, vp]),
     "rl_lmhead_logprob": (i32, [vp, i64, vp, i64, i64, i64, i64, vp, f32, vp, vp, vp, sz, vp]),
-    "rl_lmhead_workspace_size": (sz, [i64, i64]),
+    "rl_lmhead_workspace_size": (sz, [i64, i64, i64]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
@@ -423,8 +423,8 @@ def delta_apply(base, idx, words, count, bad_count, stream=None):
                                    _stream(stream)), "rl_bf16_delta_apply")
 
 
-def lmhead_workspace_size(n_tokens, vocab):
-    return int(load().rl_lmhead_workspace_size(int(n_tokens), int(vocab)))
+def lmhead_workspace_size(n_tokens, d, vocab):
+    return int(load().rl_lmhead_workspace_size(int(n_tokens), int(d), int(vocab)))
 
 
 def lmhead_logprob(hidden, weight, targets, logp_out, lse_out=None, inv_temperature=1.0, workspace=None,
@@ -432,7 +432,7 @@ def lmhead_logprob(hidden, weight, targets, logp_out, lse_out=None, inv_temperat
     """Fused LM-head log-prob (NEXT 4, forward): logp_t = log_softmax((h W^T) * inv_T)[y_t] without
     materialising the logits.  hidden bf16 [N, d] and weight bf16 [V, d] (row strides may exceed d),
     targets int32 [N]; logp_out / lse_out float32 [N]; workspace: CUDA uint8 tensor of at least
-    lmhead_workspace_size(N, V) bytes (None when that is 0)."""
+    lmhead_workspace_size(N, d, V) bytes (None when that is 0)."""
     lib = load()
     if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
         raise RLError("hidden [N, d] and weight [V, d] must share d")

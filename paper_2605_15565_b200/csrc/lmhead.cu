@@ -34,7 +34,7 @@ struct LmArgs {
   float inv_t;
   float* logp_out;
   float* lse_out;
-  float4* partial;  // [splits][n] (max2, sum, raw target logit, -) when gridDim.y > 1
+  float4* partial;  // [splits][n] (max2, sum, raw target logit, -) when gridDim.x > 1
 };
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
@@ -93,9 +93,11 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = (sm100::smem_u32(lm_smem_raw) + 1023u) & ~1023u;
-  const int64_t m0 = (int64_t)blockIdx.x * kLmBM;
-  // this CTA's vocabulary tiles [jt0, jt1) (split blockIdx.y of gridDim.y)
-  const int jt0 = (int)blockIdx.y * a.tiles_per_split;
+  // grid (splits, row blocks), split fastest: the CTAs resident together cover few token blocks, so
+  // every hidden block re-read (once per vocabulary tile) is an L2 hit shared by its splits
+  const int64_t m0 = (int64_t)blockIdx.y * kLmBM;
+  // this CTA's vocabulary tiles [jt0, jt1) (split blockIdx.x of gridDim.x)
+  const int jt0 = (int)blockIdx.x * a.tiles_per_split;
   const int jt1 = min(a.vtiles, jt0 + a.tiles_per_split);
   const int ntiles = max(0, jt1 - jt0);
   if (threadIdx.x == 0) {
@@ -194,8 +196,8 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&acc_empty[acc]);
     }
-    if (live && gridDim.y > 1) {
-      a.partial[(int64_t)blockIdx.y * a.n + row] = make_float4(m, s, zy, 0.f);
+    if (live && gridDim.x > 1) {
+      a.partial[(int64_t)blockIdx.x * a.n + row] = make_float4(m, s, zy, 0.f);
     } else if (live) {
       const float lse2 = m + log2f(s);
       if (a.lse_out) a.lse_out[row] = lse2 * RL_LN2;
@@ -234,12 +236,26 @@ __global__ void lmhead_combine_kernel(const float4* __restrict__ partial, int sp
   }
 }
 
-// vocabulary splits: minimise waves x tiles per CTA over the SMs (ties: fewer splits)
-static int lm_splits(int64_t n, int64_t vocab, int sms) {
+// Vocabulary splits S (the fast grid index, so a wave holds ~sms / S token blocks).  Two L2 effects
+// set S (measured, tools/lmbench.py, d = 4096, V = 151936):
+//   * a wave's hidden blocks (128 x d bf16 each, re-read once per vocabulary tile) must stay in L2:
+//     S = 1 puts 148 blocks = 148 MB in flight and thrashes the 126 MB L2 (70 GB of DRAM reads at
+//     N = 16384 for 1.4 GB of operands) — S_min keeps them <= 80 MB;
+//   * every further split divides the readers sharing a W tile while it is L2-resident (S = 8: 1277
+//     TFLOP/s at N = 16384, S = 2: 1514; S = 15: 42 GB of DRAM reads).
+// So S = S_min when that grid fills the GPU; smaller grids (few token blocks) search S in
+// [S_min, 16] for the fewest waves x tiles per CTA (N = 4096: S = 9, 1533 TFLOP/s; S = 5: 922).
+static int lm_splits(int64_t n, int64_t d, int64_t vocab, int sms) {
   const int64_t rb = (n + kLmBM - 1) / kLmBM, vt = (vocab + kLmBN - 1) / kLmBN;
+  const int64_t block_bytes = (int64_t)kLmBM * d * 2;
+  const int64_t smin = std::min<int64_t>(vt, std::max<int64_t>(1, (sms * block_bytes + (80ll << 20) - 1) / (80ll << 20)));
+  if (rb * smin >= sms) {
+    const int64_t tps = (vt + smin - 1) / smin;
+    return (int)((vt + tps - 1) / tps);
+  }
   int best = 1;
   int64_t best_cost = INT64_MAX;
-  for (int64_t sp = 1; sp <= std::min<int64_t>(vt, 64); ++sp) {
+  for (int64_t sp = smin; sp <= std::min<int64_t>(vt, 16); ++sp) {
     const int64_t tps = (vt + sp - 1) / sp, used = (vt + tps - 1) / tps;
     const int64_t cost = ((rb * used + sms - 1) / sms) * tps;
     if (cost < best_cost) {
@@ -291,10 +307,10 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t col
 
 }  // namespace rl
 
-extern "C" size_t rl_lmhead_workspace_size(int64_t n_tokens, int64_t vocab) {
+extern "C" size_t rl_lmhead_workspace_size(int64_t n_tokens, int64_t d, int64_t vocab) {
   using namespace rl;
-  if (n_tokens <= 0 || vocab <= 0) return 0;
-  const int sp = lm_splits(n_tokens, vocab, lm_sms());
+  if (n_tokens <= 0 || vocab <= 0 || d <= 0) return 0;
+  const int sp = lm_splits(n_tokens, d, vocab, lm_sms());
   return sp > 1 ? (size_t)sp * (size_t)n_tokens * sizeof(float4) : 0;
 }
 
@@ -322,8 +338,12 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
   a.V = vocab;
   a.kblocks = (int32_t)((d + kLmBK - 1) / kLmBK);
   a.vtiles = (int32_t)((vocab + kLmBN - 1) / kLmBN);
-  const int splits = lm_splits(n_tokens, vocab, lm_sms());
+  int splits = lm_splits(n_tokens, d, vocab, lm_sms());
+  static int forced = -1;  // RL_LM_SPLITS (development): force the split count (<= the workspace's)
+  if (forced < 0) forced = getenv("RL_LM_SPLITS") ? atoi(getenv("RL_LM_SPLITS")) : 0;
+  if (forced > 0 && forced <= splits) splits = forced;
   a.tiles_per_split = (a.vtiles + splits - 1) / splits;
+  splits = (a.vtiles + a.tiles_per_split - 1) / a.tiles_per_split;
   const size_t need = splits > 1 ? (size_t)splits * (size_t)n_tokens * sizeof(float4) : 0;
   if (need && (!workspace || workspace_bytes < need))
     return fail(RL_ERR_WORKSPACE, "workspace must be >= %zu bytes (rl_lmhead_workspace_size)", need);
@@ -338,7 +358,8 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
       return check_launch("cudaFuncSetAttribute(lmhead)");
     attr = true;
   }
-  const dim3 grid((unsigned)((n_tokens + kLmBM - 1) / kLmBM), (unsigned)splits);
+  if ((n_tokens + kLmBM - 1) / kLmBM > 65535) return fail(RL_ERR_UNSUPPORTED, "n_tokens > 65535 * 128 per call");
+  const dim3 grid((unsigned)splits, (unsigned)((n_tokens + kLmBM - 1) / kLmBM));
   lmhead_logprob_kernel<<<grid, kLmThreads, kLmSmem, (cudaStream_t)stream>>>(mh, mw, a);
   rl_status st = check_launch("lmhead_logprob_kernel");
   if (st != RL_OK || splits == 1) return st;

@@ -694,9 +694,9 @@ def test_delta_encode_apply(cuda_lib, n, frac):
 
 
 # ----------------------------------------------------------------------------- NEXT 4: LM head
-def _lm_ws(N, V):
+def _lm_ws(N, d, V):
     import paper_2605_15565_b200 as rl
-    return torch().empty(max(1, rl.lmhead_workspace_size(N, V)), dtype=torch().uint8, device="cuda")
+    return torch().empty(max(1, rl.lmhead_workspace_size(N, d, V)), dtype=torch().uint8, device="cuda")
 
 
 def _lm_inputs(N, d, V, seed, ld_h=None, ld_w=None):
@@ -732,7 +732,7 @@ def test_lmhead_logprob(cuda_lib, N, d, V, ldh, ldw):
     hb, wb, ht, wt, y = _lm_inputs(N, d, V, seed=N + d + V, ld_h=ldh, ld_w=ldw)
     logp = t.empty(N, dtype=t.float32, device="cuda")
     lse = t.empty(N, dtype=t.float32, device="cuda")
-    cuda_lib.lmhead_logprob(ht, wt, dev(y), logp, lse, workspace=_lm_ws(N, V))
+    cuda_lib.lmhead_logprob(ht, wt, dev(y), logp, lse, workspace=_lm_ws(N, d, V))
     t.cuda.synchronize()
     ref_lp, ref_lse = oracle.lmhead_logprob(hb, wb, y)
     got_lp, got_lse = logp.cpu().numpy().astype(np.float64), lse.cpu().numpy().astype(np.float64)
@@ -755,7 +755,7 @@ def test_lmhead_logprob_full_size_sampled(cuda_lib):
     y = t.randint(0, V, (N,), device="cuda", generator=g, dtype=t.int32)
     logp = t.empty(N, dtype=t.float32, device="cuda")
     lse = t.empty(N, dtype=t.float32, device="cuda")
-    cuda_lib.lmhead_logprob(ht, wt, y, logp, lse, workspace=_lm_ws(N, V))
+    cuda_lib.lmhead_logprob(ht, wt, y, logp, lse, workspace=_lm_ws(N, d, V))
     t.cuda.synchronize()
     assert bool(t.isfinite(logp).all()) and bool(t.isfinite(lse).all())
     rows = np.random.default_rng(0).choice(N, size=24, replace=False)

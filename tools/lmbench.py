@@ -21,7 +21,7 @@ def main():
     y = torch.randint(0, V, (N,), device="cuda", generator=g, dtype=torch.int32)
     lp = torch.empty(N, device="cuda")
     lse = torch.empty(N, device="cuda")
-    ws = torch.empty(max(1, rl.lmhead_workspace_size(N, V)), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(max(1, rl.lmhead_workspace_size(N, d, V)), dtype=torch.uint8, device="cuda")
     call = lambda: rl.lmhead_logprob(h, w, y, lp, lse, workspace=ws)
     call()
     torch.cuda.synchronize()
