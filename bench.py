@@ -52,7 +52,7 @@ def parse():
                     help="clip: the north_star's clipped surrogate (default); full: + decoupled proximal "
                          "ratio, k3 KL penalty (beta 1e-3, PAPER.md:572) and entropy (NEXT 2); m2po: "
                          "rl_token_logprob -> rl_m2po_mask (tau 0.01, PAPER.md:572) -> unclipped loss (NEXT 1)")
-    ap.add_argument("--config", default="single", choices=["single", "long", "vocabpar", "multi"],
+    ap.add_argument("--config", default="single", choices=["single", "long", "vocabpar", "multi", "lmhead"],
                     help="BASELINE.json config (single = the headline metric's workload, the default)")
     return ap.parse_args()
 
@@ -434,6 +434,8 @@ def main():
         os.environ["NCCL_DEBUG"] = "NONE"
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "lmhead":
+        return run_lmhead(args)
     if args.kernel:
         os.environ["RL_LOSS_KERNEL"] = args.kernel
     import numpy as np
@@ -623,6 +625,80 @@ def main():
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_lmhead(args):
+    """NEXT 4 forward (not the headline metric): rl_lmhead_logprob on one GPU — a step is one
+    call over 65,536 tokens of a Qwen3-8B-sized head (d = 4096, V = 151936, bf16); tensor roofline
+    (2 N V d flops per call) against MEASURED_PEAKS.json's bf16 figure.  Replicas only for N > 1
+    (independent token batches, no collective): every rank runs its own batch."""
+    import torch
+    import torch.distributed as dist
+    import paper_2605_15565_b200 as rl
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    rl.load()
+    N, d, V = 65536, 4096, 151936
+    g = torch.Generator(device=dev).manual_seed(1 + rank)
+    h = torch.randn(N, d, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(V, d, device=dev, generator=g) * (3.0 / d ** 0.5)).to(torch.bfloat16)
+    y = torch.randint(0, V, (N,), device=dev, generator=g, dtype=torch.int32)
+    lp = torch.empty(N, device=dev)
+    lse = torch.empty(N, device=dev)
+    ws = torch.empty(max(1, rl.lmhead_workspace_size(N, d, V)), dtype=torch.uint8, device=dev)
+    launches = 1 + (rl.lmhead_workspace_size(N, d, V) > 0)
+    for _ in range(args.warmup):
+        rl.lmhead_logprob(h, w, y, lp, lse, workspace=ws)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i in range(args.steps):
+        rl.lmhead_logprob(h, w, y, lp, lse, workspace=ws)
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = evs[0].elapsed_time(evs[-1])
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = tt.item()
+    per_call = ms / args.steps
+    flops = 2.0 * N * V * d
+    achieved = flops / (per_call / 1e3) / 1e12
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, src = 2250.0, "fallback (nominal dense bf16)"
+    if os.path.exists(pk):
+        with open(pk) as f:
+            peak, src = float(json.load(f)["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, cuBLAS burst)"
+    if rank == 0:
+        print(json.dumps({
+            "metric": "fused LM-head log-prob tokens/s (NEXT 4 forward; d=4096, V=151936)",
+            "value": world * N * args.steps / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_call, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "65,536 tokens x Qwen3-8B-sized LM head (d 4096, V 151936) per GPU per step",
+                       "config": "lmhead", "tokens_per_step": world * N, "parallelism": f"replicas x{world}",
+                       "l2": "no flush: every call streams the 1.24 GB weight >> 126 MB L2"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": src,
+                         "kernel": "lmhead_logprob_kernel (+ lmhead_combine_kernel)",
+                         "algorithmic_flops_per_launch": flops, "avg_launch_ms": per_call},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": launches * args.steps, "clocks": clk}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
