@@ -4,7 +4,9 @@
 // logp_t = x_{t,y} - lse_t with x = (h W^T) * inv_T (c3 of SURVEY.md §8(c) on the LM head's
 // output), computed without writing the [N, V] logits: the logits tile lives only in TMEM.
 //
-// Per CTA: one block of kBM = 128 token rows against every vocabulary tile of kBN = 256 rows of W.
+// Per CTA: one block of kBM = 128 token rows against one range of vocabulary tiles of kBN = 256 rows
+// of W (grid = (vocabulary splits, token blocks), split fastest; the split count is an L2 decision,
+// lm_splits below; with several splits a combine kernel merges the per-split row records).
 //   warp 0 (one lane)  TMA producer: 2-D tensor copies (128-B swizzle) of the hidden block's and
 //                      the W tile's K-slices (64 bf16 = 128 B) into a kStages-deep smem ring
 //   warp 1 (one lane)  MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M = 128, N = 256, K = 16,

@@ -766,3 +766,30 @@ def test_lmhead_logprob_full_size_sampled(cuda_lib):
     ref_lp, ref_lse = oracle.lmhead_logprob(hb, wb, yr)
     assert np.max(np.abs(logp.cpu().numpy()[rows] - ref_lp)) <= 2e-3
     assert np.max(np.abs(lse.cpu().numpy()[rows] - ref_lse)) <= 2e-3
+
+
+def test_lmhead_logprob_temperature_and_errors(cuda_lib):
+    """inv_temperature != 1 against the oracle's c3 temperature; host-detectable errors return
+    before any launch (d mismatch, non-contiguous rows, inv_temperature <= 0, short workspace)."""
+    t = torch()
+    N, d, V = 200, 96, 3001
+    hb, wb, ht, wt, y = _lm_inputs(N, d, V, seed=77)
+    logp = t.empty(N, dtype=t.float32, device="cuda")
+    cuda_lib.lmhead_logprob(ht, wt, dev(y), logp, inv_temperature=0.6, workspace=_lm_ws(N, d, V))
+    t.cuda.synchronize()
+    ref, _ = oracle.lmhead_logprob(hb, wb, y, inv_temperature=0.6)
+    ok = ~np.isnan(ref)
+    assert np.max(np.abs(logp.cpu().numpy()[ok] - ref[ok])) <= 2e-3
+    with pytest.raises(cuda_lib.RLError):
+        cuda_lib.lmhead_logprob(ht, wt[:, :64], dev(y), logp, workspace=_lm_ws(N, d, V))
+    with pytest.raises(cuda_lib.RLError):
+        cuda_lib.lmhead_logprob(ht, wt, dev(y), logp, inv_temperature=0.0, workspace=_lm_ws(N, d, V))
+    big = 20000   # more token blocks: the plan uses vocabulary splits and needs a workspace
+    hb2 = t.zeros((big, d), dtype=t.bfloat16, device="cuda")
+    need = cuda_lib.lmhead_workspace_size(big, d, 151936)
+    if need > 0:
+        w2 = t.zeros((151936, d), dtype=t.bfloat16, device="cuda")
+        y2 = t.zeros(big, dtype=t.int32, device="cuda")
+        lp2 = t.empty(big, dtype=t.float32, device="cuda")
+        with pytest.raises(cuda_lib.RLError):
+            cuda_lib.lmhead_logprob(hb2, w2, y2, lp2, workspace=t.empty(need - 1, dtype=t.uint8, device="cuda"))
