@@ -449,7 +449,9 @@ struct VfArgs {
   float* lse_out;
   double* partials;
   Knobs kn;
-  int32_t count_stats, P, me, nb;  // nb: shared-memory row buffers (2..4)
+  int32_t count_stats, P, me;
+  int32_t nb;  // vp_fused_kernel: shared-memory row buffers (2..4)
+  int32_t pf;  // vp_fused2_kernel: L2 prefetch distance in row groups (0 = off)
   uint32_t epoch;
   float4* rec[8];     // rank q's record array  [P][max_tokens]
   uint32_t* flag[8];  // rank q's flag array    [P][max_tokens]
@@ -707,7 +709,7 @@ __global__ void __launch_bounds__(kV2Cons + 32, 1) vp_fused2_kernel(const VfArgs
   // -------------------------------------------------------------------- row teams
   const int team = warp / WPR, t = tid % NT;
   const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-  const int pf = a.nb;  // L2 prefetch distance in groups (0 = off)
+  const int pf = a.pf;  // L2 prefetch distance in groups (0 = off)
   const uint32_t slice16 = (uint32_t)((a.Vr * elem_bytes<T>() + 15) / 16 * 16);
   if (t == 0)
     for (int64_t gg = 0; gg < ((int64_t)pf < ng ? (int64_t)pf : ng); ++gg)
@@ -805,7 +807,7 @@ static void launch_vp_fused2(const VfArgs& v0, int64_t slice_bytes, int grid, cu
   if (forced < 0) forced = getenv("RL_VP2_WPR") ? atoi(getenv("RL_VP2_WPR")) : 0;
   if (pf < 0) pf = getenv("RL_VP2_PF") ? std::max(0, atoi(getenv("RL_VP2_PF"))) : 1;
   VfArgs v = v0;
-  v.nb = pf;
+  v.pf = pf;
   const int64_t budget = getenv("RL_VP2_BUDGET_KB") ? (int64_t)atoi(getenv("RL_VP2_BUDGET_KB")) << 10
                                                      : (pf > 0 ? 200 << 10 : 300 << 10);
   if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16) slice_bytes = budget / (16 / forced);
