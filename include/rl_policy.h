@@ -363,6 +363,28 @@ rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* w
                             float inv_temperature, float* logp_out, float* lse_out, void* workspace,
                             size_t workspace_bytes, rl_stream stream);
 
+/* ---------------------------------------------------------------- (9) loss from log-probs
+ * c4–c7 of SURVEY.md §8(c) (PPO clipped surrogate; with the NEXT 2 terms of
+ * rl_loss_params) evaluated from per-token log-probs instead of logits: the loss statistics and
+ * the per-token gradient scale s_t of dL/dlogits = s_t (softmax − onehot) (c7), no dlogits write.
+ * Used after rl_lmhead_logprob (NEXT 4: the LM-head loss forward without logits) and by callers
+ * that already hold log-probs.  Same per-token decisions as rl_policy_loss_fwd_bwd.
+ *   logp       device f32 [n_tokens] (c3 log-probs; read for valid tokens only)
+ *   vocab      V (a target >= V is a counted bad target, masked)
+ *   targets, old_logp, loss_mask, token_seq, seq_adv, seq_version, seq_active, p: as
+ *              rl_policy_loss_fwd_bwd (RL_F_ENTROPY is rejected: the entropy needs the logits)
+ *   scale_out  device f32 [n_tokens] or NULL: s_t (0 for invalid / clipped / clamped tokens)
+ *   clipped_out device u8 [n_tokens] or NULL;  stats  device rl_loss_stats
+ *   workspace  device, >= rl_policy_loss_from_logp_workspace_size(n_tokens) bytes
+ * Errors: as rl_policy_loss_fwd_bwd; RL_ERR_UNSUPPORTED for RL_F_ENTROPY.  Deterministic. */
+size_t rl_policy_loss_from_logp_workspace_size(int64_t n_tokens);
+rl_status rl_policy_loss_from_logp(const float* logp, int64_t n_tokens, int64_t vocab, const int32_t* targets,
+                                   const float* old_logp, const uint8_t* loss_mask, const int32_t* token_seq,
+                                   const float* seq_adv, const int32_t* seq_version, const int32_t* seq_active,
+                                   const rl_loss_params* p, float* scale_out, uint8_t* clipped_out,
+                                   rl_loss_stats* stats, void* workspace, size_t workspace_bytes,
+                                   rl_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

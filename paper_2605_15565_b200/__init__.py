@@ -23,7 +23,8 @@ __all__ = [
     "policy_loss_fwd_bwd", "policy_loss_workspace_size", "policy_loss_fwd_bwd_host",
     "policy_loss_host_workspace_size", "vocab_parallel_logprob",
     "vocab_parallel_workspace_size", "m2po_mask", "m2po_workspace_size", "delta_encode", "delta_apply",
-    "delta_workspace_size", "Comm", "EXPORTED_SYMBOLS",
+    "delta_workspace_size", "lmhead_logprob", "lmhead_workspace_size", "policy_loss_from_logp",
+    "policy_loss_from_logp_workspace_size", "Comm", "EXPORTED_SYMBOLS",
 ]
 
 F32, BF16 = 0, 1
@@ -86,6 +87,8 @@ _SIGS = {
     "rl_bf16_delta_apply": (i32, [vp, i64, vp, vp, vp, i64, vp, vp]),
     "rl_lmhead_logprob": (i32, [vp, i64, vp, i64, i64, i64, i64, vp, f32, vp, vp, vp, sz, vp]),
     "rl_lmhead_workspace_size": (sz, [i64, i64, i64]),
+    "rl_policy_loss_from_logp_workspace_size": (sz, [i64]),
+    "rl_policy_loss_from_logp": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
@@ -447,4 +450,26 @@ def lmhead_logprob(hidden, weight, targets, logp_out, lse_out=None, inv_temperat
                                  _dev(workspace, "workspace") if workspace is not None else None,
                                  workspace.numel() * workspace.element_size() if workspace is not None else 0,
                                  _stream(stream)), "rl_lmhead_logprob")
+
+
+def policy_loss_from_logp_workspace_size(n_tokens):
+    return int(load().rl_policy_loss_from_logp_workspace_size(int(n_tokens)))
+
+
+def policy_loss_from_logp(logp, targets, old_logp, token_seq, seq_adv, params: LossParams, stats, workspace,
+                          vocab, loss_mask=None, seq_version=None, seq_active=None, scale_out=None,
+                          clipped_out=None, stream=None):
+    """c4–c7 from per-token log-probs (e.g. lmhead_logprob's): loss statistics into ``stats``
+    (CUDA float64, STATS_FIELDS order) and the gradient scale s_t into ``scale_out``."""
+    lib = load()
+    if stats.numel() < len(STATS_FIELDS):
+        raise RLError(f"stats needs {len(STATS_FIELDS)} float64 elements")
+    p = params._c()
+    _check(lib.rl_policy_loss_from_logp(
+        _dev(logp, "logp"), logp.numel(), int(vocab), _dev(targets, "targets"), _dev(old_logp, "old_logp"),
+        _dev(loss_mask, "loss_mask"), _dev(token_seq, "token_seq"), _dev(seq_adv, "seq_adv"),
+        _dev(seq_version, "seq_version"), _dev(seq_active, "seq_active"), C.byref(p),
+        _dev(scale_out, "scale_out"), _dev(clipped_out, "clipped_out"), _dev(stats, "stats"),
+        _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(), _stream(stream)),
+        "rl_policy_loss_from_logp")
 

@@ -793,3 +793,57 @@ def test_lmhead_logprob_temperature_and_errors(cuda_lib):
         lp2 = t.empty(big, dtype=t.float32, device="cuda")
         with pytest.raises(cuda_lib.RLError):
             cuda_lib.lmhead_logprob(hb2, w2, y2, lp2, workspace=t.empty(need - 1, dtype=t.uint8, device="cuda"))
+
+
+def test_lmhead_loss_forward(cuda_lib):
+    """NEXT 4 loss forward without logits: rl_lmhead_logprob -> rl_policy_loss_from_logp against the
+    oracle's c4-c7 on x = h W^T (oracle.lmhead_logits): loss (Z22), clip flags outside the Z23 band,
+    s_t (1e-3 relative), counters exact; a short sequence, masked tokens, one stale sequence and an
+    ignored target included."""
+    t = torch()
+    from tests.cases import clip_band
+    S, L, d, V = 12, 40, 192, 2500
+    N = S * L
+    hb, wb, ht, wt, y = _lm_inputs(N, d, V, seed=123)
+    y[1], y[2] = y[5], y[6]          # no out-of-range targets here (counted separately)
+    y[9] = -100
+    rng = np.random.default_rng(5)
+    token_seq = np.repeat(np.arange(S, dtype=np.int32), L)
+    mask = (rng.random(N) > 0.1).astype(np.uint8)
+    mask[:5] = 0
+    seq_version = np.full(S, 10, dtype=np.int32)
+    seq_version[3] = 1                # staleness 9 > 8: masked
+    adv = rng.choice([-1.3, -0.4, 0.5, 1.1], size=S).astype(np.float32)
+    x = oracle.lmhead_logits(hb, wb)
+    lp_ref, _ = oracle.token_logprob(x, y)
+    old = (lp_ref + rng.normal(0, 0.3, size=N)).astype(np.float32)
+    valid = ((mask != 0) & (y >= 0) & (token_seq != 3)).astype(np.uint8)
+    seq_active = np.bincount(token_seq, weights=valid, minlength=S).astype(np.int32)
+    op = oracle.LossParams(global_active_tokens=float(valid.sum()), trainer_version=10, max_staleness=8)
+    ref = oracle.policy_loss_fwd_bwd(x, y, old.astype(np.float64), mask, token_seq, adv.astype(np.float64),
+                                     seq_version, seq_active, op, want_dlogits=False)
+    # GPU: LM-head log-probs, then the loss from them
+    logp = t.empty(N, dtype=t.float32, device="cuda")
+    cuda_lib.lmhead_logprob(ht, wt, dev(y), logp, workspace=_lm_ws(N, d, V))
+    stats = t.zeros(12, dtype=t.float64, device="cuda")
+    scale = t.empty(N, dtype=t.float32, device="cuda")
+    clipped = t.empty(N, dtype=t.uint8, device="cuda")
+    ws = t.empty(cuda_lib.policy_loss_from_logp_workspace_size(N), dtype=t.uint8, device="cuda")
+    p = cuda_lib.LossParams(global_active_tokens=float(valid.sum()), trainer_version=10, max_staleness=8)
+    cuda_lib.policy_loss_from_logp(logp, dev(y), dev(old), dev(token_seq), dev(adv), p, stats, ws, V,
+                                   loss_mask=dev(mask), seq_version=dev(seq_version), scale_out=scale,
+                                   clipped_out=clipped)
+    t.cuda.synchronize()
+    st = stats.cpu().numpy()
+    names = cuda_lib.STATS_FIELDS
+    band = clip_band(ref["ratio"], ref["valid"], 0.2, 0.2)
+    bound = 1e-4 * max(abs(ref["loss"]), float(np.abs(ref["token_loss"]).sum()))
+    assert abs(st[names.index("loss_sum")] - ref["loss"]) <= bound + 1e-4 * float(np.abs(ref["token_loss"][band]).sum())
+    assert st[names.index("active_tokens")] == ref["stats"]["active_tokens"]
+    assert st[names.index("stale_masked")] == ref["stats"]["stale_masked"]
+    cl = clipped.cpu().numpy()
+    assert np.array_equal(cl[~band], ref["clipped"][~band])
+    sc = scale.cpu().numpy().astype(np.float64)
+    ok = ~band
+    assert np.all(np.abs(sc[ok] - ref["scale"][ok]) <= 1e-3 * np.abs(ref["scale"][ok]) + 1e-12)
+    assert np.all(sc[ref["valid"] == 0] == 0.0)
