@@ -452,6 +452,7 @@ struct VfArgs {
   int32_t count_stats, P, me;
   int32_t nb;  // vp_fused_kernel: shared-memory row buffers (2..4)
   int32_t pf;  // vp_fused2_kernel: L2 prefetch distance in row groups (0 = off)
+  int32_t trace;  // vp_fused2_kernel: record g_trace_vp2
   uint32_t epoch;
   float4* rec[8];     // rank q's record array  [P][max_tokens]
   uint32_t* flag[8];  // rank q's flag array    [P][max_tokens]
@@ -615,7 +616,12 @@ __global__ void __launch_bounds__(kVfThreads, 1) vp_fused_kernel(const VfArgs a)
 // every rank's buffer with ONE fence, waits for the peers' records of that group, combines them
 // in rank order, runs the loss epilogue and publishes the row scales — while the teams stream
 // the next group.
+// development phase trace (RL_TRACE): per CTA, team 0 thread 0's cycles in pass 1, waiting for
+// the row scales, and pass 2, plus the service lane's cycles waiting for the peers' records
+__device__ unsigned long long g_trace_vp2[256][4];
 constexpr int kV2Warps = 16;
+constexpr int kV2U1 = 10;  // pass-1 vectors in flight per thread
+constexpr int kV2U2 = 4;   // pass-2 (L2 re-read) vectors in flight per thread (10 spills: slower)
 constexpr int kV2Cons = kV2Warps * 32;
 
 template <typename T, int WPR>
@@ -664,6 +670,7 @@ __global__ void __launch_bounds__(kV2Cons + 32, 1) vp_fused2_kernel(const VfArgs
           *reinterpret_cast<volatile uint32_t*>(&a.flag[q][(int64_t)a.me * a.max_tokens + row_of(kk)]) = a.epoch;
       // the scale slot of group g-2 must be free: its pass 2 is done
       if (g >= 2) sm100::mbar_wait_polite(&done_bar[b], (uint32_t)(((g - 2) >> 1) & 1), false);
+      const long long tw0 = clock64();
       for (int64_t kk = k0; kk < k1; ++kk) {
         const int64_t row = row_of(kk);
         for (int q = 0; q < a.P; ++q) {
@@ -671,6 +678,7 @@ __global__ void __launch_bounds__(kV2Cons + 32, 1) vp_fused2_kernel(const VfArgs
           while (*f != a.epoch) __nanosleep(20);
         }
       }
+      if (a.trace && blockIdx.x < 256) g_trace_vp2[blockIdx.x][3] += (unsigned long long)(clock64() - tw0);
       __threadfence_system();
       for (int64_t kk = k0; kk < k1; ++kk) {
         const int64_t row = row_of(kk);
@@ -716,6 +724,8 @@ __global__ void __launch_bounds__(kV2Cons + 32, 1) vp_fused2_kernel(const VfArgs
       if (gg * G + team < nk)
         sm100::bulk_prefetch_l2(reinterpret_cast<const char*>(a.logits) + row_of(gg * G + team) * row_bytes, slice16);
   for (int64_t g = 0; g <= ng; ++g) {
+    const bool tr = a.trace && tid == 0 && blockIdx.x < 256;
+    long long tc = tr ? clock64() : 0;
     if (g < ng) {  // ---- pass 1 of group g: this team's row record
       const int b = (int)(g & 1);
       const int64_t kk = g * G + team;
@@ -725,7 +735,29 @@ __global__ void __launch_bounds__(kV2Cons + 32, 1) vp_fused2_kernel(const VfArgs
       const char* rp = nullptr;
       if (kk < nk) {
         rp = reinterpret_cast<const char*>(a.logits) + row_of(kk) * row_bytes;
-        st = row_stats_thread<T, NT, 8>(rp, a.Vr, k, keep, t);
+        // every load of a round in flight, predicated (no serial tail: a thread owns ~nvec / NT
+        // vectors, e.g. 18.5 at P = 4, which two rounds of kV2U1 cover)
+        const uint4* vrow = reinterpret_cast<const uint4*>(rp);
+        for (int64_t i0 = t; i0 < nvec; i0 += (int64_t)kV2U1 * NT) {
+          uint4 v[kV2U1];
+#pragma unroll
+          for (int u = 0; u < kV2U1; ++u)
+            v[u] = (i0 + u * NT < nvec) ? ld_hint_v4(vrow + i0 + u * NT, keep) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int u = 0; u < kV2U1; ++u) {
+            float f[EPV];
+            VecTraits<T>::unpack(v[u], f);
+            if (i0 + u * NT >= nvec) {
+#pragma unroll
+              for (int j = 0; j < EPV; ++j) f[j] = -INFINITY;
+            }
+            ms_update<EPV>(st, f, k);
+          }
+        }
+        for (int64_t c = nvec * EPV + t; c < a.Vr; c += NT) {
+          float f[1] = {VecTraits<T>::load1(rp, c)};
+          ms_update<1>(st, f, k);
+        }
       }
       st = warp_reduce_ms(st);
       if (WPR > 1) {
@@ -752,7 +784,17 @@ __global__ void __launch_bounds__(kV2Cons + 32, 1) vp_fused2_kernel(const VfArgs
       const int64_t gp = g - 1;
       const int b = (int)(gp & 1);
       const int64_t kk = gp * G + team;
+      if (tr) {
+        const long long t1 = clock64();
+        g_trace_vp2[blockIdx.x][0] += (unsigned long long)(t1 - tc);
+        tc = t1;
+      }
       sm100::mbar_wait(&scale_bar[b], (uint32_t)((gp >> 1) & 1));
+      if (tr) {
+        const long long t1 = clock64();
+        g_trace_vp2[blockIdx.x][1] += (unsigned long long)(t1 - tc);
+        tc = t1;
+      }
       if (kk < nk) {
         const int64_t row = row_of(kk);
         const float4 sc = grp_sc[b][team];
@@ -765,7 +807,7 @@ __global__ void __launch_bounds__(kV2Cons + 32, 1) vp_fused2_kernel(const VfArgs
         if (s == 0.f) {
           for (int64_t i = t; i < nvec; i += NT) st_stream_v4(vout + i, make_uint4(0, 0, 0, 0));
         } else {
-          constexpr int U = 4;
+          constexpr int U = kV2U2;
           for (int64_t i0 = t; i0 < nvec; i0 += U * NT) {
             uint4 v[U];
 #pragma unroll
@@ -793,6 +835,7 @@ __global__ void __launch_bounds__(kV2Cons + 32, 1) vp_fused2_kernel(const VfArgs
       }
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&done_bar[b]);
+      if (tr) g_trace_vp2[blockIdx.x][2] += (unsigned long long)(clock64() - tc);
     }
   }
 }
@@ -808,6 +851,9 @@ static void launch_vp_fused2(const VfArgs& v0, int64_t slice_bytes, int grid, cu
   if (pf < 0) pf = getenv("RL_VP2_PF") ? std::max(0, atoi(getenv("RL_VP2_PF"))) : 1;
   VfArgs v = v0;
   v.pf = pf;
+  static int trace = -1;
+  if (trace < 0) trace = getenv("RL_TRACE") ? 1 : 0;
+  v.trace = trace;
   const int64_t budget = getenv("RL_VP2_BUDGET_KB") ? (int64_t)atoi(getenv("RL_VP2_BUDGET_KB")) << 10
                                                      : (pf > 0 ? 200 << 10 : 300 << 10);
   if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16) slice_bytes = budget / (16 / forced);
@@ -1016,3 +1062,15 @@ extern "C" rl_status rl_vocab_parallel_logprob(
   if (st != RL_OK) return st;
   return launch_stats_reduce(partials, grid, stats, (p->flags & RL_F_STATS_ACCUMULATE) != 0, s);
 }
+
+// development only (not part of include/rl_policy.h): copy / clear the vp_fused2 phase trace
+extern "C" int rl_debug_trace_vp2(unsigned long long* host, size_t bytes, int clear) {
+  const size_t n = sizeof(rl::g_trace_vp2) < bytes ? sizeof(rl::g_trace_vp2) : bytes;
+  if (host && cudaMemcpyFromSymbol(host, rl::g_trace_vp2, n) != cudaSuccess) return 1;
+  if (clear) {
+    static unsigned long long zero[256 * 4] = {};
+    if (cudaMemcpyToSymbol(rl::g_trace_vp2, zero, sizeof(zero)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+

@@ -42,6 +42,11 @@ def main():
                                              token_seq=tseq, seq_adv=adv, params=p, dlogits_shard=dl, stats=stats)
     call()
     torch.cuda.synchronize()
+    tracing = os.environ.get("RL_TRACE") is not None and "--peer" in sys.argv
+    if tracing:
+        lib.rl_debug_trace_vp2.restype = ctypes.c_int
+        lib.rl_debug_trace_vp2.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+        assert lib.rl_debug_trace_vp2(None, 0, 1) == 0
     ts = []
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -50,6 +55,14 @@ def main():
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
+    if tracing:  # per-CTA cycles of team 0 / the service lane, averaged over CTAs and calls
+        buf = (ctypes.c_ulonglong * (256 * 4))()
+        assert lib.rl_debug_trace_vp2(ctypes.cast(buf, ctypes.c_void_p), ctypes.sizeof(buf), 0) == 0
+        import numpy as np
+        tr = np.frombuffer(buf, dtype=np.uint64).reshape(256, 4)[:148].astype(np.float64) / reps
+        mhz = torch.cuda.clock_rate() if hasattr(torch.cuda, "clock_rate") else 1965
+        for i, name in enumerate(["team0 pass 1", "team0 wait scale", "team0 pass 2", "service wait peers"]):
+            print(f"  {name:20s} {tr[:, i].mean() / (mhz * 1e3):8.3f} ms per call (cycles at {mhz} MHz)")
     nbytes = 2 * N * Vr * 2
     print(f"vocab-parallel shard P={P} ({Vr} cols) x {N} rows: min {min(ts):.3f} ms avg {sum(ts)/len(ts):.3f} ms"
           f"  {nbytes / min(ts) / 1e6:.1f} GB/s algorithmic (R+W)")
