@@ -191,6 +191,29 @@ def test_advantages_sum_to_zero_and_affine_invariance():
     assert np.allclose(adv, adv2, atol=1e-5)
 
 
+def test_advantages_permutation_equivariant_and_groups_independent():
+    # SURVEY §8(c) group advantage: A_i depends only on r_i and its own group's moments, so
+    # permuting members inside a group permutes A the same way, and changing another group's
+    # rewards leaves this group's A untouched (a wrong segment index fails one of the two).
+    rng = np.random.default_rng(11)
+    sizes = rng.integers(2, 12, size=20)
+    cu = np.concatenate([[0], np.cumsum(sizes)])
+    r = rng.normal(size=cu[-1])
+    adv, _ = oracle.group_advantage(r, cu, eps=1e-6)
+    perm = np.arange(cu[-1])
+    for g in range(len(sizes)):
+        perm[cu[g]:cu[g + 1]] = cu[g] + rng.permutation(sizes[g])
+    adv_p, _ = oracle.group_advantage(r[perm], cu, eps=1e-6)
+    # summation order inside a group changes, so equal up to rounding of the moments
+    assert np.allclose(np.asarray(adv_p), np.asarray(adv)[perm], rtol=0, atol=1e-6)
+    r2 = r.copy()
+    r2[cu[3]:cu[4]] = rng.normal(size=sizes[3]) * 10.0
+    adv2, _ = oracle.group_advantage(r2, cu, eps=1e-6)
+    keep = np.ones(cu[-1], bool)
+    keep[cu[3]:cu[4]] = False
+    assert np.array_equal(np.asarray(adv2)[keep], np.asarray(adv)[keep])
+
+
 def test_batch_norm_token_weighted_moments():
     rng = np.random.default_rng(4)
     cu = np.arange(0, 65, 8)
