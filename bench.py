@@ -36,6 +36,7 @@ WORKLOAD = "single-policy GRPO batch (BASELINE.json configs[1]): 32 prompts x 8 
 N_MINIBATCH = 4          # PAPER.md:574 "4 PPO mini-batches per iteration"
 SIDE_BYTES = 17          # target 4 + old_logp 4 + mask 1 + logp out 4 + token_seq 4
 OBJECTIVE = "clip"       # --objective
+KERNEL = "sv"            # --kernel
 
 
 def parse():
@@ -44,7 +45,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default=None, choices=[None, "sv", "cluster", "two_pass"])
+    ap.add_argument("--kernel", default="sv", choices=["sv", "two_pass"],
+                    help="rl_policy_loss_fwd_bwd kernel (two_pass: the development A/B option)")
+    ap.add_argument("--vp-path", default="peer", choices=["peer", "nccl"],
+                    help="vocabpar: in-kernel NVLink peer exchange (default) or the NCCL all-gather path")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
@@ -327,7 +331,7 @@ class TokenParallelWorkload:
                 e1.record(stream)
                 self.ev.append((e0, e1))
             # sv: loss_sv_kernel + two-pass fixup + stats reduce; cluster / two_pass: kernel + reduce
-            self.launches += 3 if os.environ.get("RL_LOSS_KERNEL", "sv") == "sv" else 2
+            self.launches += 3 if KERNEL == "sv" else 2
             if self.comm is not None:
                 self.comm.allreduce_f64(cl["stats"])
 
@@ -425,9 +429,9 @@ CONFIG_WORKLOADS = {
 
 
 def main():
-    global OBJECTIVE
+    global OBJECTIVE, KERNEL
     args = parse()
-    OBJECTIVE = args.objective
+    OBJECTIVE, KERNEL = args.objective, args.kernel
     # the image sets NCCL_DEBUG=VERSION, whose only output is a banner NCCL prints on stdout: keep
     # stdout to the single JSON line (an explicit WARN / INFO setting is left alone)
     if os.environ.get("NCCL_DEBUG") == "VERSION":
@@ -436,8 +440,6 @@ def main():
         return run_reference(args)
     if args.config == "lmhead":
         return run_lmhead(args)
-    if args.kernel:
-        os.environ["RL_LOSS_KERNEL"] = args.kernel
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -452,6 +454,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     rl.load()
+    if args.kernel == "two_pass":
+        rl.dev_set_option(rl.DEV_LOSS_KERNEL, 1)
+    if args.vp_path == "nccl":
+        rl.dev_set_option(rl.DEV_VP_PATH, 1)
     comm = None
     if world > 1 or args.config == "vocabpar":
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -459,16 +465,10 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
             comm = rl.Comm.from_torch()
         else:
-            import ctypes
-            buf = (ctypes.c_uint8 * 128)()
-            lib = rl.load()
-            assert lib.rl_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)) == 0
-            h = ctypes.c_void_p()
-            assert lib.rl_comm_init(ctypes.byref(h), bytes(buf), 1, 0) == 0
-            comm = rl.Comm(h.value, 1, 0)
+            comm = rl.Comm.local()
     MB = args.minibatch_tokens
     scaling = "weak"
-    kern = os.environ.get("RL_LOSS_KERNEL", "sv")
+    kern = args.kernel
     parallelism = f"dp{world} (token-parallel)"
     if args.config == "single":
         cfg = synth.get_config("single")
@@ -513,12 +513,12 @@ def main():
     elif args.config == "vocabpar":
         cfg = synth.get_config("vocabpar")
         wl = VocabParallelWorkload(rl, torch, np, synth, dev, comm, cfg, world, rank)
-        fused_vp = os.environ.get("RL_VP_PATH", "nccl") == "peer" and comm.enable_peer_exchange(cfg.n_tokens)
+        fused_vp = args.vp_path == "peer" and comm.enable_peer_exchange(cfg.n_tokens)
         scaling = "strong"
         parallelism = (f"vocab-parallel over {world} GPU: " + (
             "one fused kernel per rank, per-row (max, sum-exp, target logit) exchanged by NVLink peer stores"
             if fused_vp else "vp_stats + NCCL all-gather + vp_finish"))
-        kname = "rl_vocab_parallel_logprob (" + ("vp_fused2_kernel, in-kernel peer exchange" if fused_vp
+        kname = "rl_vocab_parallel_logprob (" + ("vp_ring_kernel, in-kernel peer exchange" if fused_vp
                                                  else "vp_stats + NCCL all-gather + vp_finish") + ")"
     else:
         raise SystemExit(f"unknown config {args.config}")

@@ -1,0 +1,29 @@
+/*
+ * rl_policy_dev.h — development hooks of librlpolicy.so (NOT part of the product ABI in
+ * rl_policy.h).  The tests and tools use them to A/B alternative kernels that are kept for
+ * parity coverage; the library never reads environment variables.
+ *
+ * rl_dev_set_option(key, value): sets a process-wide option and returns its previous value
+ * (-1 for an unknown key).  Keys:
+ *   0 RL_DEV_LOSS_KERNEL  rl_policy_loss_fwd_bwd kernel: 0 = single-visit cluster kernel
+ *                         (default), 1 = exact max-referenced two-pass kernel for every row
+ *   1 RL_DEV_VP_PATH      fused rl_vocab_parallel_logprob: 0 = in-kernel peer exchange when
+ *                         rl_comm_enable_peer_exchange succeeded (default), 1 = NCCL path
+ *   2 RL_DEV_LM_SPLITS    rl_lmhead_logprob vocabulary splits: 0 = cost model (default), else
+ *                         the split count (clamped to what the workspace holds)
+ * Options are read at launch time; set them before the calls they should affect.
+ */
+#ifndef RL_POLICY_DEV_H_
+#define RL_POLICY_DEV_H_
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+#define RL_DEV_LOSS_KERNEL 0
+#define RL_DEV_VP_PATH 1
+#define RL_DEV_LM_SPLITS 2
+int32_t rl_dev_set_option(int32_t key, int32_t value);
+#ifdef __cplusplus
+}
+#endif
+#endif

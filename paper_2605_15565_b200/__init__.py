@@ -116,8 +116,22 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    lib.rl_dev_set_option.restype = i32  # development hook (include/rl_policy_dev.h)
+    lib.rl_dev_set_option.argtypes = [i32, i32]
     _LIB = lib
     return lib
+
+
+# development options (include/rl_policy_dev.h): alternative kernels kept for A/B parity tests
+DEV_LOSS_KERNEL, DEV_VP_PATH, DEV_LM_SPLITS = 0, 1, 2
+
+
+def dev_set_option(key: int, value: int) -> int:
+    """Set a development option of the library; returns the previous value."""
+    old = load().rl_dev_set_option(key, value)
+    if old < 0:
+        raise RLError(f"unknown development option {key}")
+    return old
 
 
 def _check(status: int, what: str):
@@ -328,6 +342,17 @@ class Comm:
         h = vp()
         _check(lib.rl_comm_init(C.byref(h), raw, n, rank), "rl_comm_init")
         return cls(h.value, n, rank)
+
+    @classmethod
+    def local(cls):
+        """A single-rank communicator (P = 1: the vocab-parallel path on one GPU, the all-reduce
+        a no-op sum) without a torch process group."""
+        lib = load()
+        buf = (C.c_uint8 * 128)()
+        _check(lib.rl_comm_unique_id(C.cast(buf, vp)), "rl_comm_unique_id")
+        h = vp()
+        _check(lib.rl_comm_init(C.byref(h), bytes(buf), 1, 0), "rl_comm_init")
+        return cls(h.value, 1, 0)
 
     def split(self, color: int, key: int):
         lib = load()

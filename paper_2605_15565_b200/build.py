@@ -14,6 +14,7 @@ import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -67,19 +68,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     common = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
               "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-Xptxas", "-v",
               "--expt-relaxed-constexpr"]
-    objs, logs = [], []
-    for src in sources():
+    def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
         extra = ["-fmad=false"] if os.path.basename(src) == "advantage.cu" else []
         cmd = common + extra + ["-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
-        p = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(f"== {os.path.basename(src)}\n{p.stderr}")
-        if p.returncode != 0:
-            sys.stderr.write(p.stdout + p.stderr)
-            raise RuntimeError(f"nvcc failed on {src}")
-        objs.append(obj)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs, logs = [], []
+    # one nvcc per translation unit, in parallel (the tcgen05 / cluster units dominate)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+        for src, obj, p in ex.map(compile_one, sources()):
+            logs.append(f"== {os.path.basename(src)}\n{p.stderr}")
+            if p.returncode != 0:
+                sys.stderr.write(p.stdout + p.stderr)
+                raise RuntimeError(f"nvcc failed on {src}")
+            objs.append(obj)
     with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     tmp = LIB + ".tmp"

@@ -1,6 +1,8 @@
 // C-ABI plumbing: status strings, thread-local error detail, parameter defaults.
 #include <cstdarg>
 #include <cstdio>
+#include <atomic>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -29,7 +31,48 @@ rl_status check_launch(const char* what) {
   return RL_OK;
 }
 
+static DevInfo g_dev[kMaxDevices];
+static std::atomic<int> g_dev_ready[kMaxDevices];
+
+const DevInfo& dev_info() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  if (g_dev_ready[dev].load(std::memory_order_acquire) != 1) {
+    DevInfo d{dev, 148, 0, 0};
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (g_dev_ready[dev].load(std::memory_order_relaxed) != 1) {
+      g_dev[dev] = d;
+      g_dev_ready[dev].store(1, std::memory_order_release);
+    }
+  }
+  return g_dev[dev];
+}
+
+rl_status require_sm100() {
+  const DevInfo& d = dev_info();
+  if (d.cc_major != 10 || d.cc_minor != 0)
+    return fail(RL_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a (B200) only",
+                d.ordinal, d.cc_major, d.cc_minor);
+  return RL_OK;
+}
+
+int& dev_slot(int* table) { return table[dev_info().ordinal]; }
+
+static std::atomic<int> g_opt[OPT_COUNT];
+int dev_option(int key) { return (key >= 0 && key < OPT_COUNT) ? g_opt[key].load(std::memory_order_relaxed) : 0; }
+
 }  // namespace rl
+
+extern "C" int32_t rl_dev_set_option(int32_t key, int32_t value) {
+  if (key < 0 || key >= rl::OPT_COUNT) return -1;
+  const int old = rl::g_opt[key].exchange(value);
+  return old;
+}
 
 extern "C" const char* rl_status_string(rl_status s) {
   switch (s) {

@@ -26,7 +26,9 @@ static rl_status nccl_fail(ncclResult_t r, const char* what) {
 ncclComm_t comm_nccl(rl_comm* c) { return c->nccl; }
 int32_t comm_rank(const rl_comm* c) { return c->rank; }
 int32_t comm_size(const rl_comm* c) { return c->nranks; }
-// peer exchange layout (per rank buffer): records float4[P][max_tokens], flags uint32[P][max_tokens]
+// peer exchange layout (per rank buffer): two parity halves (the call epoch's low bit), each
+// [P source ranks][max_tokens] records of two 8-byte words {epoch << 32 | float bits}
+// (vp_ring_kernel, vocab_parallel.cu)
 bool comm_peer_exchange(rl_comm* c, int64_t n_tokens, void** peers, int64_t* max_tokens, uint32_t* epoch) {
   if (!c->xbuf || n_tokens > c->max_tokens) return false;
   for (int r = 0; r < c->nranks; ++r) peers[r] = c->peers[r];
@@ -73,7 +75,7 @@ extern "C" rl_status rl_comm_enable_peer_exchange(rl_comm* c, int64_t max_tokens
   if (!c || max_tokens < 1) return fail(RL_ERR_INVALID_ARGUMENT, "NULL comm or max_tokens < 1");
   if (c->nranks > 8) return fail(RL_ERR_UNSUPPORTED, "peer exchange supports <= 8 ranks");
   release_peer_exchange(c);
-  const size_t bytes = (size_t)c->nranks * max_tokens * (16 + 4);
+  const size_t bytes = 2 * (size_t)c->nranks * max_tokens * 16;
   if (cudaMalloc(&c->xbuf, bytes) != cudaSuccess) return check_launch("cudaMalloc(peer exchange)");
   if (cudaMemset(c->xbuf, 0, bytes) != cudaSuccess) return check_launch("cudaMemset(peer exchange)");
   cudaIpcMemHandle_t mine;
@@ -110,6 +112,24 @@ extern "C" rl_status rl_comm_enable_peer_exchange(rl_comm* c, int64_t max_tokens
     c->peers[q] = p;
   }
   delete[] all;
+  // every rank must take the same path: enable only if every rank mapped every peer (a min
+  // reduction of the per-rank success flag), else release on all ranks
+  int32_t* okd = nullptr;
+  int32_t ok = st == RL_OK ? 1 : 0;
+  if (cudaMalloc(&okd, sizeof(int32_t)) != cudaSuccess) {
+    release_peer_exchange(c);
+    return check_launch("cudaMalloc(peer exchange flag)");
+  }
+  cudaMemcpy(okd, &ok, sizeof(int32_t), cudaMemcpyHostToDevice);
+  r = ncclAllReduce(okd, okd, 1, ncclInt32, ncclMin, c->nccl, 0);
+  cudaDeviceSynchronize();
+  cudaMemcpy(&ok, okd, sizeof(int32_t), cudaMemcpyDeviceToHost);
+  cudaFree(okd);
+  if (r != ncclSuccess) {
+    release_peer_exchange(c);
+    return nccl_fail(r, "ncclAllReduce(peer exchange agreement)");
+  }
+  if (st == RL_OK && !ok) st = fail(RL_ERR_UNSUPPORTED, "another rank could not map its peers");
   if (st != RL_OK) {
     release_peer_exchange(c);
     return st;

@@ -16,6 +16,31 @@ void set_error(const char* fmt, ...);
 rl_status fail(rl_status s, const char* fmt, ...);
 rl_status check_launch(const char* what);
 
+// ---------------------------------------------------------------- per-device host state
+// Everything the launchers derive from the device (SM count, compute capability) is cached per
+// device ordinal, so one process may drive several GPUs; entry points first call
+// require_sm100() (RL_ERR_UNSUPPORTED on anything but a compute-capability 10.0 device).
+constexpr int kMaxDevices = 64;
+struct DevInfo {
+  int ordinal;
+  int sms;
+  int cc_major, cc_minor;
+};
+const DevInfo& dev_info();  // current device
+rl_status require_sm100();
+// per-device cache slot for a launcher-derived integer (0 = not computed yet)
+int& dev_slot(int* table);
+
+// Development options (include/rl_policy_dev.h): alternative kernels kept for A/B tests.
+// Set explicitly through rl_dev_set_option; the library never reads the environment.
+enum DevOpt {
+  OPT_LOSS_KERNEL = 0,  // 0 = single-visit cluster kernel (default), 1 = exact two-pass kernel
+  OPT_VP_PATH = 1,      // fused vocab-parallel loss: 0 = in-kernel peer exchange when enabled, 1 = NCCL path
+  OPT_LM_SPLITS = 2,    // LM-head vocabulary split override (0 = cost model)
+  OPT_COUNT = 3
+};
+int dev_option(int key);
+
 // ---------------------------------------------------------------- element access
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }

@@ -3,12 +3,8 @@
 // sparsity 0.989-0.993; SPEC.md:297-313 compute_delta / apply_delta).
 //
 // encode: the indices (increasing) and new words of every position where two 16-bit snapshots
-// differ — a single-pass stream compaction: each snapshot is read once (16-B loads), the ~1 % of
-// changes written once, HBM-bound on the two reads.  Persistent CTAs take 16384-word tiles in
-// index order (static assignment, several CTAs per SM); a tile's output offset comes from a
-// decoupled look-back (one warp, 32 predecessors per step) over the
-// per-tile status words (flag + count in one 64-bit word), so no tile waits for a full
-// grid-wide scan and the output stays sorted by index.
+// differ — a stream compaction that reads each snapshot once (16-B loads) and writes the ~1 % of
+// changes once, HBM-bound on the two reads (two-stage design below).
 // apply: base[idx[j]] = word[j] (scatter).
 #include <algorithm>
 #include <cstdint>
@@ -24,16 +20,6 @@ namespace rl {
 constexpr int kDtThreads = 256;
 constexpr int kDtVec = 8;                                     // 16-B vectors per thread per array
 constexpr int kDtTile = kDtThreads * kDtVec * 8;              // 16384 words per tile
-constexpr uint64_t kStAgg = 1ull << 62, kStPre = 2ull << 62, kStMask = (1ull << 62) - 1;
-
-__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 
 // bit e of the result: word e of the 8-word vectors a, b differ
 __device__ __forceinline__ uint32_t diff8(const uint4& a, const uint4& b) {
@@ -44,151 +30,8 @@ __device__ __forceinline__ uint32_t diff8(const uint4& a, const uint4& b) {
   return m;
 }
 
-__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int o) {
-  return ((uint64_t)__shfl_up_sync(0xffffffffu, (uint32_t)(v >> 32), o) << 32) |
-         __shfl_up_sync(0xffffffffu, (uint32_t)v, o);
-}
-
-// bits of the words that differ in this thread's 8 vector slots of the tile at wt; the full-tile
-// path loads and compares in two halves of 4 vector pairs (32 registers of loads in flight)
-__device__ __forceinline__ uint64_t dt_masks(const uint16_t* __restrict__ prev, const uint16_t* __restrict__ next,
-                                             int64_t wt, int64_t n) {
-  uint64_t masks = 0;
-  if (wt + kDtTile <= n) {
-    const uint4* pa = reinterpret_cast<const uint4*>(prev + wt) + threadIdx.x;
-    const uint4* pb = reinterpret_cast<const uint4*>(next + wt) + threadIdx.x;
-#pragma unroll
-    for (int h = 0; h < kDtVec; h += 4) {
-      uint4 va[4], vb[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        va[u] = ld_stream_v4(pa + (h + u) * kDtThreads);
-        vb[u] = ld_stream_v4(pb + (h + u) * kDtThreads);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) masks |= (uint64_t)diff8(va[u], vb[u]) << (8 * (h + u));
-    }
-  } else {  // the ragged last tile: guarded scalar reads
-#pragma unroll
-    for (int u = 0; u < kDtVec; ++u)
-      for (int e = 0; e < 8; ++e) {
-        const int64_t w = wt + 8 * ((int64_t)u * kDtThreads + threadIdx.x) + e;
-        if (w < n && prev[w] != next[w]) masks |= 1ull << (8 * u + e);
-      }
-  }
-  return masks;
-}
-
-// Tile layout (coalesced): thread t compares vectors u * 256 + t, u < 8, of both snapshots; the
-// tile's changes are written in index order = (u, t, word) order.  The 8 per-vector counts
-// (<= 8 each, <= 2048 per tile and vector slot) are packed in 16-bit fields of two u64 and
-// scanned once over the block.  Tiles are assigned statically (blockIdx.x + k * gridDim.x; the
-// grid is all-resident, so a look-back only waits on running CTAs); several CTAs per SM overlap
-// one tile's loads with another's scan, look-back and writes.
-__global__ void __launch_bounds__(kDtThreads, 4) delta_encode_kernel(
-    const uint16_t* __restrict__ prev, const uint16_t* __restrict__ next, int64_t n, int64_t n_tiles,
-    uint32_t* __restrict__ idx_out, uint16_t* __restrict__ word_out, int64_t capacity,
-    unsigned long long* __restrict__ count_out, uint64_t* __restrict__ status) {
-  // double-buffered by iteration parity: no barrier after a tile's scatter, so the slowest
-  // thread's writes overlap the next tile's loads
-  __shared__ uint64_t warp_tot[2][2][kDtThreads / 32];
-  __shared__ int64_t s_prefix[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int par = 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, par ^= 1) {
-    const int64_t wt = tile * kDtTile;
-    const uint64_t masks = dt_masks(prev, next, wt, n);
-    uint64_t c0 = 0, c1 = 0;  // packed per-slot counts: slots 0..3 in c0, 4..7 in c1
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      c0 |= (uint64_t)__popc((uint32_t)(masks >> (8 * u)) & 0xFFu) << (16 * u);
-      c1 |= (uint64_t)__popc((uint32_t)(masks >> (8 * (u + 4))) & 0xFFu) << (16 * u);
-    }
-    // ---- block exclusive scan of the packed counts
-    uint64_t i0 = c0, i1 = c1;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t v0 = shfl_up_u64(i0, o), v1 = shfl_up_u64(i1, o);
-      if (lane >= o) {
-        i0 += v0;
-        i1 += v1;
-      }
-    }
-    if (lane == 31) {
-      warp_tot[par][0][warp] = i0;
-      warp_tot[par][1][warp] = i1;
-    }
-    __syncthreads();
-    uint64_t b0 = 0, b1 = 0, t0 = 0, t1 = 0;
-#pragma unroll
-    for (int w = 0; w < kDtThreads / 32; ++w) {
-      const uint64_t x0 = warp_tot[par][0][w], x1 = warp_tot[par][1][w];
-      b0 += w < warp ? x0 : 0;
-      b1 += w < warp ? x1 : 0;
-      t0 += x0;
-      t1 += x1;
-    }
-    const uint64_t e0 = b0 + i0 - c0, e1 = b1 + i1 - c1;  // exclusive, per slot
-    uint32_t slot_base[kDtVec], total = 0;                  // slot offsets within the tile
-#pragma unroll
-    for (int u = 0; u < kDtVec; ++u) {
-      slot_base[u] = total;
-      total += (uint32_t)(((u < 4 ? t0 : t1) >> (16 * (u & 3))) & 0xFFFFu);
-    }
-    // ---- decoupled look-back (warp 0, 32 predecessors per step): this tile's output offset
-    if (warp == 0) {
-      int64_t prefix = 0;
-      if (tile == 0) {
-        if (lane == 0) st_release_u64(status + tile, kStPre | (uint64_t)total);
-      } else {
-        if (lane == 0) st_release_u64(status + tile, kStAgg | (uint64_t)total);
-        for (int64_t j = tile - 1;;) {  // window: tiles j - lane
-          const int64_t jj = j - lane;
-          const uint64_t v = jj >= 0 ? ld_acquire_u64(status + jj) : kStPre;  // before tile 0: prefix 0
-          const uint64_t fl = v & ~kStMask;
-          const uint32_t pre = __ballot_sync(0xffffffffu, fl == kStPre);
-          const uint32_t wait = __ballot_sync(0xffffffffu, fl == 0);
-          const int first = pre ? __ffs(pre) - 1 : 32;            // nearest inclusive prefix
-          const uint32_t need = first == 32 ? 0xffffffffu : (0xffffffffu >> (31 - first));
-          if (wait & need) continue;                               // a predecessor still counting
-          uint64_t x = lane <= first ? (v & kStMask) : 0;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-          prefix += (int64_t)x;
-          if (first < 32) break;
-          j -= 32;
-        }
-        if (lane == 0) st_release_u64(status + tile, kStPre | (uint64_t)(prefix + total));
-      }
-      if (lane == 0) {
-        if (tile == n_tiles - 1) *count_out = (unsigned long long)(prefix + total);
-        s_prefix[par] = prefix;
-      }
-    }
-    __syncthreads();
-    const int64_t prefix = s_prefix[par];
-#pragma unroll
-    for (int u = 0; u < kDtVec; ++u) {
-      uint32_t m = (uint32_t)(masks >> (8 * u)) & 0xFFu;
-      int64_t off = prefix + slot_base[u] + (int64_t)(((u < 4 ? e0 : e1) >> (16 * (u & 3))) & 0xFFFFu);
-      const int64_t w0 = wt + 8 * ((int64_t)u * kDtThreads + tid);
-      while (m) {  // ~1 % of the words: the new word is re-read (L2 hit)
-        const int e = __ffs(m) - 1;
-        m &= m - 1;
-        if (off < capacity) {
-          idx_out[off] = (uint32_t)(w0 + e);
-          word_out[off] = next[w0 + e];
-        }
-        ++off;
-      }
-    }
-    // no trailing barrier: the next tile uses the other warp_tot / s_prefix buffers, and its two
-    // barriers order every use of this tile's buffers before their reuse two tiles later
-  }
-}
-
 // ---------------------------------------------------------------------------------------------
-// Two-stage encode (default): (1) a pure streaming pass compares the snapshots tile by tile
+// Two-stage encode: (1) a pure streaming pass compares the snapshots tile by tile
 // (16,384 words, 16-B loads, no cross-CTA dependency), ranks the tile's changes in word order with
 // a block scan and writes them compacted into the tile's own staging slot (capacity kStageCap
 // changes: new word + 16-bit index within the tile) plus the tile's change count; a tile with more
@@ -376,7 +219,7 @@ static int64_t dt_tiles(int64_t n) { return (n + kDtTile - 1) / kDtTile; }
 }  // namespace rl
 
 namespace rl {
-// workspace: [tile status / two-stage tile counts: tiles+2 u64][tile offsets: tiles u64]
+// workspace: [tile counts: tiles+2 u64][tile offsets: tiles u64]
 //            [change bitmask: tiles * 2 KB][staged changes: tiles * kStageCap u32][CUB scan temp]
 struct DtLayout {
   size_t status, offs, bits, stage, temp, temp_bytes, total;
@@ -429,24 +272,9 @@ extern "C" rl_status rl_bf16_delta_encode(const void* prev, const void* next, in
     if (cudaMemsetAsync(count_out, 0, 8, s) != cudaSuccess) return check_launch("delta memset");
     return RL_OK;
   }
-  static int algo = -1;  // RL_DELTA_ALGO=onepass: the single-pass look-back kernel
-  if (algo < 0) algo = (getenv("RL_DELTA_ALGO") && strcmp(getenv("RL_DELTA_ALGO"), "onepass") == 0) ? 1 : 0;
-  static int sms = 0, ctas = 0;
-  if (!sms) {
-    int dev = 0, occ = 4;
-    sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, delta_encode_kernel, kDtThreads, 0);
-    ctas = sms * std::max(occ, 1);  // all resident: a look-back only ever waits on a running tile
-  }
-  if (algo == 1) {
-    if (cudaMemsetAsync(status, 0, (size_t)(tiles + 2) * 8, s) != cudaSuccess) return check_launch("delta memset");
-    const int grid = (int)std::min<int64_t>(tiles, ctas);
-    delta_encode_kernel<<<grid, kDtThreads, 0, s>>>((const uint16_t*)prev, (const uint16_t*)next, n_words, tiles,
-                                                    idx_out, word_out, capacity, count_out, status);
-    return check_launch("delta_encode_kernel");
-  }
+  static int sms_tab[kMaxDevices] = {};
+  int& sms = dev_slot(sms_tab);
+  if (!sms) sms = dev_info().sms;
   uint64_t* counts = status;
   uint64_t* offs = (uint64_t*)(w + L.offs);
   uint32_t* bits = (uint32_t*)(w + L.bits);

@@ -267,15 +267,7 @@ static int lm_splits(int64_t n, int64_t d, int64_t vocab, int sms) {
   }
   return best;
 }
-static int lm_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
-  }
-  return sms;
-}
+static int lm_sms() { return dev_info().sms; }
 
 typedef CUresult (*PfnTensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -341,8 +333,7 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
   a.kblocks = (int32_t)((d + kLmBK - 1) / kLmBK);
   a.vtiles = (int32_t)((vocab + kLmBN - 1) / kLmBN);
   int splits = lm_splits(n_tokens, d, vocab, lm_sms());
-  static int forced = -1;  // RL_LM_SPLITS (development): force the split count (<= the workspace's)
-  if (forced < 0) forced = getenv("RL_LM_SPLITS") ? atoi(getenv("RL_LM_SPLITS")) : 0;
+  const int forced = dev_option(OPT_LM_SPLITS);  // development: force the split count (<= the workspace's)
   if (forced > 0 && forced <= splits) splits = forced;
   a.tiles_per_split = (a.vtiles + splits - 1) / splits;
   splits = (a.vtiles + a.tiles_per_split - 1) / a.tiles_per_split;
@@ -353,13 +344,9 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
   a.inv_t = inv_temperature;
   a.logp_out = logp_out;
   a.lse_out = lse_out;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(lmhead_logprob_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) !=
-        cudaSuccess)
-      return check_launch("cudaFuncSetAttribute(lmhead)");
-    attr = true;
-  }
+  if (cudaFuncSetAttribute(lmhead_logprob_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) !=
+      cudaSuccess)
+    return check_launch("cudaFuncSetAttribute(lmhead)");
   if ((n_tokens + kLmBM - 1) / kLmBM > 65535) return fail(RL_ERR_UNSUPPORTED, "n_tokens > 65535 * 128 per call");
   const dim3 grid((unsigned)splits, (unsigned)((n_tokens + kLmBM - 1) / kLmBM));
   lmhead_logprob_kernel<<<grid, kLmThreads, kLmSmem, (cudaStream_t)stream>>>(mh, mw, a);

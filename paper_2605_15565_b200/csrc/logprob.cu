@@ -11,37 +11,6 @@
 
 namespace rl {
 
-constexpr int kLpThreads = 256;
-constexpr int kLpUnroll = 4;
-
-template <typename T>
-__global__ void __launch_bounds__(kLpThreads) token_logprob_kernel(
-    const void* __restrict__ logits, int64_t n_tokens, int64_t V, int64_t ld,
-    const int32_t* __restrict__ targets, float inv_t, float* __restrict__ logp_out,
-    float* __restrict__ lse_out, double* __restrict__ bad_count) {
-  __shared__ float red[64];
-  const float k = inv_t * RL_LOG2E;
-  const uint64_t pol = policy_evict_first();
-  const int64_t row_bytes = ld * elem_bytes<T>();
-  unsigned bad = 0;
-  for (int64_t row = blockIdx.x; row < n_tokens; row += gridDim.x) {
-    const char* rp = reinterpret_cast<const char*>(logits) + row * row_bytes;
-    const int32_t y = targets[row];
-    MS st = row_stats_thread<T, kLpThreads, kLpUnroll>(rp, V, k, pol);
-    st = block_reduce_ms<kLpThreads>(st, red);
-    if (threadIdx.x == 0) {
-      const float c2 = st.m + fast_log2(st.s);  // log2-domain log-sum-exp
-      float lp;
-      if (y >= 0 && (int64_t)y < V) lp = VecTraits<T>::load1(rp, y) * inv_t - c2 * RL_LN2;
-      else if (y < 0) lp = 0.f;
-      else { lp = __int_as_float(0x7fc00000); ++bad; }
-      logp_out[row] = lp;
-      if (lse_out) lse_out[row] = c2 * RL_LN2;
-    }
-  }
-  if (threadIdx.x == 0 && bad && bad_count) atomicAdd(bad_count, (double)bad);
-}
-
 // Warp-per-row kernel (default): each warp streams whole rows (U 16-B loads in flight per lane,
 // no block barriers) and sums e_v = 2^(x_v k - R) with the TARGET logit as reference, R = x_y k
 // (as the fused SV loss kernel, reading R1): one MUFU.EX2 per element, no max.  Since
@@ -119,18 +88,6 @@ __global__ void __launch_bounds__(kLwThreads) logprob_warp_kernel(
   if (lane == 0 && bad && bad_count) atomicAdd(bad_count, (double)bad);
 }
 
-int logprob_grid(int64_t n_tokens) {
-  static int max_ctas = 0;
-  if (!max_ctas) {
-    int dev = 0, sms = 148, occ = 4;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, token_logprob_kernel<bf16_t>, kLpThreads, 0);
-    max_ctas = sms * std::max(occ, 1);
-  }
-  return (int)std::min<int64_t>(n_tokens, max_ctas);
-}
-
 }  // namespace rl
 
 extern "C" rl_status rl_token_logprob(const void* logits, int32_t dtype, int64_t n_tokens,
@@ -148,17 +105,13 @@ extern "C" rl_status rl_token_logprob(const void* logits, int32_t dtype, int64_t
   if (((uintptr_t)logits & 15) || (ld * eb) % 16)
     return fail(RL_ERR_ALIGNMENT, "logits must be 16-B aligned with ld*elem %% 16 == 0");
   cudaStream_t s = (cudaStream_t)stream;
-  static int block_kernel = -1;  // RL_LOGPROB_KERNEL=block: the CTA-per-row online-max kernel
-  if (block_kernel < 0)
-    block_kernel = (getenv("RL_LOGPROB_KERNEL") && strcmp(getenv("RL_LOGPROB_KERNEL"), "block") == 0) ? 1 : 0;
-  if (!block_kernel) {
-    static int ctas = 0;
+  {
+    static int ctas_tab[kMaxDevices] = {};
+    int& ctas = dev_slot(ctas_tab);
     if (!ctas) {
-      int dev = 0, sms = 148, occ = 8;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      int occ = 8;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, logprob_warp_kernel<bf16_t, 4>, kLwThreads, 0);
-      ctas = sms * std::max(occ, 1);
+      ctas = dev_info().sms * std::max(occ, 1);
     }
     const int grid = (int)std::min<int64_t>((n_tokens + kLwThreads / 32 - 1) / (kLwThreads / 32), ctas);
     if (dtype == RL_BF16)
@@ -171,14 +124,4 @@ extern "C" rl_status rl_token_logprob(const void* logits, int32_t dtype, int64_t
                                                                bad_target_count);
     return check_launch("logprob_warp_kernel");
   }
-  const int grid = logprob_grid(n_tokens);
-  if (dtype == RL_BF16)
-    token_logprob_kernel<bf16_t><<<grid, kLpThreads, 0, s>>>(logits, n_tokens, vocab, ld, targets,
-                                                             inv_temperature, logp_out, lse_out,
-                                                             bad_target_count);
-  else
-    token_logprob_kernel<float><<<grid, kLpThreads, 0, s>>>(logits, n_tokens, vocab, ld, targets,
-                                                            inv_temperature, logp_out, lse_out,
-                                                            bad_target_count);
-  return check_launch("token_logprob_kernel");
 }

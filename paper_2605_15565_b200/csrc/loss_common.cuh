@@ -115,15 +115,20 @@ __device__ __forceinline__ TokRatio token_ratio_basic(float logp, float old, flo
 __device__ __forceinline__ float token_scale_basic(const TokRatio& t, float wf, float A, const Knobs& kn) {
   return (t.cl != 0 || t.clamp) ? 0.f : wf * A * t.r * kn.inv_t * kn.grad_scale;
 }
-// w = 1/N | 1/(S L_i) | 1 (c6)
+// w = 1/N | 1/(S L_i) | 1 (c6); Li = the token's sequence's active-token count
+__device__ __forceinline__ double token_weight_li(int32_t Li, double inv_tm, const Knobs& kn) {
+  if (kn.agg == RL_AGG_TOKEN_MEAN) return inv_tm;
+  if (kn.agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN)
+    return (Li > 0 && kn.global_num_seqs > 0) ? 1.0 / ((double)kn.global_num_seqs * (double)Li) : 0.0;
+  return 1.0;
+}
+// L_i of a valid token, read only when the aggregation uses it
+__device__ __forceinline__ int32_t token_li(const RowMeta& mt, const int32_t* seq_active, const Knobs& kn) {
+  return (kn.agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN && seq_active) ? seq_active[mt.seq] : 0;
+}
 __device__ __forceinline__ double token_weight(const RowMeta& mt, const int32_t* seq_active, double inv_tm,
                                                const Knobs& kn) {
-  if (kn.agg == RL_AGG_TOKEN_MEAN) return inv_tm;
-  if (kn.agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN) {
-    const int32_t Li = seq_active ? seq_active[mt.seq] : 0;
-    return (Li > 0 && kn.global_num_seqs > 0) ? 1.0 / ((double)kn.global_num_seqs * (double)Li) : 0.0;
-  }
-  return 1.0;
+  return token_weight_li(token_li(mt, seq_active, kn), inv_tm, kn);
 }
 // the token's (prox, ref) inputs, loaded only when the knobs use them
 __device__ __forceinline__ void token_extra(const Knobs& kn, int64_t row, float old, float& prox, float& ref) {
@@ -134,10 +139,10 @@ __device__ __forceinline__ void token_extra(const Knobs& kn, int64_t row, float 
 // Per-token epilogue.  Returns the gradient scale s_t (0 for invalid tokens; clipped / clamped
 // tokens keep only the KL part) and adds the token's contribution to `acc`.
 //   L = -rho min(r A, clip(r, lo, hi) A) + beta KL
-__device__ __forceinline__ float token_epilogue(const RowMeta& mt, float logp, float old, float A,
-                                                const int32_t* seq_active, double inv_tm,
-                                                const Knobs& kn, Acc& acc, uint8_t* clipped_out,
-                                                float prox = 0.f, float ref = 0.f) {
+//   (token_epilogue_li: the same with the sequence's L_i already loaded)
+__device__ __forceinline__ float token_epilogue_li(const RowMeta& mt, float logp, float old, float A, int32_t Li,
+                                                   double inv_tm, const Knobs& kn, Acc& acc, uint8_t* clipped_out,
+                                                   float prox, float ref) {
   acc.v[ST_BAD] += mt.bad ? 1.0 : 0.0;
   acc.v[ST_NEG] += mt.neg_stale ? 1.0 : 0.0;
   acc.v[ST_STALE] += mt.stale_drop ? 1.0 : 0.0;
@@ -149,7 +154,7 @@ __device__ __forceinline__ float token_epilogue(const RowMeta& mt, float logp, f
   const float u = t.r * A;
   const float kk = fminf(fmaxf(t.r, kn.lo_b), kn.hi_b) * A;
   const float L = -t.rho * fminf(u, kk) + kn.kl_coef * t.kl;
-  const double w = token_weight(mt, seq_active, inv_tm, kn);
+  const double w = token_weight_li(Li, inv_tm, kn);
   acc.v[ST_LOSS] += w * (double)L;
   acc.v[ST_ACTIVE] += 1.0;
   acc.v[ST_WSUM] += w;
@@ -160,6 +165,13 @@ __device__ __forceinline__ float token_epilogue(const RowMeta& mt, float logp, f
   acc.v[ST_KL] += w * (double)t.kl;
   if (clipped_out) *clipped_out = t.cl;
   return token_scale(t, (float)w, A, kn);
+}
+__device__ __forceinline__ float token_epilogue(const RowMeta& mt, float logp, float old, float A,
+                                                const int32_t* seq_active, double inv_tm,
+                                                const Knobs& kn, Acc& acc, uint8_t* clipped_out,
+                                                float prox = 0.f, float ref = 0.f) {
+  const int32_t Li = mt.valid ? token_li(mt, seq_active, kn) : 0;
+  return token_epilogue_li(mt, logp, old, A, Li, inv_tm, kn, acc, clipped_out, prox, ref);
 }
 
 // token_epilogue of the clipped surrogate alone (token_ratio_basic / token_scale_basic)

@@ -158,16 +158,8 @@ rl_status launch_stats_reduce(const double* partials, int n_ctas, rl_loss_stats*
 }
 
 static int two_pass_grid(int64_t n_tokens) {
-  static int ctas = 0;
-  if (!ctas) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int per_sm = 1;  // one 297 KB row in flight per SM keeps ~44 MB resident in the 126 MB L2
-    if (const char* e = getenv("RL_TWO_PASS_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));
-    ctas = std::min(sms * per_sm, kMaxStatCtas);
-  }
-  return (int)std::min<int64_t>(n_tokens, ctas);
+  // one 297 KB row in flight per SM keeps ~44 MB resident in the 126 MB L2
+  return (int)std::min<int64_t>(n_tokens, std::min(dev_info().sms, kMaxStatCtas));
 }
 
 rl_status launch_loss_two_pass(const void* logits, int32_t dtype, int64_t n, int64_t V, int64_t ld,
@@ -190,15 +182,6 @@ rl_status launch_loss_two_pass(const void* logits, int32_t dtype, int64_t n, int
   return check_launch("loss_two_pass_kernel");
 }
 
-// Row-resident cluster kernel (policy_loss_cluster.cu); returns RL_ERR_UNSUPPORTED when the
-// shape does not fit its shared-memory plan, in which case the two-pass kernel runs.
-rl_status launch_loss_cluster(const void* logits, int32_t dtype, int64_t n, int64_t V, int64_t ld,
-                              const int32_t* targets, const float* old_logp, const uint8_t* mask,
-                              const int32_t* token_seq, const float* seq_adv,
-                              const int32_t* seq_version, const int32_t* seq_active,
-                              const Knobs& kn, void* dlogits, float* logp_out, uint8_t* clipped_out,
-                              double* partials, int* n_ctas, cudaStream_t s);
-
 // Single-visit cluster kernel (policy_loss_sv.cu); rows it flags in `redo` are left to a
 // two-pass fixup launch.
 rl_status launch_loss_sv(const void* logits, int32_t dtype, int64_t n, int64_t V, int64_t ld,
@@ -208,19 +191,8 @@ rl_status launch_loss_sv(const void* logits, int32_t dtype, int64_t n, int64_t V
                          uint8_t* clipped_out, double* partials, uint8_t* redo, int* n_ctas,
                          cudaStream_t s);
 
-// Kernel choice: "sv" (default), "cluster" or "two_pass" (RL_LOSS_KERNEL).
-enum { K_SV = 0, K_TWO_PASS = 1, K_CLUSTER = 3 };
-static int loss_kernel_choice() {
-  static int choice = -1;
-  if (choice < 0) {
-    choice = K_SV;
-    if (const char* e = getenv("RL_LOSS_KERNEL")) {
-      if (strcmp(e, "two_pass") == 0) choice = K_TWO_PASS;
-      if (strcmp(e, "cluster") == 0) choice = K_CLUSTER;
-    }
-  }
-  return choice;
-}
+// Kernel choice (development option RL_DEV_LOSS_KERNEL): 0 = single visit (default), 1 = two-pass.
+enum { K_SV = 0, K_TWO_PASS = 1 };
 
 }  // namespace rl
 
@@ -281,15 +253,13 @@ extern "C" rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, i
   double* partials = (double*)workspace;
   int n_ctas = 0;
   rl_status st = RL_ERR_UNSUPPORTED;
-  const int choice = loss_kernel_choice();
-  const char* which = "two_pass";
+  const int choice = dev_option(OPT_LOSS_KERNEL) == 1 ? K_TWO_PASS : K_SV;
   if (choice == K_SV) {
     uint8_t* redo = (uint8_t*)workspace + (size_t)kMaxStatCtas * RL_LOSS_STATS_N * sizeof(double);
     st = launch_loss_sv(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask, token_seq,
                         seq_adv, seq_version, seq_active, kn, dlogits, logp_out, clipped_out, partials,
                         redo, &n_ctas, s);
     if (st == RL_OK) {  // rows the fast path flagged: exact two-pass, own partial slots
-      which = "sv";
       int n_fix = 0;
       st = launch_loss_two_pass(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask, token_seq, seq_adv, seq_version,
                                 seq_active, kn, dlogits, logp_out, clipped_out,
@@ -298,19 +268,10 @@ extern "C" rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, i
       n_ctas += n_fix;
     }
   }
-  if (choice == K_CLUSTER) {
-    st = launch_loss_cluster(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
-                             token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,
-                             clipped_out, partials, &n_ctas, s);
-    if (st == RL_OK) which = "cluster";
-  }
   if (st == RL_ERR_UNSUPPORTED)
     st = launch_loss_two_pass(logits, dtype, n_tokens, vocab, ld, targets, old_logp, loss_mask,
                               token_seq, seq_adv, seq_version, seq_active, kn, dlogits, logp_out,
                               clipped_out, partials, &n_ctas, s);
   if (st != RL_OK) return st;
-  static const bool debug = getenv("RL_DEBUG") != nullptr;
-  if (debug) fprintf(stderr, "[rl] rl_policy_loss_fwd_bwd: %s kernel, %d CTAs, n=%lld V=%lld\n", which,
-                     n_ctas, (long long)n_tokens, (long long)vocab);
   return launch_stats_reduce(partials, n_ctas, stats, acc, s);
 }

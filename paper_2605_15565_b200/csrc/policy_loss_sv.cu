@@ -57,25 +57,11 @@ enum : uint32_t { SV_NONE = 0, SV_ZERO = 1, SV_GRAD = 2 };  // how row p-1's dlo
 constexpr float kSvRedo = 0x1p115f;                         // S' bound of the fast path
 static_assert(kCacheShift == 15.f, "p_y = 2^15 / S' below");
 
-// Development trace (RL_TRACE=1): per CTA, the first 64 rows' phase times (globaltimer ns):
-// consumers 0 iteration start, 1 ref(p) received, 2 chunk loop done, 3 exchange done; service lane
-// 4 res(p) seen, 5 statistics written, 6 ref(p+2) published; 7 producer issues row p's first copy.
-constexpr int kSvTraceRows = 64, kSvTraceEv = 8, kSvTraceCtas = 256;
-__device__ unsigned long long g_trace_sv[kSvTraceCtas][kSvTraceRows][kSvTraceEv];
-#define RL_SV_EV(p, ev)                                                                              \
-  do {                                                                                               \
-    if (TRACE && blockIdx.x < kSvTraceCtas && (p) < kSvTraceRows) {                                  \
-      unsigned long long t_;                                                                         \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                         \
-      g_trace_sv[blockIdx.x][(p)][(ev)] = t_;                                                        \
-    }                                                                                                \
-  } while (0)
-
 constexpr int kSvThreads = kClThreads;  // 15 consumer warps + 1 service warp (128 registers)
 
 // XF: compile-time extensions — bit 0 the entropy moment (RL_F_ENTROPY), bit 1 the KL / proximal
 // terms (kl_coef, prox_logp); the default instantiation (XF = 0) carries neither.
-template <typename T, int CL, int NCH, bool EXACT, bool TRACE = false, int VPT = 1, int XF = 0>
+template <typename T, int CL, int NCH, bool EXACT, int VPT = 4, int XF = 0>
 __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) {
   constexpr int EPV = ClVec<T>::EPV;
   constexpr bool ENT = (XF & 1) != 0, EXT = (XF & 2) != 0;
@@ -140,7 +126,6 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
           const char* src = reinterpret_cast<const char*>(a.logits) + row * row_bytes + v0 * 16;
           for (int c = 0; c * VPT < nch; ++c) {  // one bulk copy of VPT x 7.5 KB per ring slot
             sm100::mbar_wait_a(empty_s + rp.slot * 8, rp.phase ^ 1);
-            if (c == 0) RL_SV_EV(pp, 7);
             const uint32_t bytes = (uint32_t)min(VPT * kChunkVec, my_nv - c * VPT * kChunkVec) * 16u;
             sm100::mbar_arrive_expect_tx(&full[rp.slot], bytes);
             sm100::bulk_g2s_nohint(ring + (size_t)rp.slot * (VPT * kChunkVec), src + (size_t)c * VPT * kChunkBytes,
@@ -199,7 +184,6 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
         uint32_t p = 0;
         for (int64_t row = cid; row < a.n_tokens; row += ncl, ++p) {
           sm100::mbar_wait_polite(&sh.resbar[p & 1], (p >> 1) & 1, false);
-          RL_SV_EV(p, 4);
           const float4 rs = sh.res[p & 1];
           const float S = rs.x;
           const RowMeta& mt = cur.mt;
@@ -217,7 +201,6 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
               if (a.clipped_out) a.clipped_out[row] = cl;
             }
           }
-          RL_SV_EV(p, 5);
           // ref(p+2) goes to slot (p+2) % 4: row p's slot stays intact for its late readers
           const int64_t n2 = row + 2 * ncl;
           cur = nxt;
@@ -225,7 +208,6 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
             nxt = fetch(n2);
             publish_ref(p + 2, nxt);
           }
-          RL_SV_EV(p, 6);
         }
       }
 #pragma unroll
@@ -246,7 +228,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
     uint32_t slot = 0, rph = 0;
     float xt = 0.f;  // e' of this thread's scalar tail column (V % EPV != 0)
     // row p-1's gradient (set by the exchange at the end of iteration p-1)
-    uint32_t mode = SV_NONE, qb2 = 0;
+    uint32_t mode = SV_NONE, qb2 = 0, ql2 = 0;  // q split into bf16 hi + lo (ClVec::grad_sv)
     float q = 0.f, dy = 0.f;
     int ycol = -1;
 #define RL_PRESENT(j) (EXACT ? true : ((j) < nch))
@@ -258,7 +240,6 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       const bool has_row = row < a.n_tokens;
       if (!has_row && p == 0) break;
       const uint32_t b = p & 1;
-      if (tid == 0) RL_SV_EV(p, 0);
       bool need = false;
       float mn = 0.f;
       const uint32_t q4 = p & 3;
@@ -267,7 +248,6 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
         need = (sh.refb[q4].x & 1) != 0;
         mn = sh.refa[q4].x;
       }
-      if (tid == 0) RL_SV_EV(p, 1);
       const uint64_t mn2 = f2pack(mn, mn);
       const bool stores = mode != SV_NONE;
       char* dp = reinterpret_cast<char*>(a.dlogits) + (row - ncl) * row_bytes;  // row p-1
@@ -283,16 +263,13 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
 #pragma unroll
         for (int j = 0; j < NCH; ++j) {
           if (RL_PRESENT(j)) {
-            st_stream_v4_if(out + j * kChunkVec, ClVec<T>::grad_sv(cache[j], qb2, q),
-                            stores && RL_MINE(j) && (!TRACE || !(a.debug & 1)));
+            st_stream_v4_if(out + j * kChunkVec, ClVec<T>::grad_sv(cache[j], qb2, ql2, q),
+                            stores && RL_MINE(j));
             if (NEED) {
               if (j % VPT == 0) sm100::mbar_wait_a(full_s + slot * 8, rph);
               const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)(VPT * kChunkBytes) + (j % VPT) * kChunkBytes + my_off);
               if (RL_CHUNK_END(j)) sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
-              if (TRACE && (a.debug & 2)) {
-                cache[j] = v;
-                acc2 = fadd2(acc2, f2pack(__uint_as_float(v.x & 0x7fff), 1.f));
-              } else if (ENT) {
+              if (ENT) {
                 uint64_t nx = accx;
                 const uint64_t nacc = ClVec<T>::exp_sv_ent(v, k2, mn2, acc2, nx, cache[j]);
                 acc2 = RL_MINE(j) ? nacc : acc2;
@@ -325,14 +302,11 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       }
       // target column of row p-1: rewritten by the thread that stored its vector (or tail
       // column) above — same-thread program order to the same address.
-      // target column of row p-1: rewritten by the thread that stored its vector (or tail
-      // column) above — same-thread program order to the same address.
       if (mode == SV_GRAD && ycol >= 0) {
         const bool in_tail = ycol >= a.nvec * EPV;
         const int owner = in_tail ? (int)(ycol - a.nvec * EPV) : (int)((ycol / EPV - v0) % kChunkVec);
         if (tid == owner) VecTraits<T>::store1(dp, ycol, dy);
       }
-      if (tid == 0) RL_SV_EV(p, 2);
       if (!has_row) break;
       // ---- exchange of row p: CTA sum (named barrier), cluster sum (st.async), row scale
       {
@@ -368,7 +342,6 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       for (int r = 0; r < CL; ++r) S += r == (int)crank ? Sc : sh.xch[b][r].x;
       if (ENT && tid == 0)
         for (int r = 0; r < CL; ++r) Tx += r == (int)crank ? Tc : sh.xch[b][r].y;
-      if (tid == 0) RL_SV_EV(p, 3);
       const float4 ra = sh.refa[q4];
       const float4 rc = EXT ? sh.refc[q4] : make_float4(ra.z, 0.f, 0.f, 0.f);
       const int4 rb = sh.refb[q4];
@@ -385,6 +358,10 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       q = st == 0.f ? 0.f : st * inv_s;  // (an unread row has S' = 0)
       dy = st == 0.f ? 0.f : st * (32768.f * inv_s - 1.f);  // p_y = e'_y / S' = 2^15 / S'
       qb2 = pack_bf16x2(q, q);
+      {
+        const float qh = __uint_as_float(qb2 << 16);
+        ql2 = pack_bf16x2(q - qh, q - qh);
+      }
       ycol = rb.y;
       if (tid == 0) {
         sh.res[b] = make_float4(S, lp, Tx, 0.f);
@@ -400,28 +377,21 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
   sm100::cluster_sync();  // no CTA leaves while a peer may still write its smem
 }
 
-template <typename T, int CL, int NCH, bool EXACT = false, bool TRACE = false, int VPT = 1, int XF = 0>
+template <typename T, int CL, int NCH, bool EXACT = false, int VPT = 4, int XF = 0>
 static rl_status launch_sv(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_ctas) {
   ClArgs a = a0;
-  auto kern = loss_sv_kernel<T, CL, NCH, EXACT, TRACE, VPT, XF>;
+  auto kern = loss_sv_kernel<T, CL, NCH, EXACT, VPT, XF>;
   const size_t head = (sizeof(SvShared) + 127) & ~(size_t)127;
   constexpr size_t slot_bytes = (size_t)VPT * kChunkBytes;
-  int nslots = (int)((kSmemMax - head - 256) / (slot_bytes + 16));
+  const int nslots = (int)((kSmemMax - head - 256) / (slot_bytes + 16));
   const int nch = (int)((a.h_vec + kChunkVec - 1) / kChunkVec);
-  static int slots_cap = -1;  // RL_SV_SLOTS: cap on the ring depth (tuning knob)
-  if (slots_cap < 0) slots_cap = getenv("RL_SV_SLOTS") ? atoi(getenv("RL_SV_SLOTS")) : 0;
-  if (slots_cap > 0) nslots = std::min(nslots, std::max(slots_cap, 2));
   if (nch > NCH || (EXACT && nch != NCH)) return RL_ERR_UNSUPPORTED;
   a.nslots = nslots;
   const size_t smem = ((sizeof(SvShared) + 2 * sizeof(uint64_t) * nslots + 127) & ~(size_t)127) +
                       (size_t)nslots * slot_bytes;
-  static bool attr_done = false;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return check_launch("cudaFuncSetAttribute(max dynamic smem)");
-    attr_done = true;
-  }
-  static int max_clusters = 0;
+  // the >48 KB opt-in is per device and cheap: set it on every launch
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return check_launch("cudaFuncSetAttribute(max dynamic smem)");
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -433,15 +403,17 @@ static rl_status launch_sv(const ClArgs& a0, int64_t n, cudaStream_t s, int* n_c
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static int max_clusters_tab[kMaxDevices] = {};
+  int& max_clusters = dev_slot(max_clusters_tab);
   if (!max_clusters) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = dev_info().sms;
     cfg.gridDim = dim3(sms / CL * CL);
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+    int mc = 0;
+    if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
       cudaGetLastError();
-      max_clusters = sms / CL;
+      mc = sms / CL;
     }
+    max_clusters = mc;
   }
   const int64_t ncl = std::min<int64_t>(std::min<int64_t>(n, max_clusters), kMaxStatCtas / 2 / CL);
   cfg.gridDim = dim3((unsigned)(ncl * CL));
@@ -477,53 +449,35 @@ rl_status launch_loss_sv(const void* logits, int32_t dtype, int64_t n, int64_t V
   a.redo = redo;
   a.kn = kn;
   a.nslots = 0;
-  a.prefetch_chunks = 0;
-  // RL_SV_DEBUG bits (development): 4 = spinning instead of nanosleep waits in the epilogue;
-  // with RL_TRACE also 1 = no dlogits stores, 2 = no exp2 (timing experiments, wrong results)
-  static int dbg = -1;
-  if (dbg < 0) dbg = getenv("RL_SV_DEBUG") ? atoi(getenv("RL_SV_DEBUG")) : 0;
-  a.debug = dbg;
   auto nchunks = [&](int64_t h) { return (h + kChunkVec - 1) / kChunkVec; };
   a.h_vec = (a.nvec + 1) / 2;
   const int64_t nch2 = nchunks(a.h_vec);
-  static int vpt = -1;  // RL_SV_VPT: 16-B vectors per thread per TMA bulk copy (1, 2, 4, 5, 8)
-  if (vpt < 0) vpt = getenv("RL_SV_VPT") ? atoi(getenv("RL_SV_VPT")) : 4;
-  const bool trace = getenv("RL_TRACE") != nullptr;
+  // The EXACT instantiations (V = 151936, 128256: 20 / 17 chunks per CTA) carry no scalar tail
+  // code, so they are taken only when V has no tail columns (V % 8 == 0); a vocabulary of the
+  // same width with a tail (e.g. 151665 in a 151936-wide buffer) takes the general instantiation.
+  const bool exact_ok = bf && V % 8 == 0;
   const int xf = ((kn.flags & RL_F_ENTROPY) ? 1 : 0) | ((kn.kl_coef != 0.f || kn.prox_logp) ? 2 : 0);
   if (xf) {  // NEXT-2 terms: compile-time variants of the hot shapes, the general one otherwise
 #define RL_SV_XF(X)                                                                                      \
-    if (xf == X) {                                                                                       \
-      if (bf && nch2 == 20) return launch_sv<bf16_t, 2, 20, true, false, 4, X>(a, n, s, n_ctas);        \
-      if (bf && nch2 == 17) return launch_sv<bf16_t, 2, 17, true, false, 4, X>(a, n, s, n_ctas);        \
+    if (xf == X && exact_ok) {                                                                           \
+      if (nch2 == 20) return launch_sv<bf16_t, 2, 20, true, 4, X>(a, n, s, n_ctas);                      \
+      if (nch2 == 17) return launch_sv<bf16_t, 2, 17, true, 4, X>(a, n, s, n_ctas);                      \
     }
     RL_SV_XF(1) RL_SV_XF(2) RL_SV_XF(3)
 #undef RL_SV_XF
     if (nch2 <= 20)
-      return bf ? launch_sv<bf16_t, 2, 20, false, false, 4, 3>(a, n, s, n_ctas)
-                : launch_sv<float, 2, 20, false, false, 4, 3>(a, n, s, n_ctas);
+      return bf ? launch_sv<bf16_t, 2, 20, false, 4, 3>(a, n, s, n_ctas)
+                : launch_sv<float, 2, 20, false, 4, 3>(a, n, s, n_ctas);
     return RL_ERR_UNSUPPORTED;  // very wide rows: the two-pass kernel computes them
   }
-  if (bf && nch2 == 20) {
-    if (trace) return launch_sv<bf16_t, 2, 20, true, true, 4>(a, n, s, n_ctas);
-    if (vpt == 1) return launch_sv<bf16_t, 2, 20, true, false, 1>(a, n, s, n_ctas);
-    if (vpt == 2) return launch_sv<bf16_t, 2, 20, true, false, 2>(a, n, s, n_ctas);
-    if (vpt == 5) return launch_sv<bf16_t, 2, 20, true, false, 5>(a, n, s, n_ctas);
-    if (vpt == 8) return launch_sv<bf16_t, 2, 20, true, false, 8>(a, n, s, n_ctas);
-    return launch_sv<bf16_t, 2, 20, true, false, 4>(a, n, s, n_ctas);
-  }
-  if (bf && nch2 == 17) return launch_sv<bf16_t, 2, 17, true, false, 4>(a, n, s, n_ctas);  // V = 128256
-  if (nch2 <= 2) return bf ? launch_sv<bf16_t, 2, 2, false, false, 4>(a, n, s, n_ctas) : launch_sv<float, 2, 2, false, false, 4>(a, n, s, n_ctas);
-  if (nch2 <= 5) return bf ? launch_sv<bf16_t, 2, 5, false, false, 4>(a, n, s, n_ctas) : launch_sv<float, 2, 5, false, false, 4>(a, n, s, n_ctas);
-  if (nch2 <= 10) return bf ? launch_sv<bf16_t, 2, 10, false, false, 4>(a, n, s, n_ctas) : launch_sv<float, 2, 10, false, false, 4>(a, n, s, n_ctas);
-  if (nch2 <= 20) return bf ? launch_sv<bf16_t, 2, 20, false, false, 4>(a, n, s, n_ctas) : launch_sv<float, 2, 20, false, false, 4>(a, n, s, n_ctas);
+  if (exact_ok && nch2 == 20) return launch_sv<bf16_t, 2, 20, true>(a, n, s, n_ctas);  // V = 151936
+  if (exact_ok && nch2 == 17) return launch_sv<bf16_t, 2, 17, true>(a, n, s, n_ctas);  // V = 128256
+  if (nch2 <= 2) return bf ? launch_sv<bf16_t, 2, 2>(a, n, s, n_ctas) : launch_sv<float, 2, 2>(a, n, s, n_ctas);
+  if (nch2 <= 5) return bf ? launch_sv<bf16_t, 2, 5>(a, n, s, n_ctas) : launch_sv<float, 2, 5>(a, n, s, n_ctas);
+  if (nch2 <= 10) return bf ? launch_sv<bf16_t, 2, 10>(a, n, s, n_ctas) : launch_sv<float, 2, 10>(a, n, s, n_ctas);
+  if (nch2 <= 20) return bf ? launch_sv<bf16_t, 2, 20>(a, n, s, n_ctas) : launch_sv<float, 2, 20>(a, n, s, n_ctas);
   a.h_vec = (a.nvec + 3) / 4;
-  return bf ? launch_sv<bf16_t, 4, 20, false, false, 4>(a, n, s, n_ctas) : launch_sv<float, 4, 20, false, false, 4>(a, n, s, n_ctas);
+  return bf ? launch_sv<bf16_t, 4, 20>(a, n, s, n_ctas) : launch_sv<float, 4, 20>(a, n, s, n_ctas);
 }
 
 }  // namespace rl
-
-// development only (not part of include/rl_policy.h): copy the SV phase trace to the host
-extern "C" int rl_debug_trace_sv(unsigned long long* host, size_t bytes) {
-  const size_t n = sizeof(rl::g_trace_sv) < bytes ? sizeof(rl::g_trace_sv) : bytes;
-  return cudaMemcpyFromSymbol(host, rl::g_trace_sv, n) == cudaSuccess ? 0 : 1;
-}

@@ -16,7 +16,7 @@ import numpy as np
 
 __all__ = [
     "SynthConfig", "CONFIGS", "get_config", "seq_layout", "host_logits", "device_logits",
-    "perturb_old_logp", "bf16_round_bits", "pad_ld",
+    "perturb_old_logp", "bf16_round_bits", "pad_ld", "dominant_logits",
 ]
 
 
@@ -248,3 +248,19 @@ def perturb_old_logp(logp_ref: np.ndarray, token_staleness: np.ndarray, big_delt
     bigv = rng.uniform(0.3, 1.0, size=n) * np.where(rng.uniform(size=n) < 0.5, -1.0, 1.0)
     delta = np.where(np.asarray(big_delta) != 0, bigv, delta)
     return (np.asarray(logp_ref, dtype=np.float64) + delta).astype(np.float32)
+
+
+def dominant_logits(n_rows: int, vocab: int, seed: int):
+    """Rows built to stress the bf16 gradient path (reading R2): a N(0,1)
+    background plus ONE dominant column h_t with D_t ~ U[14, 21] (over a ~152K-column N(0,1)
+    background that makes its probability ~0.75-0.9995), and a target y_t drawn uniformly among
+    the other columns — a confident model that sampled another token, so the row's largest
+    gradient element is a non-target s p_h.  Every 4th row instead puts the dominant column at
+    the target.  Returns (bf16 bits [n, V], targets int32 [n], dominant columns int32 [n])."""
+    g = np.random.Generator(np.random.Philox(key=np.array([seed, 0xD0], dtype=np.uint64)))
+    x = g.standard_normal((n_rows, vocab), dtype=np.float32)
+    h = g.integers(0, vocab, size=n_rows)
+    y = (h + g.integers(1, vocab, size=n_rows)) % vocab
+    y = np.where(np.arange(n_rows) % 4 == 3, h, y)
+    x[np.arange(n_rows), h] += g.uniform(14.0, 21.0, size=n_rows).astype(np.float32)
+    return bf16_round_bits(x), y.astype(np.int32), h.astype(np.int32)

@@ -21,4 +21,8 @@ def cuda_lib():
         pytest.fail("GPU test selected but torch.cuda.is_available() is False")
     import paper_2605_15565_b200 as rl
     rl.load()
+    # RL_TEST_DEV_OPTS="key=value,...": development options for this process (test_gpu_kernels.py)
+    for kv in filter(None, os.environ.get("RL_TEST_DEV_OPTS", "").split(",")):
+        k, v = kv.split("=")
+        rl.dev_set_option(int(k), int(v))
     return rl

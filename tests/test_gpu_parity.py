@@ -371,14 +371,18 @@ def test_extreme_rows(cuda_lib, dtype):
 
 
 def test_rows_sum_to_zero_bf16(cuda_lib):
-    """Invariant: each gradient row sums to ~0 (bf16 output: |sum| <= 4e-3 |s_t|)."""
+    """Invariant: each gradient row sums to ~0 within the bound derived in DESIGN.md §3 R2:
+    |sum_v d_v| <= 3u / (1 - u) max|d| + 2^-16 |s_t| (u = 2^-8: <= 2 bf16 roundings per non-target
+    element, 1 on the target)."""
     case = small_case(vocab=8192, dtype="bf16", seed=15, mask_mode="all", ignore_frac=0.0)
     g = run_gpu_chain(cuda_lib, case, {})
     ref = oracle_chain(case, oracle.LossParams())["loss"]
     s = ref["scale"]
     nz = s != 0
     sums = g["dlogits"][nz].sum(axis=1)
-    assert np.all(np.abs(sums) <= 4e-3 * np.abs(s[nz]) * 8)
+    amax = np.abs(g["dlogits"][nz]).max(axis=1)
+    u = 2.0 ** -8
+    assert np.all(np.abs(sums) <= 3 * u / (1 - u) * amax + 2.0 ** -16 * np.abs(s[nz]))
 
 
 def test_host_entry_point_matches_device(cuda_lib):
@@ -581,9 +585,10 @@ def test_full_size_sampled(cuda_lib, name, N, in_place, objective):
         blk = dl[c0:c0 + 4096].float()
         sums = blk.sum(dim=1).abs()
         amax = blk.abs().amax(dim=1)
-        # three bf16 roundings per element on the fast path (e' cache, q, the product: reading R2),
-        # coherent when one probability dominates the row: |sum| <= 3 * 2^-8 * max|d|
-        bad = t.nonzero(sums > 1.2e-2 * amax + 1e-5)[:, 0]
+        # reading R2: <= 2 bf16 roundings per non-target element, 1 on the target:
+        # |sum| <= 3u / (1 - u) max|d| + 2^-16 |s_t|, u = 2^-8; |s_t| <= 8 here (AGG_SUM, |A| r)
+        u = 2.0 ** -8
+        bad = t.nonzero(sums > 3 * u / (1 - u) * amax + 2.0 ** -16 * 8)[:, 0]
         assert bad.numel() == 0, [(c0 + int(r), float(sums[r]), float(amax[r])) for r in bad[:5]]
         del blk
     del logits, dl

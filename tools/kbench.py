@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--rows", type=int, default=131072)
     ap.add_argument("--vocab", type=int, default=151936)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--two-pass", action="store_true", help="the exact two-pass kernel (development option)")
     args = ap.parse_args()
     import torch
     import paper_2605_15565_b200 as rl
@@ -52,7 +53,8 @@ def main():
     t, avg = timeit(lambda: rl.token_logprob(x, y, logp))
     print(f"token_logprob   : {t:8.3f} ms  {nbytes / t / 1e6:8.1f} GB/s read (avg {avg:.3f})")
     p = rl.LossParams(agg=rl.AGG_SUM)
-    kern = os.environ.get("RL_LOSS_KERNEL", "sv")  # latched by the library on first use
+    kern = "two_pass" if args.two_pass else "sv"
+    rl.dev_set_option(rl.DEV_LOSS_KERNEL, 1 if kern == "two_pass" else 0)
     t, avg = timeit(lambda: rl.policy_loss_fwd_bwd(x, y, old, tseq, adv, p, dl, stats, ws, logp_out=logp))
     print(f"loss ({kern:8s}): {t:8.3f} ms  {2 * nbytes / t / 1e6:8.1f} GB/s R+W (avg {avg:.3f})")
     t, avg = timeit(lambda: rl.policy_loss_fwd_bwd(x, y, old, tseq, adv, p, x, stats, ws, logp_out=logp))
