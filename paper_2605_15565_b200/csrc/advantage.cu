@@ -113,6 +113,7 @@ extern "C" rl_status rl_group_advantage(const double* rewards, const int32_t* cu
       return fail(RL_ERR_WORKSPACE, "batch_norm needs %zu workspace bytes",
                   rl_group_advantage_workspace_size(n_seq));
   }
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   group_advantage_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
       rewards, cu_groups, n_groups, n_seq, std_mode, eps, batch_norm, bn_eps, seq_weight,
       (double*)workspace, adv_out, zero_var_out);

@@ -109,6 +109,7 @@ extern "C" rl_status rl_seq_bookkeeping(const int32_t* cu_seqlens, int32_t n_seq
   if (!cu_seqlens || (n_tokens > 0 && (!targets || !token_seq_out)) || (n_seq > 0 && !seq_active_out))
     return fail(RL_ERR_INVALID_ARGUMENT, "NULL required pointer");
   if (adv_token_out && !seq_adv) return fail(RL_ERR_INVALID_ARGUMENT, "adv_token_out needs seq_adv");
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   cudaStream_t s = (cudaStream_t)stream;
   if (counts_out && cudaMemsetAsync(counts_out, 0, sizeof(rl_batch_counts), s) != cudaSuccess)
     return check_launch("memset counts");

@@ -263,6 +263,7 @@ extern "C" rl_status rl_bf16_delta_encode(const void* prev, const void* next, in
   if (((uintptr_t)prev & 15) || ((uintptr_t)next & 15)) return fail(RL_ERR_ALIGNMENT, "prev/next must be 16-B aligned");
   if (!workspace || workspace_bytes < rl_bf16_delta_workspace_size(n_words))
     return fail(RL_ERR_WORKSPACE, "workspace must be >= %zu bytes", rl_bf16_delta_workspace_size(n_words));
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t tiles = dt_tiles(n_words);
   const DtLayout L = dt_layout(n_words);
@@ -301,6 +302,7 @@ extern "C" rl_status rl_bf16_delta_apply(void* base, int64_t n_words, const uint
   if ((n_words > 0 && !base) || (capacity > 0 && (!idx || !words)))
     return fail(RL_ERR_INVALID_ARGUMENT, "NULL base/idx/words");
   if (capacity == 0) return RL_OK;
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = (int)std::min<int64_t>((capacity + 255) / 256, 148 * 8);
   delta_apply_kernel<<<grid, 256, 0, s>>>((uint16_t*)base, n_words, idx, words, count, capacity, bad_index_count);

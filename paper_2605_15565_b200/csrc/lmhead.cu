@@ -323,6 +323,7 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
   if (!hidden || !weight || !targets || !logp_out) return fail(RL_ERR_INVALID_ARGUMENT, "NULL hidden/weight/targets/logp_out");
   if (((uintptr_t)hidden & 15) || ((uintptr_t)weight & 15) || (ld_hidden % 8) || (ld_weight % 8))
     return fail(RL_ERR_ALIGNMENT, "hidden / weight must be 16-B aligned with ld % 8 == 0");
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   CUtensorMap mh, mw;
   if (!make_map(&mh, hidden, n_tokens, d, ld_hidden, kLmBM) || !make_map(&mw, weight, vocab, d, ld_weight, kLmBN))
     return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");

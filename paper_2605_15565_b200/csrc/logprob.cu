@@ -104,6 +104,7 @@ extern "C" rl_status rl_token_logprob(const void* logits, int32_t dtype, int64_t
   const int64_t eb = dtype == RL_BF16 ? 2 : 4;
   if (((uintptr_t)logits & 15) || (ld * eb) % 16)
     return fail(RL_ERR_ALIGNMENT, "logits must be 16-B aligned with ld*elem %% 16 == 0");
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   cudaStream_t s = (cudaStream_t)stream;
   {
     static int ctas_tab[kMaxDevices] = {};

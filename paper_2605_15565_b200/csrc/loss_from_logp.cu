@@ -88,6 +88,7 @@ extern "C" rl_status rl_policy_loss_from_logp(const float* logp, int64_t n_token
   }
   if (!logp || !targets || !old_logp || !token_seq || !seq_adv)
     return fail(RL_ERR_INVALID_ARGUMENT, "NULL logp/targets/old_logp/token_seq/seq_adv");
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   const int grid = (int)std::min<int64_t>((n_tokens + kLfThreads - 1) / kLfThreads, 148 * 4);
   double* partials = (double*)workspace;
   loss_from_logp_kernel<<<grid, kLfThreads, 0, s>>>(logp, n_tokens, vocab, targets, old_logp, loss_mask, token_seq,

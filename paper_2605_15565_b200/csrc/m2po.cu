@@ -135,6 +135,7 @@ extern "C" rl_status rl_m2po_mask(const float* logp, const float* old_logp, cons
   const M2poLayout L = m2po_layout(n, P);
   if (!workspace || workspace_bytes < L.total)
     return fail(RL_ERR_WORKSPACE, "workspace must be >= %zu bytes", L.total);
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   cudaStream_t s = (cudaStream_t)stream;
   char* w = (char*)workspace;
   uint32_t* keys = (uint32_t*)(w + L.keys);

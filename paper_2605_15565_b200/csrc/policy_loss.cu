@@ -249,6 +249,7 @@ extern "C" rl_status rl_policy_loss_fwd_bwd(const void* logits, int32_t dtype, i
     if (a < b + bytes && b < a + bytes)
       return fail(RL_ERR_INVALID_ARGUMENT, "dlogits partially overlaps logits");
   }
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   const Knobs kn = make_knobs(p);
   double* partials = (double*)workspace;
   int n_ctas = 0;

@@ -6,13 +6,16 @@ SURVEY.md §8(e)).  Pure integer bookkeeping: no arithmetic of the method lives 
   batch counts (before) and loss statistics (after) are all-reduced.
 * vocab parallel: contiguous column ranges, every boundary a multiple of 8 columns so each
   shard row keeps 16-B aligned bf16 vectors.
+* multi-policy (configs[4]): the world splits into one contiguous trainer group per policy
+  (rl_comm_split colour = policy, key = rank in the group); each group is token-parallel on its own
+  policy's batch and the groups never communicate.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
 from typing import Sequence
 
-__all__ = ["SeqShard", "shard_sequences", "VocabShard", "shard_vocab"]
+__all__ = ["SeqShard", "shard_sequences", "VocabShard", "shard_vocab", "PolicyGroup", "policy_group"]
 
 
 @dataclass(frozen=True)
@@ -70,3 +73,34 @@ def shard_vocab(vocab: int, world: int, rank: int, align: int = 8) -> VocabShard
     u1 = u0 + per + (1 if rank < extra else 0)
     lo, hi = min(vocab, u0 * align), min(vocab, u1 * align)
     return VocabShard(lo, hi - lo)
+
+
+@dataclass(frozen=True)
+class PolicyGroup:
+    policy: int      # rl_comm_split colour
+    key: int         # rank inside the policy's trainer group (rl_comm_split key)
+    size: int        # ranks in the group
+    first: int       # global rank of the group's rank 0
+
+    @property
+    def ranks(self) -> range:
+        return range(self.first, self.first + self.size)
+
+
+def policy_group(world: int, n_policies: int, rank: int) -> PolicyGroup:
+    """Trainer group of global rank `rank` when `world` ranks serve `n_policies` policies:
+    contiguous groups, the first world % n_policies groups one rank larger (4 + 4 for the
+    paper's two policies on 8 GPUs).  With world < n_policies the single rank serves all
+    policies in turn (group 0 of size 1)."""
+    if world < 1 or n_policies < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/n_policies/rank")
+    if world < n_policies:
+        return PolicyGroup(0, rank, world, 0)
+    per, extra = divmod(world, n_policies)
+    first = 0
+    for pol in range(n_policies):
+        size = per + (1 if pol < extra else 0)
+        if rank < first + size:
+            return PolicyGroup(pol, rank - first, size, first)
+        first += size
+    raise AssertionError("unreachable")

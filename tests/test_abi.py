@@ -123,6 +123,17 @@ def test_host_validation_rejects_before_launch(lib):
                                          fake, 1 << 20, None) == 1
 
 
+def test_refuses_to_enqueue_without_an_sm100_device(lib):
+    """A call that passes every host check reaches the device check, which answers
+    RL_ERR_UNSUPPORTED on anything but a compute-capability 10.0 device (here: no device)."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a device is present: the fake pointers below would be dereferenced")
+    fake = 0x10000
+    assert lib.rl_token_logprob(fake, rl.BF16, 4, 96, 96, fake, 1.0, fake, None, None, None) == 3
+    assert b"sm_100a" in lib.rl_last_error()
+
+
 def test_zero_sized_calls_are_noops(lib):
     assert lib.rl_group_advantage(None, None, 0, 0, 0, 1e-6, 0, 1e-6, None, None, 0, None, None, None) == 0
     assert lib.rl_token_logprob(None, rl.BF16, 0, 8, 8, None, 1.0, None, None, None, None) == 0

@@ -154,7 +154,7 @@ def test_full_chain_sampled(cuda_lib, name, n_seq, in_place, objective, skip):
     S, G = n_seq, n_seq // cfg.group
     cu = np.ascontiguousarray(lay["cu_seqlens"][:S + 1]).astype(np.int32)
     cu_groups = np.arange(G + 1, dtype=np.int32) * cfg.group
-    rewards = np.ascontiguousarray(lay["rewards"][:S]).astype(np.float32)
+    rewards = np.ascontiguousarray(lay["rewards"][:S]).astype(np.float64)   # rl_group_advantage takes fp64
     ver = np.ascontiguousarray(lay["seq_version"][:S]).astype(np.int32)
     tv, ms = int(lay["trainer_version"]), int(cfg.max_staleness)
     x = t.empty((N, V), dtype=t.bfloat16, device="cuda")

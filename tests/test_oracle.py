@@ -259,6 +259,19 @@ def test_bookkeeping_brute_force():
     assert bk["neg_staleness"] == (stale < 0).sum()
     assert bk["bad_targets"] == (y >= V).sum()
     assert bk["stale_masked"] == ((mask != 0) & (y >= 0) & (y < V) & (stale[seq] > 4)).sum()
+    # staleness histogram: per sequence, bin min(s, 15); negative staleness not binned
+    assert np.array_equal(bk["stale_hist"], np.bincount(np.minimum(stale[stale >= 0], 15), minlength=16))
+
+
+def test_stale_hist_bins_and_clamp():
+    # seven sequences with staleness -1, 0, 0, 3, 15, 16, 40 (trainer version 50): bins 0:2, 3:1, 15:3
+    ver = [51, 50, 50, 47, 35, 34, 10]
+    cu = np.arange(8) * 2
+    bk = oracle.seq_bookkeeping(cu, np.ones(14, np.uint8), np.zeros(14, np.int64), 4, ver, 50, -1)
+    expect = np.zeros(16, dtype=np.int64)
+    expect[0], expect[3], expect[15] = 2, 1, 3
+    assert np.array_equal(bk["stale_hist"], expect)
+    assert bk["neg_staleness"] == 1 and bk["active_tokens"] == 12 and bk["stale_masked"] == 0
 
 
 # ----------------------------------------------------------------------------- c4-c7 loss
@@ -310,6 +323,42 @@ def test_ratio_one_loss_is_minus_weighted_mean_adv():
     ones = np.ones(S, dtype=np.float32)
     out1 = oracle.policy_loss_fwd_bwd(x, y, logp, mask, tseq, ones, None, None, p)
     assert abs(out1["loss"] + 1.0) < 1e-15
+
+
+def test_ratio_and_weight_sums_closed_forms():
+    """stats ratio_sum / weight_sum against closed forms that do not involve the logits:
+    old = logp - delta gives r_t = exp(clamp(delta_t)) for every valid token; weight_sum is 1 for
+    TOKEN_MEAN with N_active = the valid count, (#sequences with L_i > 0) / S for
+    SEQ_MEAN_TOKEN_MEAN, and the valid count for SUM; masked / stale / ignored tokens add nothing."""
+    rng = np.random.default_rng(12)
+    N, V, S = 60, 11, 6
+    x = rng.normal(size=(N, V)) * 2
+    y = rng.integers(0, V, size=N)
+    y[::13] = -100
+    logp, _ = oracle.token_logprob(x, y)
+    delta = rng.normal(size=N) * 0.4
+    delta[5], delta[6] = 30.0, -25.0          # beyond the log-ratio clamp c = 20
+    old = logp - delta
+    tseq = np.sort(rng.integers(0, S - 1, size=N))   # sequence S-1 has no tokens
+    mask = (rng.uniform(size=N) < 0.75).astype(np.uint8)
+    mask[5] = mask[6] = 1
+    ver = np.full(S, 10)
+    ver[2] = 5                                 # staleness 5 > max 3: masked
+    valid = (mask != 0) & (y >= 0) & (tseq != 2)
+    nv = int(valid.sum())
+    L = np.bincount(tseq[valid], minlength=S)
+    adv = rng.normal(size=S).astype(np.float32)
+    r = np.exp(np.clip(delta, -20.0, 20.0))
+    for agg, wsum in ((oracle.AGG_TOKEN_MEAN, 1.0), (oracle.AGG_SEQ_MEAN_TOKEN_MEAN, (L > 0).sum() / S),
+                      (oracle.AGG_SUM, float(nv))):
+        p = LossParams(agg=agg, global_active_tokens=float(nv), global_num_seqs=S, trainer_version=10,
+                       max_staleness=3)
+        out = oracle.policy_loss_fwd_bwd(x, y, old, mask, tseq, adv, ver, L, p)
+        st = out["stats"]
+        assert st["active_tokens"] == nv
+        assert abs(st["ratio_sum"] - r[valid].sum()) <= 1e-12 * r[valid].sum()
+        assert abs(st["weight_sum"] - wsum) <= 1e-12 * max(1.0, wsum)
+        assert st["clamped"] == int(valid[5]) + int(valid[6])
 
 
 def test_seq_mean_equals_token_mean_for_equal_lengths():
