@@ -20,8 +20,9 @@ definitions in DESIGN.md §3 (which restate SURVEY.md §8(c) c1–c9):
 * NEXT rows: ``policy_loss_fwd_bwd``'s ref_logp / prox_logp / want_entropy
   (k3 KL, decoupled ratio, entropy — readings N1-N3) and ``m2po_mask`` (M2PO second-moment
   masking, reading M1).
-* ``lmhead_logprob`` – NEXT 4 (forward half): c3 on x = h W^T from the LM head's hidden states
-  and weight, the logits never given.
+* ``lmhead_logprob`` / ``lmhead_loss_backward`` – NEXT 4: c3 on x = h W^T from the LM head's
+  hidden states and weight (the logits never given), and the backward dh = G W, dW = G^T h with
+  G = s (softmax - onehot) (c7 through the LM head).
 
 Parity status of every function is listed in DESIGN.md §4 ("pins").
 """
@@ -40,4 +41,4 @@ from .policy_loss import (  # noqa: F401
     vocab_combine,
 )
 from . import delta  # noqa: F401,E402
-from .lmhead import lmhead_logits, lmhead_logprob  # noqa: F401,E402
+from .lmhead import lmhead_logits, lmhead_logprob, lmhead_loss_backward  # noqa: F401,E402

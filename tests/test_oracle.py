@@ -771,3 +771,60 @@ def test_lmhead_torch_route():
     w = torch.from_numpy((wb.astype(np.uint32) << 16).view(np.float32).astype(np.float64))
     ref = -torch.nn.functional.cross_entropy(h @ w.T, torch.from_numpy(y), reduction="none")
     assert np.allclose(lp, ref.numpy(), atol=1e-12, rtol=0)
+
+
+def _lm_objective_torch(H, W, y, s, invT):
+    """F(h, W) = sum_t (s_t / invT) (-log softmax((h W^T) invT)[y_t]) in torch CPU fp64: its
+    gradients are dh = G W and dW = G^T h with G = s (p - onehot) (independent autograd route)."""
+    import torch
+    x = (H @ W.T) * invT
+    lp = torch.log_softmax(x, dim=1)
+    ok = (y >= 0) & (y < W.shape[0])
+    yy = torch.where(ok, y, torch.zeros_like(y))
+    return -(torch.where(ok, s / invT, torch.zeros_like(s)) * lp.gather(1, yy[:, None])[:, 0]).sum()
+
+
+def test_lmhead_backward_matches_torch_autograd():
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(71)
+    N, d, V = 7, 6, 11
+    H = rng.integers(-16, 17, size=(N, d)) / 8.0
+    W = rng.integers(-16, 17, size=(V, d)) / 16.0
+    y = np.array([0, 10, 3, -100, 5, 11, 7])      # an ignored and an out-of-range target: G row 0
+    s = rng.normal(size=N)
+    for invT in (1.0, 0.7):
+        dh, dW, G = oracle.lmhead_loss_backward(_bf16_bits(H), _bf16_bits(W), y, s, invT)
+        Ht = torch.tensor(H, dtype=torch.float64, requires_grad=True)
+        Wt = torch.tensor(W, dtype=torch.float64, requires_grad=True)
+        _lm_objective_torch(Ht, Wt, torch.tensor(y), torch.tensor(s), invT).backward()
+        assert np.allclose(dh, Ht.grad.numpy(), atol=1e-12, rtol=1e-12)
+        assert np.allclose(dW, Wt.grad.numpy(), atol=1e-12, rtol=1e-12)
+        assert np.all(G[3] == 0) and np.all(G[5] == 0)
+        assert np.allclose(G.sum(axis=1), 0.0, atol=1e-12)      # rows of softmax - onehot sum to 0
+
+
+def test_lmhead_backward_finite_differences():
+    """Central differences of F (pure NumPy, no autograd) at every entry of h and of W."""
+    rng = np.random.default_rng(72)
+    N, d, V = 4, 3, 5
+    H = rng.integers(-8, 9, size=(N, d)) / 8.0
+    W = rng.integers(-8, 9, size=(V, d)) / 8.0
+    y = np.array([1, 4, 0, 2])
+    s = np.array([0.5, -1.25, 2.0, 0.75])
+    invT = 0.8
+
+    def F(Hm, Wm):
+        x = (Hm @ Wm.T) * invT
+        m = x.max(axis=1, keepdims=True)
+        lse = (m + np.log(np.exp(x - m).sum(axis=1, keepdims=True)))[:, 0]
+        return float(np.sum((s / invT) * (lse - x[np.arange(N), y])))
+
+    dh, dW, _ = oracle.lmhead_loss_backward(_bf16_bits(H), _bf16_bits(W), y, s, invT)
+    eps = 1e-6
+    for M, grad in ((H, dh), (W, dW)):
+        for idx in np.ndindex(M.shape):
+            Mp, Mm = M.copy(), M.copy()
+            Mp[idx] += eps
+            Mm[idx] -= eps
+            fd = (F(Mp, W) - F(Mm, W)) / (2 * eps) if M is H else (F(H, Mp) - F(H, Mm)) / (2 * eps)
+            assert abs(fd - grad[idx]) <= 1e-7, (idx, fd, grad[idx])
