@@ -363,6 +363,35 @@ rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* w
                             float inv_temperature, float* logp_out, float* lse_out, void* workspace,
                             size_t workspace_bytes, rl_stream stream);
 
+/* ---------------------------------------------------------------- (8b) LM-head loss backward (NEXT 4)
+ * The backward half of NEXT 4: the gradients of the policy loss through the LM head x = h W^T,
+ *     G[t, v] = s_t (softmax(x_t inv_T)_v - [v == y_t])      (c7 of SURVEY.md §8(c); s_t from
+ *                                                           rl_policy_loss_from_logp, lse_t from
+ *                                                           rl_lmhead_logprob)
+ *     dhidden = G W            [n_tokens, d]   (overwritten)
+ *     dweight = G^T h          [vocab, d]      (overwritten, or added to with RL_F_STATS_ACCUMULATE)
+ * without the logits ever existing in memory: per chunk of C tokens a tcgen05 kernel recomputes each
+ * 128 x 256 logits tile in tensor memory and writes G in bf16 (one rounding) into the workspace, then
+ * two GEMMs consume it (cuBLAS, bf16 x bf16 -> fp32 accumulate; plain library GEMMs).
+ *   hidden, weight, ld_*, n_tokens, d, vocab, inv_temperature: as rl_lmhead_logprob
+ *   targets    device i32 [n_tokens] (y outside [0, vocab): G row 0)
+ *   lse        device f32 [n_tokens] natural-log lse of x_t inv_T (rl_lmhead_logprob's lse_out)
+ *   scale      device f32 [n_tokens] s_t (rl_policy_loss_from_logp's scale_out; 0 -> G row 0)
+ *   dhidden    device f32 [n_tokens, ld_dhidden] or NULL;  dweight  device f32 [vocab, ld_dweight] or NULL
+ *   flags      RL_F_STATS_ACCUMULATE: dweight += (gradient accumulation over micro-batches)
+ *   workspace  device, 16-B aligned; C = workspace_bytes / (2 * round_up(vocab, 8)) rounded down to a
+ *              multiple of 128 tokens per chunk (>= min(n_tokens, 128)); see
+ *              rl_lmhead_loss_bwd_workspace_size(chunk_tokens, vocab)
+ * Errors: RL_ERR_INVALID_ARGUMENT (sizes, strides, NULL, neither output), RL_ERR_ALIGNMENT,
+ * RL_ERR_WORKSPACE, RL_ERR_UNSUPPORTED (>= 2^31 sizes, not sm_100), RL_ERR_CUDA (tensor map, cuBLAS).
+ * Deterministic (fixed chunk order; cuBLAS without atomics). */
+size_t rl_lmhead_loss_bwd_workspace_size(int64_t chunk_tokens, int64_t vocab);
+rl_status rl_lmhead_loss_bwd(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                             int64_t n_tokens, int64_t d, int64_t vocab, const int32_t* targets, const float* lse,
+                             const float* scale, float inv_temperature, float* dhidden, int64_t ld_dhidden,
+                             float* dweight, int64_t ld_dweight, uint32_t flags, void* workspace,
+                             size_t workspace_bytes, rl_stream stream);
+
 /* ---------------------------------------------------------------- (9) loss from log-probs
  * c4–c7 of SURVEY.md §8(c) (PPO clipped surrogate; with the NEXT 2 terms of
  * rl_loss_params) evaluated from per-token log-probs instead of logits: the loss statistics and

@@ -24,7 +24,8 @@ __all__ = [
     "policy_loss_host_workspace_size", "vocab_parallel_logprob",
     "vocab_parallel_workspace_size", "m2po_mask", "m2po_workspace_size", "delta_encode", "delta_apply",
     "delta_workspace_size", "lmhead_logprob", "lmhead_workspace_size", "policy_loss_from_logp",
-    "policy_loss_from_logp_workspace_size", "Comm", "EXPORTED_SYMBOLS",
+    "policy_loss_from_logp_workspace_size", "lmhead_loss_bwd", "lmhead_loss_bwd_workspace_size", "Comm",
+    "EXPORTED_SYMBOLS",
 ]
 
 F32, BF16 = 0, 1
@@ -88,6 +89,8 @@ _SIGS = {
     "rl_lmhead_logprob": (i32, [vp, i64, vp, i64, i64, i64, i64, vp, f32, vp, vp, vp, sz, vp]),
     "rl_lmhead_workspace_size": (sz, [i64, i64, i64]),
     "rl_policy_loss_from_logp_workspace_size": (sz, [i64]),
+    "rl_lmhead_loss_bwd_workspace_size": (sz, [i64, i64]),
+    "rl_lmhead_loss_bwd": (i32, [vp, i64, vp, i64, i64, i64, i64, vp, vp, vp, f32, vp, i64, vp, i64, u32, vp, sz, vp]),
     "rl_policy_loss_from_logp": (i32, [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
@@ -475,6 +478,32 @@ def lmhead_logprob(hidden, weight, targets, logp_out, lse_out=None, inv_temperat
                                  _dev(workspace, "workspace") if workspace is not None else None,
                                  workspace.numel() * workspace.element_size() if workspace is not None else 0,
                                  _stream(stream)), "rl_lmhead_logprob")
+
+
+def lmhead_loss_bwd_workspace_size(chunk_tokens, vocab):
+    return int(load().rl_lmhead_loss_bwd_workspace_size(int(chunk_tokens), int(vocab)))
+
+
+def lmhead_loss_bwd(hidden, weight, targets, lse, scale, workspace, dhidden=None, dweight=None,
+                    inv_temperature=1.0, accumulate=False, stream=None):
+    """NEXT 4 backward: dhidden = G W, dweight (+)= G^T h with G = s (softmax(h W^T inv_T) - onehot),
+    the logits recomputed on the tensor cores, never stored (G is written per token chunk into
+    ``workspace``).  hidden bf16 [N, d], weight bf16 [V, d]; dhidden / dweight float32 [N, d] / [V, d]."""
+    lib = load()
+    if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
+        raise RLError("hidden [N, d] and weight [V, d] must share d")
+    n, d = hidden.shape
+    V = weight.shape[0]
+    for t, nm, shp in ((dhidden, "dhidden", (n, d)), (dweight, "dweight", (V, d))):
+        if t is not None and (t.dtype.itemsize != 4 or tuple(t.shape) != shp or t.stride(1) != 1):
+            raise RLError(f"{nm} must be float32 {shp} with contiguous rows")
+    _check(lib.rl_lmhead_loss_bwd(
+        _dev(hidden, "hidden"), hidden.stride(0), _dev(weight, "weight"), weight.stride(0), n, d, V,
+        _dev(targets, "targets"), _dev(lse, "lse"), _dev(scale, "scale"), float(inv_temperature),
+        _dev(dhidden, "dhidden"), dhidden.stride(0) if dhidden is not None else d,
+        _dev(dweight, "dweight"), dweight.stride(0) if dweight is not None else d,
+        F_STATS_ACCUMULATE if accumulate else 0, _dev(workspace, "workspace"),
+        workspace.numel() * workspace.element_size(), _stream(stream)), "rl_lmhead_loss_bwd")
 
 
 def policy_loss_from_logp_workspace_size(n_tokens):

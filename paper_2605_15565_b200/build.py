@@ -88,7 +88,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     tmp = LIB + ".tmp"
-    link = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-L", nccl_lib, "-l:libnccl.so.2",
+    link = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-L", nccl_lib, "-l:libnccl.so.2", "-lcublas",
             "-Xlinker", f"-rpath={nccl_lib}"]
     if verbose:
         print(" ".join(link), flush=True)

@@ -16,7 +16,10 @@
 //                      lane), online (max, sum 2^(t - max)) over the row, the target logit picked
 //                      with compile-time indices; after the last tile lse and logp are written
 // The hidden block is re-read from L2 once per vocabulary tile; W streams from HBM / L2.
+#include <cublas_v2.h>
 #include <cuda.h>
+
+#include <mutex>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -37,6 +40,11 @@ struct LmArgs {
   float* logp_out;
   float* lse_out;
   float4* partial;  // [splits][n] (max2, sum, raw target logit, -) when gridDim.x > 1
+  // gradient mode (lmhead_grad_kernel): G = s_t (softmax(x_t) - onehot(y_t)) written as bf16
+  const float* lse;     // [n] natural-log lse of the forward (rl_lmhead_logprob)
+  const float* scale;   // [n] s_t (rl_policy_loss_from_logp)
+  uint16_t* g_out;      // [n, ld_g] bf16 bits
+  int64_t ld_g;
 };
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
@@ -65,6 +73,24 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                    sm100::smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ uint64_t f2pack_lm(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack_lm(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2_lm(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fmul2_lm(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
@@ -87,9 +113,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 constexpr uint32_t kLmIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kLmBN >> 3) << 17) |
                               ((uint32_t)(kLmBM >> 4) << 24);
 
+// GRAD = false: the log-prob epilogue (online max / sum over the row's tiles, rl_lmhead_logprob).
+// GRAD = true:  the gradient epilogue (rl_lmhead_loss_bwd): every logits tile is recomputed and
+//               turned straight into G = s_t (2^(x k - lse2) - [v == y]) in bf16 (one rounding) —
+//               the logits themselves are never written.
+template <bool GRAD>
 __global__ void __launch_bounds__(kLmThreads, 1)
-    lmhead_logprob_kernel(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ CUtensorMap tm_w,
-                          const LmArgs a) {
+    lmhead_kernel(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ CUtensorMap tm_w,
+                  const LmArgs a) {
   extern __shared__ uint8_t lm_smem_raw[];
   __shared__ __align__(8) uint64_t full[kLmStages], empty[kLmStages], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_slot;
@@ -159,6 +190,49 @@ __global__ void __launch_bounds__(kLmThreads, 1)
         }
         umma_commit(&acc_full[acc]);  // accumulator complete
       }
+    }
+  } else if (GRAD) {  // ------------------------------------------------ gradient epilogue 2..5
+    const int q = warp & 3;
+    const int64_t row = m0 + q * 32 + lane;
+    const bool live = row < a.n;
+    const int32_t y = live ? a.targets[row] : -1;
+    const float k = a.inv_t * RL_LOG2E;
+    const float st = live ? a.scale[row] : 0.f;
+    const float nl2 = live ? -a.lse[row] * RL_LOG2E : 0.f;  // -lse in the log2 domain
+    const uint64_t k2 = f2pack_lm(k, k), nl22 = f2pack_lm(nl2, nl2), s2 = f2pack_lm(st, st);
+    uint16_t* grow = a.g_out + (live ? row : 0) * a.ld_g;
+    for (int j = 0; j < ntiles; ++j) {
+      const int acc = j & 1;
+      sm100::mbar_wait(&acc_full[acc], ((uint32_t)j >> 1) & 1u);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < kLmBN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * kLmBN + c * 32), v);
+        const int64_t c0 = (int64_t)(jt0 + j) * kLmBN + c * 32;
+        if (c0 >= a.V) break;  // warp-uniform
+        uint32_t o[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float e0, e1;
+          f2unpack_lm(ffma2_lm(f2pack_lm(v[2 * i], v[2 * i + 1]), k2, nl22), e0, e1);
+          float g0, g1;
+          f2unpack_lm(fmul2_lm(f2pack_lm(exp2f(e0), exp2f(e1)), s2), g0, g1);
+          if (y - c0 == 2 * i) g0 = st * (exp2f(e0) - 1.f);       // target column: s (p_y - 1)
+          if (y - c0 == 2 * i + 1) g1 = st * (exp2f(e1) - 1.f);
+          o[i] = pack_bf16x2(g0, g1);
+        }
+        if (live && c0 + 32 <= a.V) {
+          uint4* dst = reinterpret_cast<uint4*>(grow + c0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = make_uint4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        } else if (live) {
+          for (int i = 0; i < 32 && c0 + i < a.V; ++i) grow[c0 + i] = (uint16_t)(o[i >> 1] >> (16 * (i & 1)));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&acc_empty[acc]);
     }
   } else {  // ---------------------------------------------------------- epilogue warps 2..5
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
@@ -345,15 +419,122 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
   a.inv_t = inv_temperature;
   a.logp_out = logp_out;
   a.lse_out = lse_out;
-  if (cudaFuncSetAttribute(lmhead_logprob_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) !=
+  if (cudaFuncSetAttribute(lmhead_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) !=
       cudaSuccess)
     return check_launch("cudaFuncSetAttribute(lmhead)");
   if ((n_tokens + kLmBM - 1) / kLmBM > 65535) return fail(RL_ERR_UNSUPPORTED, "n_tokens > 65535 * 128 per call");
   const dim3 grid((unsigned)splits, (unsigned)((n_tokens + kLmBM - 1) / kLmBM));
-  lmhead_logprob_kernel<<<grid, kLmThreads, kLmSmem, (cudaStream_t)stream>>>(mh, mw, a);
-  rl_status st = check_launch("lmhead_logprob_kernel");
+  lmhead_kernel<false><<<grid, kLmThreads, kLmSmem, (cudaStream_t)stream>>>(mh, mw, a);
+  rl_status st = check_launch("lmhead_kernel<logprob>");
   if (st != RL_OK || splits == 1) return st;
   const int cb = (int)std::min<int64_t>((n_tokens + 255) / 256, 148 * 4);
   lmhead_combine_kernel<<<cb, 256, 0, (cudaStream_t)stream>>>(a.partial, splits, a);
   return check_launch("lmhead_combine_kernel");
+}
+
+// ------------------------------------------------------------------------------------------------
+// NEXT 4 backward: dh = G W and dW (+)= G^T h with G = s_t (softmax(x_t) - onehot(y_t)), x = (h W^T) inv_T.
+// Per chunk of C tokens: lmhead_kernel<true> recomputes the logits tiles on the tensor cores and
+// writes G (bf16) into the workspace — the logits never exist in memory — then two plain GEMMs
+// consume G (cuBLAS, bf16 x bf16 -> fp32 accumulate): dh_chunk = G W and dW += G^T h_chunk.
+// Why G is materialised per chunk: a CTA that owns a 128-row tile of G would have
+// to hold a 128 x d fp32 dh accumulator (2 MB at d = 4096) and a 256 x d dW one — 8x / 16x the
+// 256 KB of TMEM — so the contraction over V (dh) and over tokens (dW) cannot stay on chip; G in
+// bf16 costs 2 B per element against 4 d flops of GEMM per element (compute-bound by ~1000x).
+namespace rl {
+static cublasHandle_t cublas_handle() {
+  static cublasHandle_t handles[kMaxDevices] = {};
+  static std::mutex mu;
+  const int dev = dev_info().ordinal;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!handles[dev] && cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS) handles[dev] = nullptr;
+  return handles[dev];
+}
+}  // namespace rl
+
+extern "C" size_t rl_lmhead_loss_bwd_workspace_size(int64_t chunk_tokens, int64_t vocab) {
+  if (chunk_tokens <= 0 || vocab <= 0) return 0;
+  const int64_t ldg = (vocab + 7) / 8 * 8;
+  return (size_t)chunk_tokens * (size_t)ldg * 2;
+}
+
+extern "C" rl_status rl_lmhead_loss_bwd(const void* hidden, int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                                        int64_t n_tokens, int64_t d, int64_t vocab, const int32_t* targets,
+                                        const float* lse, const float* scale, float inv_temperature,
+                                        float* dhidden, int64_t ld_dhidden, float* dweight, int64_t ld_dweight,
+                                        uint32_t flags, void* workspace, size_t workspace_bytes, rl_stream stream) {
+  using namespace rl;
+  if (n_tokens < 0 || d < 1 || vocab < 1) return fail(RL_ERR_INVALID_ARGUMENT, "need n_tokens >= 0, d >= 1, vocab >= 1");
+  if (ld_hidden < d || ld_weight < d || (dhidden && ld_dhidden < d) || (dweight && ld_dweight < d))
+    return fail(RL_ERR_INVALID_ARGUMENT, "a row stride is < d");
+  if (n_tokens >= ((int64_t)1 << 31) || vocab >= ((int64_t)1 << 31) || d >= ((int64_t)1 << 31))
+    return fail(RL_ERR_UNSUPPORTED, "n_tokens, d and vocab must be < 2^31");
+  if (!(inv_temperature > 0.f) || !isfinite(inv_temperature))
+    return fail(RL_ERR_INVALID_ARGUMENT, "inv_temperature must be finite and > 0");
+  if (!dhidden && !dweight) return fail(RL_ERR_INVALID_ARGUMENT, "neither dhidden nor dweight requested");
+  if (!hidden || !weight) return fail(RL_ERR_INVALID_ARGUMENT, "NULL hidden/weight");
+  if (((uintptr_t)hidden & 15) || ((uintptr_t)weight & 15) || (ld_hidden % 8) || (ld_weight % 8))
+    return fail(RL_ERR_ALIGNMENT, "hidden / weight must be 16-B aligned with ld % 8 == 0");
+  const int64_t ldg = (vocab + 7) / 8 * 8;
+  const int64_t chunk = workspace ? (int64_t)(workspace_bytes / ((size_t)ldg * 2)) / kLmBM * kLmBM : 0;
+  if (n_tokens > 0 && chunk < std::min<int64_t>(n_tokens, kLmBM))
+    return fail(RL_ERR_WORKSPACE, "workspace must hold >= 128 (or n_tokens) G rows: >= %zu bytes",
+                rl_lmhead_loss_bwd_workspace_size(std::min<int64_t>(n_tokens, kLmBM), vocab));
+  if (((uintptr_t)workspace & 15)) return fail(RL_ERR_ALIGNMENT, "workspace must be 16-B aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool acc_w = (flags & RL_F_STATS_ACCUMULATE) != 0;  // dW += (else dW =)
+  if (n_tokens == 0) {
+    if (dweight && !acc_w && cudaMemset2DAsync(dweight, (size_t)ld_dweight * 4, 0, (size_t)d * 4, (size_t)vocab, s) !=
+                                 cudaSuccess)
+      return check_launch("memset dweight");
+    return RL_OK;
+  }
+  if (!targets || !lse || !scale) return fail(RL_ERR_INVALID_ARGUMENT, "NULL targets/lse/scale");
+  if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
+  cublasHandle_t h = cublas_handle();
+  if (!h) return fail(RL_ERR_CUDA, "cublasCreate failed");
+  if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return fail(RL_ERR_CUDA, "cublasSetStream failed");
+  if (cudaFuncSetAttribute(lmhead_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) != cudaSuccess)
+    return check_launch("cudaFuncSetAttribute(lmhead grad)");
+  CUtensorMap mw;
+  if (!make_map(&mw, weight, vocab, d, ld_weight, kLmBN)) return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  uint16_t* G = (uint16_t*)workspace;
+  const float one = 1.f, zero = 0.f;
+  for (int64_t t0 = 0; t0 < n_tokens; t0 += chunk) {
+    const int64_t C = std::min(chunk, n_tokens - t0);
+    const void* h0 = (const char*)hidden + (size_t)t0 * ld_hidden * 2;
+    CUtensorMap mh;
+    if (!make_map(&mh, h0, C, d, ld_hidden, kLmBM)) return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    LmArgs a{};
+    a.targets = targets + t0;
+    a.n = C;
+    a.V = vocab;
+    a.kblocks = (int32_t)((d + kLmBK - 1) / kLmBK);
+    a.vtiles = (int32_t)((vocab + kLmBN - 1) / kLmBN);
+    int splits = lm_splits(C, d, vocab, lm_sms());
+    a.tiles_per_split = (a.vtiles + splits - 1) / splits;
+    splits = (a.vtiles + a.tiles_per_split - 1) / a.tiles_per_split;
+    a.inv_t = inv_temperature;
+    a.lse = lse + t0;
+    a.scale = scale + t0;
+    a.g_out = G;
+    a.ld_g = ldg;
+    const dim3 grid((unsigned)splits, (unsigned)((C + kLmBM - 1) / kLmBM));
+    lmhead_kernel<true><<<grid, kLmThreads, kLmSmem, s>>>(mh, mw, a);
+    if (rl_status st = check_launch("lmhead_kernel<grad>"); st != RL_OK) return st;
+    // row-major operands as column-major GEMMs: dh^T [d x C] = W^T [d x V] . G^T [V x C]
+    if (dhidden &&
+        cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)d, (int)C, (int)vocab, &one, weight, CUDA_R_16BF, (int)ld_weight,
+                     G, CUDA_R_16BF, (int)ldg, &zero, dhidden + (size_t)t0 * ld_dhidden, CUDA_R_32F, (int)ld_dhidden,
+                     CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+      return fail(RL_ERR_CUDA, "cublasGemmEx (dh = G W) failed");
+    // dW^T [d x V] (+)= h^T [d x C] . G [C x V]
+    const float* beta = (acc_w || t0 > 0) ? &one : &zero;
+    if (dweight &&
+        cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)d, (int)vocab, (int)C, &one, h0, CUDA_R_16BF, (int)ld_hidden,
+                     G, CUDA_R_16BF, (int)ldg, beta, dweight, CUDA_R_32F, (int)ld_dweight, CUBLAS_COMPUTE_32F,
+                     CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+      return fail(RL_ERR_CUDA, "cublasGemmEx (dW += G^T h) failed");
+  }
+  return check_launch("rl_lmhead_loss_bwd");
 }

@@ -852,3 +852,74 @@ def test_lmhead_loss_forward(cuda_lib):
     ok = ~band
     assert np.all(np.abs(sc[ok] - ref["scale"][ok]) <= 1e-3 * np.abs(ref["scale"][ok]) + 1e-12)
     assert np.all(sc[ref["valid"] == 0] == 0.0)
+
+
+# ----------------------------------------------------------------------------- NEXT 4 backward
+def _lm_bwd_check(cuda_lib, N, d, V, seed, chunk=None, ld_h=None, ld_w=None, inv_t=1.0, vrows=None):
+    """rl_lmhead_loss_bwd against oracle.lmhead_loss_backward.  Tolerance: G is
+    one bf16 rounding of s (p - onehot) (relative u = 2^-8) and the GEMMs accumulate in fp32, so
+    |d dh| <= 2^-7 ||G_t||_1 max_v |W_vj| and |d dW[v]| <= 2^-7 (|G[:, v]|^T |h|) (+ 1e-7 abs)."""
+    t = torch()
+    hb, wb, ht, wt, y = _lm_inputs(N, d, V, seed=seed, ld_h=ld_h, ld_w=ld_w)
+    y = y.copy()
+    y[3] = -100                              # ignored target: zero G row
+    rng = np.random.default_rng(seed + 1)
+    s = rng.normal(size=N).astype(np.float32)
+    s[5] = 0.0                               # s_t = 0 (masked / clipped token): zero G row
+    lse = t.empty(N, dtype=t.float32, device="cuda")
+    logp = t.empty(N, dtype=t.float32, device="cuda")
+    cuda_lib.lmhead_logprob(ht, wt, dev(y), logp, lse_out=lse, inv_temperature=inv_t, workspace=_lm_ws(N, d, V))
+    C = chunk or N
+    ws = t.empty(cuda_lib.lmhead_loss_bwd_workspace_size(C, V), dtype=t.uint8, device="cuda")
+    dh = t.full((N, d), float("nan"), dtype=t.float32, device="cuda")
+    dW = t.full((V, d), float("nan"), dtype=t.float32, device="cuda")
+    cuda_lib.lmhead_loss_bwd(ht, wt, dev(y), lse, dev(s), ws, dhidden=dh, dweight=dW, inv_temperature=inv_t)
+    t.cuda.synchronize()
+    hbd, wbd = hb, wb
+    dh_ref, dW_ref, G = oracle.lmhead_loss_backward(hbd, wbd, y, s.astype(np.float64), inv_t)
+    W64, H64 = oracle.decode_bf16(wbd), oracle.decode_bf16(hbd)
+    u2 = 2.0 ** -7
+    tol_dh = u2 * np.abs(G).sum(axis=1)[:, None] * np.abs(W64).max(axis=0)[None, :] + 1e-7
+    g_dh = dh.cpu().numpy()
+    assert np.all(np.abs(g_dh - dh_ref) <= tol_dh), np.max(np.abs(g_dh - dh_ref) / tol_dh)
+    assert np.all(g_dh[3] == 0) and np.all(g_dh[5] == 0) and np.all(g_dh[2] == 0)   # y < 0, s = 0, y >= V
+    rows = np.arange(V) if vrows is None else vrows
+    g_dW = dW[t.from_numpy(rows).cuda()].cpu().numpy()
+    tol_dW = u2 * (np.abs(G[:, rows]).T @ np.abs(H64)) + 1e-7
+    assert np.all(np.abs(g_dW - dW_ref[rows]) <= tol_dW), np.max(np.abs(g_dW - dW_ref[rows]) / tol_dW)
+    return ht, wt, y, lse, s, dW, ws
+
+
+@pytest.mark.parametrize("N,d,V,chunk,ld_h,ld_w,inv_t", [
+    (300, 192, 1000, None, None, None, 1.0),     # ragged token block (300 = 2 x 128 + 44), V % 256 != 0
+    (300, 192, 1003, 128, 200, 208, 0.7),        # 3 chunks, padded strides, V % 32 != 0, temperature
+    (128, 64, 8, None, None, None, 1.0),         # one vocabulary tile narrower than 32 columns
+])
+def test_lmhead_loss_bwd(cuda_lib, N, d, V, chunk, ld_h, ld_w, inv_t):
+    _lm_bwd_check(cuda_lib, N, d, V, seed=N + V, chunk=chunk, ld_h=ld_h, ld_w=ld_w, inv_t=inv_t)
+
+
+def test_lmhead_loss_bwd_accumulate_and_errors(cuda_lib):
+    """RL_F_STATS_ACCUMULATE adds into dweight (two micro-batches = their sum); bad arguments are
+    rejected before enqueue."""
+    t = torch()
+    N, d, V = 256, 128, 700
+    ht, wt, y, lse, s, dW, ws = _lm_bwd_check(cuda_lib, N, d, V, seed=9)
+    acc = dW.clone()
+    cuda_lib.lmhead_loss_bwd(ht, wt, dev(y), lse, dev(s), ws, dweight=acc, accumulate=True)
+    t.cuda.synchronize()
+    assert t.allclose(acc, 2 * dW, rtol=1e-6, atol=1e-7)
+    with pytest.raises(cuda_lib.RLError):     # workspace below one 128-token chunk
+        cuda_lib.lmhead_loss_bwd(ht, wt, dev(y), lse, dev(s), ws[:1000], dweight=acc)
+    with pytest.raises(cuda_lib.RLError):     # no output requested
+        cuda_lib.lmhead_loss_bwd(ht, wt, dev(y), lse, dev(s), ws)
+
+
+@pytest.mark.slow
+def test_lmhead_loss_bwd_full_size(cuda_lib):
+    """d = 4096, V = 151936 (the policy's LM head), 256 tokens (two token blocks, 594 vocabulary
+    tiles): dh of every token and dW on 2,048 sampled vocabulary rows plus every target row."""
+    N, d, V = 256, 4096, 151936
+    rng = np.random.default_rng(77)
+    vrows = np.unique(np.concatenate([rng.choice(V, size=2048, replace=False), (7 * np.arange(64)) % V]))
+    _lm_bwd_check(cuda_lib, N, d, V, seed=77, vrows=vrows)
