@@ -1,6 +1,6 @@
 """Fused LM-head log-prob throughput (development tool, NEXT 4): rl_lmhead_logprob on N tokens of
 a d = 4096, V = 151936 bf16 head (Qwen3-8B sized), TFLOP/s of the GEMM it contains (2 N V d).
-    python tools/lmbench.py [--rows 16384] [--reps 5]"""
+    python tools/lmbench.py [--rows 16384] [--reps 5] [--bwd [--chunk C]]"""
 import os
 import sys
 
@@ -47,6 +47,26 @@ def main():
     print(f"lmhead N={N} d={d} V={V}: min {min(ts):.3f} ms avg {sum(ts)/len(ts):.3f} ms "
           f"{fl / min(ts) / 1e9:.1f} TFLOP/s; cuBLAS h[:2048] @ W^T: {tc:.3f} ms "
           f"{2.0 * 2048 * V * d / tc / 1e9:.1f} TFLOP/s")
+    if "--bwd" in sys.argv:  # NEXT 4 backward: G recompute (2NVd) + dh (2NVd) + dW (2NVd)
+        C = int(sys.argv[sys.argv.index("--chunk") + 1]) if "--chunk" in sys.argv else min(N, 8192)
+        s = torch.randn(N, device="cuda", generator=g) * 1e-4
+        wsb = torch.empty(rl.lmhead_loss_bwd_workspace_size(C, V), dtype=torch.uint8, device="cuda")
+        dh = torch.empty(N, d, device="cuda")
+        dW = torch.empty(V, d, device="cuda")
+        bwd = lambda: rl.lmhead_loss_bwd(h, w, y, lse, s, wsb, dhidden=dh, dweight=dW)
+        bwd()
+        torch.cuda.synchronize()
+        tb = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            bwd()
+            b.record()
+            torch.cuda.synchronize()
+            tb.append(a.elapsed_time(b))
+        flb = 6.0 * N * V * d
+        print(f"lmhead bwd N={N} chunk={C}: min {min(tb):.3f} ms avg {sum(tb)/len(tb):.3f} ms "
+              f"{flb / min(tb) / 1e9:.1f} TFLOP/s (6 N V d)")
 
 
 if __name__ == "__main__":
