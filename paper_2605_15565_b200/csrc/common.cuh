@@ -37,7 +37,8 @@ enum DevOpt {
   OPT_LOSS_KERNEL = 0,  // 0 = single-visit cluster kernel (default), 1 = exact two-pass kernel
   OPT_VP_PATH = 1,      // fused vocab-parallel loss: 0 = in-kernel peer exchange when enabled, 1 = NCCL path
   OPT_LM_SPLITS = 2,    // LM-head vocabulary split override (0 = cost model)
-  OPT_COUNT = 3
+  OPT_VP_KERNEL = 3,    // peer-exchange vocab-parallel kernel: 0 = register cache when it fits, 1 = L2 ring
+  OPT_COUNT = 4
 };
 int dev_option(int key);
 

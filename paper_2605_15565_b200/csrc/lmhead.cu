@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
     const bool live = row < a.n;
     const int32_t y = live ? a.targets[row] : -1;
     const float k = a.inv_t * RL_LOG2E;
-    const float st = live ? a.scale[row] : 0.f;
+    const float st = (live && y >= 0 && y < a.V) ? a.scale[row] : 0.f;  // y outside [0, V): G row 0
     const float nl2 = live ? -a.lse[row] * RL_LOG2E : 0.f;  // -lse in the log2 domain
     const uint64_t k2 = f2pack_lm(k, k), nl22 = f2pack_lm(nl2, nl2), s2 = f2pack_lm(st, st);
     uint16_t* grow = a.g_out + (live ? row : 0) * a.ld_g;

@@ -663,6 +663,315 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Fused vocab-parallel loss, register-cache form: vp_cache_kernel<NV, R> (the default for bf16
+// shards of <= 4800 16-B vectors, i.e. the P >= 4 shard widths of V = 151936).
+//
+// One HBM read and one exp2 per element: a CTA walks its rows; each consumer thread holds NV
+// vectors (vector t + 480 i) of a row slice in registers, converted in place into
+//     e'_v = 2^(x_v k - m_w)          m_w = the max of x k over the thread's WARP (no CTA barrier)
+// and keeps them (bf16) for R rows while the row statistics travel: warp partials
+// (m_w, S_w = sum e') -> publisher lane combines the 15 warps into c2_r = lse2 of the shard and
+// sends (c2_r, z_y) to every rank (LL words, as vp_ring_kernel) -> the collector warp polls the P
+// records of the row, combines them in rank order (identical on every rank), runs the token
+// epilogue and publishes (s_t, c2, dy, target column).  R - 1 rows after a row was loaded its
+// gradient is written from the cache:  dlogits_v = e'_v q_w,  q_w = s_t 2^(m_w - c2)  (q split
+// into bf16 hi + lo, HMUL2 + HFMA2: one rounding in the product, reading R2), target column
+// dy = s_t (p_y - 1).  So the exchange latency hides behind R - 1 rows of streaming.
+//   warps 0..14   consumers
+//   warp 15       lane 0 TMA producer (ring of 30 KB slots), lane 1 publisher, lanes 8..15 collector
+//                 (lane 8 + q polls rank q's record; lane 8 runs the epilogue and statistics).
+// 16 warps = 4 per SM sub-partition, so each thread may use 128 registers (the NV = 10 cache is 80).
+constexpr int kVcThreads = 512;
+constexpr int kVcColl = 8;  // first collector lane
+constexpr int kVcStat = 32, kVcScale = 32;
+
+struct VcShared {
+  uint64_t stats_full[kVcStat], stats_free[kVcStat];
+  uint64_t scale_full[kVcScale], scale_free[kVcScale];
+  float2 red[kVcStat][15];
+  float zyv[kVcStat];
+  float4 sc[kVcScale];  // (s, c2, dy, target column or -1)
+};
+
+template <int NV, int R>
+__global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a) {
+  using V = ClVec<bf16_t>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  VcShared& sh = *reinterpret_cast<VcShared*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + sizeof(VcShared));
+  uint64_t* empty = full + a.nslots;
+  unsigned char* ring = smem + ((sizeof(VcShared) + 16 * (size_t)a.nslots + 127) & ~(size_t)127);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t nk = blockIdx.x < a.n ? (a.n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t row_bytes = a.ld * 2;
+  const int nvec = (int)(a.Vr / 8);
+  const int nch = (nvec + kVrChunkVec - 1) / kVrChunkVec;
+  const float k = a.kn.inv_t * RL_LOG2E;
+  auto row_of = [&](int64_t kk) { return (int64_t)blockIdx.x + kk * gridDim.x; };
+  if (tid == 0) {
+    for (int i = 0; i < a.nslots; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], 15);
+    }
+    for (int i = 0; i < kVcStat; ++i) {
+      sm100::mbar_init(&sh.stats_full[i], 15);
+      sm100::mbar_init(&sh.stats_free[i], 1);
+      sh.zyv[i] = 0.f;
+    }
+    for (int i = 0; i < kVcScale; ++i) {
+      sm100::mbar_init(&sh.scale_full[i], 1);
+      sm100::mbar_init(&sh.scale_free[i], 15);
+    }
+    sm100::fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t full_s = sm100::smem_u32(full), empty_s = sm100::smem_u32(empty);
+  const uint32_t ring_s = sm100::smem_u32(ring);
+
+  if (warp == 15) {
+    if (lane == 0) {  // -------------------------------------------------------- TMA producer
+      RingPos rp{0, 0};
+      for (int64_t kk = 0; kk < nk; ++kk) {
+        const char* src = reinterpret_cast<const char*>(a.logits) + row_of(kk) * row_bytes;
+        for (int c = 0; c < nch; ++c) {
+          sm100::mbar_wait_a(empty_s + rp.slot * 8, rp.phase ^ 1);
+          const uint32_t bytes = (uint32_t)min(kVrChunkVec, nvec - c * kVrChunkVec) * 16u;
+          sm100::mbar_arrive_expect_tx(&full[rp.slot], bytes);
+          sm100::bulk_g2s_nohint(ring + (size_t)rp.slot * kVrSlot, src + (size_t)c * kVrSlot, bytes, &full[rp.slot]);
+          rp.advance(1, a.nslots);
+        }
+      }
+    } else if (lane == 1) {  // --------------------------------------------------- publisher
+      const unsigned long long ep = (unsigned long long)a.epoch << 32;
+      for (int64_t kk = 0; kk < nk; ++kk) {
+        const int ss = (int)(kk % kVcStat);
+        sm100::mbar_wait_polite(&sh.stats_full[ss], (uint32_t)((kk / kVcStat) & 1), false);
+        float M = -INFINITY;
+        for (int w = 0; w < 15; ++w) M = fmaxf(M, sh.red[ss][w].x);
+        float S = 0.f;
+        for (int w = 0; w < 15; ++w) {
+          const float2 r = sh.red[ss][w];
+          if (r.x != -INFINITY) S += r.y * fast_exp2(r.x - M);
+        }
+        const float zy = sh.zyv[ss];
+        sh.zyv[ss] = 0.f;
+        sm100::mbar_arrive(&sh.stats_free[ss]);
+        const float c2 = S > 0.f ? M + fast_log2(S) : -INFINITY;
+        const int64_t row = row_of(kk);
+        for (int q = 0; q < a.P; ++q)
+          st_ll2(a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2, ep | __float_as_uint(c2), ep | __float_as_uint(zy));
+      }
+    } else if (lane >= kVcColl && lane < kVcColl + 8) {  // ------------------------- collector
+      const int cl = lane - kVcColl;  // this lane polls rank cl's records
+      constexpr unsigned kMask = 0xffu << kVcColl;
+    const double inv_tm = token_mean_inv(a.kn);
+    Acc acc;
+    acc.zero();
+    // row kk + 1's level-1 metadata is loaded while row kk is combined (lane 0)
+    int32_t ny = 0, nseq = 0;
+    uint8_t nmask = 1;
+    float nold = 0.f, nprox = 0.f, nref = 0.f;
+    auto load_l1 = [&](int64_t kk) {
+      if (cl == 0 && kk < nk) {
+        const int64_t row = row_of(kk);
+        ny = a.targets[row];
+        nseq = a.token_seq ? a.token_seq[row] : 0;
+        nmask = a.mask ? a.mask[row] : 1;
+        nold = a.old_logp[row];
+        token_extra(a.kn, row, nold, nprox, nref);
+      }
+    };
+    load_l1(0);
+    for (int64_t kk = 0; kk < nk; ++kk) {
+      const int64_t row = row_of(kk);
+      const int32_t y = ny, seq = nseq;
+      const uint8_t mk = nmask;
+      const float old = nold, prox = nprox, ref = nref;
+      int32_t ver = 0, act = 0;
+      float A = 0.f;
+      if (cl == 0) {
+        if (a.seq_version) ver = a.seq_version[seq];
+        if (mk != 0 && y >= 0 && (int64_t)y < a.Vtot) {
+          A = a.seq_adv[seq];
+          if (a.seq_active) act = a.seq_active[seq];
+        }
+      }
+      float c2q = -INFINITY, zyq = 0.f;
+      if (cl < a.P) {
+        const unsigned long long* slot = a.xr[a.me] + ((int64_t)cl * a.max_tokens + row) * 2;
+        unsigned long long w0, w1;
+        const unsigned long long t0 = globaltimer();
+        for (int it = 0;; ++it) {
+          ld_ll2(slot, w0, w1);
+          if ((w0 >> 32) == a.epoch && (w1 >> 32) == a.epoch) break;
+          __nanosleep(32);  // shares its warp with the producer and publisher lanes
+          if ((it & 1023) == 1023 && globaltimer() - t0 > (unsigned long long)kVrTimeoutNs) {
+            printf("rl_vocab_parallel_logprob: rank %d waited > %lld s for rank %d's record of row %lld "
+                   "(epoch %u); a peer is not running the matching call\n",
+                   a.me, kVrTimeoutNs / 1000000000LL, cl, (long long)row, a.epoch);
+            __trap();
+          }
+        }
+        c2q = __uint_as_float((uint32_t)w0);
+        zyq = __uint_as_float((uint32_t)w1);
+      }
+      load_l1(kk + 1);
+      float M = -INFINITY;
+      for (int q = 0; q < a.P; ++q) M = fmaxf(M, __shfl_sync(kMask, c2q, kVcColl + q));
+      float S = 0.f, zy = 0.f;
+      for (int q = 0; q < a.P; ++q) {
+        const float cq = __shfl_sync(kMask, c2q, kVcColl + q);
+        const float zq = __shfl_sync(kMask, zyq, kVcColl + q);
+        if (cq != -INFINITY) S += fast_exp2(cq - M);
+        zy += zq;
+      }
+      if (cl == 0) {
+        const float c2 = M + fast_log2(S);
+        RowMeta mt;
+        mt.y = y;
+        mt.seq = a.token_seq ? seq : 0;
+        mt.in_range = y >= 0 && (int64_t)y < a.Vtot;
+        mt.bad = (int64_t)y >= a.Vtot;
+        const int32_t stale = a.seq_version ? a.kn.trainer_version - ver : 0;
+        mt.neg_stale = stale < 0;
+        mt.stale_drop = !mt.neg_stale && a.kn.max_staleness >= 0 && stale > a.kn.max_staleness;
+        const bool m_on = mk != 0;
+        mt.valid = m_on && mt.in_range && !mt.neg_stale && !mt.stale_drop;
+        mt.stale_drop = mt.stale_drop && m_on && mt.in_range;
+        const float lp = logp_from(mt, zy, c2);
+        if (a.logp_out) a.logp_out[row] = lp;
+        if (a.lse_out) a.lse_out[row] = c2 * RL_LN2;
+        Acc tmp;
+        tmp.zero();
+        const int32_t Li = (mt.valid && a.kn.agg == RL_AGG_SEQ_MEAN_TOKEN_MEAN) ? act : 0;
+        const float st = token_epilogue_li(mt, lp, mt.valid ? old : 0.f, mt.valid ? A : 0.f, Li, inv_tm, a.kn,
+                                           tmp, nullptr, prox, ref);
+        if (a.count_stats)
+          for (int i = 0; i < RL_LOSS_STATS_N; ++i) acc.v[i] += tmp.v[i];
+        const int64_t yl = (int64_t)y - a.off;
+        const int ycol = (mt.in_range && yl >= 0 && yl < a.Vr) ? (int)yl : -1;
+        const float dy = st * (fast_exp2(zy * RL_LOG2E - c2) - 1.f);
+        const int sl = (int)(kk % kVcScale);
+        if (kk >= kVcScale) sm100::mbar_wait_polite(&sh.scale_free[sl], (uint32_t)(((kk / kVcScale) - 1) & 1), false);
+        sh.sc[sl] = make_float4(st, c2, dy, __int_as_float(ycol));
+        sm100::mbar_arrive(&sh.scale_full[sl]);
+      }
+    }
+    if (cl == 0)
+      for (int i = 0; i < RL_LOSS_STATS_N; ++i) a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = acc.v[i];
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------------------ consumers
+  uint4 cache[R][NV];
+  float mw[R];
+  const uint32_t my_off = (uint32_t)tid * 16u;
+  const uint64_t k2 = f2pack(k, k);
+  uint32_t slot = 0, rph = 0;
+  int32_t y_next = nk > 0 ? a.targets[row_of(0)] : 0;
+  // load row kk into cache[r] (raw bf16), then convert in place to e' (bf16) and post the warp record
+  auto load_row = [&](auto rc, int64_t kk) {
+    constexpr int r = decltype(rc)::value;
+    const int32_t y = y_next;
+    if (kk + 1 < nk) y_next = a.targets[row_of(kk + 1)];
+    const int64_t yl = (int64_t)y - a.off;
+    const int yv = (y >= 0 && yl >= 0 && yl < a.Vr) ? (int)(yl >> 3) : -1;  // target's vector
+    typename V::MaxT mx = V::max_init();
+#pragma unroll
+    for (int c = 0; c < (NV + 3) / 4; ++c) {
+      if (c < nch) {
+        sm100::mbar_wait_a(full_s + slot * 8, rph);
+        const uint32_t sb = ring_s + slot * (uint32_t)kVrSlot;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = 4 * c + u;
+          if (i < NV) {
+            const bool ok = i * kVrCons + tid < nvec;
+            cache[r][i] = ok ? sm100::lds128_a(sb + u * (kVrCons * 16) + my_off) : V::neg_inf_vec();
+            V::max_acc(cache[r][i], mx);
+          }
+        }
+        sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+        if (++slot == (uint32_t)a.nslots) {
+          slot = 0;
+          rph ^= 1u;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (4 * c + u < NV) cache[r][4 * c + u] = V::neg_inf_vec();
+      }
+    }
+    // z_y from the raw vector that holds it (its owner thread; compile-time vector index)
+    float zy = 0.f;
+    bool own = false;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (yv == i * kVrCons + tid) {
+        const uint4 v = cache[r][i];
+        const int e = (int)(yl & 7);
+        const uint32_t wd = e < 2 ? v.x : e < 4 ? v.y : e < 6 ? v.z : v.w;
+        zy = (e & 1) ? bf16_hi(wd) : bf16_lo(wd);
+        own = true;
+      }
+    }
+    const float m = warp_max(V::max_to_float(mx)) * k;
+    mw[r] = m;
+    float s = 0.f;
+    if (m != -INFINITY) {
+      const uint64_t mn2 = f2pack(-m, -m);
+      uint64_t acc2 = f2pack(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc2 = V::exp_sv(cache[r][i], k2, mn2, acc2, cache[r][i]);
+      float lo, hi;
+      f2unpack(acc2, lo, hi);
+      s = lo + hi;
+    }
+    s = warp_sum(s);
+    const int ss = (int)(kk % kVcStat);
+    if (kk >= kVcStat) sm100::mbar_wait(&sh.stats_free[ss], (uint32_t)(((kk / kVcStat) - 1) & 1));
+    if (own) sh.zyv[ss] = zy * a.kn.inv_t;
+    __syncwarp();
+    if (lane == 0) {
+      sh.red[ss][warp] = make_float2(m, s);
+      sm100::mbar_arrive(&sh.stats_full[ss]);
+    }
+  };
+  // dlogits of row kk from cache[r]
+  auto grad_row = [&](auto rc, int64_t kk) {
+    constexpr int r = decltype(rc)::value;
+    const int64_t row = row_of(kk);
+    const int sl = (int)(kk % kVcScale);
+    sm100::mbar_wait(&sh.scale_full[sl], (uint32_t)((kk / kVcScale) & 1));
+    const float4 sc = sh.sc[sl];
+    const float st = sc.x, c2 = sc.y, dy = sc.z;
+    const int ycol = __float_as_int(sc.w);
+    const float q = st == 0.f ? 0.f : st * fast_exp2(mw[r] - c2);
+    const uint32_t qb2 = pack_bf16x2(q, q);
+    const float qh = __uint_as_float(qb2 << 16);
+    const uint32_t ql2 = pack_bf16x2(q - qh, q - qh);
+    uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.dlogits) + row * row_bytes) + tid;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      st_stream_v4_if(out + i * kVrCons, V::grad_sv(cache[r][i], qb2, ql2, q), i * kVrCons + tid < nvec);
+    if (st != 0.f && ycol >= 0 && ((ycol >> 3) % kVrCons) == tid)  // same thread, after its vector store
+      VecTraits<bf16_t>::store1(reinterpret_cast<char*>(a.dlogits) + row * row_bytes, ycol, dy);
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(&sh.scale_free[sl]);
+  };
+  for (int64_t p0 = 0; p0 < nk + R - 1; p0 += R) {
+    static_for<0, R>([&](auto rc) {
+      constexpr int r = decltype(rc)::value;
+      const int64_t p = p0 + r;
+      if (p < nk) load_row(rc, p);
+      const int64_t g = p - (R - 1);
+      if (g >= 0 && g < nk) grad_row(std::integral_constant<int, (r + 1) % R>{}, g);
+    });
+  }
+}
+
 // L2 window of the ring kernel: D rows per CTA between a slice's two reads; G rows per service
 // group, published LG groups before they are combined.  D >= (LG + 1) G - 1 is required (the
 // service combines group g - LG only after the consumers finished pass 1 of group g); the
@@ -771,6 +1080,21 @@ extern "C" rl_status rl_vocab_parallel_logprob(
     const size_t par = (size_t)(epoch & 1) * P * max_tok * 2;  // u64 words
     for (int q = 0; q < 8; ++q) v.xr[q] = q < P ? reinterpret_cast<unsigned long long*>(peers[q]) + par : nullptr;
     const int grid = (int)std::min<int64_t>(n_tokens, std::min(dev_info().sms, kMaxStatCtas));
+    // bf16 shards of <= 4800 whole vectors: the register-cache kernel (one read, one exp2 per
+    // element); anything else: the L2 re-read ring kernel (same exchange protocol)
+    const int64_t nv = vocab_shard / 8;
+    if (dtype == RL_BF16 && vocab_shard % 8 == 0 && nv >= 1 && nv <= 10 * kVrCons && dev_option(OPT_VP_KERNEL) != 1) {
+      const size_t head = (sizeof(VcShared) + 127) & ~(size_t)127;
+      v.nslots = (int)((kSmemMax - head - 256) / (kVrSlot + 16));
+      const size_t smem = ((sizeof(VcShared) + 16 * (size_t)v.nslots + 127) & ~(size_t)127) + (size_t)v.nslots * kVrSlot;
+      auto kern = nv <= 5 * kVrCons ? vp_cache_kernel<5, 3> : vp_cache_kernel<10, 2>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return check_launch("cudaFuncSetAttribute(vp_cache_kernel)");
+      kern<<<grid, kVcThreads, smem, s>>>(v);
+      rl_status stc = check_launch("vp_cache_kernel");
+      if (stc != RL_OK) return stc;
+      return launch_stats_reduce(partials, grid, stats, accumulate, s);
+    }
     const int64_t slice_bytes = (vocab_shard / (16 / eb)) * 16;
     vr_geometry(P, std::max<int64_t>(slice_bytes, 16), grid, &v.G, &v.LG, &v.D);
     const size_t head = (sizeof(VrShared) + 127) & ~(size_t)127;
