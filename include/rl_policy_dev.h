@@ -11,6 +11,8 @@
  *                         rl_comm_enable_peer_exchange succeeded (default), 1 = NCCL path
  *   2 RL_DEV_LM_SPLITS    rl_lmhead_logprob vocabulary splits: 0 = cost model (default), else
  *                         the split count (clamped to what the workspace holds)
+ *   3 RL_DEV_VP_KERNEL    peer-exchange vocab-parallel kernel: 0 = register-cache kernel when the
+ *                         shard fits it (default), 1 = the L2 re-read ring kernel
  * Options are read at launch time; set them before the calls they should affect.
  */
 #ifndef RL_POLICY_DEV_H_
@@ -22,6 +24,7 @@ extern "C" {
 #define RL_DEV_LOSS_KERNEL 0
 #define RL_DEV_VP_PATH 1
 #define RL_DEV_LM_SPLITS 2
+#define RL_DEV_VP_KERNEL 3
 int32_t rl_dev_set_option(int32_t key, int32_t value);
 #ifdef __cplusplus
 }

@@ -307,7 +307,7 @@ R2_ABS = 2.0 ** -16
 
 # ------------------------------------------------------------------------------- C4 vocab-parallel
 @pytest.mark.parametrize("W", [18992, 37984, 151936])
-@pytest.mark.parametrize("path", ["nccl", "peer"])
+@pytest.mark.parametrize("path", ["nccl", "peer", "peer_ring"])
 def test_vocab_parallel_production_widths(cuda_lib, W, path):
     """rl_vocab_parallel_logprob at P = 1 with the per-rank column width of P = 8 (18,992), P = 4
     (37,984) and the whole vocabulary: the kernels' multi-chunk slice geometry of configs[3], on the
@@ -345,8 +345,9 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
                       global_active_tokens=n_act)
     comm = rl.Comm.local()
     try:
-        if path == "peer":
+        if path.startswith("peer"):
             assert comm.enable_peer_exchange(N)
+            rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 0)
         else:
             rl.dev_set_option(rl.DEV_VP_PATH, 1)
         dl = t.empty_like(x)
@@ -362,6 +363,7 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
         t.cuda.synchronize()
     finally:
         rl.dev_set_option(rl.DEV_VP_PATH, 0)
+        rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
         comm.destroy()
     g_lp = logp.cpu().numpy()
     assert np.all(np.abs(g_lp - lp_all) <= LOGP_ATOL), np.abs(g_lp - lp_all).max()

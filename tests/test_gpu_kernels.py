@@ -15,6 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("opts,select", [
     ("0=1", "tiny or ragged or knobs or unit_scale or masked or extreme or sum_to_zero or objective"),  # two-pass loss
     ("1=1", "vocab_parallel"),  # NCCL vocab-parallel path
+    ("3=1", "vocab_parallel"),  # L2 re-read ring kernel instead of the register-cache kernel
 ])
 def test_alternate_kernels(opts, select):
     env = dict(os.environ, RL_TEST_DEV_OPTS=opts)

@@ -31,8 +31,10 @@ def main():
     stats = torch.zeros(12, dtype=torch.float64, device="cuda")
     ws = torch.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=torch.uint8, device="cuda")
     p = rl.LossParams(agg=rl.AGG_SUM)
-    if "--peer" in sys.argv:  # in-kernel exchange (vp_ring_kernel)
+    if "--peer" in sys.argv:  # in-kernel exchange (vp_cache_kernel; --ring: vp_ring_kernel)
         assert comm.enable_peer_exchange(N)
+        if "--ring" in sys.argv:
+            rl.dev_set_option(rl.DEV_VP_KERNEL, 1)
     else:
         rl.dev_set_option(rl.DEV_VP_PATH, 1)
     call = lambda: rl.vocab_parallel_logprob(x, y, 0, Vr, comm, logp, ws, vocab_shard=Vr, old_logp=old,
