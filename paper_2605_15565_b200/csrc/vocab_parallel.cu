@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
 
 // ---------------------------------------------------------------------------------------
 // Fused vocab-parallel loss, register-cache form: vp_cache_kernel<NV, R> (the default for bf16
-// shards of <= 4800 16-B vectors, i.e. the P >= 4 shard widths of V = 151936).
+// shards of <= 4928 16-B vectors, i.e. the P >= 4 shard widths of V = 151936).
 //
 // One HBM read and one exp2 per element: a CTA walks its rows; each consumer thread holds NV
 // vectors (vector t + 480 i) of a row slice in registers, converted in place into
@@ -678,18 +678,23 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
 // gradient is written from the cache:  dlogits_v = e'_v q_w,  q_w = s_t 2^(m_w - c2)  (q split
 // into bf16 hi + lo, HMUL2 + HFMA2: one rounding in the product, reading R2), target column
 // dy = s_t (p_y - 1).  So the exchange latency hides behind R - 1 rows of streaming.
-//   warps 0..14   consumers
-//   warp 15       lane 0 TMA producer (ring of 30 KB slots), lane 1 publisher, lanes 8..15 collector
-//                 (lane 8 + q polls rank q's record; lane 8 runs the epilogue and statistics).
-// 16 warps = 4 per SM sub-partition, so each thread may use 128 registers (the NV = 10 cache is 80).
-constexpr int kVcThreads = 512;
+//   warps 0..13   consumers (thread t holds vectors t + 448 i, i < NV)
+//   warp 14       lane 0: TMA producer (ring of 28 KB slots) — alone in its warp, so a copy is
+//                 issued the moment a slot frees (sharing the warp with polling lanes starved it)
+//   warp 15       lane 0 publisher; lanes 8..15 collector (lane 8 + q polls rank q's record; lane 8
+//                 runs the epilogue and the statistics)
+// 16 warps = 4 per SM sub-partition, so each thread may use 128 registers (the NV = 11 cache is 88).
+constexpr int kVcWarps = 14, kVcCons = kVcWarps * 32;
+constexpr int kVcThreads = kVcCons + 64;
+constexpr int kVcChunkVec = 4 * kVcCons;      // 16-B vectors per ring slot (4 per consumer thread)
+constexpr int kVcSlot = kVcChunkVec * 16;      // 28 KB
 constexpr int kVcColl = 8;  // first collector lane
 constexpr int kVcStat = 32, kVcScale = 32;
 
 struct VcShared {
   uint64_t stats_full[kVcStat], stats_free[kVcStat];
   uint64_t scale_full[kVcScale], scale_free[kVcScale];
-  float2 red[kVcStat][15];
+  float2 red[kVcStat][kVcWarps];
   float zyv[kVcStat];
   float4 sc[kVcScale];  // (s, c2, dy, target column or -1)
 };
@@ -706,22 +711,22 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
   const int64_t nk = blockIdx.x < a.n ? (a.n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t row_bytes = a.ld * 2;
   const int nvec = (int)(a.Vr / 8);
-  const int nch = (nvec + kVrChunkVec - 1) / kVrChunkVec;
+  const int nch = (nvec + kVcChunkVec - 1) / kVcChunkVec;
   const float k = a.kn.inv_t * RL_LOG2E;
   auto row_of = [&](int64_t kk) { return (int64_t)blockIdx.x + kk * gridDim.x; };
   if (tid == 0) {
     for (int i = 0; i < a.nslots; ++i) {
       sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&empty[i], 15);
+      sm100::mbar_init(&empty[i], kVcWarps);
     }
     for (int i = 0; i < kVcStat; ++i) {
-      sm100::mbar_init(&sh.stats_full[i], 15);
+      sm100::mbar_init(&sh.stats_full[i], kVcWarps);
       sm100::mbar_init(&sh.stats_free[i], 1);
       sh.zyv[i] = 0.f;
     }
     for (int i = 0; i < kVcScale; ++i) {
       sm100::mbar_init(&sh.scale_full[i], 1);
-      sm100::mbar_init(&sh.scale_free[i], 15);
+      sm100::mbar_init(&sh.scale_free[i], kVcWarps);
     }
     sm100::fence_mbar_init();
   }
@@ -729,28 +734,32 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
   const uint32_t full_s = sm100::smem_u32(full), empty_s = sm100::smem_u32(empty);
   const uint32_t ring_s = sm100::smem_u32(ring);
 
-  if (warp == 15) {
+  if (warp == kVcWarps) {
     if (lane == 0) {  // -------------------------------------------------------- TMA producer
       RingPos rp{0, 0};
       for (int64_t kk = 0; kk < nk; ++kk) {
         const char* src = reinterpret_cast<const char*>(a.logits) + row_of(kk) * row_bytes;
         for (int c = 0; c < nch; ++c) {
           sm100::mbar_wait_a(empty_s + rp.slot * 8, rp.phase ^ 1);
-          const uint32_t bytes = (uint32_t)min(kVrChunkVec, nvec - c * kVrChunkVec) * 16u;
+          const uint32_t bytes = (uint32_t)min(kVcChunkVec, nvec - c * kVcChunkVec) * 16u;
           sm100::mbar_arrive_expect_tx(&full[rp.slot], bytes);
-          sm100::bulk_g2s_nohint(ring + (size_t)rp.slot * kVrSlot, src + (size_t)c * kVrSlot, bytes, &full[rp.slot]);
+          sm100::bulk_g2s_nohint(ring + (size_t)rp.slot * kVcSlot, src + (size_t)c * kVcSlot, bytes, &full[rp.slot]);
           rp.advance(1, a.nslots);
         }
       }
-    } else if (lane == 1) {  // --------------------------------------------------- publisher
+    }
+    return;
+  }
+  if (warp == kVcWarps + 1) {
+    if (lane == 0) {  // --------------------------------------------------------- publisher
       const unsigned long long ep = (unsigned long long)a.epoch << 32;
       for (int64_t kk = 0; kk < nk; ++kk) {
         const int ss = (int)(kk % kVcStat);
         sm100::mbar_wait_polite(&sh.stats_full[ss], (uint32_t)((kk / kVcStat) & 1), false);
         float M = -INFINITY;
-        for (int w = 0; w < 15; ++w) M = fmaxf(M, sh.red[ss][w].x);
+        for (int w = 0; w < kVcWarps; ++w) M = fmaxf(M, sh.red[ss][w].x);
         float S = 0.f;
-        for (int w = 0; w < 15; ++w) {
+        for (int w = 0; w < kVcWarps; ++w) {
           const float2 r = sh.red[ss][w];
           if (r.x != -INFINITY) S += r.y * fast_exp2(r.x - M);
         }
@@ -883,13 +892,13 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     for (int c = 0; c < (NV + 3) / 4; ++c) {
       if (c < nch) {
         sm100::mbar_wait_a(full_s + slot * 8, rph);
-        const uint32_t sb = ring_s + slot * (uint32_t)kVrSlot;
+        const uint32_t sb = ring_s + slot * (uint32_t)kVcSlot;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int i = 4 * c + u;
           if (i < NV) {
-            const bool ok = i * kVrCons + tid < nvec;
-            cache[r][i] = ok ? sm100::lds128_a(sb + u * (kVrCons * 16) + my_off) : V::neg_inf_vec();
+            const bool ok = i * kVcCons + tid < nvec;
+            cache[r][i] = ok ? sm100::lds128_a(sb + u * (kVcCons * 16) + my_off) : V::neg_inf_vec();
             V::max_acc(cache[r][i], mx);
           }
         }
@@ -909,7 +918,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     bool own = false;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      if (yv == i * kVrCons + tid) {
+      if (yv == i * kVcCons + tid) {
         const uint4 v = cache[r][i];
         const int e = (int)(yl & 7);
         const uint32_t wd = e < 2 ? v.x : e < 4 ? v.y : e < 6 ? v.z : v.w;
@@ -955,8 +964,8 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.dlogits) + row * row_bytes) + tid;
 #pragma unroll
     for (int i = 0; i < NV; ++i)
-      st_stream_v4_if(out + i * kVrCons, V::grad_sv(cache[r][i], qb2, ql2, q), i * kVrCons + tid < nvec);
-    if (st != 0.f && ycol >= 0 && ((ycol >> 3) % kVrCons) == tid)  // same thread, after its vector store
+      st_stream_v4_if(out + i * kVcCons, V::grad_sv(cache[r][i], qb2, ql2, q), i * kVcCons + tid < nvec);
+    if (st != 0.f && ycol >= 0 && ((ycol >> 3) % kVcCons) == tid)  // same thread, after its vector store
       VecTraits<bf16_t>::store1(reinterpret_cast<char*>(a.dlogits) + row * row_bytes, ycol, dy);
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(&sh.scale_free[sl]);
@@ -1083,11 +1092,11 @@ extern "C" rl_status rl_vocab_parallel_logprob(
     // bf16 shards of <= 4800 whole vectors: the register-cache kernel (one read, one exp2 per
     // element); anything else: the L2 re-read ring kernel (same exchange protocol)
     const int64_t nv = vocab_shard / 8;
-    if (dtype == RL_BF16 && vocab_shard % 8 == 0 && nv >= 1 && nv <= 10 * kVrCons && dev_option(OPT_VP_KERNEL) != 1) {
+    if (dtype == RL_BF16 && vocab_shard % 8 == 0 && nv >= 1 && nv <= 11 * kVcCons && dev_option(OPT_VP_KERNEL) != 1) {
       const size_t head = (sizeof(VcShared) + 127) & ~(size_t)127;
-      v.nslots = (int)((kSmemMax - head - 256) / (kVrSlot + 16));
-      const size_t smem = ((sizeof(VcShared) + 16 * (size_t)v.nslots + 127) & ~(size_t)127) + (size_t)v.nslots * kVrSlot;
-      auto kern = nv <= 5 * kVrCons ? vp_cache_kernel<5, 3> : vp_cache_kernel<10, 2>;
+      v.nslots = (int)((kSmemMax - head - 256) / (kVcSlot + 16));
+      const size_t smem = ((sizeof(VcShared) + 16 * (size_t)v.nslots + 127) & ~(size_t)127) + (size_t)v.nslots * kVcSlot;
+      auto kern = nv <= 6 * kVcCons ? vp_cache_kernel<6, 3> : vp_cache_kernel<11, 2>;
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return check_launch("cudaFuncSetAttribute(vp_cache_kernel)");
       kern<<<grid, kVcThreads, smem, s>>>(v);
