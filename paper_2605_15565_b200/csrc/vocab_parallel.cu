@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
 // shards of <= 4928 16-B vectors, i.e. the P >= 4 shard widths of V = 151936).
 //
 // One HBM read and one exp2 per element: a CTA walks its rows; each consumer thread holds NV
-// vectors (vector t + 480 i) of a row slice in registers, converted in place into
+// vectors (vector t + 448 i) of a row slice in registers, converted in place into
 //     e'_v = 2^(x_v k - m_w)          m_w = the max of x k over the thread's WARP (no CTA barrier)
 // and keeps them (bf16) for R rows while the row statistics travel: warp partials
 // (m_w, S_w = sum e') -> publisher lane combines the 15 warps into c2_r = lse2 of the shard and
@@ -681,8 +681,9 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
 //   warps 0..13   consumers (thread t holds vectors t + 448 i, i < NV)
 //   warp 14       lane 0: TMA producer (ring of 28 KB slots) — alone in its warp, so a copy is
 //                 issued the moment a slot frees (sharing the warp with polling lanes starved it)
-//   warp 15       lane 0 publisher; lanes 8..15 collector (lane 8 + q polls rank q's record; lane 8
-//                 runs the epilogue and the statistics)
+//   warp 15       lane 0 publisher; lanes 8..31 collector: G = min(8, 24 / P) groups of P lanes, group
+//                 g owning rows g, g + G, ... (lane q polls rank q's record, lane 0 of the group runs
+//                 the epilogue), so G rows are combined concurrently
 // 16 warps = 4 per SM sub-partition, so each thread may use 128 registers (the NV = 11 cache is 88).
 constexpr int kVcWarps = 14, kVcCons = kVcWarps * 32;
 constexpr int kVcThreads = kVcCons + 64;
@@ -697,6 +698,7 @@ struct VcShared {
   float2 red[kVcStat][kVcWarps];
   float zyv[kVcStat];
   float4 sc[kVcScale];  // (s, c2, dy, target column or -1)
+  double acc[8][RL_LOSS_STATS_N];  // collector groups' statistics
 };
 
 template <int NV, int R>
@@ -771,9 +773,15 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         for (int q = 0; q < a.P; ++q)
           st_ll2(a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2, ep | __float_as_uint(c2), ep | __float_as_uint(zy));
       }
-    } else if (lane >= kVcColl && lane < kVcColl + 8) {  // ------------------------- collector
-      const int cl = lane - kVcColl;  // this lane polls rank cl's records
-      constexpr unsigned kMask = 0xffu << kVcColl;
+    } else if (lane >= kVcColl) {  // ------------------------------------------------ collector
+      // lanes 8..31 form G = min(8, 24 / P) groups of P lanes; group g owns rows g, g + G, ... (its
+      // own serial poll -> combine -> epilogue chain), lane q of a group polls rank q's record
+      const int cl = lane - kVcColl;
+      const int G = min(8, 24 / a.P);
+      const int grp = cl / a.P, q = cl - grp * a.P;
+      const int lead = kVcColl + grp * a.P;
+      const unsigned gmask = (a.P == 32 ? 0xffffffffu : ((1u << a.P) - 1u)) << lead;
+      if (grp < G) {
     const double inv_tm = token_mean_inv(a.kn);
     Acc acc;
     acc.zero();
@@ -782,7 +790,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     uint8_t nmask = 1;
     float nold = 0.f, nprox = 0.f, nref = 0.f;
     auto load_l1 = [&](int64_t kk) {
-      if (cl == 0 && kk < nk) {
+      if (q == 0 && kk < nk) {
         const int64_t row = row_of(kk);
         ny = a.targets[row];
         nseq = a.token_seq ? a.token_seq[row] : 0;
@@ -791,15 +799,15 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         token_extra(a.kn, row, nold, nprox, nref);
       }
     };
-    load_l1(0);
-    for (int64_t kk = 0; kk < nk; ++kk) {
+    load_l1(grp);
+    for (int64_t kk = grp; kk < nk; kk += G) {
       const int64_t row = row_of(kk);
       const int32_t y = ny, seq = nseq;
       const uint8_t mk = nmask;
       const float old = nold, prox = nprox, ref = nref;
       int32_t ver = 0, act = 0;
       float A = 0.f;
-      if (cl == 0) {
+      if (q == 0) {
         if (a.seq_version) ver = a.seq_version[seq];
         if (mk != 0 && y >= 0 && (int64_t)y < a.Vtot) {
           A = a.seq_adv[seq];
@@ -807,8 +815,8 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         }
       }
       float c2q = -INFINITY, zyq = 0.f;
-      if (cl < a.P) {
-        const unsigned long long* slot = a.xr[a.me] + ((int64_t)cl * a.max_tokens + row) * 2;
+      {
+        const unsigned long long* slot = a.xr[a.me] + ((int64_t)q * a.max_tokens + row) * 2;
         unsigned long long w0, w1;
         const unsigned long long t0 = globaltimer();
         for (int it = 0;; ++it) {
@@ -818,24 +826,24 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
           if ((it & 1023) == 1023 && globaltimer() - t0 > (unsigned long long)kVrTimeoutNs) {
             printf("rl_vocab_parallel_logprob: rank %d waited > %lld s for rank %d's record of row %lld "
                    "(epoch %u); a peer is not running the matching call\n",
-                   a.me, kVrTimeoutNs / 1000000000LL, cl, (long long)row, a.epoch);
+                   a.me, kVrTimeoutNs / 1000000000LL, q, (long long)row, a.epoch);
             __trap();
           }
         }
         c2q = __uint_as_float((uint32_t)w0);
         zyq = __uint_as_float((uint32_t)w1);
       }
-      load_l1(kk + 1);
+      load_l1(kk + G);
       float M = -INFINITY;
-      for (int q = 0; q < a.P; ++q) M = fmaxf(M, __shfl_sync(kMask, c2q, kVcColl + q));
+      for (int j = 0; j < a.P; ++j) M = fmaxf(M, __shfl_sync(gmask, c2q, lead + j));
       float S = 0.f, zy = 0.f;
-      for (int q = 0; q < a.P; ++q) {
-        const float cq = __shfl_sync(kMask, c2q, kVcColl + q);
-        const float zq = __shfl_sync(kMask, zyq, kVcColl + q);
+      for (int j = 0; j < a.P; ++j) {
+        const float cq = __shfl_sync(gmask, c2q, lead + j);
+        const float zq = __shfl_sync(gmask, zyq, lead + j);
         if (cq != -INFINITY) S += fast_exp2(cq - M);
         zy += zq;
       }
-      if (cl == 0) {
+      if (q == 0) {
         const float c2 = M + fast_log2(S);
         RowMeta mt;
         mt.y = y;
@@ -867,8 +875,15 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         sm100::mbar_arrive(&sh.scale_full[sl]);
       }
     }
-    if (cl == 0)
-      for (int i = 0; i < RL_LOSS_STATS_N; ++i) a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + i] = acc.v[i];
+      if (q == 0)
+        for (int i = 0; i < RL_LOSS_STATS_N; ++i) sh.acc[grp][i] = acc.v[i];
+      }
+      __syncwarp(0xffffffffu << kVcColl);
+      if (cl < RL_LOSS_STATS_N) {  // group-ordered (deterministic) sum of the groups' statistics
+        double tsum = 0.0;
+        for (int g = 0; g < G; ++g) tsum += sh.acc[g][cl];
+        a.partials[(int64_t)blockIdx.x * RL_LOSS_STATS_N + cl] = tsum;
+      }
     }
     return;
   }
