@@ -671,8 +671,8 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
 // vectors (vector t + 448 i) of a row slice in registers, converted in place into
 //     e'_v = 2^(x_v k - m_w)          m_w = the max of x k over the thread's WARP (no CTA barrier)
 // and keeps them (bf16) for R rows while the row statistics travel: warp partials
-// (m_w, S_w = sum e') -> publisher lane combines the 15 warps into c2_r = lse2 of the shard and
-// sends (c2_r, z_y) to every rank (LL words, as vp_ring_kernel) -> the collector warp polls the P
+// (m_w, S_w = sum e') -> the LAST consumer warp to post its record (a shared-memory counter) combines
+// the 14 warps into c2_r = lse2 of the shard and sends (c2_r, z_y) to every rank (LL words, as vp_ring_kernel) -> the collector warp polls the P
 // records of the row, combines them in rank order (identical on every rank), runs the token
 // epilogue and publishes (s_t, c2, dy, target column).  R - 1 rows after a row was loaded its
 // gradient is written from the cache:  dlogits_v = e'_v q_w,  q_w = s_t 2^(m_w - c2)  (q split
@@ -681,19 +681,19 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
 //   warps 0..13   consumers (thread t holds vectors t + 448 i, i < NV)
 //   warp 14       lane 0: TMA producer (ring of 28 KB slots) — alone in its warp, so a copy is
 //                 issued the moment a slot frees (sharing the warp with polling lanes starved it)
-//   warp 15       lane 0 publisher; lanes 8..31 collector: G = min(8, 24 / P) groups of P lanes, group
-//                 g owning rows g, g + G, ... (lane q polls rank q's record, lane 0 of the group runs
-//                 the epilogue), so G rows are combined concurrently
+//   warp 15       collector: G = min(8, 32 / P) groups of P lanes, group g owning rows g, g + G, ...
+//                 (lane q polls rank q's record, lane 0 of the group runs the epilogue), so G rows
+//                 are combined concurrently
 // 16 warps = 4 per SM sub-partition, so each thread may use 128 registers (the NV = 11 cache is 88).
 constexpr int kVcWarps = 14, kVcCons = kVcWarps * 32;
 constexpr int kVcThreads = kVcCons + 64;
 constexpr int kVcChunkVec = 4 * kVcCons;      // 16-B vectors per ring slot (4 per consumer thread)
 constexpr int kVcSlot = kVcChunkVec * 16;      // 28 KB
-constexpr int kVcColl = 8;  // first collector lane
+constexpr int kVcColl = 0;  // first collector lane
 constexpr int kVcStat = 32, kVcScale = 32;
 
 struct VcShared {
-  uint64_t stats_full[kVcStat], stats_free[kVcStat];
+  uint32_t cnt[kVcStat];    // consumer warps that posted the row's record
   uint64_t scale_full[kVcScale], scale_free[kVcScale];
   float2 red[kVcStat][kVcWarps];
   float zyv[kVcStat];
@@ -722,8 +722,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
       sm100::mbar_init(&empty[i], kVcWarps);
     }
     for (int i = 0; i < kVcStat; ++i) {
-      sm100::mbar_init(&sh.stats_full[i], kVcWarps);
-      sm100::mbar_init(&sh.stats_free[i], 1);
+      sh.cnt[i] = 0;
       sh.zyv[i] = 0.f;
     }
     for (int i = 0; i < kVcScale; ++i) {
@@ -753,31 +752,11 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     return;
   }
   if (warp == kVcWarps + 1) {
-    if (lane == 0) {  // --------------------------------------------------------- publisher
-      const unsigned long long ep = (unsigned long long)a.epoch << 32;
-      for (int64_t kk = 0; kk < nk; ++kk) {
-        const int ss = (int)(kk % kVcStat);
-        sm100::mbar_wait_polite(&sh.stats_full[ss], (uint32_t)((kk / kVcStat) & 1), false);
-        float M = -INFINITY;
-        for (int w = 0; w < kVcWarps; ++w) M = fmaxf(M, sh.red[ss][w].x);
-        float S = 0.f;
-        for (int w = 0; w < kVcWarps; ++w) {
-          const float2 r = sh.red[ss][w];
-          if (r.x != -INFINITY) S += r.y * fast_exp2(r.x - M);
-        }
-        const float zy = sh.zyv[ss];
-        sh.zyv[ss] = 0.f;
-        sm100::mbar_arrive(&sh.stats_free[ss]);
-        const float c2 = S > 0.f ? M + fast_log2(S) : -INFINITY;
-        const int64_t row = row_of(kk);
-        for (int q = 0; q < a.P; ++q)
-          st_ll2(a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2, ep | __float_as_uint(c2), ep | __float_as_uint(zy));
-      }
-    } else if (lane >= kVcColl) {  // ------------------------------------------------ collector
+    {  // ----------------------------------------------------------------------- collector
       // lanes 8..31 form G = min(8, 24 / P) groups of P lanes; group g owns rows g, g + G, ... (its
       // own serial poll -> combine -> epilogue chain), lane q of a group polls rank q's record
       const int cl = lane - kVcColl;
-      const int G = min(8, 24 / a.P);
+      const int G = min(8, 32 / a.P);
       const int grp = cl / a.P, q = cl - grp * a.P;
       const int lead = kVcColl + grp * a.P;
       const unsigned gmask = (a.P == 32 ? 0xffffffffu : ((1u << a.P) - 1u)) << lead;
@@ -822,7 +801,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         for (int it = 0;; ++it) {
           ld_ll2(slot, w0, w1);
           if ((w0 >> 32) == a.epoch && (w1 >> 32) == a.epoch) break;
-          __nanosleep(32);  // shares its warp with the producer and publisher lanes
+          __nanosleep(32);  // the warp's other groups poll their own rows
           if ((it & 1023) == 1023 && globaltimer() - t0 > (unsigned long long)kVrTimeoutNs) {
             printf("rl_vocab_parallel_logprob: rank %d waited > %lld s for rank %d's record of row %lld "
                    "(epoch %u); a peer is not running the matching call\n",
@@ -954,13 +933,30 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
       s = lo + hi;
     }
     s = warp_sum(s);
+    // slot ss is reused 32 rows later: the consumer warps stay within a few rows of each other
+    // (a ring slot is refilled only once all 14 warps released it)
     const int ss = (int)(kk % kVcStat);
-    if (kk >= kVcStat) sm100::mbar_wait(&sh.stats_free[ss], (uint32_t)(((kk / kVcStat) - 1) & 1));
     if (own) sh.zyv[ss] = zy * a.kn.inv_t;
     __syncwarp();
     if (lane == 0) {
       sh.red[ss][warp] = make_float2(m, s);
-      sm100::mbar_arrive(&sh.stats_full[ss]);
+      if (sm100::atom_add_acqrel(sm100::smem_u32(&sh.cnt[ss]), 1u) == kVcWarps - 1) {  // last warp: publish
+        float M = -INFINITY;
+        for (int w = 0; w < kVcWarps; ++w) M = fmaxf(M, sh.red[ss][w].x);
+        float S = 0.f;
+        for (int w = 0; w < kVcWarps; ++w) {
+          const float2 rw = sh.red[ss][w];
+          if (rw.x != -INFINITY) S += rw.y * fast_exp2(rw.x - M);
+        }
+        const float zr = sh.zyv[ss];
+        sh.zyv[ss] = 0.f;
+        atomicExch(&sh.cnt[ss], 0u);
+        const float c2 = S > 0.f ? M + fast_log2(S) : -INFINITY;
+        const unsigned long long ep = (unsigned long long)a.epoch << 32;
+        const int64_t row = row_of(kk);
+        for (int q = 0; q < a.P; ++q)
+          st_ll2(a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2, ep | __float_as_uint(c2), ep | __float_as_uint(zr));
+      }
     }
   };
   // dlogits of row kk from cache[r]
