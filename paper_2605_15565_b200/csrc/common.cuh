@@ -38,7 +38,9 @@ enum DevOpt {
   OPT_VP_PATH = 1,      // fused vocab-parallel loss: 0 = in-kernel peer exchange when enabled, 1 = NCCL path
   OPT_LM_SPLITS = 2,    // LM-head vocabulary split override (0 = cost model)
   OPT_VP_KERNEL = 3,    // peer-exchange vocab-parallel kernel: 0 = register cache when it fits, 1 = L2 ring
-  OPT_COUNT = 4
+  OPT_VC_GROUPS = 4,    // vp_cache_kernel collector groups override (0 = min(8, 32 / P))
+  OPT_VC_ROWS = 5,      // vp_cache_kernel rows held for the P >= 8 widths: 0 / 3 = three, 4 = four
+  OPT_COUNT = 6
 };
 int dev_option(int key);
 

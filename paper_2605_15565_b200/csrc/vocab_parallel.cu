@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
       // lanes 8..31 form G = min(8, 24 / P) groups of P lanes; group g owns rows g, g + G, ... (its
       // own serial poll -> combine -> epilogue chain), lane q of a group polls rank q's record
       const int cl = lane - kVcColl;
-      const int G = min(8, 32 / a.P);
+      const int G = a.G > 0 ? min(a.G, 32 / a.P) : min(8, 32 / a.P);
       const int grp = cl / a.P, q = cl - grp * a.P;
       const int lead = kVcColl + grp * a.P;
       const unsigned gmask = (a.P == 32 ? 0xffffffffu : ((1u << a.P) - 1u)) << lead;
@@ -1107,7 +1107,9 @@ extern "C" rl_status rl_vocab_parallel_logprob(
       const size_t head = (sizeof(VcShared) + 127) & ~(size_t)127;
       v.nslots = (int)((kSmemMax - head - 256) / (kVcSlot + 16));
       const size_t smem = ((sizeof(VcShared) + 16 * (size_t)v.nslots + 127) & ~(size_t)127) + (size_t)v.nslots * kVcSlot;
-      auto kern = nv <= 6 * kVcCons ? vp_cache_kernel<6, 3> : vp_cache_kernel<11, 2>;
+      auto kern = nv > 6 * kVcCons ? vp_cache_kernel<11, 2>
+                  : dev_option(OPT_VC_ROWS) == 4 ? vp_cache_kernel<6, 4> : vp_cache_kernel<6, 3>;
+      v.G = std::min(8, std::max(0, dev_option(OPT_VC_GROUPS)));
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return check_launch("cudaFuncSetAttribute(vp_cache_kernel)");
       kern<<<grid, kVcThreads, smem, s>>>(v);

@@ -35,6 +35,10 @@ def main():
         assert comm.enable_peer_exchange(N)
         if "--ring" in sys.argv:
             rl.dev_set_option(rl.DEV_VP_KERNEL, 1)
+        if "--groups" in sys.argv:
+            rl.dev_set_option(rl.DEV_VC_GROUPS, int(sys.argv[sys.argv.index("--groups") + 1]))
+        if "--rows4" in sys.argv:
+            rl.dev_set_option(rl.DEV_VC_ROWS, 4)
     else:
         rl.dev_set_option(rl.DEV_VP_PATH, 1)
     call = lambda: rl.vocab_parallel_logprob(x, y, 0, Vr, comm, logp, ws, vocab_shard=Vr, old_logp=old,
