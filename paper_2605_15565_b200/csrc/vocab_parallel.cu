@@ -669,13 +669,13 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
 //
 // One HBM read and one exp2 per element: a CTA walks its rows; each consumer thread holds NV
 // vectors (vector t + 448 i) of a row slice in registers, converted in place into
-//     e'_v = 2^(x_v k - m_t)          m_t = the max of x k over the thread's own NV vectors
+//     e'_v = 2^(x_v k - m_w)          m_w = the max of x k over the thread's WARP (no CTA barrier)
 // and keeps them (bf16) for R rows while the row statistics travel: warp partials
-// (m_w, S_w) reduced from the threads' (m_t, sum e') -> the LAST consumer warp to post its record (a shared-memory counter) combines
+// (m_w, S_w = sum e') -> the LAST consumer warp to post its record (a shared-memory counter) combines
 // the 14 warps into c2_r = lse2 of the shard and sends (c2_r, z_y) to every rank (LL words, as vp_ring_kernel) -> the collector warp polls the P
 // records of the row, combines them in rank order (identical on every rank), runs the token
 // epilogue and publishes (s_t, c2, dy, target column).  R - 1 rows after a row was loaded its
-// gradient is written from the cache:  dlogits_v = e'_v q_t,  q_t = s_t 2^(m_t - c2)  (q split
+// gradient is written from the cache:  dlogits_v = e'_v q_w,  q_w = s_t 2^(m_w - c2)  (q split
 // into bf16 hi + lo, HMUL2 + HFMA2: one rounding in the product, reading R2), target column
 // dy = s_t (p_y - 1).  So the exchange latency hides behind R - 1 rows of streaming.
 //   warps 0..13   consumers (thread t holds vectors t + 448 i, i < NV)
@@ -920,8 +920,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         own = true;
       }
     }
-    // the thread's own max is its exponent reference: the exps start without a warp reduction
-    const float m = V::max_to_float(mx) * k;
+    const float m = warp_max(V::max_to_float(mx)) * k;
     mw[r] = m;
     float s = 0.f;
     if (m != -INFINITY) {
@@ -933,14 +932,14 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
       f2unpack(acc2, lo, hi);
       s = lo + hi;
     }
-    const MS wr = warp_reduce_ms(MS{m, s});  // the warp's record (off the e' path)
+    s = warp_sum(s);
     // slot ss is reused 32 rows later: the consumer warps stay within a few rows of each other
     // (a ring slot is refilled only once all 14 warps released it)
     const int ss = (int)(kk % kVcStat);
     if (own) sh.zyv[ss] = zy * a.kn.inv_t;
     __syncwarp();
     if (lane == 0) {
-      sh.red[ss][warp] = make_float2(wr.m, wr.s);
+      sh.red[ss][warp] = make_float2(m, s);
       if (sm100::atom_add_acqrel(sm100::smem_u32(&sh.cnt[ss]), 1u) == kVcWarps - 1) {  // last warp: publish
         float M = -INFINITY;
         for (int w = 0; w < kVcWarps; ++w) M = fmaxf(M, sh.red[ss][w].x);
