@@ -701,6 +701,13 @@ struct VcShared {
   double acc[8][RL_LOSS_STATS_N];  // collector groups' statistics
 };
 
+// warp max in one instruction (redux.sync .f32, sm_100a)
+__device__ __forceinline__ float warp_max_redux(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 template <int NV, int R>
 __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a) {
   using V = ClVec<bf16_t>;
@@ -920,7 +927,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         own = true;
       }
     }
-    const float m = warp_max(V::max_to_float(mx)) * k;
+    const float m = warp_max_redux(V::max_to_float(mx)) * k;
     mw[r] = m;
     float s = 0.f;
     if (m != -INFINITY) {

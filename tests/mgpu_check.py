@@ -5,7 +5,8 @@
 token parallel: whole-sequence shards, rl_batch_counts all-reduced through rl_comm before the
 loss, rl_loss_stats after it -> global loss / counts equal the unsplit oracle, each rank's dlogits
 rows equal the oracle's rows.  vocab parallel: column shards, NCCL all-gather combine -> logp on
-every rank and each dlogits shard equal the oracle.  comm split by colour.
+every rank and each dlogits shard equal the oracle (NCCL path and in-kernel peer path, at V = 5003
+and at the production V = 151936 with back-to-back peer calls).  M2PO global mask.  comm split.
 """
 import os
 import sys
@@ -131,6 +132,66 @@ def main():
                   fails.append(f"{mode} vp row {i} not zero")
           elif vs.size and np.abs(gv[i] - refrow).max() > 1e-2 * abs(s_all[i]):
               fails.append(f"{mode} vp row {i} dlogits")
+
+    # ------------------------------------------------------------------ vocab parallel, V = 151936
+    # the production width: every rank holds its shard of the same seeded [N, 151936] logits (P = 2:
+    # 75,968 columns -> vp_ring_kernel; P = 4 / 8: 37,984 / 18,992 -> vp_cache_kernel); three
+    # back-to-back peer calls with NO collective in between (the exchange slots alternate by epoch
+    # parity), each call's stats kept apart; the last call checked against the oracle on 256 rows
+    import synth
+    Vf, Nf = 151936, 4096
+    xf = torch.empty((Nf, Vf), dtype=torch.bfloat16, device=dev)
+    yf = torch.empty(Nf, dtype=torch.int32, device=dev)
+    synth.device_logits(xf, Vf, 0, 4, targets_out=yf)
+    vs = shard_vocab(Vf, world, rank)
+    xs = xf[:, vs.offset:vs.offset + vs.size].contiguous()
+    rows = np.sort(np.random.default_rng(5).choice(Nf, size=256, replace=False))
+    bits_rows = xf[torch.from_numpy(rows).to(dev)].view(torch.int16).cpu().numpy().view(np.uint16)
+    lp_ref_rows, _ = oracle.token_logprob(oracle.decode_bf16(bits_rows), yf.cpu().numpy()[rows])
+    maskf = np.zeros(Nf, dtype=np.uint8)
+    maskf[rows] = 1
+    oldf = np.zeros(Nf, dtype=np.float32)
+    oldf[rows] = (lp_ref_rows + np.random.default_rng(6).normal(size=256) * 0.05).astype(np.float32)
+    tseqf = (np.arange(Nf) // 512).astype(np.int32)
+    advf = np.random.default_rng(7).normal(size=Nf // 512).astype(np.float32)
+    pf = rl.LossParams(agg=rl.AGG_SUM)
+    dlf = torch.empty_like(xs)
+    lpf = torch.empty(Nf, dtype=torch.float32, device=dev)
+    wsf = torch.empty(rl.vocab_parallel_workspace_size(Nf, world), dtype=torch.uint8, device=dev)
+    if comm.enable_peer_exchange(Nf):
+        st_calls = [torch.zeros(12, dtype=torch.float64, device=dev) for _ in range(3)]
+        for c in range(3):
+            rl.vocab_parallel_logprob(xs, yf, vs.offset, Vf, comm, lpf, wsf, old_logp=d(oldf), loss_mask=d(maskf),
+                                      token_seq=d(tseqf), seq_adv=d(advf), params=pf, dlogits_shard=dlf,
+                                      stats=st_calls[c])
+        for c in range(3):
+            comm.allreduce_f64(st_calls[c])
+        torch.cuda.synchronize()
+        sts = [c.cpu().numpy() for c in st_calls]
+        if not (np.array_equal(sts[0], sts[1]) and np.array_equal(sts[1], sts[2])):
+            fails.append("full-width vp: back-to-back calls differ")
+        yh = yf.cpu().numpy()
+        outf = oracle.policy_loss_fwd_bwd(oracle.decode_bf16(bits_rows), yh[rows], oldf[rows], maskf[rows],
+                                          tseqf[rows], advf.astype(np.float64), None, None,
+                                          oracle.LossParams(agg=oracle.AGG_SUM))
+        lpg = lpf.cpu().numpy()[rows]
+        if np.abs(lpg - outf["logp"]).max() > 2e-3:
+            fails.append(f"full-width vp logp err {np.abs(lpg - outf['logp']).max()}")
+        sc = max(abs(outf["loss"]), float(np.abs(outf["token_loss"]).sum()))
+        if abs(sts[2][0] - outf["loss"]) > 1e-4 * sc or sts[2][1] != outf["stats"]["active_tokens"]:
+            fails.append(f"full-width vp loss {sts[2][0]} vs {outf['loss']}")
+        gs = oracle.decode_bf16(dlf[torch.from_numpy(rows).to(dev)].view(torch.int16).cpu().numpy().view(np.uint16))
+        for k, i in enumerate(rows):
+            refrow = outf["dlogits"][k, vs.offset:vs.offset + vs.size]
+            s_k = outf["scale"][k]
+            if s_k == 0:
+                if np.any(gs[k] != 0):
+                    fails.append(f"full-width vp row {i} not zero")
+            elif np.abs(gs[k] - refrow).max() > 1e-2 * abs(s_k):
+                fails.append(f"full-width vp row {i} dlogits err {np.abs(gs[k] - refrow).max() / abs(s_k)}")
+    else:
+        fails.append("full-width vp: peer exchange unavailable")
+    del xf, xs, dlf
 
     # ------------------------------------------------------------------ M2PO global selection
     # every rank passes its own n tokens; the mask must equal the oracle's over the concatenation
