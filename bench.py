@@ -52,11 +52,16 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
+    ap.add_argument("--vp-width-of", type=int, default=0,
+                    help="vocabpar on ONE GPU: one rank's share of a P-way split (a [65536, V/P] shard as its own "
+                         "vocabulary, exchange with itself) — the per-rank work of configs[3] at P")
+    ap.add_argument("--resident", action="store_true",
+                    help="single: the rank's whole 524,288-token batch as ONE resident in-place call (159 GB)")
     ap.add_argument("--objective", default="clip", choices=["clip", "full", "m2po"],
                     help="clip: the north_star's clipped surrogate (default); full: + decoupled proximal "
                          "ratio, k3 KL penalty (beta 1e-3, PAPER.md:572) and entropy (NEXT 2); m2po: "
                          "rl_token_logprob -> rl_m2po_mask (tau 0.01, PAPER.md:572) -> unclipped loss (NEXT 1)")
-    ap.add_argument("--config", default="single", choices=["single", "long", "vocabpar", "multi", "lmhead"],
+    ap.add_argument("--config", default="single", choices=["single", "tiny", "long", "vocabpar", "multi", "lmhead"],
                     help="BASELINE.json config (single = the headline metric's workload, the default)")
     return ap.parse_args()
 
@@ -231,7 +236,7 @@ class TokenParallelWorkload:
     advantages (group + batch normalisation) -> fused loss of every call (stats all-reduced)."""
 
     def __init__(self, rl, torch, np, synth, dev, comm, cfg, seqs, MB, n_calls, rank, max_staleness,
-                 n_pool=2, dlogits_buf=None):
+                 n_pool=2, dlogits_buf=None, in_place=False):
         self.rl, self.torch, self.comm = rl, torch, comm
         V, T = cfg.vocab, cfg.seq_len
         self.V, self.MB, self.n_calls = V, MB, n_calls
@@ -245,7 +250,9 @@ class TokenParallelWorkload:
             g.manual_seed(991 + rank)
             self.pool_ref = [o + 0.2 * torch.randn(o.shape, generator=g, device=dev) for o in self.pool_old]
             self.pool_prox = [o + 0.02 * torch.randn(o.shape, generator=g, device=dev) for o in self.pool_old]
-        if dlogits_buf is not None:  # shared [MB * V_max] bf16 buffer viewed as [MB, V]
+        if in_place:                 # dlogits overwrite the (single) resident logits buffer
+            self.dlogits = self.pool[0]
+        elif dlogits_buf is not None:  # shared [MB * V_max] bf16 buffer viewed as [MB, V]
             self.dlogits = dlogits_buf[:MB * V].view(MB, V)
         else:
             self.dlogits = torch.empty((MB, V), dtype=torch.bfloat16, device=dev)
@@ -258,21 +265,18 @@ class TokenParallelWorkload:
         self.zero_var = torch.empty(G, dtype=torch.uint8, device=dev)
         self.seq_active = torch.zeros(S_all, dtype=torch.int32, device=dev)
         self.ws_adv = torch.empty(rl.group_advantage_workspace_size(S_all), dtype=torch.uint8, device=dev)
-        # per call: a contiguous token range of this rank's sequences (MB tokens = MB/T sequences)
+        # the rank's step batch: n_calls mini-batches of MB tokens (MB/T sequences each) starting at
+        # sequence s0; ONE bookkeeping call covers all of them (token_seq relative to s0), so the
+        # batch counts come out of the library whole (no host-side sum) and are all-reduced
         tok0 = s0 * T
-        self.calls = []
+        self.s0, self.n_seq_rank = s0, n_calls * MB // T
         mask_all = lay["loss_mask"]
-        for c in range(n_calls):
-            t0 = tok0 + c * MB
-            sa = t0 // T
-            sb = sa + MB // T
-            self.calls.append(dict(
-                cu=torch.from_numpy((np.arange(MB // T + 1) * T).astype(np.int32)).to(dev),
-                mask=torch.from_numpy(mask_all[t0:t0 + MB]).to(dev), sa=sa, sb=sb,
-                tok=torch.empty(MB, dtype=torch.int32, device=dev),
-                counts=torch.zeros(20, dtype=torch.float64, device=dev),
-                stats=torch.zeros(12, dtype=torch.float64, device=dev),
-                logp=torch.empty(MB, dtype=torch.float32, device=dev)))
+        self.cu_rank = torch.from_numpy((np.arange(self.n_seq_rank + 1) * T).astype(np.int32)).to(dev)
+        self.mask_rank = torch.from_numpy(np.ascontiguousarray(mask_all[tok0:tok0 + n_calls * MB])).to(dev)
+        self.y_rank = torch.cat([self.pool_y[c % len(self.pool_y)] for c in range(n_calls)])
+        self.tok_rank = torch.empty(n_calls * MB, dtype=torch.int32, device=dev)
+        self.calls = [dict(stats=torch.zeros(12, dtype=torch.float64, device=dev),
+                           logp=torch.empty(MB, dtype=torch.float32, device=dev)) for _ in range(n_calls)]
         self.total_counts = torch.zeros(20, dtype=torch.float64, device=dev)
         self.ws = torch.empty(rl.policy_loss_workspace_size(MB, V), dtype=torch.uint8, device=dev)
         self.tokens_per_step = n_calls * MB
@@ -290,14 +294,13 @@ class TokenParallelWorkload:
     def step(self, record):
         rl, torch = self.rl, self.torch
         P = len(self.pool)
-        for c, cl in enumerate(self.calls):
-            rl.seq_bookkeeping(cl["cu"], self.pool_y[c % P], self.V, cl["tok"], self.seq_active[cl["sa"]:cl["sb"]],
-                               loss_mask=cl["mask"], seq_version=self.seq_version[cl["sa"]:cl["sb"]],
-                               trainer_version=self.trainer_version, max_staleness=self.max_staleness,
-                               counts_out=cl["counts"])
-            self.launches += 2
-        # N_active of the whole (policy) batch: the calls' counts summed, then over ranks
-        torch.sum(torch.stack([cl["counts"] for cl in self.calls]), dim=0, out=self.total_counts)
+        s0, ns, MB = self.s0, self.n_seq_rank, self.MB
+        rl.seq_bookkeeping(self.cu_rank, self.y_rank, self.V, self.tok_rank, self.seq_active[s0:s0 + ns],
+                           loss_mask=self.mask_rank, seq_version=self.seq_version[s0:s0 + ns],
+                           trainer_version=self.trainer_version, max_staleness=self.max_staleness,
+                           counts_out=self.total_counts)
+        self.launches += 2
+        # N_active of the whole (policy) batch: the rank's counts, all-reduced over the policy's ranks
         if self.comm is not None:
             self.comm.allreduce_f64(self.total_counts)
         rl.group_advantage(self.rewards, self.cu_groups, self.adv, self.zero_var, batch_norm=True,
@@ -307,11 +310,11 @@ class TokenParallelWorkload:
         for c, cl in enumerate(self.calls):
             p = rl.LossParams(trainer_version=self.trainer_version, max_staleness=self.max_staleness,
                               active_tokens_dev=self.total_counts[0:1])
-            mask = cl["mask"]
+            mask = self.mask_rank[c * MB:(c + 1) * MB]
             if self.m2po:  # NEXT 1: fresh log-probs -> global second-moment mask -> unclipped loss
                 rl.token_logprob(self.pool[c % P], self.pool_y[c % P], self.m2_logp)
                 rl.m2po_mask(self.m2_logp, self.pool_old[c % P], self.m2_mask, self.m2_stats, self.m2_ws,
-                             tau=0.01, valid=cl["mask"], comm=self.comm)
+                             tau=0.01, valid=mask, comm=self.comm)
                 mask = self.m2_mask
                 p.clip_eps_low = p.clip_eps_high = 1e30
                 p.active_tokens_dev = self.m2_stats[4:5]
@@ -322,9 +325,9 @@ class TokenParallelWorkload:
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            rl.policy_loss_fwd_bwd(self.pool[c % P], self.pool_y[c % P], self.pool_old[c % P], cl["tok"],
-                                   self.adv[cl["sa"]:cl["sb"]], p, self.dlogits, cl["stats"], self.ws,
-                                   loss_mask=mask, seq_version=self.seq_version[cl["sa"]:cl["sb"]],
+            rl.policy_loss_fwd_bwd(self.pool[c % P], self.pool_y[c % P], self.pool_old[c % P],
+                                   self.tok_rank[c * MB:(c + 1) * MB], self.adv[s0:s0 + ns], p, self.dlogits,
+                                   cl["stats"], self.ws, loss_mask=mask, seq_version=self.seq_version[s0:s0 + ns],
                                    logp_out=cl["logp"])
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
@@ -344,11 +347,13 @@ class VocabParallelWorkload:
     """Config vocabpar (BASELINE.json configs[3]): 65,536 tokens, V split over the ranks; one step
     = rl_vocab_parallel_logprob with the fused loss on the rank's column shard."""
 
-    def __init__(self, rl, torch, np, synth, dev, comm, cfg, world, rank):
+    def __init__(self, rl, torch, np, synth, dev, comm, cfg, world, rank, width_of=0):
         from paper_2605_15565_b200.parallel import shard_vocab
         self.rl, self.torch, self.comm = rl, torch, comm
         V = cfg.vocab
         N = cfg.n_tokens
+        if width_of > 1 and world == 1:   # one rank's shard width as the whole (own) vocabulary
+            V = shard_vocab(V, width_of, 0).size
         sh = shard_vocab(V, world, rank)
         self.off, self.Vr = sh.offset, sh.size
         ld = max(8, (self.Vr + 7) // 8 * 8)
@@ -440,13 +445,15 @@ def main():
         return run_reference(args)
     if args.config == "lmhead":
         return run_lmhead(args)
+    if args.config == "tiny":
+        return run_tiny(args)
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2605_15565_b200 as rl
     import synth
-    from paper_2605_15565_b200.parallel import shard_sequences
+    from paper_2605_15565_b200.parallel import policy_group, shard_sequences
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -475,7 +482,16 @@ def main():
         cfg = synth.get_config("single", seed=cfg.seed + 1000 * rank)   # each rank its own batch (DP)
         n_calls = N_MINIBATCH
         S = n_calls * MB // cfg.seq_len
-        wl = TokenParallelWorkload(rl, torch, np, synth, dev, comm, cfg, (0, S), MB, n_calls, rank, -1)
+        if args.resident:   # C2 also timed as one resident batch with in-place dlogits
+            need = n_calls * MB * cfg.vocab * 2 + (4 << 30)
+            free = torch.cuda.mem_get_info(dev)[0]
+            if free < need:
+                raise SystemExit(f"--resident needs {need / 2**30:.1f} GiB free, {free / 2**30:.1f} GiB available")
+            MB, n_calls = n_calls * MB, 1
+            wl = TokenParallelWorkload(rl, torch, np, synth, dev, comm, cfg, (0, S), MB, 1, rank, -1, n_pool=1,
+                                       in_place=True)
+        else:
+            wl = TokenParallelWorkload(rl, torch, np, synth, dev, comm, cfg, (0, S), MB, n_calls, rank, -1)
         # each rank's own batch: restrict advantages to its sequences
         wl.rewards, wl.cu_groups = wl.rewards[:S], wl.cu_groups[:S // cfg.group + 1]
         wl.adv, wl.zero_var = wl.adv[:S], wl.zero_var[:S // cfg.group]
@@ -490,12 +506,12 @@ def main():
         scaling = "strong"
         kname = f"rl_policy_loss_fwd_bwd ({kern})"
     elif args.config == "multi":
-        half = max(1, world // 2)
-        policy = 0 if world == 1 else rank // half
+        grp = policy_group(world, 2, rank)          # contiguous trainer group per policy (4 + 4 of 8)
+        policy = grp.policy
         cfgs = [synth.get_config("multi_a"), synth.get_config("multi_b")]
-        sub = comm.split(policy, rank) if comm is not None else None
-        ranks_pp = half if world > 1 else 1
-        prank = rank % half if world > 1 else 0
+        sub = comm.split(policy, grp.key) if comm is not None else None
+        ranks_pp = grp.size
+        prank = grp.key
         cfg = cfgs[policy]
         sh = shard_sequences(np.arange(cfg.n_seq + 1) * cfg.seq_len, ranks_pp, prank)
         n_calls = sh.n_tokens // MB
@@ -512,13 +528,17 @@ def main():
         kname = f"rl_policy_loss_fwd_bwd ({kern})"
     elif args.config == "vocabpar":
         cfg = synth.get_config("vocabpar")
-        wl = VocabParallelWorkload(rl, torch, np, synth, dev, comm, cfg, world, rank)
+        wl = VocabParallelWorkload(rl, torch, np, synth, dev, comm, cfg, world, rank, args.vp_width_of)
         fused_vp = args.vp_path == "peer" and comm.enable_peer_exchange(cfg.n_tokens)
         scaling = "strong"
         parallelism = (f"vocab-parallel over {world} GPU: " + (
             "one fused kernel per rank, per-row (max, sum-exp, target logit) exchanged by NVLink peer stores"
             if fused_vp else "vp_stats + NCCL all-gather + vp_finish"))
-        kname = "rl_vocab_parallel_logprob (" + ("vp_ring_kernel, in-kernel peer exchange" if fused_vp
+        if args.vp_width_of > 1 and world == 1:
+            parallelism = (f"ONE GPU doing one rank's share of a {args.vp_width_of}-way vocabulary split "
+                           f"({wl.Vr} columns as its own vocabulary, exchange with itself)")
+        vk = "vp_cache_kernel" if (wl.Vr % 8 == 0 and wl.Vr // 8 <= 11 * 448) else "vp_ring_kernel"
+        kname = "rl_vocab_parallel_logprob (" + (f"{vk}, in-kernel peer exchange" if fused_vp
                                                  else "vp_stats + NCCL all-gather + vp_finish") + ")"
     else:
         raise SystemExit(f"unknown config {args.config}")
@@ -544,12 +564,12 @@ def main():
         w.launches = 0
         w.ev = []
     stream = torch.cuda.current_stream()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(args.steps):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i in range(args.steps):
         step(True)
-    t1.record(stream)
+        evs[i + 1].record(stream)    # step boundaries: the per-step distribution (no extra sync)
+    t0, t1 = evs[0], evs[-1]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -566,6 +586,19 @@ def main():
         dist.all_reduce(tok_all)
     tokens_step = tok_all.item() if args.config != "vocabpar" else float(wls[0].tokens_per_step)
     value = tokens_step * args.steps / (elapsed_ms / 1e3)
+    # per-step distribution (this rank's step boundaries; the headline is the max-over-ranks total)
+    step_ms = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])
+    step_stats = {"p10": float(np.percentile(step_ms, 10)), "p50": float(np.median(step_ms)),
+                  "p90": float(np.percentile(step_ms, 90)), "min": float(step_ms.min()), "max": float(step_ms.max())}
+    # loss-active tokens of the step (valid tokens: masks, ignored targets and staleness applied)
+    # (total_counts is already summed over the workload's comm group: each rank adds its share)
+    active_step = sum(float(w.total_counts[0].item()) / (w.comm.nranks if w.comm is not None else 1)
+                      for w in wls if hasattr(w, "total_counts"))
+    if world > 1:
+        at = torch.tensor([active_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(at)
+        active_step = at.item()
+    active_rate = active_step * args.steps / (elapsed_ms / 1e3) if active_step else None
 
     # roofline of the dominant kernel: algorithmic bytes per launch / its average launch duration
     w0 = wls[0]
@@ -580,8 +613,8 @@ def main():
     if args.config == "single":
         if not args.no_e2e:
             S_mb = MB // 2048
-            e2e = measure_e2e(rl, torch, dev, w0.pool[0], w0.pool_y[0], w0.pool_old[0], w0.calls[0]["tok"],
-                              w0.adv[:S_mb], w0.calls[0]["mask"], w0.seq_version[:S_mb],
+            e2e = measure_e2e(rl, torch, dev, w0.pool[0], w0.pool_y[0], w0.pool_old[0], w0.tok_rank[:MB],
+                              w0.adv[:S_mb], w0.mask_rank[:MB], w0.seq_version[:S_mb],
                               {"trainer_version": w0.trainer_version}, w0.V, args)
             if world > 1:
                 tt = torch.tensor([e2e["seconds"]], dtype=torch.float64, device=dev)
@@ -600,7 +633,9 @@ def main():
 
     if rank == 0:
         workload = CONFIG_WORKLOADS[args.config]
-        if MB != 131072:
+        if args.resident:
+            workload = "one resident in-place call over the whole 524,288-token batch: " + workload
+        elif MB != 131072:
             workload = f"PROFILING ONLY ({MB}-token calls): " + workload
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -621,6 +656,7 @@ def main():
                          "bytes_per_token": w0.bytes_per_token, "avg_launch_ms": avg_ms,
                          "frac_of_8TBs": achieved / 8000.0},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
+            "step_ms": step_stats, "active_tokens_per_s": active_rate,
         }
         print(json.dumps(line), flush=True)
     if comm is not None:
@@ -629,11 +665,119 @@ def main():
         dist.destroy_process_group()
 
 
+def run_tiny(args):
+    """configs[0] (BASELINE.json "tiny: 2 prompts x 4 responses x 64 tokens, vocab 1024, fp32 logits, 1
+    GPU (CPU oracle in seconds)"): a step is the whole chain on the device — bookkeeping, group
+    advantages (+ batch normalisation), the fused loss — over the 512 tokens; the full fp64 oracle
+    chain on the same inputs is timed beside it on the host.  Launch-bound by construction (a 4 MB
+    batch): reported for the record, not a roofline claim.  Replicas only (N > 1: rank 0 reports)."""
+    import numpy as np
+    import torch
+    import paper_2605_15565_b200 as rl
+    import synth
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank = int(os.environ.get("RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    rl.load()
+    cfg = synth.get_config("tiny")
+    lay = synth.seq_layout(cfg)
+    N, V, S, G = cfg.n_tokens, cfg.vocab, cfg.n_seq, cfg.n_seq // cfg.group
+    x_h, y_h = synth.host_logits(cfg, np.arange(N), cfg.seed, "f32")
+    y_h = np.where(lay["ignore"] != 0, -100, y_h).astype(np.int32)
+    x = torch.from_numpy(x_h).to(dev)
+    y = torch.from_numpy(y_h).to(dev)
+    # behaviour log-probs: a setup rl_token_logprob pass + synth's seeded drift (untimed input synthesis)
+    lp0 = torch.empty(N, device=dev)
+    rl.token_logprob(x, y, lp0)
+    tstale = (lay["trainer_version"] - lay["seq_version"])[np.repeat(np.arange(S), cfg.seq_len)]
+    old_h = synth.perturb_old_logp(np.where(y_h >= 0, lp0.cpu().numpy(), 0.0), tstale, lay["big_delta"], cfg, cfg.seed)
+    old = torch.from_numpy(old_h).to(dev)
+    cu = torch.from_numpy(lay["cu_seqlens"].astype(np.int32)).to(dev)
+    cug = torch.from_numpy(lay["cu_groups"].astype(np.int32)).to(dev)
+    rew = torch.from_numpy(lay["rewards"].astype(np.float64)).to(dev)
+    mask = torch.from_numpy(lay["loss_mask"]).to(dev)
+    ver = torch.from_numpy(lay["seq_version"].astype(np.int32)).to(dev)
+    tok = torch.empty(N, dtype=torch.int32, device=dev)
+    act = torch.empty(S, dtype=torch.int32, device=dev)
+    counts = torch.zeros(20, dtype=torch.float64, device=dev)
+    adv = torch.empty(S, device=dev)
+    zv = torch.empty(G, dtype=torch.uint8, device=dev)
+    ws_a = torch.empty(rl.group_advantage_workspace_size(S), dtype=torch.uint8, device=dev)
+    dl = torch.empty_like(x)
+    stats = torch.zeros(12, dtype=torch.float64, device=dev)
+    ws = torch.empty(rl.policy_loss_workspace_size(N, V, rl.F32), dtype=torch.uint8, device=dev)
+    logp = torch.empty(N, device=dev)
+    p = rl.LossParams(trainer_version=lay["trainer_version"], max_staleness=cfg.max_staleness,
+                      active_tokens_dev=counts[0:1])
+
+    def step():
+        rl.seq_bookkeeping(cu, y, V, tok, act, loss_mask=mask, seq_version=ver, trainer_version=lay["trainer_version"],
+                           max_staleness=cfg.max_staleness, counts_out=counts)
+        rl.group_advantage(rew, cug, adv, zv, batch_norm=True, seq_weight=act, workspace=ws_a)
+        rl.policy_loss_fwd_bwd(x, y, old, tok, adv, p, dl, stats, ws, loss_mask=mask, seq_version=ver, logp_out=logp)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i in range(args.steps):
+        step()
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = evs[0].elapsed_time(evs[-1])
+    step_ms = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])
+    # the oracle, as it stands, over the same 512 tokens (the whole chain), on this host
+    import oracle
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        bk = oracle.seq_bookkeeping(lay["cu_seqlens"], lay["loss_mask"], y_h, V, lay["seq_version"],
+                                    lay["trainer_version"], cfg.max_staleness)
+        adv_o, _ = oracle.group_advantage(lay["rewards"], lay["cu_groups"], batch_norm=True,
+                                          seq_weight=bk["seq_active"])
+        oracle.policy_loss_fwd_bwd(x_h.astype(np.float64), y_h, old_h, lay["loss_mask"], bk["token_seq"], adv_o,
+                                   lay["seq_version"], bk["seq_active"],
+                                   oracle.LossParams(global_active_tokens=float(bk["active_tokens"]),
+                                                     trainer_version=lay["trainer_version"],
+                                                     max_staleness=cfg.max_staleness))
+    osecs = (time.perf_counter() - t0) / reps
+    if rank == 0:
+        bpt = 2 * V * 4 + SIDE_BYTES
+        per = float(np.median(step_ms))
+        print(json.dumps({
+            "metric": METRIC, "value": N * args.steps / (ms / 1e3), "unit": "tokens/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "tiny (BASELINE.json configs[0]): 2 prompts x 4 responses x 64 tokens, V=1024, "
+                                   "fp32 logits, 1 GPU", "config": "tiny", "tokens_per_step": N,
+                       "l2": "not flushed: a 4 MB batch is L2-resident; launch-bound (reported for the record)"},
+            "roofline": {"bound": "hbm", "achieved": N * bpt / (per / 1e3) / 1e9, "peak": measured_peak_hbm()[0],
+                         "unit": "GB/s", "frac": N * bpt / (per / 1e3) / 1e9 / measured_peak_hbm()[0],
+                         "traffic": None, "kernel": "whole chain (bookkeeping + advantages + loss, 5 launches)",
+                         "note": "launch-bound: 4 MB per step"},
+            "cpu_baseline": {"value": N / osecs, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                             "sample": f"the full fp64 oracle chain over all {N} tokens: {osecs:.3f} s per pass"},
+            "e2e": None, "gpu_launches": 5 * args.steps, "clocks": clk,
+            "step_ms": {"p10": float(np.percentile(step_ms, 10)), "p50": per,
+                        "p90": float(np.percentile(step_ms, 90))}}), flush=True)
+
+
 def run_lmhead(args):
-    """NEXT 4 forward (not the headline metric): rl_lmhead_logprob on one GPU — a step is one
-    call over 65,536 tokens of a Qwen3-8B-sized head (d = 4096, V = 151936, bf16); tensor roofline
-    (2 N V d flops per call) against MEASURED_PEAKS.json's bf16 figure.  Replicas only for N > 1
-    (independent token batches, no collective): every rank runs its own batch."""
+    """NEXT 4 (not the headline metric): the LM-head policy-loss training step without logits on
+    one GPU — rl_lmhead_logprob (tcgen05 GEMM + online softmax) -> rl_policy_loss_from_logp (loss
+    statistics and s_t) -> rl_lmhead_loss_bwd (tcgen05 logits recompute into G = s (p - onehot) per
+    16,384-token chunk + cuBLAS dh = G W, dW += G^T h) over 65,536 tokens of a Qwen3-8B-sized head
+    (d = 4096, V = 151936, bf16).  Tensor roofline: 8 N V d flops per step (2 forward + 2 recompute
+    + 2 dh + 2 dW) against MEASURED_PEAKS.json's sustained bf16 figure (a long step).  Replicas only
+    for N > 1 (independent token batches, no collective)."""
+    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2605_15565_b200 as rl
@@ -645,7 +789,7 @@ def run_lmhead(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     rl.load()
-    N, d, V = 65536, 4096, 151936
+    N, d, V, C = 65536, 4096, 151936, 16384
     g = torch.Generator(device=dev).manual_seed(1 + rank)
     h = torch.randn(N, d, device=dev, generator=g).to(torch.bfloat16)
     w = (torch.randn(V, d, device=dev, generator=g) * (3.0 / d ** 0.5)).to(torch.bfloat16)
@@ -653,9 +797,30 @@ def run_lmhead(args):
     lp = torch.empty(N, device=dev)
     lse = torch.empty(N, device=dev)
     ws = torch.empty(max(1, rl.lmhead_workspace_size(N, d, V)), dtype=torch.uint8, device=dev)
-    launches = 1 + (rl.lmhead_workspace_size(N, d, V) > 0)
-    for _ in range(args.warmup):
+    # the loss inputs: 256-token sequences, behaviour log-probs = a setup forward pass + drift
+    L = 256
+    S = N // L
+    tseq = (torch.arange(N, device=dev) // L).to(torch.int32)
+    adv = torch.randn(S, device=dev, generator=g)
+    rl.lmhead_logprob(h, w, y, lp, lse, workspace=ws)
+    old = lp + 0.02 * torch.randn(N, device=dev, generator=g)
+    stats = torch.zeros(12, dtype=torch.float64, device=dev)
+    scale = torch.empty(N, device=dev)
+    ws_l = torch.empty(rl.policy_loss_from_logp_workspace_size(N), dtype=torch.uint8, device=dev)
+    p = rl.LossParams(global_active_tokens=float(N))
+    ws_b = torch.empty(rl.lmhead_loss_bwd_workspace_size(C, V), dtype=torch.uint8, device=dev)
+    dh = torch.empty(N, d, device=dev)
+    dW = torch.empty(V, d, device=dev)
+    fwd_launches = 1 + (rl.lmhead_workspace_size(N, d, V) > 0)
+    launches = fwd_launches + 2 + 3 * (N // C)   # fwd (+combine), loss + reduce, per chunk: grad kernel + 2 GEMMs
+
+    def step():
         rl.lmhead_logprob(h, w, y, lp, lse, workspace=ws)
+        rl.policy_loss_from_logp(lp, y, old, tseq, adv, p, stats, ws_l, V, scale_out=scale)
+        rl.lmhead_loss_bwd(h, w, y, lse, scale, ws_b, dhidden=dh, dweight=dW)
+
+    for _ in range(max(3, args.warmup)):
+        step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -664,9 +829,14 @@ def run_lmhead(args):
     time.sleep(0.3)
     stream = torch.cuda.current_stream()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    fe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     evs[0].record(stream)
     for i in range(args.steps):
+        fe[i][0].record(stream)
         rl.lmhead_logprob(h, w, y, lp, lse, workspace=ws)
+        fe[i][1].record(stream)
+        rl.policy_loss_from_logp(lp, y, old, tseq, adv, p, stats, ws_l, V, scale_out=scale)
+        rl.lmhead_loss_bwd(h, w, y, lse, scale, ws_b, dhidden=dh, dweight=dW)
         evs[i + 1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -677,28 +847,38 @@ def run_lmhead(args):
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = tt.item()
-    per_call = ms / args.steps
-    flops = 2.0 * N * V * d
-    achieved = flops / (per_call / 1e3) / 1e12
+    per_step = ms / args.steps
+    step_ms = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])
+    fwd_ms = float(np.mean([a.elapsed_time(b) for a, b in fe]))
+    flops = 8.0 * N * V * d
+    achieved = flops / (per_step / 1e3) / 1e12
     pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peak, src = 2250.0, "fallback (nominal dense bf16)"
     if os.path.exists(pk):
         with open(pk) as f:
-            peak, src = float(json.load(f)["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, cuBLAS burst)"
+            peak, src = float(json.load(f)["bf16_tflops_sustained"]), \
+                "measured (MEASURED_PEAKS.json bf16_tflops_sustained: cuBLAS 8192^3 back to back for 4 s)"
     if rank == 0:
         print(json.dumps({
-            "metric": "fused LM-head log-prob tokens/s (NEXT 4 forward; d=4096, V=151936)",
+            "metric": "fused LM-head policy-loss step tokens/s (NEXT 4 fwd + bwd; d=4096, V=151936)",
             "value": world * N * args.steps / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_call, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "65,536 tokens x Qwen3-8B-sized LM head (d 4096, V 151936) per GPU per step",
+            "config": {"workload": "65,536 tokens x Qwen3-8B-sized LM head (d 4096, V 151936) per GPU per step: "
+                                   "log-prob forward, loss, backward to dh and dW; logits never materialised",
                        "config": "lmhead", "tokens_per_step": world * N, "parallelism": f"replicas x{world}",
-                       "l2": "no flush: every call streams the 1.24 GB weight >> 126 MB L2"},
+                       "bwd_chunk_tokens": C,
+                       "l2": "no flush: every GEMM streams the 1.24 GB weight >> 126 MB L2"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": src,
-                         "kernel": "lmhead_logprob_kernel (+ lmhead_combine_kernel)",
-                         "algorithmic_flops_per_launch": flops, "avg_launch_ms": per_call},
-            "cpu_baseline": None, "e2e": None, "gpu_launches": launches * args.steps, "clocks": clk}), flush=True)
+                         "kernel": "the step: lmhead_kernel<logprob> + lmhead_kernel<grad> + cuBLAS dh / dW GEMMs",
+                         "algorithmic_flops_per_launch": flops, "avg_launch_ms": per_step,
+                         "forward_ms": fwd_ms, "forward_tflops": 2.0 * N * V * d / (fwd_ms / 1e3) / 1e12,
+                         "backward_ms": per_step - fwd_ms,
+                         "backward_tflops": 6.0 * N * V * d / ((per_step - fwd_ms) / 1e3) / 1e12},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": launches * args.steps, "clocks": clk,
+            "step_ms": {"p10": float(np.percentile(step_ms, 10)), "p50": float(np.median(step_ms)),
+                        "p90": float(np.percentile(step_ms, 90))}}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -706,11 +886,14 @@ def run_lmhead(args):
 def measure_e2e(rl, torch, dev, x_dev, y_dev, old_dev, tok_dev, adv_dev, mask_dev, ver_dev, lay, V, args):
     """End-to-end through rl_policy_loss_fwd_bwd_host: every step copies its logits and side
     arrays from pinned host memory (H2D inside the timed region), runs the fused kernel and
-    reads back the loss statistics and per-token log-probs (D2H)."""
-    E = 32768                      # tokens per e2e step (9.96 GB of bf16 logits)
+    reads back the gradient dlogits (bf16, the same size as the logits), the per-token
+    log-probs and the loss statistics (D2H) — the library overlaps the H2D of chunk c+1, the
+    kernel on chunk c and the D2H of chunk c-1 (PCIe is full duplex)."""
+    E = 32768                      # tokens per e2e step (9.96 GB of bf16 logits in, 9.96 GB of dlogits out)
     CH = 4096                      # staging chunk
     x = torch.empty((E, V), dtype=torch.bfloat16, pin_memory=True)
     x.copy_(x_dev[:E])
+    dlh = torch.empty((E, V), dtype=torch.bfloat16, pin_memory=True)
     y, old, tok = y_dev[:E].cpu().pin_memory(), old_dev[:E].cpu().pin_memory(), tok_dev[:E].cpu().pin_memory()
     mask = mask_dev[:E].cpu().pin_memory()
     n_seq = E // 2048
@@ -724,13 +907,14 @@ def measure_e2e(rl, torch, dev, x_dev, y_dev, old_dev, tok_dev, adv_dev, mask_de
         if i == warm:
             t0 = time.perf_counter()
         rl.policy_loss_fwd_bwd_host(x, y, old, tok, adv, p, ws, CH, loss_mask=mask, seq_version=ver,
-                                    logp_out=logp)
+                                    logp_out=logp, dlogits=dlh)
     secs = time.perf_counter() - t0
     h2d = E * V * 2 + E * (4 + 4 + 4 + 1) + n_seq * 8
-    d2h = E * 4 + 80
+    d2h = E * V * 2 + E * 4 + 8 * 12
     return {"value": E * steps / secs, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "seconds": secs, "tokens": E * steps,
-            "sample": f"{E} tokens per step through rl_policy_loss_fwd_bwd_host, {CH}-token chunks"}
+            "sample": f"{E} tokens per step through rl_policy_loss_fwd_bwd_host, {CH}-token chunks, "
+                      "logits in and dlogits out through pinned host memory"}
 
 
 if __name__ == "__main__":
