@@ -20,10 +20,12 @@ timeout 600 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > $O/bench_sh
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > $O/ncu_launch.log 2>&1
 echo "launch list rc=$?" >> $O/status.txt
-prof() { local name=$1 kern=$2; shift 2; timeout 600 ncu --set full --clock-control none --import-source on -k regex:$kern -s 1 -c 1 \
+prof() { local name=$1 kern=$2 skip=$3; shift 3; timeout 600 ncu --set full --clock-control none --import-source on -k regex:$kern -s $skip -c 1 \
   -o $O/prof_$name "$@" > $O/ncu_$name.log 2>&1; echo "prof $name rc=$?" >> $O/status.txt; }
-prof loss_sv loss_sv_kernel python tools/kbench.py --rows 16384 --reps 2
-prof vpcache8 vp_cache python tools/vpbench.py --P 8 --rows 65536 --reps 2 --peer
-prof vpcache4 vp_cache python tools/vpbench.py --P 4 --rows 65536 --reps 2 --peer
-prof lmgrad "lmhead_kernel<true>|lmhead_kernelILb1" python tools/lmbench.py --rows 16384 --reps 1 --bwd
-prof lmfwd "lmhead_kernel<false>|lmhead_kernelILb0" python tools/lmbench.py --rows 16384 --reps 1
+prof loss_sv loss_sv_kernel 1 python tools/kbench.py --rows 16384 --reps 2
+prof vpcache8 vp_cache 1 python tools/vpbench.py --P 8 --rows 65536 --reps 2 --peer
+prof vpcache4 vp_cache 1 python tools/vpbench.py --P 4 --rows 65536 --reps 2 --peer
+# lmbench --bwd --reps 1 launches lmhead_kernel as: forward (warm), forward (timed), then the backward's
+# gradient kernel once per 8,192-token chunk: skip 2 -> the first gradient launch; skip 1 -> a forward
+prof lmgrad lmhead_kernel 2 python tools/lmbench.py --rows 16384 --reps 1 --bwd
+prof lmfwd lmhead_kernel 1 python tools/lmbench.py --rows 16384 --reps 1

@@ -1,5 +1,10 @@
-"""Write the round's ncu evidence under profiles/ from gpurun_out/ (run here, no GPU needed).
-    python tools/summarize_profiles.py r01"""
+"""Write the round's ncu evidence under profiles/ from gpurun_out/<dir>/ (run here, no GPU needed).
+    python tools/summarize_profiles.py r02 gpurun_out/r2
+
+Inputs (tools/bench_round.sh): launches.csv (ncu launch list of a short default bench) and
+prof_<name>.ncu-rep (ncu --set full, one launch each).  Outputs: profiles/launches_<tag>.csv,
+profiles/ncu_summary_<tag>.md and profiles/ncu_traffic.json (per-launch DRAM bytes of the SV kernel
+at the bench's launch size, read by bench.py's roofline "traffic")."""
 import collections
 import csv
 import io
@@ -9,12 +14,26 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
+UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+# name -> (what one captured launch processes, algorithmic bytes or flops of it, the bench's launch scale)
+KERNELS = {
+    "loss_sv": dict(title="loss_sv_kernel: fused fwd+bwd, 16,384 rows x 151,936 bf16 columns (tools/kbench.py)",
+                    rows=16384, bytes_per_row=2 * 151936 * 2 + 17, bench_rows=131072),
+    "vpcache8": dict(title="vp_cache_kernel<6,3>: one rank's shard at P = 8, 65,536 rows x 18,992 columns "
+                           "(tools/vpbench.py --peer)", rows=65536, bytes_per_row=2 * 18992 * 2 + 17, bench_rows=65536),
+    "vpcache4": dict(title="vp_cache_kernel<11,2>: one rank's shard at P = 4, 65,536 rows x 37,984 columns",
+                     rows=65536, bytes_per_row=2 * 37984 * 2 + 17, bench_rows=65536),
+    "lmgrad": dict(title="lmhead_kernel<grad>: logits recompute + G = s (p - onehot), 8,192 tokens x d 4,096 x "
+                         "V 151,936 (one backward chunk of tools/lmbench.py --bwd)", tokens=8192, d=4096, V=151936),
+    "lmfwd": dict(title="lmhead_kernel<logprob>: 16,384 tokens x d 4,096 x V 151,936 (tools/lmbench.py)",
+                  tokens=16384, d=4096, V=151936),
+}
 
 
-def launches(tag):
-    rows = list(csv.reader(open(os.path.join(OUT, "launches_bench.csv"))))
+def launches(src, tag):
+    rows = list(csv.reader(open(os.path.join(src, "launches.csv"))))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h, data = rows[hi], rows[hi + 1:]
     ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
@@ -36,9 +55,6 @@ def launches(tag):
     return "\n".join(lines)
 
 
-UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-
-
 def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
@@ -46,46 +62,55 @@ def raw(rep):
 
 
 def main():
-    tag = sys.argv[1]
+    tag, src = sys.argv[1], sys.argv[2]
     os.makedirs(PROF, exist_ok=True)
-    summary = [f"# ncu evidence, round {tag}", "", "## Launch list of bench.py (our kernels)", "```",
-               launches(tag), "```", ""]
+    summary = [f"# ncu evidence, round {tag} (source: {src}; builder-run, B200, --clock-control none)", "",
+               "## Launch list of bench.py (our kernels)", "```", launches(src, tag), "```", ""]
     traffic = {}
-    for name, rep, rows in (("sv", "prof_loss.ncu-rep", 16384), ("logprob", "prof_logprob.ncu-rep", 16384),
-                            ("vp_finish", "prof_vpfin.ncu-rep", 16384)):
-        p = os.path.join(OUT, rep)
+    for name, kd in KERNELS.items():
+        p = os.path.join(src, f"prof_{name}.ncu-rep")
         if not os.path.exists(p):
             continue
         d, units = raw(p)
+
         def g(k):
             try:
-                return float(d[k].replace(",", ""))
+                return float(d[k].replace(",", "")) * UNITS.get(units.get(k, ""), 1.0)
             except (KeyError, ValueError):
                 return float("nan")
-        rd = g("dram__bytes_read.sum") * UNITS[units["dram__bytes_read.sum"]]
-        wr = g("dram__bytes_write.sum") * UNITS[units["dram__bytes_write.sum"]]
-        unit = 1.0
-        per_tok = (rd + wr) / rows
-        launch_rows = 65536 if name == "vp_finish" else 131072  # the bench's launch of that kernel
-        traffic[name] = {"dram_bytes_per_launch": per_tok * launch_rows, "dram_bytes_per_token": per_tok,
-                         "captured_rows": rows, "read_bytes": rd * unit, "write_bytes": wr * unit,
-                         "note": f"ncu --set full of a {rows}-row launch; per-launch figure scaled to the "
-                                 f"bench's {launch_rows}-row launch"}
-        cols = 37984 if name == "vp_finish" else 151936
-        summary += [f"## ncu --set full: {name} kernel ({rows} rows x {cols} bf16 columns)", "```"]
+        rd, wr = g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
+        summary += [f"## {name}: {kd['title']}", "```"]
         for k in ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
                   "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
                   "sm__throughput.avg.pct_of_peak_sustained_elapsed",
                   "smsp__issue_active.avg.pct_of_peak_sustained_active",
                   "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+                  "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+                  "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
                   "lts__t_sector_hit_rate.pct", "launch__registers_per_thread", "launch__grid_size",
-                  "launch__block_size", "launch__cluster_dim_x" if "launch__cluster_dim_x" in d else "launch__grid_size",
-                  "sm__ctas_launched.sum"]:
+                  "launch__block_size", "launch__cluster_dim_x", "sm__ctas_launched.sum"]:
             if k in d:
-                summary.append(f"{k:60s} {d[k]} {units.get(k, '')}")
-        alg = {"sv": 2 * 151936 * 2 + 17, "logprob": 151936 * 2 + 12, "vp_finish": 2 * 37984 * 2 + 17}[name]
-        summary.append(f"{'algorithmic bytes per token':60s} {alg}")
-        summary.append(f"{'dram bytes per token (measured)':60s} {per_tok:.0f}")
+                summary.append(f"{k:62s} {d[k]} {units.get(k, '')}")
+        if "rows" in kd:
+            alg = kd["bytes_per_row"]
+            per_row = (rd + wr) / kd["rows"]
+            summary.append(f"{'algorithmic bytes per row':62s} {alg}")
+            summary.append(f"{'dram bytes per row (measured)':62s} {per_row:.0f}  ({per_row / alg:.4f} x algorithmic)")
+            traffic[name] = {"dram_bytes_per_launch": per_row * kd["bench_rows"], "dram_bytes_per_row": per_row,
+                             "algorithmic_bytes_per_row": alg, "captured_rows": kd["rows"], "read_bytes": rd,
+                             "write_bytes": wr, "note": f"ncu --set full of a {kd['rows']}-row launch; per-launch "
+                                                        f"figure scaled to the bench's {kd['bench_rows']}-row launch"}
+        else:
+            ops = (kd["tokens"] + kd["V"]) * kd["d"] * 2
+            flops = 2.0 * kd["tokens"] * kd["V"] * kd["d"]
+            t = g("gpu__time_duration.sum") / 1e9 if units.get("gpu__time_duration.sum") == "ns" else \
+                float(d["gpu__time_duration.sum"].replace(",", "")) * {"usecond": 1e-6, "msecond": 1e-3}.get(
+                    units.get("gpu__time_duration.sum", "msecond"), 1e-3)
+            summary.append(f"{'operand bytes (h + W, bf16)':62s} {ops:.3e}")
+            summary.append(f"{'dram read / operand bytes':62s} {rd / ops:.3f}")
+            summary.append(f"{'dram write bytes':62s} {wr:.3e}"
+                           + (f"  (G written: {kd['tokens'] * kd['V'] * 2:.3e})" if name == "lmgrad" else ""))
+            summary.append(f"{'TFLOP/s (2 N V d / duration, under ncu)':62s} {flops / t / 1e12:.1f}")
         st = sorted(((k, g(k)) for k in d if k.startswith("smsp__pcsamp_warps_issue_stalled")
                      and not k.endswith("not_issued")), key=lambda kv: -kv[1])
         tot = sum(v for _, v in st if v == v)
@@ -93,6 +118,8 @@ def main():
         for k, v in st[:8]:
             summary.append(f"   {k.replace('smsp__pcsamp_warps_issue_stalled_', ''):28s} {100 * v / tot:6.2f}%")
         summary += ["```", ""]
+    if "loss_sv" in traffic:
+        traffic["sv"] = traffic["loss_sv"]   # the key bench.py reads
     with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     with open(os.path.join(PROF, f"ncu_summary_{tag}.md"), "w") as f:
