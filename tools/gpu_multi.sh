@@ -13,3 +13,7 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --mas
 done
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29535 \
   bench.py --gpus $N --steps 20 --warmup 3 > $O/bench_single.json 2> $O/bench_single.err; echo "rc=$?" >> $O/bench_single.err
+for cfg in long multi; do
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29536 \
+  bench.py --gpus $N --config $cfg --steps 20 --warmup 3 --no-e2e --no-cpu > $O/bench_$cfg.json 2> $O/bench_$cfg.err; echo "rc=$?" >> $O/bench_$cfg.err
+done
