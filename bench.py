@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
+    ap.add_argument("--vp-kernel", default="cache", choices=["cache", "ring"],
+                    help="vocabpar peer path: register-cache kernel when the shard fits (default) or the L2 ring")
     ap.add_argument("--vp-width-of", type=int, default=0,
                     help="vocabpar on ONE GPU: one rank's share of a P-way split (a [65536, V/P] shard as its own "
                          "vocabulary, exchange with itself) — the per-rank work of configs[3] at P")
@@ -465,6 +467,8 @@ def main():
         rl.dev_set_option(rl.DEV_LOSS_KERNEL, 1)
     if args.vp_path == "nccl":
         rl.dev_set_option(rl.DEV_VP_PATH, 1)
+    if args.vp_kernel == "ring":
+        rl.dev_set_option(rl.DEV_VP_KERNEL, 1)
     comm = None
     if world > 1 or args.config == "vocabpar":
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -537,7 +541,8 @@ def main():
         if args.vp_width_of > 1 and world == 1:
             parallelism = (f"ONE GPU doing one rank's share of a {args.vp_width_of}-way vocabulary split "
                            f"({wl.Vr} columns as its own vocabulary, exchange with itself)")
-        vk = "vp_cache_kernel" if (wl.Vr % 8 == 0 and wl.Vr // 8 <= 11 * 448) else "vp_ring_kernel"
+        vk = "vp_cache_kernel" if (wl.Vr % 8 == 0 and wl.Vr // 8 <= 11 * 448 and args.vp_kernel == "cache") \
+            else "vp_ring_kernel"
         kname = "rl_vocab_parallel_logprob (" + (f"{vk}, in-kernel peer exchange" if fused_vp
                                                  else "vp_stats + NCCL all-gather + vp_finish") + ")"
     else:
