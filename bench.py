@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
     ap.add_argument("--vp-kernel", default="cache", choices=["cache", "ring"],
                     help="vocabpar peer path: register-cache kernel when the shard fits (default) or the L2 ring")
+    ap.add_argument("--vc-rows", type=int, default=-1,
+                    help="vocabpar peer path, vp_cache_kernel: rows parked in shared memory (-1 = default)")
     ap.add_argument("--vp-width-of", type=int, default=0,
                     help="vocabpar on ONE GPU: one rank's share of a P-way split (a [65536, V/P] shard as its own "
                          "vocabulary, exchange with itself) — the per-rank work of configs[3] at P")
@@ -469,6 +471,8 @@ def main():
         rl.dev_set_option(rl.DEV_VP_PATH, 1)
     if args.vp_kernel == "ring":
         rl.dev_set_option(rl.DEV_VP_KERNEL, 1)
+    if args.vc_rows >= 0:
+        rl.dev_set_option(rl.DEV_VC_ROWS, args.vc_rows + 1)
     comm = None
     if world > 1 or args.config == "vocabpar":
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

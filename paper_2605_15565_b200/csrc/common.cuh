@@ -39,7 +39,7 @@ enum DevOpt {
   OPT_LM_SPLITS = 2,    // LM-head vocabulary split override (0 = cost model)
   OPT_VP_KERNEL = 3,    // peer-exchange vocab-parallel kernel: 0 = register cache when it fits, 1 = L2 ring
   OPT_VC_GROUPS = 4,    // vp_cache_kernel collector groups override (0 = min(8, 32 / P))
-  OPT_VC_ROWS = 5,      // vp_cache_kernel rows held for the P >= 8 widths: 0 / 3 = three, 4 = four
+  OPT_VC_ROWS = 5,      // vp_cache_kernel rows parked in shared memory: 0 = default, else that number + 1
   OPT_COUNT = 6
 };
 int dev_option(int key);

@@ -708,7 +708,7 @@ __device__ __forceinline__ float warp_max_redux(float v) {
   return r;
 }
 
-template <int NV, int R>
+template <int NV, int R, int RS>
 __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a) {
   using V = ClVec<bf16_t>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -741,6 +741,9 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
   __syncthreads();
   const uint32_t full_s = sm100::smem_u32(full), empty_s = sm100::smem_u32(empty);
   const uint32_t ring_s = sm100::smem_u32(ring);
+  // RS older rows of e' parked in shared memory after the ring (thread t's vector i of slot s at
+  // ((s NV + i) 448 + t) 16: conflict-free, only the owning thread touches it)
+  const uint32_t rowc_s = ring_s + (uint32_t)a.nslots * (uint32_t)kVcSlot;
 
   if (warp == kVcWarps) {
     if (lane == 0) {  // -------------------------------------------------------- TMA producer
@@ -876,7 +879,6 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
 
   // ------------------------------------------------------------------------------ consumers
   uint4 cache[R][NV];
-  float mw[R];
   const uint32_t my_off = (uint32_t)tid * 16u;
   const uint64_t k2 = f2pack(k, k);
   uint32_t slot = 0, rph = 0;
@@ -927,8 +929,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         own = true;
       }
     }
-    const float m = warp_max_redux(V::max_to_float(mx)) * k;
-    mw[r] = m;
+    const float m = warp_max_redux(V::max_to_float(mx)) * k;  // also the row's red[].x (grad reads it)
     float s = 0.f;
     if (m != -INFINITY) {
       const uint64_t mn2 = f2pack(-m, -m);
@@ -966,38 +967,64 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
       }
     }
   };
-  // dlogits of row kk from cache[r]
-  auto grad_row = [&](auto rc, int64_t kk) {
-    constexpr int r = decltype(rc)::value;
+  // dlogits of row kk from its e' vectors (getv(i): the cached vector i of this thread)
+  auto grad_vecs = [&](int64_t kk, auto&& getv) {
     const int64_t row = row_of(kk);
     const int sl = (int)(kk % kVcScale);
     sm100::mbar_wait(&sh.scale_full[sl], (uint32_t)((kk / kVcScale) & 1));
     const float4 sc = sh.sc[sl];
     const float st = sc.x, c2 = sc.y, dy = sc.z;
     const int ycol = __float_as_int(sc.w);
-    const float q = st == 0.f ? 0.f : st * fast_exp2(mw[r] - c2);
+    const float mw = sh.red[kk % kVcStat][warp].x;  // this warp's exponent reference of the row
+    const float q = st == 0.f ? 0.f : st * fast_exp2(mw - c2);
     const uint32_t qb2 = pack_bf16x2(q, q);
     const float qh = __uint_as_float(qb2 << 16);
     const uint32_t ql2 = pack_bf16x2(q - qh, q - qh);
     uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.dlogits) + row * row_bytes) + tid;
 #pragma unroll
     for (int i = 0; i < NV; ++i)
-      st_stream_v4_if(out + i * kVcCons, V::grad_sv(cache[r][i], qb2, ql2, q), i * kVcCons + tid < nvec);
+      st_stream_v4_if(out + i * kVcCons, V::grad_sv(getv(i), qb2, ql2, q), i * kVcCons + tid < nvec);
     if (st != 0.f && ycol >= 0 && ((ycol >> 3) % kVcCons) == tid)  // same thread, after its vector store
       VecTraits<bf16_t>::store1(reinterpret_cast<char*>(a.dlogits) + row * row_bytes, ycol, dy);
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(&sh.scale_free[sl]);
   };
-  for (int64_t p0 = 0; p0 < nk + R - 1; p0 += R) {
-    static_for<0, R>([&](auto rc) {
-      constexpr int r = decltype(rc)::value;
-      const int64_t p = p0 + r;
-      if (p < nk) load_row(rc, p);
-      const int64_t g = p - (R - 1);
-      if (g >= 0 && g < nk) grad_row(std::integral_constant<int, (r + 1) % R>{}, g);
-    });
+  if constexpr (RS == 0) {
+    // window R - 1 rows: row p is loaded into cache[p % R], row p - R + 1 written from cache[(p + 1) % R]
+    for (int64_t p0 = 0; p0 < nk + R - 1; p0 += R) {
+      static_for<0, R>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        const int64_t p = p0 + r;
+        if (p < nk) load_row(rc, p);
+        const int64_t g = p - (R - 1);
+        constexpr int rg = (r + 1) % R;
+        if (g >= 0 && g < nk) grad_vecs(g, [&](int i) { return cache[rg][i]; });
+      });
+    }
+  } else {
+    // window R + RS - 1 rows: before row p is loaded into cache[p % R], the row held there (p - R)
+    // moves to shared-memory slot (p - R) % RS, whose row (p - R - RS) is written out first
+    for (int64_t p0 = 0; p0 < nk + R + RS; p0 += R) {
+      static_for<0, R>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        const int64_t p = p0 + r;
+        const int64_t g = p - R - RS;
+        if (g >= 0 && g < nk) {
+          const uint32_t base = rowc_s + (uint32_t)((g % RS) * NV * kVcCons) * 16u + my_off;
+          grad_vecs(g, [&](int i) { return sm100::lds128_a(base + (uint32_t)(i * kVcCons * 16)); });
+        }
+        const int64_t mv = p - R;
+        if (mv >= 0 && mv < nk) {
+          const uint32_t base = rowc_s + (uint32_t)((mv % RS) * NV * kVcCons) * 16u + my_off;
+#pragma unroll
+          for (int i = 0; i < NV; ++i) sm100::sts128(base + (uint32_t)(i * kVcCons * 16), cache[r][i]);
+        }
+        if (p < nk) load_row(rc, p);
+      });
+    }
   }
 }
+
 
 // L2 window of the ring kernel: D rows per CTA between a slice's two reads; G rows per service
 // group, published LG groups before they are combined.  D >= (LG + 1) G - 1 is required (the
@@ -1111,11 +1138,19 @@ extern "C" rl_status rl_vocab_parallel_logprob(
     // element); anything else: the L2 re-read ring kernel (same exchange protocol)
     const int64_t nv = vocab_shard / 8;
     if (dtype == RL_BF16 && vocab_shard % 8 == 0 && nv >= 1 && nv <= 11 * kVcCons && dev_option(OPT_VP_KERNEL) != 1) {
+      // rows parked in shared memory (RS): the exchange window is R + RS - 1 rows
+      const bool wide = nv > 6 * kVcCons;
+      const int rs_opt = dev_option(OPT_VC_ROWS);  // 0 = default, else RS + 1
+      const int RS = rs_opt > 0 ? std::min(rs_opt - 1, wide ? 1 : 2) : (wide ? 1 : 2);
+      const int NVc = wide ? 11 : 6;
       const size_t head = (sizeof(VcShared) + 127) & ~(size_t)127;
-      v.nslots = (int)((kSmemMax - head - 256) / (kVcSlot + 16));
-      const size_t smem = ((sizeof(VcShared) + 16 * (size_t)v.nslots + 127) & ~(size_t)127) + (size_t)v.nslots * kVcSlot;
-      auto kern = nv > 6 * kVcCons ? vp_cache_kernel<11, 2>
-                  : dev_option(OPT_VC_ROWS) == 4 ? vp_cache_kernel<6, 4> : vp_cache_kernel<6, 3>;
+      const size_t rowc = (size_t)RS * NVc * kVcCons * 16;
+      v.nslots = (int)((kSmemMax - head - rowc - 256) / (kVcSlot + 16));
+      const size_t smem = ((sizeof(VcShared) + 16 * (size_t)v.nslots + 127) & ~(size_t)127) +
+                          (size_t)v.nslots * kVcSlot + rowc;
+      auto kern = wide ? (RS == 1 ? vp_cache_kernel<11, 2, 1> : vp_cache_kernel<11, 2, 0>)
+                       : (RS == 2 ? vp_cache_kernel<6, 3, 2> : RS == 1 ? vp_cache_kernel<6, 3, 1>
+                                                                      : vp_cache_kernel<6, 3, 0>);
       v.G = std::min(8, std::max(0, dev_option(OPT_VC_GROUPS)));
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return check_launch("cudaFuncSetAttribute(vp_cache_kernel)");

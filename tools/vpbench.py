@@ -37,8 +37,8 @@ def main():
             rl.dev_set_option(rl.DEV_VP_KERNEL, 1)
         if "--groups" in sys.argv:
             rl.dev_set_option(rl.DEV_VC_GROUPS, int(sys.argv[sys.argv.index("--groups") + 1]))
-        if "--rows4" in sys.argv:
-            rl.dev_set_option(rl.DEV_VC_ROWS, 4)
+        if "--rs" in sys.argv:   # rows parked in shared memory
+            rl.dev_set_option(rl.DEV_VC_ROWS, int(sys.argv[sys.argv.index("--rs") + 1]) + 1)
     else:
         rl.dev_set_option(rl.DEV_VP_PATH, 1)
     call = lambda: rl.vocab_parallel_logprob(x, y, 0, Vr, comm, logp, ws, vocab_shard=Vr, old_logp=old,
