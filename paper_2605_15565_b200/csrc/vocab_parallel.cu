@@ -694,6 +694,8 @@ constexpr int kVcStat = 32, kVcScale = 32;
 
 struct VcShared {
   uint32_t cnt[kVcStat];    // consumer warps that posted the row's record
+  uint64_t pub_full[kVcStat];  // the row's shard record (c2, z_y) is in pub[]
+  float2 pub[kVcStat];
   uint64_t scale_full[kVcScale], scale_free[kVcScale];
   float2 red[kVcStat][kVcWarps];
   float zyv[kVcStat];
@@ -731,6 +733,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     for (int i = 0; i < kVcStat; ++i) {
       sh.cnt[i] = 0;
       sh.zyv[i] = 0.f;
+      sm100::mbar_init(&sh.pub_full[i], 1);
     }
     for (int i = 0; i < kVcScale; ++i) {
       sm100::mbar_init(&sh.scale_full[i], 1);
@@ -802,6 +805,14 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
           A = a.seq_adv[seq];
           if (a.seq_active) act = a.seq_active[seq];
         }
+      }
+      {  // publish this rank's record of the row: lane q of the group sends it to rank q
+        const int ss = (int)(kk % kVcStat);
+        sm100::mbar_wait(&sh.pub_full[ss], (uint32_t)((kk / kVcStat) & 1));
+        const float2 pr = sh.pub[ss];
+        const unsigned long long ep = (unsigned long long)a.epoch << 32;
+        st_ll2(a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2, ep | __float_as_uint(pr.x),
+               ep | __float_as_uint(pr.y));
       }
       float c2q = -INFINITY, zyq = 0.f;
       {
@@ -959,11 +970,10 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         const float zr = sh.zyv[ss];
         sh.zyv[ss] = 0.f;
         atomicExch(&sh.cnt[ss], 0u);
-        const float c2 = S > 0.f ? M + fast_log2(S) : -INFINITY;
-        const unsigned long long ep = (unsigned long long)a.epoch << 32;
-        const int64_t row = row_of(kk);
-        for (int q = 0; q < a.P; ++q)
-          st_ll2(a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2, ep | __float_as_uint(c2), ep | __float_as_uint(zr));
+        // hand the record to the collector, which sends it (remote NVLink stores stay off the
+        // consumers' path: a consumer warp stalled on them holds every ring slot of the CTA)
+        sh.pub[ss] = make_float2(S > 0.f ? M + fast_log2(S) : -INFINITY, zr);
+        sm100::mbar_arrive(&sh.pub_full[ss]);
       }
     }
   };
@@ -1141,7 +1151,7 @@ extern "C" rl_status rl_vocab_parallel_logprob(
       // rows parked in shared memory (RS): the exchange window is R + RS - 1 rows
       const bool wide = nv > 6 * kVcCons;
       const int rs_opt = dev_option(OPT_VC_ROWS);  // 0 = default, else RS + 1
-      const int RS = rs_opt > 0 ? std::min(rs_opt - 1, wide ? 1 : 2) : (wide ? 1 : 2);
+      const int RS = rs_opt > 0 ? std::min(rs_opt - 1, wide ? 1 : 2) : (wide ? 1 : 0);
       const int NVc = wide ? 11 : 6;
       const size_t head = (sizeof(VcShared) + 127) & ~(size_t)127;
       const size_t rowc = (size_t)RS * NVc * kVcCons * 16;
