@@ -59,7 +59,13 @@ def _stale(force: bool) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    """variant "trace": a development build with -DRL_VC_TRACE (vp_cache_kernel cycle counters,
+    rl_debug_vc_trace) into librlpolicy_trace.so; never the product library."""
+    global BUILD, LIB
+    if variant:
+        BUILD = os.path.join(ROOT, f"build_{variant}")
+        LIB = os.path.join(PKG, f"librlpolicy_{variant}.so")
     if not _stale(force):
         return LIB
     os.makedirs(BUILD, exist_ok=True)
@@ -67,7 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = _nvcc()
     common = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
               "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-Xptxas", "-v",
-              "--expt-relaxed-constexpr"]
+              "--expt-relaxed-constexpr"] + (["-DRL_VC_TRACE"] if variant == "trace" else [])
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
         extra = ["-fmad=false"] if os.path.basename(src) == "advantage.cu" else []
@@ -101,5 +107,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    v = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else ""
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=v))

@@ -692,6 +692,18 @@ constexpr int kVcSlot = kVcChunkVec * 16;      // 28 KB
 constexpr int kVcColl = 0;  // first collector lane
 constexpr int kVcStat = 32, kVcScale = 32;
 
+#ifdef RL_VC_TRACE
+// development build only (python -m paper_2605_15565_b200.build --variant trace): per-CTA cycle
+// counters — 0 consumer wait for the row scale, 1 consumer wait for ring data, 2 collector wait for
+// the row's own record, 3 collector poll for the peers' records, 4 collector chain per row, 5 rows
+__device__ unsigned long long g_vc_trace[256][8];
+#define RL_VC_T0(v) const long long v = clock64()
+#define RL_VC_ADD(i, v) do { if (blockIdx.x < 256) atomicAdd(&g_vc_trace[blockIdx.x][i], (unsigned long long)(clock64() - (v))); } while (0)
+#else
+#define RL_VC_T0(v)
+#define RL_VC_ADD(i, v)
+#endif
+
 struct VcShared {
   uint32_t cnt[kVcStat];    // consumer warps that posted the row's record
   uint64_t pub_full[kVcStat];  // the row's shard record (c2, z_y) is in pub[]
@@ -806,15 +818,18 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
           if (a.seq_active) act = a.seq_active[seq];
         }
       }
+      RL_VC_T0(tc0);
       {  // publish this rank's record of the row: lane q of the group sends it to rank q
         const int ss = (int)(kk % kVcStat);
         sm100::mbar_wait(&sh.pub_full[ss], (uint32_t)((kk / kVcStat) & 1));
+        if (grp == 0 && q == 0) RL_VC_ADD(2, tc0);
         const float2 pr = sh.pub[ss];
         const unsigned long long ep = (unsigned long long)a.epoch << 32;
         st_ll2(a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2, ep | __float_as_uint(pr.x),
                ep | __float_as_uint(pr.y));
       }
       float c2q = -INFINITY, zyq = 0.f;
+      RL_VC_T0(tc1);
       {
         const unsigned long long* slot = a.xr[a.me] + ((int64_t)q * a.max_tokens + row) * 2;
         unsigned long long w0, w1;
@@ -833,6 +848,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         c2q = __uint_as_float((uint32_t)w0);
         zyq = __uint_as_float((uint32_t)w1);
       }
+      if (grp == 0 && q == 0) RL_VC_ADD(3, tc1);
       load_l1(kk + G);
       float M = -INFINITY;
       for (int j = 0; j < a.P; ++j) M = fmaxf(M, __shfl_sync(gmask, c2q, lead + j));
@@ -873,6 +889,12 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         if (kk >= kVcScale) sm100::mbar_wait_polite(&sh.scale_free[sl], (uint32_t)(((kk / kVcScale) - 1) & 1), false);
         sh.sc[sl] = make_float4(st, c2, dy, __int_as_float(ycol));
         sm100::mbar_arrive(&sh.scale_full[sl]);
+        if (grp == 0) {
+          RL_VC_ADD(4, tc0);
+#ifdef RL_VC_TRACE
+          if (blockIdx.x < 256) atomicAdd(&g_vc_trace[blockIdx.x][5], 1ull);
+#endif
+        }
       }
     }
       if (q == 0)
@@ -905,7 +927,9 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
 #pragma unroll
     for (int c = 0; c < (NV + 3) / 4; ++c) {
       if (c < nch) {
+        RL_VC_T0(tf0);
         sm100::mbar_wait_a(full_s + slot * 8, rph);
+        if (tid == 0) RL_VC_ADD(1, tf0);
         const uint32_t sb = ring_s + slot * (uint32_t)kVcSlot;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -981,7 +1005,9 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
   auto grad_vecs = [&](int64_t kk, auto&& getv) {
     const int64_t row = row_of(kk);
     const int sl = (int)(kk % kVcScale);
+    RL_VC_T0(tw0);
     sm100::mbar_wait(&sh.scale_full[sl], (uint32_t)((kk / kVcScale) & 1));
+    if (tid == 0) RL_VC_ADD(0, tw0);
     const float4 sc = sh.sc[sl];
     const float st = sc.x, c2 = sc.y, dy = sc.z;
     const int ycol = __float_as_int(sc.w);
@@ -1214,3 +1240,16 @@ extern "C" rl_status rl_vocab_parallel_logprob(
   if (st != RL_OK) return st;
   return launch_stats_reduce(partials, tgrid, stats, accumulate, s);
 }
+
+#ifdef RL_VC_TRACE
+// development build only: copy (and optionally clear) the vp_cache_kernel cycle counters
+extern "C" int rl_debug_vc_trace(unsigned long long* host, size_t bytes, int clear) {
+  const size_t n = sizeof(rl::g_vc_trace) < bytes ? sizeof(rl::g_vc_trace) : bytes;
+  if (host && cudaMemcpyFromSymbol(host, rl::g_vc_trace, n) != cudaSuccess) return 1;
+  if (clear) {
+    static unsigned long long zero[256 * 8] = {};
+    if (cudaMemcpyToSymbol(rl::g_vc_trace, zero, sizeof(zero)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+#endif
