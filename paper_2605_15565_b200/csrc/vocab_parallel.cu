@@ -285,6 +285,7 @@ struct VrArgs {
   Knobs kn;
   int32_t count_stats, P, me;
   int32_t G, LG, D, nslots;
+  int32_t pub_mode;  // vp_cache_kernel: 0 collector sends (strong), 1 last consumer warp (weak), 2 collector (weak)
   uint32_t epoch;
   unsigned long long* xr[8];  // rank q's slots of this call's parity: [src P][max_tokens] x 2 words
 };
@@ -300,6 +301,11 @@ struct VrShared {
 
 __device__ __forceinline__ void st_ll2(unsigned long long* p, unsigned long long a, unsigned long long b) {
   asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+// weak (posted) form: no ordering with the thread's later accesses is requested, so the store does
+// not hold up the issuing thread; each 8-byte word stays single-copy atomic
+__device__ __forceinline__ void st_ll2_weak(unsigned long long* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 __device__ __forceinline__ void ld_ll2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
   asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
@@ -825,8 +831,9 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         if (grp == 0 && q == 0) RL_VC_ADD(2, tc0);
         const float2 pr = sh.pub[ss];
         const unsigned long long ep = (unsigned long long)a.epoch << 32;
-        st_ll2(a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2, ep | __float_as_uint(pr.x),
-               ep | __float_as_uint(pr.y));
+        unsigned long long* dst = a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2;
+        if (a.pub_mode == 0) st_ll2(dst, ep | __float_as_uint(pr.x), ep | __float_as_uint(pr.y));
+        else if (a.pub_mode == 2) st_ll2_weak(dst, ep | __float_as_uint(pr.x), ep | __float_as_uint(pr.y));
       }
       float c2q = -INFINITY, zyq = 0.f;
       RL_VC_T0(tc1);
@@ -994,9 +1001,17 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         const float zr = sh.zyv[ss];
         sh.zyv[ss] = 0.f;
         atomicExch(&sh.cnt[ss], 0u);
-        // hand the record to the collector, which sends it (remote NVLink stores stay off the
-        // consumers' path: a consumer warp stalled on them holds every ring slot of the CTA)
-        sh.pub[ss] = make_float2(S > 0.f ? M + fast_log2(S) : -INFINITY, zr);
+        const float c2r = S > 0.f ? M + fast_log2(S) : -INFINITY;
+        if (a.pub_mode == 1) {  // this warp sends the record itself, weak (posted) stores
+          const unsigned long long ep = (unsigned long long)a.epoch << 32;
+          const int64_t row = row_of(kk);
+          for (int q = 0; q < a.P; ++q)
+            st_ll2_weak(a.xr[q] + ((int64_t)a.me * a.max_tokens + row) * 2, ep | __float_as_uint(c2r),
+                        ep | __float_as_uint(zr));
+        }
+        // hand the record to the collector, which sends it (pub_mode 0 / 2: remote NVLink stores
+        // stay off the consumers' path; a consumer warp stalled on them holds every ring slot)
+        sh.pub[ss] = make_float2(c2r, zr);
         sm100::mbar_arrive(&sh.pub_full[ss]);
       }
     }
@@ -1188,6 +1203,7 @@ extern "C" rl_status rl_vocab_parallel_logprob(
                        : (RS == 2 ? vp_cache_kernel<6, 3, 2> : RS == 1 ? vp_cache_kernel<6, 3, 1>
                                                                       : vp_cache_kernel<6, 3, 0>);
       v.G = std::min(8, std::max(0, dev_option(OPT_VC_GROUPS)));
+      v.pub_mode = std::min(2, std::max(0, dev_option(OPT_VC_PUB)));
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return check_launch("cudaFuncSetAttribute(vp_cache_kernel)");
       kern<<<grid, kVcThreads, smem, s>>>(v);
