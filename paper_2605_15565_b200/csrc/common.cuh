@@ -40,7 +40,7 @@ enum DevOpt {
   OPT_VP_KERNEL = 3,    // peer-exchange vocab-parallel kernel: 0 = register cache when it fits, 1 = L2 ring
   OPT_VC_GROUPS = 4,    // vp_cache_kernel collector groups override (0 = min(8, 32 / P))
   OPT_VC_ROWS = 5,      // vp_cache_kernel rows parked in shared memory: 0 = default, else that number + 1
-  OPT_VC_PUB = 6,       // vp_cache_kernel record send: 0 collector strong, 1 last warp weak, 2 collector weak
+  OPT_VC_PUB = 6,       // vp_cache_kernel record send, value + 1: 0 collector strong, 1 last warp weak (default), 2 collector weak
   OPT_COUNT = 7
 };
 int dev_option(int key);

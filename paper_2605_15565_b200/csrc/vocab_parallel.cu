@@ -1203,7 +1203,7 @@ extern "C" rl_status rl_vocab_parallel_logprob(
                        : (RS == 2 ? vp_cache_kernel<6, 3, 2> : RS == 1 ? vp_cache_kernel<6, 3, 1>
                                                                       : vp_cache_kernel<6, 3, 0>);
       v.G = std::min(8, std::max(0, dev_option(OPT_VC_GROUPS)));
-      v.pub_mode = std::min(2, std::max(0, dev_option(OPT_VC_PUB)));
+      v.pub_mode = dev_option(OPT_VC_PUB) > 0 ? std::min(2, dev_option(OPT_VC_PUB) - 1) : 1;  // default: last warp, weak
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return check_launch("cudaFuncSetAttribute(vp_cache_kernel)");
       kern<<<grid, kVcThreads, smem, s>>>(v);

@@ -29,7 +29,7 @@ def main():
     lib.rl_debug_vc_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
     comm = rl.Comm.from_torch() if world > 1 else rl.Comm.local()
     if "--pub" in sys.argv:
-        rl.dev_set_option(6, int(sys.argv[sys.argv.index("--pub") + 1]))
+        rl.dev_set_option(6, int(sys.argv[sys.argv.index("--pub") + 1]) + 1)
     if "--rs" in sys.argv:
         rl.dev_set_option(5, int(sys.argv[sys.argv.index("--rs") + 1]) + 1)
     V, N = 151936, 65536
