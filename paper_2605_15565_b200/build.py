@@ -61,7 +61,8 @@ def _stale(force: bool) -> bool:
 
 def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     """variant "trace": a development build with -DRL_VC_TRACE (vp_cache_kernel cycle counters,
-    rl_debug_vc_trace) into librlpolicy_trace.so; never the product library."""
+    rl_debug_vc_trace) into librlpolicy_trace.so; variant "checks": -DRL_DEBUG_CHECKS (device-side
+    bounds assertions) into librlpolicy_checks.so.  Neither is the product library."""
     global BUILD, LIB
     if variant:
         BUILD = os.path.join(ROOT, f"build_{variant}")
@@ -73,7 +74,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     nvcc = _nvcc()
     common = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
               "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-Xptxas", "-v",
-              "--expt-relaxed-constexpr"] + (["-DRL_VC_TRACE"] if variant == "trace" else [])
+              "--expt-relaxed-constexpr"] + {"trace": ["-DRL_VC_TRACE"], "checks": ["-DRL_DEBUG_CHECKS"]}.get(variant, [])
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
         extra = ["-fmad=false"] if os.path.basename(src) == "advantage.cu" else []

@@ -45,6 +45,26 @@ enum DevOpt {
 };
 int dev_option(int key);
 
+// ---------------------------------------------------------------- debug checks
+// python -m paper_2605_15565_b200.build --variant checks (-DRL_DEBUG_CHECKS): bounds / index
+// assertions at the kernels' global stores and ring accesses (the stand-in for compute-sanitizer,
+// which this GPU pool refuses); compiled out of the product library.
+#ifdef RL_DEBUG_CHECKS
+#include <cstdio>
+#define RL_DCHECK(c)                                                                                    \
+  do {                                                                                                  \
+    if (!(c)) {                                                                                         \
+      printf("RL_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, blockIdx.x, \
+             threadIdx.x);                                                                              \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define RL_DCHECK(c) \
+  do {               \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- element access
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }

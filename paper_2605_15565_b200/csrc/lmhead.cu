@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
           if (y - c0 == 2 * i + 1) g1 = st * (exp2f(e1) - 1.f);
           o[i] = pack_bf16x2(g0, g1);
         }
+        RL_DCHECK(!live || (row < a.n && c0 < a.V && c0 + 32 <= a.ld_g + 31));
         if (live && c0 + 32 <= a.V) {
           uint4* dst = reinterpret_cast<uint4*>(grow + c0);
 #pragma unroll

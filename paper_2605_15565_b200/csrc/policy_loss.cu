@@ -90,9 +90,11 @@ __global__ void __launch_bounds__(kL2Threads) loss_two_pass_kernel(
       }
       const int64_t c0 = i * EPV;
       onehot_sub(f, y - c0, s);  // static indices: f stays in registers
+      RL_DCHECK(i < nvec);
       st_stream_v4(vout + i, VecTraits<T>::pack(f));
     }
     for (int64_t c = nvec * EPV + threadIdx.x; c < V; c += kL2Threads) {
+      RL_DCHECK(c < V);
       const float x = VecTraits<T>::load1(rp, c);
       const float pv = fast_exp2(fmaf(x, k, -c2));
       if (ent) pz = fmaf(pv, x, pz);

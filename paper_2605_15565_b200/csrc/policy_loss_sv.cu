@@ -263,9 +263,12 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
 #pragma unroll
         for (int j = 0; j < NCH; ++j) {
           if (RL_PRESENT(j)) {
+            RL_DCHECK(!(stores && RL_MINE(j)) ||
+                      (row - ncl >= 0 && row - ncl < a.n_tokens && v0 + tid + j * kChunkVec < a.nvec));
             st_stream_v4_if(out + j * kChunkVec, ClVec<T>::grad_sv(cache[j], qb2, ql2, q),
                             stores && RL_MINE(j));
             if (NEED) {
+              RL_DCHECK(slot < (uint32_t)nslots && row < a.n_tokens);
               if (j % VPT == 0) sm100::mbar_wait_a(full_s + slot * 8, rph);
               const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)(VPT * kChunkBytes) + (j % VPT) * kChunkBytes + my_off);
               if (RL_CHUNK_END(j)) sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
@@ -292,6 +295,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       };
       chunk_loop(std::integral_constant<int, 2>{});  // runtime need (one loop body: no spills)
       if (tail_mine) {
+        RL_DCHECK(!stores || (a.nvec * EPV + tid < a.V && row - ncl < a.n_tokens));
         if (stores) VecTraits<T>::store1(dp, a.nvec * EPV + tid, xt * q);
         xt = 0.f;
         if (need) {
@@ -305,6 +309,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
       if (mode == SV_GRAD && ycol >= 0) {
         const bool in_tail = ycol >= a.nvec * EPV;
         const int owner = in_tail ? (int)(ycol - a.nvec * EPV) : (int)((ycol / EPV - v0) % kChunkVec);
+        RL_DCHECK(tid != owner || (ycol < a.V && row - ncl >= 0 && row - ncl < a.n_tokens));
         if (tid == owner) VecTraits<T>::store1(dp, ycol, dy);
       }
       if (!has_row) break;

@@ -629,6 +629,7 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
     if (j >= D) {  // ---- pass 2 of row j - D
       const int64_t kk = j - D;
       const int64_t row = row_of(kk);
+      RL_DCHECK(row < a.n);
       const int sl = (int)(kk % kVrScale);
       sm100::mbar_wait(&sh.scale_full[sl], (uint32_t)((kk / kVrScale) & 1));
       const float4 r = sh.sc[sl];
@@ -662,6 +663,7 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
         VecTraits<T>::store1(dp, cc, v);
       }
       // the target column: rewritten by the thread that stored its vector (same-thread order)
+      RL_DCHECK(ycol < a.Vr);
       if (s != 0.f && ycol >= 0 && ycol < tail0 && (ycol / EPV) % kVrCons == tid) VecTraits<T>::store1(dp, ycol, dy);
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&sh.scale_free[sl]);
@@ -838,6 +840,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
       float c2q = -INFINITY, zyq = 0.f;
       RL_VC_T0(tc1);
       {
+        RL_DCHECK(q < a.P && row < a.max_tokens);
         const unsigned long long* slot = a.xr[a.me] + ((int64_t)q * a.max_tokens + row) * 2;
         unsigned long long w0, w1;
         const unsigned long long t0 = globaltimer();
@@ -934,6 +937,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
 #pragma unroll
     for (int c = 0; c < (NV + 3) / 4; ++c) {
       if (c < nch) {
+        RL_DCHECK(slot < (uint32_t)a.nslots && row_of(kk) < a.n);
         RL_VC_T0(tf0);
         sm100::mbar_wait_a(full_s + slot * 8, rph);
         if (tid == 0) RL_VC_ADD(1, tf0);
@@ -1032,6 +1036,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     const float qh = __uint_as_float(qb2 << 16);
     const uint32_t ql2 = pack_bf16x2(q - qh, q - qh);
     uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.dlogits) + row * row_bytes) + tid;
+    RL_DCHECK(row < a.n && ycol < a.Vr);
 #pragma unroll
     for (int i = 0; i < NV; ++i)
       st_stream_v4_if(out + i * kVcCons, V::grad_sv(getv(i), qb2, ql2, q), i * kVcCons + tid < nvec);
@@ -1062,6 +1067,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         const int64_t g = p - R - RS;
         if (g >= 0 && g < nk) {
           const uint32_t base = rowc_s + (uint32_t)((g % RS) * NV * kVcCons) * 16u + my_off;
+          RL_DCHECK(base + (uint32_t)((NV - 1) * kVcCons * 16) < rowc_s + (uint32_t)(RS * NV * kVcCons * 16));
           grad_vecs(g, [&](int i) { return sm100::lds128_a(base + (uint32_t)(i * kVcCons * 16)); });
         }
         const int64_t mv = p - R;
