@@ -1,6 +1,7 @@
 // Shared device helpers for the sm_100a kernels of the policy-loss path.
 // (CUDA side only; the CPU oracle in oracle/ shares nothing with this file.)
 #pragma once
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -50,7 +51,6 @@ int dev_option(int key);
 // assertions at the kernels' global stores and ring accesses (the stand-in for compute-sanitizer,
 // which this GPU pool refuses); compiled out of the product library.
 #ifdef RL_DEBUG_CHECKS
-#include <cstdio>
 #define RL_DCHECK(c)                                                                                    \
   do {                                                                                                  \
     if (!(c)) {                                                                                         \
