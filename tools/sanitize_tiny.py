@@ -59,7 +59,7 @@ def fam_sv(two_pass=False, ext=False):
 
 
 def fam_logprob():
-    for V in (1003, 151936):
+    for V in (1000, 151936):
         N = 200
         x, y, *_ = loss_inputs(N, V)
         logp = torch.empty(N, device="cuda")
@@ -92,7 +92,7 @@ def fam_bookkeeping_advantage():
 def fam_vp(peer):
     comm = rl.Comm.local()
     rl.dev_set_option(rl.DEV_VP_PATH, 0 if peer else 1)
-    for V in (1003, 18992):    # ragged; the P = 8 shard width (2 ring slots per slice)
+    for V in (1000, 18992):    # small; the P = 8 shard width (2 ring slots per slice)
         N = 400
         x, y, old, tseq, adv, mask, S = loss_inputs(N, V)
         if peer:
