@@ -215,6 +215,8 @@ def group_advantage(rewards, cu_groups, adv_out, zero_var_out=None, std_mode=STD
                     eps=1e-6, batch_norm=False, bn_eps=1e-6, seq_weight=None, workspace=None,
                     stream=None):
     lib = load()
+    if rewards.element_size() != 8 or cu_groups.element_size() != 4:
+        raise RLError("rewards must be float64 and cu_groups int32 (rl_group_advantage)")
     n_groups = cu_groups.numel() - 1
     n_seq = rewards.numel()
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()

@@ -79,7 +79,7 @@ def fam_bookkeeping_advantage():
     rl.seq_bookkeeping(cu, y, V, tok, act, loss_mask=(torch.rand(N, device="cuda") < 0.5).to(torch.uint8),
                        seq_version=torch.tensor([3, 9, 10, 12], dtype=torch.int32, device="cuda"),
                        trainer_version=11, max_staleness=1, counts_out=counts)
-    rewards = torch.rand(64, device="cuda")
+    rewards = torch.rand(64, device="cuda", dtype=torch.float64)
     cug = torch.arange(0, 65, 8, dtype=torch.int32, device="cuda")
     adv = torch.empty(64, device="cuda")
     zv = torch.empty(8, dtype=torch.uint8, device="cuda")
