@@ -13,6 +13,12 @@
  *                         the split count (clamped to what the workspace holds)
  *   3 RL_DEV_VP_KERNEL    peer-exchange vocab-parallel kernel: 0 = register-cache kernel when the
  *                         shard fits it (default), 1 = the L2 re-read ring kernel
+ *   4 RL_DEV_VC_GROUPS    vp_cache_kernel collector groups (0 = min(8, 32 / P))
+ *   5 RL_DEV_VC_ROWS      vp_cache_kernel rows parked in shared memory + 1 (0 = default)
+ *   6 RL_DEV_VC_PUB       vp_cache_kernel record send + 1: 0 collector (strong stores), 1 last
+ *                         consumer warp (weak stores; default), 2 collector (weak stores)
+ *   7 RL_DEV_LM_PAIR      LM-head kernels: 0 = CTA pairs (cta_group::2) when there are >= 2 token
+ *                         blocks (default), 1 = single CTAs
  * Options are read at launch time; set them before the calls they should affect.
  */
 #ifndef RL_POLICY_DEV_H_
@@ -25,6 +31,10 @@ extern "C" {
 #define RL_DEV_VP_PATH 1
 #define RL_DEV_LM_SPLITS 2
 #define RL_DEV_VP_KERNEL 3
+#define RL_DEV_VC_GROUPS 4
+#define RL_DEV_VC_ROWS 5
+#define RL_DEV_VC_PUB 6
+#define RL_DEV_LM_PAIR 7
 int32_t rl_dev_set_option(int32_t key, int32_t value);
 #ifdef __cplusplus
 }

@@ -27,6 +27,11 @@
 namespace rl {
 
 constexpr int kLmBM = 128, kLmBN = 256, kLmBK = 64, kLmStages = 4;
+// PAIR mode (cta_group::2): a cluster of two CTAs = 256 token rows x one 256-row W tile per MMA
+// (M = 256); each CTA stages its own 128 token rows and HALF of the W tile (128 rows), so the W
+// bytes per SM halve and six 32 KB stages fit where four 48 KB ones did
+constexpr int kLmPairStages = 6;
+constexpr uint32_t kLmPairBBytes = (kLmBN / 2) * kLmBK * 2;
 constexpr int kLmThreads = 192;
 constexpr uint32_t kLmABytes = kLmBM * kLmBK * 2, kLmBBytes = kLmBN * kLmBK * 2;
 constexpr uint32_t kLmStageBytes = kLmABytes + kLmBBytes;  // 48 KB
@@ -112,17 +117,56 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
 constexpr uint32_t kLmIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kLmBN >> 3) << 17) |
                               ((uint32_t)(kLmBM >> 4) << 24);
+constexpr uint32_t kLmPairIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kLmBN >> 3) << 17) |
+                                  ((uint32_t)((2 * kLmBM) >> 4) << 24);
+
+// PAIR-mode primitives: the MMA of the CTA pair (issued by the leader), its commit multicast to
+// both CTAs' barrier at the same offset, and the TMA load whose completion lands on the LEADER's
+// barrier (a shared::cluster address from mapa)
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   sm100::smem_u32(bar)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(sm100::smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
 
 // GRAD = false: the log-prob epilogue (online max / sum over the row's tiles, rl_lmhead_logprob).
 // GRAD = true:  the gradient epilogue (rl_lmhead_loss_bwd): every logits tile is recomputed and
 //               turned straight into G = s_t (2^(x k - lse2) - [v == y]) in bf16 (one rounding) —
 //               the logits themselves are never written.
-template <bool GRAD>
+// PAIR: launched as clusters of (1, 2, 1) CTAs — consecutive token blocks share every W tile
+template <bool GRAD, bool PAIR = false>
 __global__ void __launch_bounds__(kLmThreads, 1)
     lmhead_kernel(const __grid_constant__ CUtensorMap tm_h, const __grid_constant__ CUtensorMap tm_w,
                   const LmArgs a) {
+  constexpr int STAGES = PAIR ? kLmPairStages : kLmStages;
+  constexpr uint32_t BBYTES = PAIR ? kLmPairBBytes : kLmBBytes;
+  constexpr uint32_t STAGE = kLmABytes + BBYTES;
   extern __shared__ uint8_t lm_smem_raw[];
-  __shared__ __align__(8) uint64_t full[kLmStages], empty[kLmStages], acc_full[2], acc_empty[2];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2];
+  const uint32_t crank = PAIR ? sm100::cluster_ctarank() : 0;
+  const bool leader = crank == 0;
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = (sm100::smem_u32(lm_smem_raw) + 1023u) & ~1023u;
@@ -134,24 +178,32 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   const int jt1 = min(a.vtiles, jt0 + a.tiles_per_split);
   const int ntiles = max(0, jt1 - jt0);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kLmStages; ++i) {
-      sm100::mbar_init(&full[i], 1);
+    for (int i = 0; i < STAGES; ++i) {
+      sm100::mbar_init(&full[i], PAIR ? 2 : 1);  // PAIR: the leader's full[] takes both producers
       sm100::mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&acc_full[i], 1);
-      sm100::mbar_init(&acc_empty[i], 4);
+      sm100::mbar_init(&acc_empty[i], PAIR ? 8 : 4);  // PAIR: both CTAs' epilogue warps, at the leader
     }
     sm100::fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     sm100::smem_u32(&tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       sm100::smem_u32(&tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       sm100::smem_u32(&tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) sm100::cluster_sync();  // the peer's barriers exist before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const int total = ntiles * a.kblocks;
@@ -159,36 +211,50 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
       for (int it = 0; it < total; ++it) {
-        const int st = it % kLmStages;
-        const uint32_t ph = (uint32_t)(it / kLmStages) & 1u;
+        const int st = it % STAGES;
+        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
         sm100::mbar_wait(&empty[st], ph ^ 1u);
         const int j = jt0 + it / a.kblocks, kb = it % a.kblocks;
-        const uint32_t sa = sbase + (uint32_t)st * kLmStageBytes, sb = sa + kLmABytes;
-        sm100::mbar_arrive_expect_tx(&full[st], kLmStageBytes);
-        tma_load_2d(sa, &tm_h, kb * kLmBK, (int32_t)m0, &full[st]);
-        tma_load_2d(sb, &tm_w, kb * kLmBK, j * kLmBN, &full[st]);
+        const uint32_t sa = sbase + (uint32_t)st * STAGE, sb = sa + kLmABytes;
+        if (PAIR) {  // both CTAs' copies complete on the leader's full[st]; the leader expects both
+          const uint32_t lbar = cluster_addr(&full[st], 0);
+          if (leader) sm100::mbar_arrive_expect_tx(&full[st], 2 * STAGE);
+          else sm100::mbar_arrive_remote(&full[st], 0);
+          tma_load_2d_pair(sa, &tm_h, kb * kLmBK, (int32_t)m0, lbar);
+          tma_load_2d_pair(sb, &tm_w, kb * kLmBK, j * kLmBN + (int32_t)crank * (kLmBN / 2), lbar);
+        } else {
+          sm100::mbar_arrive_expect_tx(&full[st], STAGE);
+          tma_load_2d(sa, &tm_h, kb * kLmBK, (int32_t)m0, &full[st]);
+          tma_load_2d(sb, &tm_w, kb * kLmBK, j * kLmBN, &full[st]);
+        }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+    if (lane == 0 && leader) {  // --------------------------------------- MMA issuer (PAIR: the leader)
       int it = 0;
       for (int j = 0; j < ntiles; ++j) {
         const int acc = j & 1;
-        sm100::mbar_wait(&acc_empty[acc], (((uint32_t)j >> 1) & 1u) ^ 1u);
+        if (PAIR) sm100::mbar_wait_cluster(&acc_empty[acc], (((uint32_t)j >> 1) & 1u) ^ 1u);
+        else sm100::mbar_wait(&acc_empty[acc], (((uint32_t)j >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t td = tmem + (uint32_t)acc * kLmBN;
         for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
-          const int st = it % kLmStages;
-          sm100::mbar_wait(&full[st], (uint32_t)(it / kLmStages) & 1u);
+          const int st = it % STAGES;
+          if (PAIR) sm100::mbar_wait_cluster(&full[st], (uint32_t)(it / STAGES) & 1u);
+          else sm100::mbar_wait(&full[st], (uint32_t)(it / STAGES) & 1u);
           tc_fence_after();
-          const uint32_t sa = sbase + (uint32_t)st * kLmStageBytes, sb = sa + kLmABytes;
+          const uint32_t sa = sbase + (uint32_t)st * STAGE, sb = sa + kLmABytes;
           const uint64_t ad = umma_desc_sw128(sa), bd = umma_desc_sw128(sb);
 #pragma unroll
-          for (int k = 0; k < kLmBK / 16; ++k)  // K = 16 bf16 = 32 B per MMA: start address + 2 (16-B units)
-            umma_bf16(td, ad + 2 * k, bd + 2 * k, kLmIdesc, (kb | k) != 0);
-          umma_commit(&empty[st]);  // smem slot free once these MMAs have read it
+          for (int k = 0; k < kLmBK / 16; ++k) {  // K = 16 bf16 = 32 B per MMA: start address + 2 (16-B units)
+            if (PAIR) umma_bf16_pair(td, ad + 2 * k, bd + 2 * k, kLmPairIdesc, (kb | k) != 0);
+            else umma_bf16(td, ad + 2 * k, bd + 2 * k, kLmIdesc, (kb | k) != 0);
+          }
+          if (PAIR) umma_commit_pair(&empty[st]);  // both CTAs' slot st free once these MMAs read it
+          else umma_commit(&empty[st]);
         }
-        umma_commit(&acc_full[acc]);  // accumulator complete
+        if (PAIR) umma_commit_pair(&acc_full[acc]);  // accumulator complete (each CTA its 128 rows)
+        else umma_commit(&acc_full[acc]);
       }
     }
   } else if (GRAD) {  // ------------------------------------------------ gradient epilogue 2..5
@@ -233,7 +299,10 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&acc_empty[acc]);
+      if (lane == 0) {
+        if (PAIR) sm100::mbar_arrive_remote(&acc_empty[acc], 0);  // the leader's barrier
+        else sm100::mbar_arrive(&acc_empty[acc]);
+      }
     }
   } else {  // ---------------------------------------------------------- epilogue warps 2..5
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
@@ -271,7 +340,10 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&acc_empty[acc]);
+      if (lane == 0) {
+        if (PAIR) sm100::mbar_arrive_remote(&acc_empty[acc], 0);  // the leader's barrier
+        else sm100::mbar_arrive(&acc_empty[acc]);
+      }
     }
     if (live && gridDim.x > 1) {
       a.partial[(int64_t)blockIdx.x * a.n + row] = make_float4(m, s, zy, 0.f);
@@ -285,10 +357,12 @@ __global__ void __launch_bounds__(kLmThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) sm100::cluster_sync();  // both CTAs done (incl. remote arrivals) before either deallocates
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -374,6 +448,44 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t col
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Launch the LM-head kernel over a (splits, token blocks) grid: CTA pairs (cta_group::2, clusters of
+// (1, 2, 1), token blocks padded to even) when there are >= 2 token blocks — unless the development
+// option RL_DEV_LM_PAIR selects single CTAs.  w_base/ld_w/vocab/d describe W for the tensor maps.
+template <bool GRAD>
+static rl_status launch_lm(int splits, int64_t n_rows, const CUtensorMap& mh, const void* w_base, int64_t vocab,
+                           int64_t d, int64_t ld_w, const LmArgs& a, cudaStream_t s) {
+  const int64_t rb = (n_rows + kLmBM - 1) / kLmBM;
+  const bool pair = rb >= 2 && dev_option(OPT_LM_PAIR) != 1;
+  CUtensorMap mw;
+  if (!make_map(&mw, w_base, vocab, d, ld_w, pair ? kLmBN / 2 : kLmBN))
+    return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  if (!pair) {
+    if (cudaFuncSetAttribute(lmhead_kernel<GRAD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) !=
+        cudaSuccess)
+      return check_launch("cudaFuncSetAttribute(lmhead)");
+    lmhead_kernel<GRAD, false><<<dim3((unsigned)splits, (unsigned)rb), kLmThreads, kLmSmem, s>>>(mh, mw, a);
+    return check_launch(GRAD ? "lmhead_kernel<grad>" : "lmhead_kernel<logprob>");
+  }
+  auto kern = lmhead_kernel<GRAD, true>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) != cudaSuccess)
+    return check_launch("cudaFuncSetAttribute(lmhead pair)");
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 2;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)splits, (unsigned)((rb + 1) / 2 * 2));
+  cfg.blockDim = dim3(kLmThreads);
+  cfg.dynamicSmemBytes = kLmSmem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, mh, mw, a) != cudaSuccess)
+    return check_launch(GRAD ? "lmhead_kernel<grad, pair>" : "lmhead_kernel<logprob, pair>");
+  return check_launch(GRAD ? "lmhead_kernel<grad, pair>" : "lmhead_kernel<logprob, pair>");
+}
+
 }  // namespace rl
 
 extern "C" size_t rl_lmhead_workspace_size(int64_t n_tokens, int64_t d, int64_t vocab) {
@@ -399,9 +511,8 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
   if (((uintptr_t)hidden & 15) || ((uintptr_t)weight & 15) || (ld_hidden % 8) || (ld_weight % 8))
     return fail(RL_ERR_ALIGNMENT, "hidden / weight must be 16-B aligned with ld % 8 == 0");
   if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
-  CUtensorMap mh, mw;
-  if (!make_map(&mh, hidden, n_tokens, d, ld_hidden, kLmBM) || !make_map(&mw, weight, vocab, d, ld_weight, kLmBN))
-    return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  CUtensorMap mh;
+  if (!make_map(&mh, hidden, n_tokens, d, ld_hidden, kLmBM)) return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   LmArgs a;
   a.targets = targets;
   a.n = n_tokens;
@@ -420,13 +531,8 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
   a.inv_t = inv_temperature;
   a.logp_out = logp_out;
   a.lse_out = lse_out;
-  if (cudaFuncSetAttribute(lmhead_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) !=
-      cudaSuccess)
-    return check_launch("cudaFuncSetAttribute(lmhead)");
-  if ((n_tokens + kLmBM - 1) / kLmBM > 65535) return fail(RL_ERR_UNSUPPORTED, "n_tokens > 65535 * 128 per call");
-  const dim3 grid((unsigned)splits, (unsigned)((n_tokens + kLmBM - 1) / kLmBM));
-  lmhead_kernel<false><<<grid, kLmThreads, kLmSmem, (cudaStream_t)stream>>>(mh, mw, a);
-  rl_status st = check_launch("lmhead_kernel<logprob>");
+  if ((n_tokens + kLmBM - 1) / kLmBM > 65534) return fail(RL_ERR_UNSUPPORTED, "n_tokens > 65534 * 128 per call");
+  rl_status st = launch_lm<false>(splits, n_tokens, mh, weight, vocab, d, ld_weight, a, (cudaStream_t)stream);
   if (st != RL_OK || splits == 1) return st;
   const int cb = (int)std::min<int64_t>((n_tokens + 255) / 256, 148 * 4);
   lmhead_combine_kernel<<<cb, 256, 0, (cudaStream_t)stream>>>(a.partial, splits, a);
@@ -495,10 +601,7 @@ extern "C" rl_status rl_lmhead_loss_bwd(const void* hidden, int64_t ld_hidden, c
   cublasHandle_t h = cublas_handle();
   if (!h) return fail(RL_ERR_CUDA, "cublasCreate failed");
   if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return fail(RL_ERR_CUDA, "cublasSetStream failed");
-  if (cudaFuncSetAttribute(lmhead_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) != cudaSuccess)
-    return check_launch("cudaFuncSetAttribute(lmhead grad)");
-  CUtensorMap mw;
-  if (!make_map(&mw, weight, vocab, d, ld_weight, kLmBN)) return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+
   uint16_t* G = (uint16_t*)workspace;
   const float one = 1.f, zero = 0.f;
   for (int64_t t0 = 0; t0 < n_tokens; t0 += chunk) {
@@ -520,9 +623,7 @@ extern "C" rl_status rl_lmhead_loss_bwd(const void* hidden, int64_t ld_hidden, c
     a.scale = scale + t0;
     a.g_out = G;
     a.ld_g = ldg;
-    const dim3 grid((unsigned)splits, (unsigned)((C + kLmBM - 1) / kLmBM));
-    lmhead_kernel<true><<<grid, kLmThreads, kLmSmem, s>>>(mh, mw, a);
-    if (rl_status st = check_launch("lmhead_kernel<grad>"); st != RL_OK) return st;
+    if (rl_status st = launch_lm<true>(splits, C, mh, weight, vocab, d, ld_weight, a, s); st != RL_OK) return st;
     // row-major operands as column-major GEMMs: dh^T [d x C] = W^T [d x V] . G^T [V x C]
     if (dhidden &&
         cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)d, (int)C, (int)vocab, &one, weight, CUDA_R_16BF, (int)ld_weight,

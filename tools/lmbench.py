@@ -15,6 +15,8 @@ def main():
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 5
     d, V = 4096, 151936
     rl.load()
+    if "--single" in sys.argv:   # single-CTA kernels instead of cta_group::2 pairs (development A/B)
+        rl.dev_set_option(rl.DEV_LM_PAIR, 1)
     g = torch.Generator(device="cuda").manual_seed(1)
     h = torch.randn(N, d, device="cuda", generator=g).to(torch.bfloat16)
     w = (torch.randn(V, d, device="cuda", generator=g) * (3.0 / d ** 0.5)).to(torch.bfloat16)
