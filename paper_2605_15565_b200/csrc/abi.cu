@@ -27,7 +27,7 @@ rl_status fail(rl_status s, const char* fmt, ...) {
 
 rl_status check_launch(const char* what) {
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(RL_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail(RL_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
   return RL_OK;
 }
 

@@ -50,6 +50,7 @@ struct LmArgs {
   const float* scale;   // [n] s_t (rl_policy_loss_from_logp)
   uint16_t* g_out;      // [n, ld_g] bf16 bits
   int64_t ld_g;
+  int32_t xy_swap;      // grid (token blocks, splits) instead of (splits, token blocks)
 };
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
@@ -172,9 +173,11 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   const uint32_t sbase = (sm100::smem_u32(lm_smem_raw) + 1023u) & ~1023u;
   // grid (splits, row blocks), split fastest: the CTAs resident together cover few token blocks, so
   // every hidden block re-read (once per vocabulary tile) is an L2 hit shared by its splits
-  const int64_t m0 = (int64_t)blockIdx.y * kLmBM;
-  // this CTA's vocabulary tiles [jt0, jt1) (split blockIdx.x of gridDim.x)
-  const int jt0 = (int)blockIdx.x * a.tiles_per_split;
+  // (a.xy_swap: pairs launched along x — grid (token blocks, splits), clusters (2, 1, 1))
+  const uint32_t split_idx = a.xy_swap ? blockIdx.y : blockIdx.x;
+  const int64_t m0 = (int64_t)(a.xy_swap ? blockIdx.x : blockIdx.y) * kLmBM;
+  // this CTA's vocabulary tiles [jt0, jt1) (split split_idx)
+  const int jt0 = (int)split_idx * a.tiles_per_split;
   const int jt1 = min(a.vtiles, jt0 + a.tiles_per_split);
   const int ntiles = max(0, jt1 - jt0);
   if (threadIdx.x == 0) {
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       }
     }
     if (live && gridDim.x > 1) {
-      a.partial[(int64_t)blockIdx.x * a.n + row] = make_float4(m, s, zy, 0.f);
+      a.partial[(int64_t)split_idx * a.n + row] = make_float4(m, s, zy, 0.f);
     } else if (live) {
       const float lse2 = m + log2f(s);
       if (a.lse_out) a.lse_out[row] = lse2 * RL_LN2;
@@ -469,19 +472,22 @@ static rl_status launch_lm(int splits, int64_t n_rows, const CUtensorMap& mh, co
   auto kern = lmhead_kernel<GRAD, true>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) != cudaSuccess)
     return check_launch("cudaFuncSetAttribute(lmhead pair)");
+  const bool swap = dev_option(OPT_LM_PAIR) == 2;  // development: pairs along x
+  LmArgs b = a;
+  b.xy_swap = swap ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 2;
+  attr[0].val.clusterDim.x = swap ? 2 : 1;
+  attr[0].val.clusterDim.y = swap ? 1 : 2;
   attr[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3((unsigned)splits, (unsigned)((rb + 1) / 2 * 2));
+  cfg.gridDim = swap ? dim3((unsigned)((rb + 1) / 2 * 2), (unsigned)splits) : dim3((unsigned)splits, (unsigned)((rb + 1) / 2 * 2));
   cfg.blockDim = dim3(kLmThreads);
   cfg.dynamicSmemBytes = kLmSmem;
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, mh, mw, a) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, kern, mh, mw, b) != cudaSuccess)
     return check_launch(GRAD ? "lmhead_kernel<grad, pair>" : "lmhead_kernel<logprob, pair>");
   return check_launch(GRAD ? "lmhead_kernel<grad, pair>" : "lmhead_kernel<logprob, pair>");
 }
@@ -513,7 +519,7 @@ extern "C" rl_status rl_lmhead_logprob(const void* hidden, int64_t ld_hidden, co
   if (rl_status e = require_sm100(); e != RL_OK) return e;  // RL_ERR_UNSUPPORTED off sm_100
   CUtensorMap mh;
   if (!make_map(&mh, hidden, n_tokens, d, ld_hidden, kLmBM)) return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  LmArgs a;
+  LmArgs a{};
   a.targets = targets;
   a.n = n_tokens;
   a.V = vocab;
