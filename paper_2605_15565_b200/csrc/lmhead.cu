@@ -50,7 +50,7 @@ struct LmArgs {
   const float* scale;   // [n] s_t (rl_policy_loss_from_logp)
   uint16_t* g_out;      // [n, ld_g] bf16 bits
   int64_t ld_g;
-  int32_t xy_swap;      // grid (token blocks, splits) instead of (splits, token blocks)
+  int32_t n_splits;     // PAIR launches: the split count (the grid is 1-D)
 };
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
@@ -173,9 +173,17 @@ __global__ void __launch_bounds__(kLmThreads, 1)
   const uint32_t sbase = (sm100::smem_u32(lm_smem_raw) + 1023u) & ~1023u;
   // grid (splits, row blocks), split fastest: the CTAs resident together cover few token blocks, so
   // every hidden block re-read (once per vocabulary tile) is an L2 hit shared by its splits
-  // (a.xy_swap: pairs launched along x — grid (token blocks, splits), clusters (2, 1, 1))
-  const uint32_t split_idx = a.xy_swap ? blockIdx.y : blockIdx.x;
-  const int64_t m0 = (int64_t)(a.xy_swap ? blockIdx.x : blockIdx.y) * kLmBM;
+  // PAIR: a 1-D grid of clusters (2, 1, 1), linear index = ((pair * splits + split) * 2 + rank), so
+  // the split stays the fastest-varying index (the L2 order of the single-CTA grid) and the two CTAs
+  // of a cluster are the pair's token blocks 2 pair and 2 pair + 1
+  uint32_t split_idx = blockIdx.x;
+  int64_t tblock = blockIdx.y;
+  if (PAIR) {
+    const uint32_t q = blockIdx.x >> 1;
+    split_idx = q % (uint32_t)a.n_splits;
+    tblock = (int64_t)(q / (uint32_t)a.n_splits) * 2 + (blockIdx.x & 1);
+  }
+  const int64_t m0 = tblock * kLmBM;
   // this CTA's vocabulary tiles [jt0, jt1) (split split_idx)
   const int jt0 = (int)split_idx * a.tiles_per_split;
   const int jt1 = min(a.vtiles, jt0 + a.tiles_per_split);
@@ -472,16 +480,16 @@ static rl_status launch_lm(int splits, int64_t n_rows, const CUtensorMap& mh, co
   auto kern = lmhead_kernel<GRAD, true>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLmSmem) != cudaSuccess)
     return check_launch("cudaFuncSetAttribute(lmhead pair)");
-  const bool swap = dev_option(OPT_LM_PAIR) == 2;  // development: pairs along x
+  // clusters of two along a 1-D grid over the linear (pair, split, rank) index
   LmArgs b = a;
-  b.xy_swap = swap ? 1 : 0;
+  b.n_splits = splits;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = swap ? 2 : 1;
-  attr[0].val.clusterDim.y = swap ? 1 : 2;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.gridDim = swap ? dim3((unsigned)((rb + 1) / 2 * 2), (unsigned)splits) : dim3((unsigned)splits, (unsigned)((rb + 1) / 2 * 2));
+  cfg.gridDim = dim3((unsigned)((rb + 1) / 2 * 2 * splits), 1, 1);
   cfg.blockDim = dim3(kLmThreads);
   cfg.dynamicSmemBytes = kLmSmem;
   cfg.stream = s;

@@ -17,8 +17,7 @@ def main():
     rl.load()
     if "--single" in sys.argv:   # single-CTA kernels instead of cta_group::2 pairs (development A/B)
         rl.dev_set_option(rl.DEV_LM_PAIR, 1)
-    if "--pairx" in sys.argv:    # pairs along the grid's x dimension
-        rl.dev_set_option(rl.DEV_LM_PAIR, 2)
+
     g = torch.Generator(device="cuda").manual_seed(1)
     h = torch.randn(N, d, device="cuda", generator=g).to(torch.bfloat16)
     w = (torch.randn(V, d, device="cuda", generator=g) * (3.0 / d ** 0.5)).to(torch.bfloat16)
