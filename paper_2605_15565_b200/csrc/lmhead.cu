@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
         if (PAIR) {  // both CTAs' copies complete on the leader's full[st]; the leader expects both
           const uint32_t lbar = cluster_addr(&full[st], 0);
           if (leader) sm100::mbar_arrive_expect_tx(&full[st], 2 * STAGE);
-          else sm100::mbar_arrive_remote(&full[st], 0);
+          else sm100::mbar_arrive_remote_relaxed(&full[st], 0);
           tma_load_2d_pair(sa, &tm_h, kb * kLmBK, (int32_t)m0, lbar);
           tma_load_2d_pair(sb, &tm_w, kb * kLmBK, j * kLmBN + (int32_t)crank * (kLmBN / 2), lbar);
         } else {
@@ -245,14 +245,12 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       int it = 0;
       for (int j = 0; j < ntiles; ++j) {
         const int acc = j & 1;
-        if (PAIR) sm100::mbar_wait_cluster(&acc_empty[acc], (((uint32_t)j >> 1) & 1u) ^ 1u);
-        else sm100::mbar_wait(&acc_empty[acc], (((uint32_t)j >> 1) & 1u) ^ 1u);
+        sm100::mbar_wait(&acc_empty[acc], (((uint32_t)j >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t td = tmem + (uint32_t)acc * kLmBN;
         for (int kb = 0; kb < a.kblocks; ++kb, ++it) {
           const int st = it % STAGES;
-          if (PAIR) sm100::mbar_wait_cluster(&full[st], (uint32_t)(it / STAGES) & 1u);
-          else sm100::mbar_wait(&full[st], (uint32_t)(it / STAGES) & 1u);
+          sm100::mbar_wait(&full[st], (uint32_t)(it / STAGES) & 1u);
           tc_fence_after();
           const uint32_t sa = sbase + (uint32_t)st * STAGE, sb = sa + kLmABytes;
           const uint64_t ad = umma_desc_sw128(sa), bd = umma_desc_sw128(sb);
@@ -311,7 +309,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (PAIR) sm100::mbar_arrive_remote(&acc_empty[acc], 0);  // the leader's barrier
+        if (PAIR) sm100::mbar_arrive_remote_relaxed(&acc_empty[acc], 0);  // the leader's barrier
         else sm100::mbar_arrive(&acc_empty[acc]);
       }
     }
@@ -352,7 +350,7 @@ __global__ void __launch_bounds__(kLmThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (PAIR) sm100::mbar_arrive_remote(&acc_empty[acc], 0);  // the leader's barrier
+        if (PAIR) sm100::mbar_arrive_remote_relaxed(&acc_empty[acc], 0);  // the leader's barrier
         else sm100::mbar_arrive(&acc_empty[acc]);
       }
     }
