@@ -17,8 +17,9 @@
  *   5 RL_DEV_VC_ROWS      vp_cache_kernel rows parked in shared memory + 1 (0 = default)
  *   6 RL_DEV_VC_PUB       vp_cache_kernel record send + 1: 0 collector (strong stores), 1 last
  *                         consumer warp (weak stores; default), 2 collector (weak stores)
- *   7 RL_DEV_LM_PAIR      LM-head kernels: 0 = CTA pairs (cta_group::2) when there are >= 2 token
- *                         blocks (default), 1 = single CTAs
+ *   7 RL_DEV_LM_PAIR      LM-head kernels: 0 = CTA pairs (cta_group::2) for the backward's gradient
+ *                         kernel, single CTAs for the log-prob kernel (default); 1 = single CTAs;
+ *                         2 = pairs for both (pairs need >= 2 token blocks)
  * Options are read at launch time; set them before the calls they should affect.
  */
 #ifndef RL_POLICY_DEV_H_

@@ -464,7 +464,12 @@ template <bool GRAD>
 static rl_status launch_lm(int splits, int64_t n_rows, const CUtensorMap& mh, const void* w_base, int64_t vocab,
                            int64_t d, int64_t ld_w, const LmArgs& a, cudaStream_t s) {
   const int64_t rb = (n_rows + kLmBM - 1) / kLmBM;
-  const bool pair = rb >= 2 && dev_option(OPT_LM_PAIR) != 1;
+  // measured (tools/lmbench.py, d 4096, V 151936): pairs win for the gradient kernel (1,537 vs 1,433
+  // TFLOP/s for the backward at N = 16K, 1,300 vs 1,275 at 128K) but not for the log-prob kernel
+  // (1,496 vs 1,476 at 16K, 1,292 vs 1,372 at 128K: ncu shows 20 GB of DRAM reads against 2.9 GB
+  // for single CTAs — the cluster schedule loses the W-tile L2 reuse across token blocks)
+  const int opt = dev_option(OPT_LM_PAIR);  // 0 default, 1 single CTAs, 2 pairs
+  const bool pair = rb >= 2 && (opt == 2 || (opt == 0 && GRAD));
   CUtensorMap mw;
   if (!make_map(&mw, w_base, vocab, d, ld_w, pair ? kLmBN / 2 : kLmBN))
     return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");

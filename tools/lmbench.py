@@ -17,6 +17,8 @@ def main():
     rl.load()
     if "--single" in sys.argv:   # single-CTA kernels instead of cta_group::2 pairs (development A/B)
         rl.dev_set_option(rl.DEV_LM_PAIR, 1)
+    if "--pairs" in sys.argv:    # pairs for the forward too
+        rl.dev_set_option(rl.DEV_LM_PAIR, 2)
 
     g = torch.Generator(device="cuda").manual_seed(1)
     h = torch.randn(N, d, device="cuda", generator=g).to(torch.bfloat16)
