@@ -1198,7 +1198,7 @@ extern "C" rl_status rl_vocab_parallel_logprob(
       // rows parked in shared memory (RS): the exchange window is R + RS - 1 rows
       const bool wide = nv > 6 * kVcCons;
       const int rs_opt = dev_option(OPT_VC_ROWS);  // 0 = default, else RS + 1
-      const int RS = rs_opt > 0 ? std::min(rs_opt - 1, wide ? 1 : 2) : (wide ? 1 : 0);
+      const int RS = rs_opt > 0 ? std::min(rs_opt - 1, wide ? 1 : 2) : 1;
       const int NVc = wide ? 11 : 6;
       const size_t head = (sizeof(VcShared) + 127) & ~(size_t)127;
       const size_t rowc = (size_t)RS * NVc * kVcCons * 16;
@@ -1209,7 +1209,9 @@ extern "C" rl_status rl_vocab_parallel_logprob(
                        : (RS == 2 ? vp_cache_kernel<6, 3, 2> : RS == 1 ? vp_cache_kernel<6, 3, 1>
                                                                       : vp_cache_kernel<6, 3, 0>);
       v.G = std::min(8, std::max(0, dev_option(OPT_VC_GROUPS)));
-      v.pub_mode = dev_option(OPT_VC_PUB) > 0 ? std::min(2, dev_option(OPT_VC_PUB) - 1) : 1;  // default: last warp, weak
+      // record send (measured, tools/vptrace.py / vpbench.py): across GPUs the last consumer warp's
+      // weak stores (2.31 vs 2.42 ms at P = 4 on 4 GPUs); one rank: the collector's (weak) store
+      v.pub_mode = dev_option(OPT_VC_PUB) > 0 ? std::min(2, dev_option(OPT_VC_PUB) - 1) : (P > 1 ? 1 : 2);
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return check_launch("cudaFuncSetAttribute(vp_cache_kernel)");
       kern<<<grid, kVcThreads, smem, s>>>(v);
