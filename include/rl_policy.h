@@ -260,18 +260,23 @@ rl_status rl_comm_allreduce_f64(rl_comm* c, double* buf, size_t n, rl_stream str
 
 /* Collective (every rank of `c`, same max_tokens): allocate this rank's peer-exchange buffer for
  * vocab-parallel calls of up to max_tokens rows and map every peer's buffer into this process
- * (CUDA IPC over NVLink / NVSwitch; handles exchanged with one NCCL all-gather).  Afterwards
- * rl_vocab_parallel_logprob with the fused loss runs as ONE kernel per rank that exchanges the
- * per-row (max, sum-exp, target logit) records with peer stores and flags inside the kernel,
- * with the row slice held in shared memory (logits read once, dlogits written once).  Returns
- * RL_ERR_UNSUPPORTED (and leaves the NCCL path in use) if a peer is not P2P-accessible.  The
- * buffers are released by rl_comm_destroy. */
+ * (CUDA IPC over NVLink / NVSwitch; handles exchanged with one NCCL all-gather).  Enabled only if
+ * EVERY rank mapped every peer (an NCCL min-reduction of the per-rank result), so all ranks take
+ * the same path.  Afterwards rl_vocab_parallel_logprob with the fused loss runs as ONE kernel per
+ * rank that sends each row's shard record (log2-domain lse of the shard, target logit) to every
+ * rank as two 8-byte words tagged with the call's epoch (slots double-buffered by epoch parity)
+ * and polls the peers' records inside the kernel: vp_cache_kernel for bf16 shards of <= 4,928
+ * whole 16-B vectors (row slices held in registers: logits read once, one exp per element),
+ * vp_ring_kernel otherwise (slices re-read from L2).  A rank that never publishes makes its peers
+ * trap after 30 s (RL_ERR_CUDA) instead of hanging.  Returns RL_ERR_UNSUPPORTED (and leaves the
+ * NCCL path in use on every rank) if a peer is not P2P-accessible; > 8 ranks are unsupported.
+ * The buffers are released by rl_comm_destroy; calling it again re-maps (collective). */
 rl_status rl_comm_enable_peer_exchange(rl_comm* c, int64_t max_tokens);
 
 /* Vocab-parallel log-prob (+ optional fused loss/grad on the local shard), c8 of DESIGN.md §3.
  * Each rank holds the columns [vocab_offset, vocab_offset + vocab_shard) of every row.
- * With rl_comm_enable_peer_exchange and the fused loss requested: one kernel per rank (row
- *   slices in shared memory, records exchanged through peer memory, see above).  Otherwise:
+ * With rl_comm_enable_peer_exchange and the fused loss requested: one kernel per rank (records
+ *   exchanged through peer memory, see above: 2 HBM units per element).  Otherwise:
  * Phase 1 (kernel): per row (m_r, s_r, t_y-if-owned) over the local shard.
  * Phase 2 (NCCL all-gather over NVLink of the 3 floats per row).
  * Phase 3 (kernel): M = max m_r, S = sum s_r 2^(m_r - M), lse, logp (identical on all ranks);
