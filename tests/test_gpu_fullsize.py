@@ -372,3 +372,64 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
                   rows_bits(dl, rows, W), stats.cpu().numpy(), ref=ref, prox=prox)
     others = np.setdiff1d(np.arange(N), rows)[::8]
     assert not rows_bits(dl, others, W).any()
+
+
+# ------------------------------------------------------------------------------- vocab-parallel edge cases
+@pytest.mark.parametrize("N", [1, 7, 149, 1000])
+@pytest.mark.parametrize("W", [8, 1000, 1004, 18992])
+@pytest.mark.parametrize("path", ["peer", "peer_ring", "nccl"])
+def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
+    """Few rows (fewer than the 148 CTAs: idle CTAs, one row per CTA), a single 16-B vector per row
+    (W = 8), widths with and without whole vectors per consumer thread, on both peer kernels and the
+    NCCL path: logp, loss and every dlogits row against the oracle."""
+    rl, t = cuda_lib, torch()
+    x = t.empty((N, W), dtype=t.bfloat16, device="cuda")
+    yd = t.empty(N, dtype=t.int32, device="cuda")
+    synth.device_logits(x, W, 0, W + N, targets_out=yd)
+    y = yd.cpu().numpy()
+    y[::5] = -100
+    yd = dev(y)
+    bits = rows_bits(x, np.arange(N), W)
+    lp_ref = oracle_logp_rows(bits, y)
+    rng = np.random.default_rng(N + W)
+    old = np.where(y >= 0, lp_ref + rng.normal(size=N) * 0.1, 0.0).astype(np.float32)
+    tseq = (np.arange(N) // 3).astype(np.int32)
+    adv = rng.normal(size=int(tseq[-1]) + 1).astype(np.float32)
+    mask = (rng.uniform(size=N) < 0.9).astype(np.uint8)
+    comm = rl.Comm.local()
+    try:
+        if path.startswith("peer"):
+            assert comm.enable_peer_exchange(N)
+            rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 0)
+        else:
+            rl.dev_set_option(rl.DEV_VP_PATH, 1)
+        dl = t.empty_like(x)
+        stats = t.zeros(12, dtype=t.float64, device="cuda")
+        ws = t.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=t.uint8, device="cuda")
+        logp = t.empty(N, device="cuda")
+        p = rl.LossParams(agg=rl.AGG_SUM)
+        rl.vocab_parallel_logprob(x, yd, 0, W, comm, logp, ws, old_logp=dev(old), loss_mask=dev(mask),
+                                  token_seq=dev(tseq), seq_adv=dev(adv), params=p, dlogits_shard=dl, stats=stats)
+        t.cuda.synchronize()
+    finally:
+        rl.dev_set_option(rl.DEV_VP_PATH, 0)
+        rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
+        comm.destroy()
+    out = oracle.policy_loss_fwd_bwd(oracle.decode_bf16(bits), y, old, mask, tseq, adv.astype(np.float64), None,
+                                     None, oracle.LossParams(agg=oracle.AGG_SUM))
+    g_lp = logp.cpu().numpy()
+    ok = y >= 0
+    assert np.all(np.abs(g_lp[ok] - out["logp"][ok]) <= LOGP_ATOL)
+    st = stats.cpu().numpy()
+    band = clip_band(out["ratio"], out["valid"], 0.2, 0.2)
+    if not band.any():
+        sc = max(abs(out["loss"]), float(np.abs(out["token_loss"]).sum()), 1e-30)
+        assert abs(st[0] - out["loss"]) <= LOSS_RTOL * sc
+        d = oracle.decode_bf16(rows_bits(dl, np.arange(N), W))
+        for k in range(N):
+            s = out["scale"][k]
+            if s == 0:
+                assert np.all(d[k] == 0), k
+            else:
+                assert np.abs(d[k] - out["dlogits"][k]).max() <= DLOGIT_ROW_RTOL * abs(s), k
+    assert st[1] == out["stats"]["active_tokens"]
