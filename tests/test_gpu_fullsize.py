@@ -383,7 +383,8 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
     (W = 8), widths with and without whole vectors per consumer thread, on both peer kernels and the
     NCCL path: logp, loss and every dlogits row against the oracle."""
     rl, t = cuda_lib, torch()
-    x = t.empty((N, W), dtype=t.bfloat16, device="cuda")
+    ld = (W + 7) // 8 * 8                     # row stride: 16-B aligned rows (W = 1004: 4 tail columns)
+    x = t.empty((N, ld), dtype=t.bfloat16, device="cuda")
     yd = t.empty(N, dtype=t.int32, device="cuda")
     synth.device_logits(x, W, 0, W + N, targets_out=yd)
     y = yd.cpu().numpy()
@@ -408,7 +409,7 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
         ws = t.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=t.uint8, device="cuda")
         logp = t.empty(N, device="cuda")
         p = rl.LossParams(agg=rl.AGG_SUM)
-        rl.vocab_parallel_logprob(x, yd, 0, W, comm, logp, ws, old_logp=dev(old), loss_mask=dev(mask),
+        rl.vocab_parallel_logprob(x, yd, 0, W, comm, logp, ws, vocab_shard=W, old_logp=dev(old), loss_mask=dev(mask),
                                   token_seq=dev(tseq), seq_adv=dev(adv), params=p, dlogits_shard=dl, stats=stats)
         t.cuda.synchronize()
     finally:
