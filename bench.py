@@ -51,6 +51,7 @@ def parse():
                     help="vocabpar: in-kernel NVLink peer exchange (default) or the NCCL all-gather path")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="tiny: launch the chain directly, no CUDA graph")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
     ap.add_argument("--vp-kernel", default="cache", choices=["cache", "ring"],
                     help="vocabpar peer path: register-cache kernel when the shard fits (default) or the L2 ring")
@@ -729,6 +730,20 @@ def run_tiny(args):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    # the 5-launch chain is launch-bound: capture it once as a CUDA graph and replay it per step
+    # (the library enqueues on torch's current stream, so the capture sees every launch)
+    graph = None
+    if not args.no_graph:
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cs):
+                step()
+        torch.cuda.current_stream().wait_stream(cs)
+        graph.replay()
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else step
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -736,7 +751,7 @@ def run_tiny(args):
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     evs[0].record(stream)
     for i in range(args.steps):
-        step()
+        run()
         evs[i + 1].record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
@@ -766,6 +781,7 @@ def run_tiny(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "tiny (BASELINE.json configs[0]): 2 prompts x 4 responses x 64 tokens, V=1024, "
                                    "fp32 logits, 1 GPU", "config": "tiny", "tokens_per_step": N,
+                       "cuda_graph": graph is not None,
                        "l2": "not flushed: a 4 MB batch is L2-resident; launch-bound (reported for the record)"},
             "roofline": {"bound": "hbm", "achieved": N * bpt / (per / 1e3) / 1e9, "peak": measured_peak_hbm()[0],
                          "unit": "GB/s", "frac": N * bpt / (per / 1e3) / 1e9 / measured_peak_hbm()[0],
