@@ -546,7 +546,8 @@ def main():
         if args.vp_width_of > 1 and world == 1:
             parallelism = (f"ONE GPU doing one rank's share of a {args.vp_width_of}-way vocabulary split "
                            f"({wl.Vr} columns as its own vocabulary, exchange with itself)")
-        vk = "vp_cache_kernel" if (wl.Vr % 8 == 0 and wl.Vr // 8 <= 11 * 448 and args.vp_kernel == "cache") \
+        fits = wl.Vr % 8 == 0 and wl.Vr // 8 <= 11 * 448
+        vk = "vp_cache_kernel" if (fits and args.vp_kernel == "cache" and (world == 1 or wl.Vr // 8 <= 6 * 448)) \
             else "vp_ring_kernel"
         kname = "rl_vocab_parallel_logprob (" + (f"{vk}, in-kernel peer exchange" if fused_vp
                                                  else "vp_stats + NCCL all-gather + vp_finish") + ")"

@@ -38,7 +38,7 @@ enum DevOpt {
   OPT_LOSS_KERNEL = 0,  // 0 = single-visit cluster kernel (default), 1 = exact two-pass kernel
   OPT_VP_PATH = 1,      // fused vocab-parallel loss: 0 = in-kernel peer exchange when enabled, 1 = NCCL path
   OPT_LM_SPLITS = 2,    // LM-head vocabulary split override (0 = cost model)
-  OPT_VP_KERNEL = 3,    // peer-exchange vocab-parallel kernel: 0 = register cache when it fits, 1 = L2 ring
+  OPT_VP_KERNEL = 3,    // peer-exchange vocab-parallel kernel: 0 = default (see vocab_parallel.cu), 1 = L2 ring, 2 = register cache when it fits
   OPT_VC_GROUPS = 4,    // vp_cache_kernel collector groups override (0 = min(8, 32 / P))
   OPT_VC_ROWS = 5,      // vp_cache_kernel rows parked in shared memory: 0 = default, else that number + 1
   OPT_VC_PUB = 6,       // vp_cache_kernel record send, value + 1: 0 collector strong, 1 last warp weak (default), 2 collector weak

@@ -347,7 +347,7 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
     try:
         if path.startswith("peer"):
             assert comm.enable_peer_exchange(N)
-            rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 0)
+            rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 2)
         else:
             rl.dev_set_option(rl.DEV_VP_PATH, 1)
         dl = t.empty_like(x)
@@ -401,7 +401,7 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
     try:
         if path.startswith("peer"):
             assert comm.enable_peer_exchange(N)
-            rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 0)
+            rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 2)
         else:
             rl.dev_set_option(rl.DEV_VP_PATH, 1)
         dl = t.empty_like(x)
