@@ -158,39 +158,42 @@ def main():
     dlf = torch.empty_like(xs)
     lpf = torch.empty(Nf, dtype=torch.float32, device=dev)
     wsf = torch.empty(rl.vocab_parallel_workspace_size(Nf, world), dtype=torch.uint8, device=dev)
-    if comm.enable_peer_exchange(Nf):
-        st_calls = [torch.zeros(12, dtype=torch.float64, device=dev) for _ in range(3)]
-        for c in range(3):
-            rl.vocab_parallel_logprob(xs, yf, vs.offset, Vf, comm, lpf, wsf, old_logp=d(oldf), loss_mask=d(maskf),
-                                      token_seq=d(tseqf), seq_adv=d(advf), params=pf, dlogits_shard=dlf,
-                                      stats=st_calls[c])
-        for c in range(3):
-            comm.allreduce_f64(st_calls[c])
-        torch.cuda.synchronize()
-        sts = [c.cpu().numpy() for c in st_calls]
-        if not (np.array_equal(sts[0], sts[1]) and np.array_equal(sts[1], sts[2])):
-            fails.append("full-width vp: back-to-back calls differ")
-        yh = yf.cpu().numpy()
-        outf = oracle.policy_loss_fwd_bwd(oracle.decode_bf16(bits_rows), yh[rows], oldf[rows], maskf[rows],
-                                          tseqf[rows], advf.astype(np.float64), None, None,
-                                          oracle.LossParams(agg=oracle.AGG_SUM))
-        lpg = lpf.cpu().numpy()[rows]
-        if np.abs(lpg - outf["logp"]).max() > 2e-3:
-            fails.append(f"full-width vp logp err {np.abs(lpg - outf['logp']).max()}")
-        sc = max(abs(outf["loss"]), float(np.abs(outf["token_loss"]).sum()))
-        if abs(sts[2][0] - outf["loss"]) > 1e-4 * sc or sts[2][1] != outf["stats"]["active_tokens"]:
-            fails.append(f"full-width vp loss {sts[2][0]} vs {outf['loss']}")
-        gs = oracle.decode_bf16(dlf[torch.from_numpy(rows).to(dev)].view(torch.int16).cpu().numpy().view(np.uint16))
-        for k, i in enumerate(rows):
-            refrow = outf["dlogits"][k, vs.offset:vs.offset + vs.size]
-            s_k = outf["scale"][k]
-            if s_k == 0:
-                if np.any(gs[k] != 0):
-                    fails.append(f"full-width vp row {i} not zero")
-            elif np.abs(gs[k] - refrow).max() > 1e-2 * abs(s_k):
-                fails.append(f"full-width vp row {i} dlogits err {np.abs(gs[k] - refrow).max() / abs(s_k)}")
-    else:
-        fails.append("full-width vp: peer exchange unavailable")
+    for vk in (0, 2):   # RL_DEV_VP_KERNEL: the default kernel choice, then the register cache forced
+        rl.dev_set_option(rl.DEV_VP_KERNEL, vk)
+        if comm.enable_peer_exchange(Nf):
+            st_calls = [torch.zeros(12, dtype=torch.float64, device=dev) for _ in range(3)]
+            for c in range(3):
+                rl.vocab_parallel_logprob(xs, yf, vs.offset, Vf, comm, lpf, wsf, old_logp=d(oldf), loss_mask=d(maskf),
+                                          token_seq=d(tseqf), seq_adv=d(advf), params=pf, dlogits_shard=dlf,
+                                          stats=st_calls[c])
+            for c in range(3):
+                comm.allreduce_f64(st_calls[c])
+            torch.cuda.synchronize()
+            sts = [c.cpu().numpy() for c in st_calls]
+            if not (np.array_equal(sts[0], sts[1]) and np.array_equal(sts[1], sts[2])):
+                fails.append(f"full-width vp (kernel option {vk}): back-to-back calls differ")
+            yh = yf.cpu().numpy()
+            outf = oracle.policy_loss_fwd_bwd(oracle.decode_bf16(bits_rows), yh[rows], oldf[rows], maskf[rows],
+                                              tseqf[rows], advf.astype(np.float64), None, None,
+                                              oracle.LossParams(agg=oracle.AGG_SUM))
+            lpg = lpf.cpu().numpy()[rows]
+            if np.abs(lpg - outf["logp"]).max() > 2e-3:
+                fails.append(f"full-width vp ({vk}) logp err {np.abs(lpg - outf['logp']).max()}")
+            sc = max(abs(outf["loss"]), float(np.abs(outf["token_loss"]).sum()))
+            if abs(sts[2][0] - outf["loss"]) > 1e-4 * sc or sts[2][1] != outf["stats"]["active_tokens"]:
+                fails.append(f"full-width vp loss {sts[2][0]} vs {outf['loss']}")
+            gs = oracle.decode_bf16(dlf[torch.from_numpy(rows).to(dev)].view(torch.int16).cpu().numpy().view(np.uint16))
+            for k, i in enumerate(rows):
+                refrow = outf["dlogits"][k, vs.offset:vs.offset + vs.size]
+                s_k = outf["scale"][k]
+                if s_k == 0:
+                    if np.any(gs[k] != 0):
+                        fails.append(f"full-width vp row {i} not zero")
+                elif np.abs(gs[k] - refrow).max() > 1e-2 * abs(s_k):
+                    fails.append(f"full-width vp row {i} dlogits err {np.abs(gs[k] - refrow).max() / abs(s_k)}")
+        else:
+            fails.append("full-width vp: peer exchange unavailable")
+    rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
     del xf, xs, dlf
 
     # ------------------------------------------------------------------ M2PO global selection
