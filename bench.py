@@ -37,6 +37,7 @@ N_MINIBATCH = 4          # PAPER.md:574 "4 PPO mini-batches per iteration"
 SIDE_BYTES = 17          # target 4 + old_logp 4 + mask 1 + logp out 4 + token_seq 4
 OBJECTIVE = "clip"       # --objective
 KERNEL = "sv"            # --kernel
+SKIP_MASKED = False      # --skip-masked
 
 
 def parse():
@@ -52,6 +53,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="tiny: launch the chain directly, no CUDA graph")
+    ap.add_argument("--skip-masked", action="store_true",
+                    help="RL_F_SKIP_MASKED_READS: masked rows are not read (write-only zeros; logp 0 there)")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
     ap.add_argument("--vp-kernel", default="cache", choices=["cache", "ring"],
                     help="vocabpar peer path: register-cache kernel when the shard fits (default) or the L2 ring")
@@ -327,6 +330,8 @@ class TokenParallelWorkload:
             if self.full:
                 p.kl_coef, p.ref_logp, p.prox_logp = 1e-3, self.pool_ref[c % P], self.pool_prox[c % P]
                 p.flags |= rl.F_ENTROPY
+            if SKIP_MASKED:
+                p.flags |= rl.F_SKIP_MASKED_READS
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -439,9 +444,9 @@ CONFIG_WORKLOADS = {
 
 
 def main():
-    global OBJECTIVE, KERNEL
+    global OBJECTIVE, KERNEL, SKIP_MASKED
     args = parse()
-    OBJECTIVE, KERNEL = args.objective, args.kernel
+    OBJECTIVE, KERNEL, SKIP_MASKED = args.objective, args.kernel, args.skip_masked
     # the image sets NCCL_DEBUG=VERSION, whose only output is a banner NCCL prints on stdout: keep
     # stdout to the single JSON line (an explicit WARN / INFO setting is left alone)
     if os.environ.get("NCCL_DEBUG") == "VERSION":
@@ -657,7 +662,7 @@ def main():
                        "tokens_per_rank_per_step": tokens_rank, "call_tokens": launch_tokens,
                        "vocab": w0.V, "parallelism": parallelism, "loss_kernel": kern,
                        "l2": "no flush: every loss call streams a distinct >= 2.5 GB logits buffer >> 126 MB L2",
-                       "agg": "token_mean", "batch_norm": True,
+                       "agg": "token_mean", "batch_norm": True, "skip_masked_reads": SKIP_MASKED,
                        "objective": {"full": "clipped decoupled surrogate + k3 KL (beta 1e-3) + entropy",
                                      "m2po": "M2PO: log-prob pass + second-moment mask (tau 0.01) + unclipped loss",
                                      }.get(args.objective, "clipped surrogate")},

@@ -11,6 +11,7 @@ run tiny --config tiny --steps 50
 run objective_full --objective full --no-e2e --no-cpu
 run objective_m2po --objective m2po --no-e2e --no-cpu
 run long --config long --no-e2e --no-cpu --steps 10
+run long_skip --config long --no-e2e --no-cpu --steps 10 --skip-masked
 run multi --config multi --no-e2e --no-cpu --steps 10
 run vp_w8 --config vocabpar --vp-width-of 8
 run vp_w4 --config vocabpar --vp-width-of 4
