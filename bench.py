@@ -619,6 +619,10 @@ def main():
     # roofline of the dominant kernel: algorithmic bytes per launch / its average launch duration
     w0 = wls[0]
     launch_tokens = w0.MB if hasattr(w0, "MB") else w0.N
+    if SKIP_MASKED and hasattr(w0, "total_counts"):   # masked rows are written, not read
+        frac = float(w0.total_counts[0].item()) / max(1.0, float(w0.tokens_per_step) *
+                                                      (w0.comm.nranks if w0.comm is not None else 1))
+        w0.bytes_per_token = w0.V * 2 * (1 + frac) + SIDE_BYTES
     alg_bytes = launch_tokens * w0.bytes_per_token
     avg_ms = w0.kernel_ms()
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
