@@ -153,3 +153,16 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f
+
+
+def test_dev_options_header_matches_binding(lib):
+    """include/rl_policy_dev.h and the binding's DEV_* constants name the same option keys, and the
+    library accepts exactly those keys (an unknown key answers -1 and changes nothing)."""
+    src = open(os.path.join(ROOT, "include", "rl_policy_dev.h")).read()
+    keys = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define RL_DEV_([A-Z0-9_]+) (\d+)", src)}
+    assert keys, "no RL_DEV_* keys in the header"
+    for name, k in keys.items():
+        assert getattr(rl, "DEV_" + name) == k, name
+        old = lib.rl_dev_set_option(k, 0)
+        assert old >= 0 and lib.rl_dev_set_option(k, old) == 0
+    assert lib.rl_dev_set_option(max(keys.values()) + 1, 1) == -1
