@@ -457,6 +457,148 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t col
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// ------------------------------------------------------------------------------------------------
+// The backward's two GEMMs on tcgen05 (lm_gemm_kernel): C[M, N] (+)= A[M, K] B[K, N] in fp32 from
+// bf16 operands in HBM, one 128 x 256 output tile per CTA, the K loop through a 4-stage TMA ring.
+//   dh = G W:     A = G  [C, V]  K-major (row-major, K = V contiguous)
+//                 B = W  [V, d]  MN-major (row-major, N = d contiguous)
+//   dW = G^T h:   A = G^T        MN-major (G row-major, M = V contiguous)
+//                 B = h  [C, d]  MN-major
+// An MN-major operand tile is staged as 64-element-wide column slabs (one 2-D TMA box of 64 x 64,
+// 128-B swizzle, 8 KB each): descriptor LBO = 8 KB between slabs, SBO = 1 KB between 8-row groups,
+// and each K = 16 step advances the start by 16 rows x 128 B; the instruction descriptor's
+// a_major / b_major bits (15 / 16) select the MN-major reading.
+constexpr int kGmBM = 128, kGmBN = 256, kGmBK = 64, kGmStages = 4, kGmThreads = 192;
+constexpr uint32_t kGmABytes = kGmBM * kGmBK * 2, kGmBBytes = kGmBN * kGmBK * 2;
+constexpr uint32_t kGmStage = kGmABytes + kGmBBytes;  // 48 KB
+constexpr size_t kGmSmem = (size_t)kGmStages * kGmStage + 1024;
+
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(8192 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
+struct GmArgs {
+  float* out;
+  int64_t ldo;
+  int32_t M, N, kblocks;
+  int32_t accumulate;
+};
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kGmThreads, 1)
+    lm_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                   const GmArgs g) {
+  constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                             ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(kGmBN >> 3) << 17) |
+                             ((uint32_t)(kGmBM >> 4) << 24);
+  extern __shared__ uint8_t gm_smem_raw[];
+  __shared__ __align__(8) uint64_t full[kGmStages], empty[kGmStages], acc_full;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t sbase = (sm100::smem_u32(gm_smem_raw) + 1023u) & ~1023u;
+  const int32_t m0 = (int32_t)blockIdx.y * kGmBM, n0 = (int32_t)blockIdx.x * kGmBN;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGmStages; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], 1);
+    }
+    sm100::mbar_init(&acc_full, 1);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     sm100::smem_u32(&tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      for (int kb = 0; kb < g.kblocks; ++kb) {
+        const int st = kb % kGmStages;
+        sm100::mbar_wait(&empty[st], ((uint32_t)(kb / kGmStages) & 1u) ^ 1u);
+        const uint32_t sa = sbase + (uint32_t)st * kGmStage, sb = sa + kGmABytes;
+        sm100::mbar_arrive_expect_tx(&full[st], kGmStage);
+        const int32_t k0 = kb * kGmBK;
+        if (A_MN) {  // two 64-wide M slabs of the row-major [K, M] operand
+          tma_load_2d(sa, &tm_a, m0, k0, &full[st]);
+          tma_load_2d(sa + 8192, &tm_a, m0 + 64, k0, &full[st]);
+        } else {
+          tma_load_2d(sa, &tm_a, k0, m0, &full[st]);
+        }
+        if (B_MN) {  // four 64-wide N slabs of the row-major [K, N] operand
+#pragma unroll
+          for (int q = 0; q < 4; ++q) tma_load_2d(sb + q * 8192, &tm_b, n0 + 64 * q, k0, &full[st]);
+        } else {
+          tma_load_2d(sb, &tm_b, k0, n0, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      for (int kb = 0; kb < g.kblocks; ++kb) {
+        const int st = kb % kGmStages;
+        sm100::mbar_wait(&full[st], (uint32_t)(kb / kGmStages) & 1u);
+        tc_fence_after();
+        const uint32_t sa = sbase + (uint32_t)st * kGmStage, sb = sa + kGmABytes;
+        const uint64_t ad = A_MN ? umma_desc_mn_sw128(sa) : umma_desc_sw128(sa);
+        const uint64_t bd = B_MN ? umma_desc_mn_sw128(sb) : umma_desc_sw128(sb);
+#pragma unroll
+        for (int k = 0; k < kGmBK / 16; ++k) {
+          // K step of 16: K-major +32 B (2 units), MN-major +16 rows x 128 B (128 units)
+          const uint64_t ao = A_MN ? 128ull * k : 2ull * k, bo = B_MN ? 128ull * k : 2ull * k;
+          umma_bf16(tmem, ad + ao, bd + bo, IDESC, (kb | k) != 0);
+        }
+        umma_commit(&empty[st]);
+      }
+      umma_commit(&acc_full);
+    }
+  } else {  // ---------------------------------------------------------- epilogue warps 2..5
+    const int q = warp & 3;
+    const int32_t row = m0 + q * 32 + lane;
+    sm100::mbar_wait(&acc_full, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < kGmBN / 32; ++c) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
+      const int32_t col = n0 + c * 32;
+      if (row < g.M && col < g.N) {
+        float* o = g.out + (int64_t)row * g.ldo + col;
+        if (col + 32 <= g.N && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+          float4* o4 = reinterpret_cast<float4*>(o);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 w = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            if (g.accumulate) {
+              const float4 p = o4[i];
+              w.x += p.x;
+              w.y += p.y;
+              w.z += p.z;
+              w.w += p.w;
+            }
+            o4[i] = w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (col + i < g.N) o[i] = g.accumulate ? o[i] + v[i] : v[i];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  }
+}
+
 // Launch the LM-head kernel over a (splits, token blocks) grid: CTA pairs (cta_group::2, clusters of
 // (1, 2, 1), token blocks padded to even) when there are >= 2 token blocks — unless the development
 // option RL_DEV_LM_PAIR selects single CTAs.  w_base/ld_w/vocab/d describe W for the tensor maps.
@@ -501,6 +643,26 @@ static rl_status launch_lm(int splits, int64_t n_rows, const CUtensorMap& mh, co
   if (cudaLaunchKernelEx(&cfg, kern, mh, mw, b) != cudaSuccess)
     return check_launch(GRAD ? "lmhead_kernel<grad, pair>" : "lmhead_kernel<logprob, pair>");
   return check_launch(GRAD ? "lmhead_kernel<grad, pair>" : "lmhead_kernel<logprob, pair>");
+}
+
+template <bool A_MN, bool B_MN>
+static rl_status lm_gemm(const CUtensorMap& ta, const CUtensorMap& tb, float* out, int64_t ldo, int64_t M, int64_t N,
+                         int64_t K, bool accumulate, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return RL_OK;
+  GmArgs g;
+  g.out = out;
+  g.ldo = ldo;
+  g.M = (int32_t)M;
+  g.N = (int32_t)N;
+  g.kblocks = (int32_t)((K + kGmBK - 1) / kGmBK);
+  g.accumulate = accumulate ? 1 : 0;
+  if (cudaFuncSetAttribute(lm_gemm_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGmSmem) !=
+      cudaSuccess)
+    return check_launch("cudaFuncSetAttribute(lm_gemm)");
+  if ((M + kGmBM - 1) / kGmBM > 65535) return fail(RL_ERR_UNSUPPORTED, "lm_gemm: M too large");
+  const dim3 grid((unsigned)((N + kGmBN - 1) / kGmBN), (unsigned)((M + kGmBM - 1) / kGmBM));
+  lm_gemm_kernel<A_MN, B_MN><<<grid, kGmThreads, kGmSmem, s>>>(ta, tb, g);
+  return check_launch(A_MN ? "lm_gemm_kernel<dW>" : "lm_gemm_kernel<dh>");
 }
 
 }  // namespace rl
@@ -641,14 +803,34 @@ extern "C" rl_status rl_lmhead_loss_bwd(const void* hidden, int64_t ld_hidden, c
     a.g_out = G;
     a.ld_g = ldg;
     if (rl_status st = launch_lm<true>(splits, C, mh, weight, vocab, d, ld_weight, a, s); st != RL_OK) return st;
-    // row-major operands as column-major GEMMs: dh^T [d x C] = W^T [d x V] . G^T [V x C]
+    const float* beta = (acc_w || t0 > 0) ? &one : &zero;
+    if (dev_option(OPT_LM_GEMM) != 1) {  // the backward's GEMMs on tcgen05 (lm_gemm_kernel)
+      CUtensorMap tg_k, tg_mn, tw_mn, th_mn;
+      if (dhidden) {  // dh_chunk [C, d] = G [C, V] . W [V, d]
+        if (!make_map(&tg_k, G, C, vocab, ldg, kGmBM) || !make_map(&tw_mn, weight, vocab, d, ld_weight, kGmBK))
+          return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+        if (rl_status st = lm_gemm<false, true>(tg_k, tw_mn, dhidden + (size_t)t0 * ld_dhidden, ld_dhidden, C, d,
+                                                vocab, false, s);
+            st != RL_OK)
+          return st;
+      }
+      if (dweight) {  // dW [V, d] (+)= G^T [V, C] . h_chunk [C, d]
+        if (!make_map(&tg_mn, G, C, vocab, ldg, kGmBK) || !make_map(&th_mn, h0, C, d, ld_hidden, kGmBK))
+          return fail(RL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+        if (rl_status st = lm_gemm<true, true>(tg_mn, th_mn, dweight, ld_dweight, vocab, d, C, beta == &one, s);
+            st != RL_OK)
+          return st;
+      }
+      continue;
+    }
+    // cuBLAS (development option RL_DEV_LM_GEMM): row-major operands as column-major GEMMs:
+    // dh^T [d x C] = W^T [d x V] . G^T [V x C]
     if (dhidden &&
         cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)d, (int)C, (int)vocab, &one, weight, CUDA_R_16BF, (int)ld_weight,
                      G, CUDA_R_16BF, (int)ldg, &zero, dhidden + (size_t)t0 * ld_dhidden, CUDA_R_32F, (int)ld_dhidden,
                      CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
       return fail(RL_ERR_CUDA, "cublasGemmEx (dh = G W) failed");
     // dW^T [d x V] (+)= h^T [d x C] . G [C x V]
-    const float* beta = (acc_w || t0 > 0) ? &one : &zero;
     if (dweight &&
         cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)d, (int)vocab, (int)C, &one, h0, CUDA_R_16BF, (int)ld_hidden,
                      G, CUDA_R_16BF, (int)ldg, beta, dweight, CUDA_R_32F, (int)ld_dweight, CUBLAS_COMPUTE_32F,
