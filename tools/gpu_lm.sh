@@ -1,6 +1,9 @@
 #!/bin/bash
 set -u
 O=gpurun_out/${1:-lm}; mkdir -p $O
-# one 8,192-token chunk: dh GEMM (lm_gemm_kernel<false,true>) then dW GEMM (<true,true>)
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:lm_gemm -c 2 -o $O/prof_gemm \
-  python tools/lmbench.py --rows 8192 --reps 1 --bwd --chunk 8192 > $O/ncu_gemm.log 2>&1; echo "ncu rc=$?" >> $O/ncu_gemm.log
+for mode in "" "--cublas"; do
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches$mode.csv \
+  python tools/lmbench.py --rows 16384 --reps 2 --bwd --chunk 16384 $mode > $O/ncu$mode.log 2>&1; echo "rc=$?" >> $O/ncu$mode.log
+timeout 300 python tools/lmbench.py --rows 16384 --reps 5 --bwd --chunk 16384 $mode >> $O/lmbench.log 2>&1
+done
+nvidia-smi --query-gpu=clocks.sm,power.draw,clocks_throttle_reasons.active --format=csv >> $O/lmbench.log
