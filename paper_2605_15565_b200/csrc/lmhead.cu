@@ -483,79 +483,122 @@ struct GmArgs {
   int64_t ldo;
   int32_t M, N, kblocks;
   int32_t accumulate;
+  int32_t nblocks;  // PAIR launches: N blocks (the grid is 1-D)
 };
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, bool PAIR>
 __global__ void __launch_bounds__(kGmThreads, 1)
     lm_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    const GmArgs g) {
+  // PAIR: clusters of two CTAs, one 256 x 256 output tile per pair (tcgen05 cta_group::2, M = 256):
+  // each CTA stages its own 128 rows of A and half of the tile's N columns of B (MN-major B only)
+  static_assert(!PAIR || B_MN, "paired tiles split an MN-major B operand");
+  constexpr int STAGES = PAIR ? 6 : kGmStages;
+  constexpr uint32_t BBYTES = PAIR ? kGmBBytes / 2 : kGmBBytes;
+  constexpr uint32_t STAGE = kGmABytes + BBYTES;
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
                              ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(kGmBN >> 3) << 17) |
-                             ((uint32_t)(kGmBM >> 4) << 24);
+                             ((uint32_t)((PAIR ? 2 * kGmBM : kGmBM) >> 4) << 24);
   extern __shared__ uint8_t gm_smem_raw[];
-  __shared__ __align__(8) uint64_t full[kGmStages], empty[kGmStages], acc_full;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], acc_full;
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = (sm100::smem_u32(gm_smem_raw) + 1023u) & ~1023u;
-  const int32_t m0 = (int32_t)blockIdx.y * kGmBM, n0 = (int32_t)blockIdx.x * kGmBN;
+  const uint32_t crank = PAIR ? sm100::cluster_ctarank() : 0;
+  const bool leader = crank == 0;
+  int32_t m0, n0;
+  if (PAIR) {  // 1-D grid of clusters: (pair tile = N block fastest, then M pair) x rank
+    const uint32_t pt = blockIdx.x >> 1;
+    n0 = (int32_t)(pt % (uint32_t)g.nblocks) * kGmBN;
+    m0 = (int32_t)((pt / (uint32_t)g.nblocks) * 2 + crank) * kGmBM;
+  } else {
+    m0 = (int32_t)blockIdx.y * kGmBM;
+    n0 = (int32_t)blockIdx.x * kGmBN;
+  }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kGmStages; ++i) {
-      sm100::mbar_init(&full[i], 1);
+    for (int i = 0; i < STAGES; ++i) {
+      sm100::mbar_init(&full[i], PAIR ? 2 : 1);
       sm100::mbar_init(&empty[i], 1);
     }
     sm100::mbar_init(&acc_full, 1);
     sm100::fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                     sm100::smem_u32(&tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                       sm100::smem_u32(&tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                       sm100::smem_u32(&tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) sm100::cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
       for (int kb = 0; kb < g.kblocks; ++kb) {
-        const int st = kb % kGmStages;
-        sm100::mbar_wait(&empty[st], ((uint32_t)(kb / kGmStages) & 1u) ^ 1u);
-        const uint32_t sa = sbase + (uint32_t)st * kGmStage, sb = sa + kGmABytes;
-        sm100::mbar_arrive_expect_tx(&full[st], kGmStage);
+        const int st = kb % STAGES;
+        sm100::mbar_wait(&empty[st], ((uint32_t)(kb / STAGES) & 1u) ^ 1u);
+        const uint32_t sa = sbase + (uint32_t)st * STAGE, sb = sa + kGmABytes;
         const int32_t k0 = kb * kGmBK;
-        if (A_MN) {  // two 64-wide M slabs of the row-major [K, M] operand
-          tma_load_2d(sa, &tm_a, m0, k0, &full[st]);
-          tma_load_2d(sa + 8192, &tm_a, m0 + 64, k0, &full[st]);
+        if (PAIR) {
+          const uint32_t lbar = cluster_addr(&full[st], 0);
+          if (leader) sm100::mbar_arrive_expect_tx(&full[st], 2 * STAGE);
+          else sm100::mbar_arrive_remote_relaxed(&full[st], 0);
+          if (A_MN) {
+            tma_load_2d_pair(sa, &tm_a, m0, k0, lbar);
+            tma_load_2d_pair(sa + 8192, &tm_a, m0 + 64, k0, lbar);
+          } else {
+            tma_load_2d_pair(sa, &tm_a, k0, m0, lbar);
+          }
+          const int32_t nh = n0 + (int32_t)crank * (kGmBN / 2);  // this CTA's half of the N columns
+          tma_load_2d_pair(sb, &tm_b, nh, k0, lbar);
+          tma_load_2d_pair(sb + 8192, &tm_b, nh + 64, k0, lbar);
         } else {
-          tma_load_2d(sa, &tm_a, k0, m0, &full[st]);
-        }
-        if (B_MN) {  // four 64-wide N slabs of the row-major [K, N] operand
+          sm100::mbar_arrive_expect_tx(&full[st], STAGE);
+          if (A_MN) {  // two 64-wide M slabs of the row-major [K, M] operand
+            tma_load_2d(sa, &tm_a, m0, k0, &full[st]);
+            tma_load_2d(sa + 8192, &tm_a, m0 + 64, k0, &full[st]);
+          } else {
+            tma_load_2d(sa, &tm_a, k0, m0, &full[st]);
+          }
+          if (B_MN) {  // four 64-wide N slabs of the row-major [K, N] operand
 #pragma unroll
-          for (int q = 0; q < 4; ++q) tma_load_2d(sb + q * 8192, &tm_b, n0 + 64 * q, k0, &full[st]);
-        } else {
-          tma_load_2d(sb, &tm_b, k0, n0, &full[st]);
+            for (int q = 0; q < 4; ++q) tma_load_2d(sb + q * 8192, &tm_b, n0 + 64 * q, k0, &full[st]);
+          } else {
+            tma_load_2d(sb, &tm_b, k0, n0, &full[st]);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+    if (lane == 0 && leader) {  // --------------------------------------- MMA issuer (PAIR: the leader)
       for (int kb = 0; kb < g.kblocks; ++kb) {
-        const int st = kb % kGmStages;
-        sm100::mbar_wait(&full[st], (uint32_t)(kb / kGmStages) & 1u);
+        const int st = kb % STAGES;
+        sm100::mbar_wait(&full[st], (uint32_t)(kb / STAGES) & 1u);
         tc_fence_after();
-        const uint32_t sa = sbase + (uint32_t)st * kGmStage, sb = sa + kGmABytes;
+        const uint32_t sa = sbase + (uint32_t)st * STAGE, sb = sa + kGmABytes;
         const uint64_t ad = A_MN ? umma_desc_mn_sw128(sa) : umma_desc_sw128(sa);
         const uint64_t bd = B_MN ? umma_desc_mn_sw128(sb) : umma_desc_sw128(sb);
 #pragma unroll
         for (int k = 0; k < kGmBK / 16; ++k) {
           // K step of 16: K-major +32 B (2 units), MN-major +16 rows x 128 B (128 units)
           const uint64_t ao = A_MN ? 128ull * k : 2ull * k, bo = B_MN ? 128ull * k : 2ull * k;
-          umma_bf16(tmem, ad + ao, bd + bo, IDESC, (kb | k) != 0);
+          if (PAIR) umma_bf16_pair(tmem, ad + ao, bd + bo, IDESC, (kb | k) != 0);
+          else umma_bf16(tmem, ad + ao, bd + bo, IDESC, (kb | k) != 0);
         }
-        umma_commit(&empty[st]);
+        if (PAIR) umma_commit_pair(&empty[st]);
+        else umma_commit(&empty[st]);
       }
-      umma_commit(&acc_full);
+      if (PAIR) umma_commit_pair(&acc_full);
+      else umma_commit(&acc_full);
     }
   } else {  // ---------------------------------------------------------- epilogue warps 2..5
     const int q = warp & 3;
@@ -592,10 +635,12 @@ __global__ void __launch_bounds__(kGmThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) sm100::cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+    if (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -656,13 +701,36 @@ static rl_status lm_gemm(const CUtensorMap& ta, const CUtensorMap& tb, float* ou
   g.N = (int32_t)N;
   g.kblocks = (int32_t)((K + kGmBK - 1) / kGmBK);
   g.accumulate = accumulate ? 1 : 0;
-  if (cudaFuncSetAttribute(lm_gemm_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGmSmem) !=
-      cudaSuccess)
-    return check_launch("cudaFuncSetAttribute(lm_gemm)");
-  if ((M + kGmBM - 1) / kGmBM > 65535) return fail(RL_ERR_UNSUPPORTED, "lm_gemm: M too large");
-  const dim3 grid((unsigned)((N + kGmBN - 1) / kGmBN), (unsigned)((M + kGmBM - 1) / kGmBM));
-  lm_gemm_kernel<A_MN, B_MN><<<grid, kGmThreads, kGmSmem, s>>>(ta, tb, g);
-  return check_launch(A_MN ? "lm_gemm_kernel<dW>" : "lm_gemm_kernel<dh>");
+  const int64_t mb = (M + kGmBM - 1) / kGmBM, nb = (N + kGmBN - 1) / kGmBN;
+  g.nblocks = (int32_t)nb;
+  const bool pair = B_MN && mb >= 2 && dev_option(OPT_LM_PAIR) != 1;
+  if (!pair) {
+    auto kern = lm_gemm_kernel<A_MN, B_MN, false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGmSmem) != cudaSuccess)
+      return check_launch("cudaFuncSetAttribute(lm_gemm)");
+    if (mb > 65535) return fail(RL_ERR_UNSUPPORTED, "lm_gemm: M too large");
+    kern<<<dim3((unsigned)nb, (unsigned)mb), kGmThreads, kGmSmem, s>>>(ta, tb, g);
+    return check_launch(A_MN ? "lm_gemm_kernel<dW>" : "lm_gemm_kernel<dh>");
+  }
+  // B_MN is always true on this path (static_assert in the kernel)
+  auto kern = lm_gemm_kernel<A_MN, true, true>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGmSmem) != cudaSuccess)
+    return check_launch("cudaFuncSetAttribute(lm_gemm pair)");
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)((mb + 1) / 2 * 2 * nb), 1, 1);
+  cfg.blockDim = dim3(kGmThreads);
+  cfg.dynamicSmemBytes = kGmSmem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ta, tb, g) != cudaSuccess)
+    return check_launch(A_MN ? "lm_gemm_kernel<dW, pair>" : "lm_gemm_kernel<dh, pair>");
+  return check_launch(A_MN ? "lm_gemm_kernel<dW, pair>" : "lm_gemm_kernel<dh, pair>");
 }
 
 }  // namespace rl
