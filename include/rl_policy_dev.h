@@ -22,8 +22,8 @@
  *   7 RL_DEV_LM_PAIR      LM-head kernels: 0 = CTA pairs (cta_group::2) for the backward's gradient
  *                         kernel, single CTAs for the log-prob kernel (default); 1 = single CTAs;
  *                         2 = pairs for both (pairs need >= 2 token blocks)
- *   8 RL_DEV_LM_GEMM      rl_lmhead_loss_bwd's dh / dW GEMMs: 0 = lm_gemm_kernel on tcgen05 (default),
- *                         1 = cuBLAS
+ *   8 RL_DEV_LM_GEMM      rl_lmhead_loss_bwd's dh / dW GEMMs: 0 / 1 = cuBLAS (default), 2 = the
+ *                         hand-written lm_gemm_kernel on tcgen05 (with RL_DEV_LM_PAIR = 2: CTA pairs)
  * Options are read at launch time; set them before the calls they should affect.
  */
 #ifndef RL_POLICY_DEV_H_

@@ -895,10 +895,10 @@ def _lm_bwd_check(cuda_lib, N, d, V, seed, chunk=None, ld_h=None, ld_w=None, inv
     (300, 192, 1003, 128, 200, 208, 0.7),        # 3 chunks, padded strides, V % 32 != 0, temperature
     (128, 64, 8, None, None, None, 1.0),         # one vocabulary tile narrower than 32 columns
 ])
-@pytest.mark.parametrize("pair_opt,gemm_opt", [(0, 0), (1, 0), (2, 0), (0, 1)])
+@pytest.mark.parametrize("pair_opt,gemm_opt", [(0, 0), (1, 0), (2, 0), (0, 2), (1, 2), (2, 2)])
 def test_lmhead_loss_bwd(cuda_lib, N, d, V, chunk, ld_h, ld_w, inv_t, pair_opt, gemm_opt):
-    """RL_DEV_LM_PAIR: default / single CTAs / pairs everywhere; RL_DEV_LM_GEMM: the tcgen05 GEMMs
-    (default) or cuBLAS for dh and dW."""
+    """RL_DEV_LM_PAIR: default / single CTAs / pairs everywhere; RL_DEV_LM_GEMM: cuBLAS (default) or
+    the hand-written tcgen05 GEMMs (lm_gemm_kernel, single CTAs or pairs) for dh and dW."""
     old = cuda_lib.dev_set_option(cuda_lib.DEV_LM_PAIR, pair_opt)
     old_g = cuda_lib.dev_set_option(cuda_lib.DEV_LM_GEMM, gemm_opt)
     try:

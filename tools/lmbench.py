@@ -19,8 +19,8 @@ def main():
         rl.dev_set_option(rl.DEV_LM_PAIR, 1)
     if "--pairs" in sys.argv:    # pairs for the forward too
         rl.dev_set_option(rl.DEV_LM_PAIR, 2)
-    if "--cublas" in sys.argv:   # the backward's dh / dW GEMMs through cuBLAS
-        rl.dev_set_option(rl.DEV_LM_GEMM, 1)
+    if "--own-gemm" in sys.argv:  # the backward's dh / dW GEMMs on lm_gemm_kernel (tcgen05)
+        rl.dev_set_option(rl.DEV_LM_GEMM, 2)
 
     g = torch.Generator(device="cuda").manual_seed(1)
     h = torch.randn(N, d, device="cuda", generator=g).to(torch.bfloat16)
