@@ -56,8 +56,9 @@ def parse():
     ap.add_argument("--skip-masked", action="store_true",
                     help="RL_F_SKIP_MASKED_READS: masked rows are not read (write-only zeros; logp 0 there)")
     ap.add_argument("--minibatch-tokens", type=int, default=131072)
-    ap.add_argument("--vp-kernel", default="cache", choices=["cache", "ring"],
-                    help="vocabpar peer path: register-cache kernel when the shard fits (default) or the L2 ring")
+    ap.add_argument("--vp-kernel", default="auto", choices=["auto", "cache", "ring"],
+                    help="vocabpar peer path: the library's choice (auto), the register-cache kernel whenever the "
+                         "shard fits it, or the L2 ring")
     ap.add_argument("--vc-rows", type=int, default=-1,
                     help="vocabpar peer path, vp_cache_kernel: rows parked in shared memory (-1 = default)")
     ap.add_argument("--vp-width-of", type=int, default=0,
@@ -475,8 +476,8 @@ def main():
         rl.dev_set_option(rl.DEV_LOSS_KERNEL, 1)
     if args.vp_path == "nccl":
         rl.dev_set_option(rl.DEV_VP_PATH, 1)
-    if args.vp_kernel == "ring":
-        rl.dev_set_option(rl.DEV_VP_KERNEL, 1)
+    if args.vp_kernel != "auto":
+        rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if args.vp_kernel == "ring" else 2)
     if args.vc_rows >= 0:
         rl.dev_set_option(rl.DEV_VC_ROWS, args.vc_rows + 1)
     comm = None

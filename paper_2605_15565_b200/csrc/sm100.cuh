@@ -178,10 +178,14 @@ __device__ __forceinline__ uint4 lds128_a(uint32_t addr) {
 
 namespace rl {
 namespace sm100 {
-// mbarrier arrive by lane 0 of a converged warp, predicated (no branch / no warp-sync): the
-// preceding ld.shared of every lane is the same warp instruction as lane 0's, whose result the
-// arrive is ordered after.
+// mbarrier arrive by lane 0 for the whole warp (a consumer releasing a ring slot).  The
+// __syncwarp is required: the lanes leave an mbarrier try_wait loop independently (a try_wait that
+// times out while the copy lands can answer differently per lane), so without it lane 0 could
+// release the slot — and the producer refill it — before another lane's ld.shared of it ran
+// (measured: rare wrong row statistics in vp_cache_kernel once its consumers caught up with the
+// copies).
 __device__ __forceinline__ void mbar_arrive_lane0(uint32_t bar, uint32_t lane) {
+  __syncwarp();
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\t"
       "@p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar),

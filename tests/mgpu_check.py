@@ -158,27 +158,36 @@ def main():
     dlf = torch.empty_like(xs)
     lpf = torch.empty(Nf, dtype=torch.float32, device=dev)
     wsf = torch.empty(rl.vocab_parallel_workspace_size(Nf, world), dtype=torch.uint8, device=dev)
-    for vk in (0, 2):   # RL_DEV_VP_KERNEL: the default kernel choice, then the register cache forced
+    # RL_DEV_VP_KERNEL: the default kernel choice, then the register cache forced with each record
+    # send mode (RL_DEV_VC_PUB: default, collector strong, last warp weak, collector weak)
+    for vk, pub in ((0, 0), (2, 0), (2, 1), (2, 2), (2, 3)):
+        rl.dev_set_option(rl.DEV_VC_PUB, pub)
         rl.dev_set_option(rl.DEV_VP_KERNEL, vk)
         if comm.enable_peer_exchange(Nf):
             st_calls = [torch.zeros(12, dtype=torch.float64, device=dev) for _ in range(3)]
+            lp_calls = []
             for c in range(3):
                 rl.vocab_parallel_logprob(xs, yf, vs.offset, Vf, comm, lpf, wsf, old_logp=d(oldf), loss_mask=d(maskf),
                                           token_seq=d(tseqf), seq_adv=d(advf), params=pf, dlogits_shard=dlf,
                                           stats=st_calls[c])
+                lp_calls.append(lpf.clone())
             for c in range(3):
                 comm.allreduce_f64(st_calls[c])
             torch.cuda.synchronize()
             sts = [c.cpu().numpy() for c in st_calls]
             if not (np.array_equal(sts[0], sts[1]) and np.array_equal(sts[1], sts[2])):
-                fails.append(f"full-width vp (kernel option {vk}): back-to-back calls differ")
+                lps = [c.cpu().numpy() for c in lp_calls]
+                bad = [np.flatnonzero(lps[c] != lps[2]) for c in range(2)]
+                fails.append(f"full-width vp (kernel option {vk}, pub {pub}): back-to-back calls differ: "
+                             f"stats {sts[0][:4]} {sts[1][:4]} {sts[2][:4]}; logp rows differing from call 2: "
+                             f"{[(len(b), b[:6].tolist(), lps[c][b[:3]].tolist(), lps[2][b[:3]].tolist()) for c, b in enumerate(bad)]}")
             yh = yf.cpu().numpy()
             outf = oracle.policy_loss_fwd_bwd(oracle.decode_bf16(bits_rows), yh[rows], oldf[rows], maskf[rows],
                                               tseqf[rows], advf.astype(np.float64), None, None,
                                               oracle.LossParams(agg=oracle.AGG_SUM))
             lpg = lpf.cpu().numpy()[rows]
             if np.abs(lpg - outf["logp"]).max() > 2e-3:
-                fails.append(f"full-width vp ({vk}) logp err {np.abs(lpg - outf['logp']).max()}")
+                fails.append(f"full-width vp ({vk}, {pub}) logp err {np.abs(lpg - outf['logp']).max()}")
             sc = max(abs(outf["loss"]), float(np.abs(outf["token_loss"]).sum()))
             if abs(sts[2][0] - outf["loss"]) > 1e-4 * sc or sts[2][1] != outf["stats"]["active_tokens"]:
                 fails.append(f"full-width vp loss {sts[2][0]} vs {outf['loss']}")
@@ -194,6 +203,7 @@ def main():
         else:
             fails.append("full-width vp: peer exchange unavailable")
     rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
+    rl.dev_set_option(rl.DEV_VC_PUB, 0)
     del xf, xs, dlf
 
     # ------------------------------------------------------------------ M2PO global selection

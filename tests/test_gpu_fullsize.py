@@ -434,3 +434,57 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
             else:
                 assert np.abs(d[k] - out["dlogits"][k]).max() <= DLOGIT_ROW_RTOL * abs(s), k
     assert st[1] == out["stats"]["active_tokens"]
+
+
+# ------------------------------------------------------------------------------- determinism
+@pytest.mark.parametrize("kind,W", [("sv", 151936), ("peer", 37984), ("peer", 18992), ("peer_ring", 37984),
+                                    ("nccl", 37984)])
+def test_repeated_calls_bitwise_identical(cuda_lib, kind, W):
+    """Five back-to-back calls on the same inputs give bit-identical log-probs, statistics and
+    dlogits (the reduction order is fixed, §8(a) a6).  Guards the TMA-ring consumer protocol: a warp
+    releasing a ring slot before all its lanes read it (fixed in sm100::mbar_arrive_lane0) showed up
+    as rare, slightly different row statistics between identical calls."""
+    rl, t = cuda_lib, torch()
+    N = 16384
+    x = t.empty((N, W), dtype=t.bfloat16, device="cuda")
+    yd = t.empty(N, dtype=t.int32, device="cuda")
+    synth.device_logits(x, W, 0, 11, targets_out=yd)
+    g = t.Generator(device="cuda").manual_seed(3)
+    old = -t.rand(N, device="cuda", generator=g) * 4
+    L = 512
+    tseq = (t.arange(N, device="cuda") // L).to(t.int32)
+    adv = t.randn(N // L, device="cuda", generator=g)
+    p = rl.LossParams(global_active_tokens=float(N))
+    stats = t.zeros(12, dtype=t.float64, device="cuda")
+    logp = t.empty(N, device="cuda")
+    dl = t.empty_like(x)
+    outs = []
+    comm = None
+    try:
+        if kind == "sv":
+            ws = t.empty(rl.policy_loss_workspace_size(N, W), dtype=t.uint8, device="cuda")
+            call = lambda: rl.policy_loss_fwd_bwd(x, yd, old, tseq, adv, p, dl, stats, ws, logp_out=logp)
+        else:
+            comm = rl.Comm.local()
+            if kind.startswith("peer"):
+                assert comm.enable_peer_exchange(N)
+                rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if kind == "peer_ring" else 2)
+            else:
+                rl.dev_set_option(rl.DEV_VP_PATH, 1)
+            ws = t.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=t.uint8, device="cuda")
+            call = lambda: rl.vocab_parallel_logprob(x, yd, 0, W, comm, logp, ws, old_logp=old, token_seq=tseq,
+                                                     seq_adv=adv, params=p, dlogits_shard=dl, stats=stats)
+        for _ in range(5):
+            stats.zero_()
+            call()
+            outs.append((logp.clone(), stats.clone(), dl.view(t.int16)[::7].clone()))
+        t.cuda.synchronize()
+    finally:
+        rl.dev_set_option(rl.DEV_VP_PATH, 0)
+        rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
+        if comm is not None:
+            comm.destroy()
+    for c in range(1, 5):
+        for a, b, what in zip(outs[0], outs[c], ("logp", "stats", "dlogits")):
+            diff = (a != b).nonzero()
+            assert diff.numel() == 0, (kind, W, c, what, diff[:8].flatten().tolist())
