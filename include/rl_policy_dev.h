@@ -24,6 +24,8 @@
  *                         2 = pairs for both (pairs need >= 2 token blocks)
  *   8 RL_DEV_LM_GEMM      rl_lmhead_loss_bwd's dh / dW GEMMs: 0 / 1 = cuBLAS (default), 2 = the
  *                         hand-written lm_gemm_kernel on tcgen05 (with RL_DEV_LM_PAIR = 2: CTA pairs)
+ *   9 RL_DEV_VR_DELAY     vp_ring_kernel rows between the two reads of a row slice (0 = the L2-window
+ *                         rule, default; else that many, with one row per service group)
  * Options are read at launch time; set them before the calls they should affect.
  */
 #ifndef RL_POLICY_DEV_H_
@@ -41,6 +43,7 @@ extern "C" {
 #define RL_DEV_VC_PUB 6
 #define RL_DEV_LM_PAIR 7
 #define RL_DEV_LM_GEMM 8
+#define RL_DEV_VR_DELAY 9
 int32_t rl_dev_set_option(int32_t key, int32_t value);
 #ifdef __cplusplus
 }

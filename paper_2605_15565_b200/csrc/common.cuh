@@ -44,7 +44,8 @@ enum DevOpt {
   OPT_VC_PUB = 6,       // vp_cache_kernel record send, value + 1: 0 collector strong, 1 last warp weak (default), 2 collector weak
   OPT_LM_PAIR = 7,      // LM-head kernels: 0 = pairs for the gradient kernel only, 1 = single CTAs, 2 = pairs for both
   OPT_LM_GEMM = 8,      // LM-head backward GEMMs: 0 / 1 = cuBLAS (default), 2 = lm_gemm_kernel (tcgen05)
-  OPT_COUNT = 9
+  OPT_VR_DELAY = 9,     // vp_ring_kernel rows between a slice's two reads (0 = L2-window rule; sets G = 1)
+  OPT_COUNT = 10
 };
 int dev_option(int key);
 
