@@ -703,8 +703,10 @@ constexpr int kVcStat = 32, kVcScale = 32;
 #ifdef RL_VC_TRACE
 // development build only (python -m paper_2605_15565_b200.build --variant trace): per-CTA cycle
 // counters — 0 consumer wait for the row scale, 1 consumer wait for ring data, 2 collector wait for
-// the row's own record, 3 collector poll for the peers' records, 4 collector chain per row, 5 rows
-__device__ unsigned long long g_vc_trace[256][8];
+// the row's own record, 3 collector poll for the peers' records, 4 collector chain per row, 5 rows,
+// 6 consumer thread 0's cycles in the kernel, 7 the CTA's SM id (last call), 8 collector: peers'
+// records in -> row scale posted
+__device__ unsigned long long g_vc_trace[256][12];
 #define RL_VC_T0(v) const long long v = clock64()
 #define RL_VC_ADD(i, v) do { if (blockIdx.x < 256) atomicAdd(&g_vc_trace[blockIdx.x][i], (unsigned long long)(clock64() - (v))); } while (0)
 #else
@@ -797,35 +799,47 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     const double inv_tm = token_mean_inv(a.kn);
     Acc acc;
     acc.zero();
-    // row kk + 1's level-1 metadata is loaded while row kk is combined (lane 0)
-    int32_t ny = 0, nseq = 0;
-    uint8_t nmask = 1;
-    float nold = 0.f, nprox = 0.f, nref = 0.f;
-    auto load_l1 = [&](int64_t kk) {
+    // metadata pipeline (lane 0 of the group), so no global-load latency sits between the peers'
+    // records and the row's scale: while row kk is combined, the sequence-indexed (level-2) loads
+    // of row kk + G and the row-indexed (level-1) loads of row kk + 2G are in flight
+    struct Meta {
+      int32_t y = 0, seq = 0, ver = 0, act = 0;
+      uint8_t mk = 1;
+      float old = 0.f, prox = 0.f, ref = 0.f, A = 0.f;
+    };
+    auto load_l1 = [&](Meta& m, int64_t kk) {
       if (q == 0 && kk < nk) {
         const int64_t row = row_of(kk);
-        ny = a.targets[row];
-        nseq = a.token_seq ? a.token_seq[row] : 0;
-        nmask = a.mask ? a.mask[row] : 1;
-        nold = a.old_logp[row];
-        token_extra(a.kn, row, nold, nprox, nref);
+        m.y = a.targets[row];
+        m.seq = a.token_seq ? a.token_seq[row] : 0;
+        m.mk = a.mask ? a.mask[row] : 1;
+        m.old = a.old_logp[row];
+        token_extra(a.kn, row, m.old, m.prox, m.ref);
       }
     };
-    load_l1(grp);
-    for (int64_t kk = grp; kk < nk; kk += G) {
-      const int64_t row = row_of(kk);
-      const int32_t y = ny, seq = nseq;
-      const uint8_t mk = nmask;
-      const float old = nold, prox = nprox, ref = nref;
-      int32_t ver = 0, act = 0;
-      float A = 0.f;
-      if (q == 0) {
-        if (a.seq_version) ver = a.seq_version[seq];
-        if (mk != 0 && y >= 0 && (int64_t)y < a.Vtot) {
-          A = a.seq_adv[seq];
-          if (a.seq_active) act = a.seq_active[seq];
+    auto load_l2 = [&](Meta& m, int64_t kk) {
+      if (q == 0 && kk < nk) {
+        if (a.seq_version) m.ver = a.seq_version[m.seq];
+        if (m.mk != 0 && m.y >= 0 && (int64_t)m.y < a.Vtot) {
+          m.A = a.seq_adv[m.seq];
+          if (a.seq_active) m.act = a.seq_active[m.seq];
         }
       }
+    };
+    Meta mnext, mnext2;
+    load_l1(mnext, grp);
+    load_l2(mnext, grp);
+    load_l1(mnext2, grp + G);
+    for (int64_t kk = grp; kk < nk; kk += G) {
+      const int64_t row = row_of(kk);
+      const Meta cur = mnext;
+      mnext = mnext2;
+      load_l2(mnext, kk + G);
+      mnext2 = Meta{};
+      load_l1(mnext2, kk + 2 * G);
+      const int32_t y = cur.y, seq = cur.seq, ver = cur.ver, act = cur.act;
+      const uint8_t mk = cur.mk;
+      const float old = cur.old, prox = cur.prox, ref = cur.ref, A = cur.A;
       RL_VC_T0(tc0);
       {  // publish this rank's record of the row: lane q of the group sends it to rank q
         const int ss = (int)(kk % kVcStat);
@@ -859,7 +873,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         zyq = __uint_as_float((uint32_t)w1);
       }
       if (grp == 0 && q == 0) RL_VC_ADD(3, tc1);
-      load_l1(kk + G);
+      RL_VC_T0(tc2);
       float M = -INFINITY;
       for (int j = 0; j < a.P; ++j) M = fmaxf(M, __shfl_sync(gmask, c2q, lead + j));
       float S = 0.f, zy = 0.f;
@@ -901,6 +915,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         sm100::mbar_arrive(&sh.scale_full[sl]);
         if (grp == 0) {
           RL_VC_ADD(4, tc0);
+          RL_VC_ADD(8, tc2);
 #ifdef RL_VC_TRACE
           if (blockIdx.x < 256) atomicAdd(&g_vc_trace[blockIdx.x][5], 1ull);
 #endif
@@ -921,6 +936,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
   }
 
   // ------------------------------------------------------------------------------ consumers
+  RL_VC_T0(tk0);
   uint4 cache[R][NV];
   const uint32_t my_off = (uint32_t)tid * 16u;
   const uint64_t k2 = f2pack(k, k);
@@ -1080,6 +1096,14 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
       });
     }
   }
+#ifdef RL_VC_TRACE
+  if (tid == 0 && blockIdx.x < 256) {  // 6: consumer thread 0's cycles in the kernel, 7: SM id
+    RL_VC_ADD(6, tk0);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_vc_trace[blockIdx.x][7] = smid;
+  }
+#endif
 }
 
 
@@ -1284,7 +1308,7 @@ extern "C" int rl_debug_vc_trace(unsigned long long* host, size_t bytes, int cle
   const size_t n = sizeof(rl::g_vc_trace) < bytes ? sizeof(rl::g_vc_trace) : bytes;
   if (host && cudaMemcpyFromSymbol(host, rl::g_vc_trace, n) != cudaSuccess) return 1;
   if (clear) {
-    static unsigned long long zero[256 * 8] = {};
+    static unsigned long long zero[256 * 12] = {};
     if (cudaMemcpyToSymbol(rl::g_vc_trace, zero, sizeof(zero)) != cudaSuccess) return 1;
   }
   return 0;

@@ -32,6 +32,7 @@ def main():
         rl.dev_set_option(6, int(sys.argv[sys.argv.index("--pub") + 1]) + 1)
     if "--rs" in sys.argv:
         rl.dev_set_option(5, int(sys.argv[sys.argv.index("--rs") + 1]) + 1)
+    rl.dev_set_option(rl.DEV_VP_KERNEL, 2)   # the register-cache kernel (the only one with counters)
     V, N = 151936, 65536
     W = int(sys.argv[sys.argv.index("--width-of") + 1]) if "--width-of" in sys.argv else world
     sh = shard_vocab(V, W, rank % W)
@@ -65,18 +66,20 @@ def main():
         call()
     b.record()
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (256 * 8))()
+    buf = (ctypes.c_ulonglong * (256 * 12))()
     assert lib.rl_debug_vc_trace(ctypes.cast(buf, ctypes.c_void_p), ctypes.sizeof(buf), 0) == 0
-    tr = np.frombuffer(buf, dtype=np.uint64).reshape(256, 8)[:148].astype(np.float64)
+    tr = np.frombuffer(buf, dtype=np.uint64).reshape(256, 12)[:148].astype(np.float64)
     rows_per_cta = N / 148 * reps
     ghz = 1.965
     names = ["consumer wait scale", "consumer wait data", "collector wait own record",
              "collector poll peers", "collector chain / row"]
     line = [f"[rank {rank}] {a.elapsed_time(b) / reps:.3f} ms/call, Vr={Vr}"]
-    for i, nm in enumerate(names):
+    for i, nm in list(enumerate(names)) + [(8, "collector records -> scale")]:
         per = tr[:, i].mean() / (rows_per_cta if i < 2 else max(1.0, tr[:, 5].mean())) / (ghz * 1e3)
         line.append(f"{nm}: {per:.2f} us/row")
     print("; ".join(line), flush=True)
+    if "--dump" in sys.argv:   # per-CTA counters of this rank (cross-rank straggler analysis)
+        np.save(sys.argv[sys.argv.index("--dump") + 1] + f"_rank{rank}.npy", tr)
     comm.destroy()
     if world > 1:
         dist.destroy_process_group()
