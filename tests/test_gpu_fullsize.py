@@ -488,3 +488,50 @@ def test_repeated_calls_bitwise_identical(cuda_lib, kind, W):
         for a, b, what in zip(outs[0], outs[c], ("logp", "stats", "dlogits")):
             diff = (a != b).nonzero()
             assert diff.numel() == 0, (kind, W, c, what, diff[:8].flatten().tolist())
+
+
+# ------------------------------------------------------------------------------- padded vocabulary
+@pytest.mark.parametrize("in_place", [False, True])
+def test_padded_vocab_tail_columns(cuda_lib, in_place):
+    """V = 151,665 (Qwen2.5's vocabulary, not a multiple of 8) in rows of ld = 151,936: the default
+    kernel must take its generic instantiation (the exact-width ones assume whole 16-B vectors) and
+    cover the 1 scalar tail column of every row — targets placed in the last 9 columns, sampled rows
+    against the oracle, the pad columns beyond V left untouched."""
+    rl, t = cuda_lib, torch()
+    N, V, ld = 8192, 151665, 151936
+    x = t.empty((N, ld), dtype=t.bfloat16, device="cuda")
+    yd = t.empty(N, dtype=t.int32, device="cuda")
+    synth.device_logits(x, V, 0, 21, targets_out=yd)
+    x[:, V:] = 7.0                                 # pad columns: must stay as they are
+    y = yd.cpu().numpy()
+    y[::3] = V - 1 - (np.arange(len(y[::3])) % 9)  # targets in the tail (incl. the scalar column)
+    y[::11] = -100
+    yd = dev(y)
+    rows = np.sort(np.random.default_rng(9).choice(N, size=N_SAMPLED, replace=False))
+    mask = np.zeros(N, dtype=np.uint8)
+    mask[rows] = 1
+    L = 512
+    tseq = (np.arange(N) // L).astype(np.int32)
+    adv = np.random.default_rng(10).normal(size=N // L).astype(np.float32)
+    bits = rows_bits(x, rows, V)
+    lp_ref = oracle_logp_rows(bits, y[rows])
+    rng = np.random.default_rng(12)
+    old = np.zeros(N, dtype=np.float32)
+    ok = y[rows] >= 0
+    old[rows] = np.where(ok, lp_ref + rng.normal(size=len(rows)) * 0.05, 0.0).astype(np.float32)
+    old[rows] = nudge_out_of_band(old[rows], lp_ref, ok.astype(np.uint8))
+    n_act = float((mask[rows] != 0)[ok].sum())
+    p = rl.LossParams(global_active_tokens=n_act)
+    dl = x if in_place else t.full_like(x, 7.0)
+    stats = t.zeros(12, dtype=t.float64, device="cuda")
+    ws = t.empty(rl.policy_loss_workspace_size(N, V), dtype=t.uint8, device="cuda")
+    logp = t.empty(N, device="cuda")
+    clipped = t.empty(N, dtype=t.uint8, device="cuda")
+    rl.policy_loss_fwd_bwd(x, yd, dev(old), dev(tseq), dev(adv), p, dl, stats, ws, loss_mask=dev(mask),
+                           logp_out=logp, clipped_out=clipped, vocab=V)
+    t.cuda.synchronize()
+    g_lp = logp.cpu().numpy()
+    po = oracle.LossParams(global_active_tokens=n_act)
+    check_sampled(bits, rows, y, old, mask, tseq, adv.astype(np.float64), None, None, po, g_lp,
+                  rows_bits(dl, rows, V), stats.cpu().numpy(), g_clipped=clipped.cpu().numpy())
+    assert t.all(dl[:, V:] == 7.0), "pad columns beyond V were written"
