@@ -74,7 +74,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     nvcc = _nvcc()
     common = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
               "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-Xptxas", "-v",
-              "--expt-relaxed-constexpr"] + {"trace": ["-DRL_VC_TRACE"], "checks": ["-DRL_DEBUG_CHECKS"]}.get(variant, [])
+              "--expt-relaxed-constexpr"] + {"trace": ["-DRL_VC_TRACE"], "checks": ["-DRL_DEBUG_CHECKS"],
+                                           "ab": ["-DRL_AB"]}.get(variant, [])
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
         extra = ["-fmad=false"] if os.path.basename(src) == "advantage.cu" else []

@@ -72,6 +72,8 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
   const size_t ring_off = (sizeof(SvShared) + 2 * sizeof(uint64_t) * a.nslots + 127) & ~(size_t)127;
   uint4* ring = reinterpret_cast<uint4*>(smem_raw + ring_off);
   const int nslots = a.nslots;
+  const uint32_t rt_zero = (uint32_t)nslots >> 31;  // 0 at run time (sm100::mbar_release_after)
+  uint32_t dep = 0;                                  // bits of the ring vectors this thread read
   const uint32_t full_s = sm100::smem_u32(full), empty_s = sm100::smem_u32(empty);
   const uint32_t ring_s = sm100::smem_u32(ring);
 
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
   if (tid == 0) {
     for (int i = 0; i < nslots; ++i) {
       sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&empty[i], kNcw);
+      sm100::mbar_init(&empty[i], kNcw * sm100::kRelPerWarp);
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&sh.xbar[i], 1);
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
               RL_DCHECK(slot < (uint32_t)nslots && row < a.n_tokens);
               if (j % VPT == 0) sm100::mbar_wait_a(full_s + slot * 8, rph);
               const uint4 v = sm100::lds128_a(ring_s + slot * (uint32_t)(VPT * kChunkBytes) + (j % VPT) * kChunkBytes + my_off);
-              if (RL_CHUNK_END(j)) sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+              dep ^= v.x;
               if (ENT) {
                 uint64_t nx = accx;
                 const uint64_t nacc = ClVec<T>::exp_sv_ent(v, k2, mn2, acc2, nx, cache[j]);
@@ -283,6 +285,8 @@ __global__ void __launch_bounds__(kSvThreads, 1) loss_sv_kernel(const ClArgs a) 
                 const uint64_t nacc = ClVec<T>::exp_sv(v, k2, mn2, acc2, cache[j]);
                 acc2 = RL_MINE(j) ? nacc : acc2;
               }
+              // release the slot after the chunk's arithmetic consumed its data (no extra stall)
+              if (RL_CHUNK_END(j)) sm100::mbar_release_after(empty_s + slot * 8, dep, rt_zero);
               if (RL_CHUNK_END(j) && ++slot == (uint32_t)nslots) {
                 slot = 0;
                 rph ^= 1u;

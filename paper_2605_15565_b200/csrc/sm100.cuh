@@ -178,20 +178,35 @@ __device__ __forceinline__ uint4 lds128_a(uint32_t addr) {
 
 namespace rl {
 namespace sm100 {
-// mbarrier arrive by lane 0 for the whole warp (a consumer releasing a ring slot).  The
-// __syncwarp is required: the lanes leave an mbarrier try_wait loop independently (a try_wait that
-// times out while the copy lands can answer differently per lane), so without it lane 0 could
-// release the slot — and the producer refill it — before another lane's ld.shared of it ran
-// (measured: rare wrong row statistics in vp_cache_kernel once its consumers caught up with the
-// copies).
-__device__ __forceinline__ void mbar_arrive_lane0(uint32_t bar, uint32_t lane) {
-  __syncwarp();
+// A consumer thread releases a TMA ring slot (the slot's empty barrier counts every consumer
+// THREAD).  The arrive must not take effect before this thread's ld.shared of the slot has read
+// it, or the producer may refill the slot under the load.  On sm_100a an
+// mbarrier.arrive.release issued right after ld.shared — by lane 0 for its warp or by each lane
+// for itself — was measured to overtake the load when the warp's loads queue behind global
+// traffic (rare wrong row statistics in back-to-back 4-GPU vocab-parallel calls: tools/race_check.py).
+// So the arrive's predicate depends on the loaded data: `dep` = bits of the vectors this thread
+// read from the slot, `zero` = a runtime 0 that ptxas cannot fold; (dep != zero || zero == 0) is
+// always true, but the arrive issues only once the loads have returned.
+#ifdef RL_AB
+constexpr int kRelPerWarp = 1;  // A/B build: lane 0 releases for its warp
+__device__ __forceinline__ void mbar_release_after(uint32_t bar, uint32_t dep, uint32_t zero) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\t"
+      "{\n\t.reg .pred p, q;\n\t.reg .u32 l;\n\tmov.u32 l, %%laneid;\n\tsetp.ne.u32 p, %1, %2;\n\t"
+      "setp.eq.u32 q, %2, 0;\n\tor.pred p, p, q;\n\tsetp.eq.and.u32 p, l, 0, p;\n\t"
       "@p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar),
-      "r"(lane)
+      "r"(dep), "r"(zero)
       : "memory");
 }
+#else
+constexpr int kRelPerWarp = 32;  // every consumer thread arrives for itself
+__device__ __forceinline__ void mbar_release_after(uint32_t bar, uint32_t dep, uint32_t zero) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, %2;\n\tsetp.eq.u32 q, %2, 0;\n\tor.pred p, p, q;\n\t"
+      "@p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar),
+      "r"(dep), "r"(zero)
+      : "memory");
+}
+#endif
 }  // namespace sm100
 }  // namespace rl
 

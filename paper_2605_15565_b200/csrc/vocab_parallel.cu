@@ -132,11 +132,11 @@ __global__ void __launch_bounds__(kVtThreads, 1) vp_finish_tma_kernel(
   if (tid == 0) {
     for (int i = 0; i < nslots; ++i) {
       sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&empty[i], 15);
+      sm100::mbar_init(&empty[i], 15 * sm100::kRelPerWarp);
     }
     for (int i = 0; i < kVtScale; ++i) {
       sm100::mbar_init(&scbar[i], 1);
-      sm100::mbar_init(&donebar[i], 15);
+      sm100::mbar_init(&donebar[i], 15 * sm100::kRelPerWarp);
     }
     sm100::fence_mbar_init();
   }
@@ -191,6 +191,8 @@ __global__ void __launch_bounds__(kVtThreads, 1) vp_finish_tma_kernel(
   }
   // ---- consumers
   uint32_t slot = 0, rph = 0;
+  const uint32_t rt_zero = (uint32_t)nslots >> 31;  // 0 at run time (sm100::mbar_release_after)
+  uint32_t dep = 0;                                  // bits of what this thread read from the ring
   const uint32_t my_off = (uint32_t)tid * 16u;
   for (int64_t kk = 0; kk < nk; ++kk) {
     const int64_t row = (int64_t)blockIdx.x + kk * gridDim.x;
@@ -217,10 +219,11 @@ __global__ void __launch_bounds__(kVtThreads, 1) vp_finish_tma_kernel(
             onehot_sub(f, yl - c0, s);  // static indices: f stays in registers
             o = VecTraits<T>::pack(f);
           }
+          dep ^= o.x;
           st_stream_v4(vout + i, o);
         }
       }
-      sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+      sm100::mbar_release_after(empty_s + slot * 8, dep, rt_zero);
       if (++slot == (uint32_t)nslots) {
         slot = 0;
         rph ^= 1u;
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(kVtThreads, 1) vp_finish_tma_kernel(
       if (s != 0.f && cc == yl) v -= s;
       VecTraits<T>::store1(dp, cc, v);
     }
-    sm100::mbar_arrive_lane0(sm100::smem_u32(&donebar[q]), lane);
+    sm100::mbar_release_after(sm100::smem_u32(&donebar[q]), dep, rt_zero);
   }
 }
 
@@ -365,7 +368,7 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
   if (tid == 0) {
     for (int i = 0; i < a.nslots; ++i) {
       sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&empty[i], 15);
+      sm100::mbar_init(&empty[i], 15 * sm100::kRelPerWarp);
     }
     for (int i = 0; i < kVrStat; ++i) {
       sm100::mbar_init(&sh.stats_full[i], 15);
@@ -550,6 +553,7 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
   // ------------------------------------------------------------------------------ consumers
   using V = ClVec<T>;
   uint32_t slot = 0, rph = 0;
+  const uint32_t rt_zero = (uint32_t)a.nslots >> 31;  // 0 at run time (sm100::mbar_release_after)
   const uint32_t my_off = (uint32_t)tid * 16u;
   const uint64_t k2 = f2pack(k, k);
   const int64_t tail0 = nvec * EPV;
@@ -587,7 +591,7 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
           }
           own = true;
         }
-        sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+        sm100::mbar_release_after(empty_s + slot * 8, v[0].x ^ v[kVrVpt - 1].w, rt_zero);
         if (++slot == (uint32_t)a.nslots) {
           slot = 0;
           rph ^= 1u;
@@ -644,7 +648,7 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
         uint4 v[kVrVpt];
 #pragma unroll
         for (int u = 0; u < kVrVpt; ++u) v[u] = sm100::lds128_a(sb + u * (kVrCons * 16) + my_off);
-        sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+        sm100::mbar_release_after(empty_s + slot * 8, v[0].x ^ v[kVrVpt - 1].w, rt_zero);
         if (++slot == (uint32_t)a.nslots) {
           slot = 0;
           rph ^= 1u;
@@ -750,7 +754,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
   if (tid == 0) {
     for (int i = 0; i < a.nslots; ++i) {
       sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&empty[i], kVcWarps);
+      sm100::mbar_init(&empty[i], kVcWarps * sm100::kRelPerWarp);
     }
     for (int i = 0; i < kVcStat; ++i) {
       sh.cnt[i] = 0;
@@ -941,6 +945,8 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
   const uint32_t my_off = (uint32_t)tid * 16u;
   const uint64_t k2 = f2pack(k, k);
   uint32_t slot = 0, rph = 0;
+  const uint32_t rt_zero = (uint32_t)a.nslots >> 31;  // 0 at run time (sm100::mbar_release_after)
+  uint32_t dep = 0;                                    // bits of the ring vectors this thread read
   int32_t y_next = nk > 0 ? a.targets[row_of(0)] : 0;
   // load row kk into cache[r] (raw bf16), then convert in place to e' (bf16) and post the warp record
   auto load_row = [&](auto rc, int64_t kk) {
@@ -950,6 +956,10 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     const int64_t yl = (int64_t)y - a.off;
     const int yv = (y >= 0 && yl >= 0 && yl < a.Vr) ? (int)(yl >> 3) : -1;  // target's vector
     typename V::MaxT mx = V::max_init();
+    // a chunk's slot is released after the NEXT chunk's loads were issued (its own loads have
+    // returned by then, so the data-dependent release does not stall); the row's last slot after
+    // the chunk loop
+    uint32_t pend = 0;  // empty-barrier address of the slot awaiting release (0: none)
 #pragma unroll
     for (int c = 0; c < (NV + 3) / 4; ++c) {
       if (c < nch) {
@@ -958,6 +968,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         sm100::mbar_wait_a(full_s + slot * 8, rph);
         if (tid == 0) RL_VC_ADD(1, tf0);
         const uint32_t sb = ring_s + slot * (uint32_t)kVcSlot;
+        const uint32_t dprev = dep;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int i = 4 * c + u;
@@ -965,9 +976,11 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
             const bool ok = i * kVcCons + tid < nvec;
             cache[r][i] = ok ? sm100::lds128_a(sb + u * (kVcCons * 16) + my_off) : V::neg_inf_vec();
             V::max_acc(cache[r][i], mx);
+            dep ^= cache[r][i].x;
           }
         }
-        sm100::mbar_arrive_lane0(empty_s + slot * 8, lane);
+        if (pend) sm100::mbar_release_after(pend, dprev, rt_zero);
+        pend = empty_s + slot * 8;
         if (++slot == (uint32_t)a.nslots) {
           slot = 0;
           rph ^= 1u;
@@ -978,6 +991,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
           if (4 * c + u < NV) cache[r][4 * c + u] = V::neg_inf_vec();
       }
     }
+    if (pend) sm100::mbar_release_after(pend, dep, rt_zero);
     // z_y from the raw vector that holds it (its owner thread; compile-time vector index)
     float zy = 0.f;
     bool own = false;

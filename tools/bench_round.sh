@@ -15,6 +15,7 @@ run long_skip --config long --no-e2e --no-cpu --steps 10 --skip-masked
 run multi --config multi --no-e2e --no-cpu --steps 10
 run vp_w8 --config vocabpar --vp-width-of 8
 run vp_w4 --config vocabpar --vp-width-of 4
+run vp_w2 --config vocabpar --vp-width-of 2
 run lmhead --config lmhead --steps 10
 run resident --resident --no-e2e --no-cpu --steps 10
 timeout 600 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > $O/bench_short.log 2>&1 && \
@@ -26,6 +27,8 @@ prof() { local name=$1 kern=$2 skip=$3; shift 3; timeout 600 ncu --set full --cl
 prof loss_sv loss_sv_kernel 1 python tools/kbench.py --rows 16384 --reps 2
 prof vpcache8 vp_cache 1 python tools/vpbench.py --P 8 --rows 65536 --reps 2 --peer
 prof vpcache4 vp_cache 1 python tools/vpbench.py --P 4 --rows 65536 --reps 2 --peer
+prof ring4 vp_ring 1 python tools/vpbench.py --P 4 --rows 65536 --reps 2 --peer --ring
+prof ring2 vp_ring 1 python tools/vpbench.py --P 2 --rows 65536 --reps 2 --peer --ring
 # lmbench --bwd --reps 1 launches lmhead_kernel as: forward (warm), forward (timed), then the backward's
 # gradient kernel once per 8,192-token chunk: skip 2 -> the first gradient launch; skip 1 -> a forward
 prof lmgrad lmhead_kernel 2 python tools/lmbench.py --rows 16384 --reps 1 --bwd
