@@ -19,7 +19,7 @@ run vp_w2 --config vocabpar --vp-width-of 2
 run lmhead --config lmhead --steps 10
 run resident --resident --no-e2e --no-cpu --steps 10
 timeout 600 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > $O/bench_short.log 2>&1 && \
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  timeout 900 ncu --nvtx --nvtx-include timed/ --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > $O/ncu_launch.log 2>&1
 echo "launch list rc=$?" >> $O/status.txt
 prof() { local name=$1 kern=$2 skip=$3; shift 3; timeout 600 ncu --set full --clock-control none --import-source on -k regex:$kern -s $skip -c 1 \

@@ -38,24 +38,43 @@ KERNELS = {
 }
 
 
+def _base(name):
+    """'void rl::loss_sv_kernel<bf16_t, 2>(rl::ClArgs)' -> 'loss_sv_kernel'"""
+    n = name.split("(")[0].replace("void ", "").split("<")[0]
+    return n.split("::")[-1].strip()
+
+
+def _library_kernels():
+    """__global__ function names defined in the library's sources"""
+    import glob
+    import re
+    names = set()
+    for f in glob.glob(os.path.join(ROOT, "paper_2605_15565_b200", "csrc", "*.cu")):
+        names |= set(re.findall(r"__global__\s+void\s+(?:__launch_bounds__\([^)]*\)\s+)?(\w+)\s*\(", open(f).read()))
+    return names
+
+
 def launches(src, tag):
     rows = list(csv.reader(open(os.path.join(src, "launches.csv"))))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h, data = rows[hi], rows[hi + 1:]
     ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
-    ours = [(r[ki], float(r[vi].replace(",", ""))) for r in data
-            if len(r) > vi and r[mi] == "gpu__time_duration.sum" and r[ki].startswith(("void rl::", "rl::"))]
+    timed = [r for r in data if len(r) > vi and r[mi] == "gpu__time_duration.sum"]
+    n_all = len(timed)
+    ours = [(r[ki], float(r[vi].replace(",", ""))) for r in timed if _base(r[ki]) in _library_kernels()]
     with open(os.path.join(PROF, f"launches_{tag}.csv"), "w") as f:
-        f.write("# ncu --metrics gpu__time_duration.sum --clock-control none, command: python bench.py "
-                "--steps 2 --warmup 1 --no-e2e --no-cpu (cold-cache, serialised launches; compare shares)\n")
-        f.write("# only this library's kernels (the step launches no others at N=1)\nkernel,ns\n")
+        f.write("# ncu --nvtx --nvtx-include timed/ --metrics gpu__time_duration.sum --clock-control none, command: "
+                "python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu (the timed region only; cold-cache, "
+                "serialised launches: compare shares)\n")
+        f.write(f"# launches in the timed region: {n_all}, of this library: {len(ours)}\nkernel,ns\n")
         for k, v in ours:
             f.write(f"\"{k[:90]}\",{v:.0f}\n")
     agg = collections.defaultdict(list)
     for k, v in ours:
-        agg[k.split("(")[0].replace("void ", "")[:70]].append(v)
+        agg[k.split("(")[0].replace("void ", "").replace("rl::", "")[:70]].append(v)
     tot = sum(sum(v) for v in agg.values())
-    lines = [f"{'kernel':72s} {'n':>5s} {'avg_us':>10s} {'share':>7s}"]
+    lines = [f"launches in bench.py's timed region (ncu --nvtx-include timed/): {n_all}, of this library: "
+             f"{len(ours)}", f"{'kernel':72s} {'n':>5s} {'avg_us':>10s} {'share':>7s}"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"{k:72s} {len(v):5d} {sum(v) / len(v) / 1e3:10.1f} {100 * sum(v) / tot:6.2f}%")
     return "\n".join(lines)
