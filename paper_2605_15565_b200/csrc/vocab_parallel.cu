@@ -991,7 +991,6 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
           if (4 * c + u < NV) cache[r][4 * c + u] = V::neg_inf_vec();
       }
     }
-    if (pend) sm100::mbar_release_after(pend, dep, rt_zero);
     // z_y from the raw vector that holds it (its owner thread; compile-time vector index)
     float zy = 0.f;
     bool own = false;
@@ -1016,6 +1015,8 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
       f2unpack(acc2, lo, hi);
       s = lo + hi;
     }
+    // the row's last slot: released once the row's max / exp pass consumed its data (no wait)
+    if (pend) sm100::mbar_release_after(pend, dep, rt_zero);
     s = warp_sum(s);
     // slot ss is reused 32 rows later: the consumer warps stay within a few rows of each other
     // (a ring slot is refilled only once all 14 warps released it)
