@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--vp-kernel", default="auto", choices=["auto", "cache", "ring"],
                     help="vocabpar peer path: the library's choice (auto), the register-cache kernel whenever the "
                          "shard fits it, or the L2 ring")
+    ap.add_argument("--dev-opt", action="append", default=[], metavar="KEY=VALUE",
+                    help="development option of the library (include/rl_policy_dev.h), repeatable; for A/B runs")
     ap.add_argument("--vc-rows", type=int, default=-1,
                     help="vocabpar peer path, vp_cache_kernel: rows parked in shared memory (-1 = default)")
     ap.add_argument("--vp-width-of", type=int, default=0,
@@ -480,6 +482,9 @@ def main():
         rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if args.vp_kernel == "ring" else 2)
     if args.vc_rows >= 0:
         rl.dev_set_option(rl.DEV_VC_ROWS, args.vc_rows + 1)
+    for kv in args.dev_opt:
+        k, v = kv.split("=")
+        rl.dev_set_option(int(k), int(v))
     comm = None
     if world > 1 or args.config == "vocabpar":
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
