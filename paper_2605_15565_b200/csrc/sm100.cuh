@@ -187,17 +187,6 @@ namespace sm100 {
 // So the arrive's predicate depends on the loaded data: `dep` = bits of the vectors this thread
 // read from the slot, `zero` = a runtime 0 that ptxas cannot fold; (dep != zero || zero == 0) is
 // always true, but the arrive issues only once the loads have returned.
-#ifdef RL_AB
-constexpr int kRelPerWarp = 1;  // A/B build: lane 0 releases for its warp
-__device__ __forceinline__ void mbar_release_after(uint32_t bar, uint32_t dep, uint32_t zero) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\t.reg .u32 l;\n\tmov.u32 l, %%laneid;\n\tsetp.ne.u32 p, %1, %2;\n\t"
-      "setp.eq.u32 q, %2, 0;\n\tor.pred p, p, q;\n\tsetp.eq.and.u32 p, l, 0, p;\n\t"
-      "@p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar),
-      "r"(dep), "r"(zero)
-      : "memory");
-}
-#else
 constexpr int kRelPerWarp = 32;  // every consumer thread arrives for itself
 __device__ __forceinline__ void mbar_release_after(uint32_t bar, uint32_t dep, uint32_t zero) {
   asm volatile(
@@ -206,7 +195,6 @@ __device__ __forceinline__ void mbar_release_after(uint32_t bar, uint32_t dep, u
       "r"(dep), "r"(zero)
       : "memory");
 }
-#endif
 }  // namespace sm100
 }  // namespace rl
 
