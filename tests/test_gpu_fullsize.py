@@ -307,7 +307,7 @@ R2_ABS = 2.0 ** -16
 
 # ------------------------------------------------------------------------------- C4 vocab-parallel
 @pytest.mark.parametrize("W", [18992, 37984, 151936])
-@pytest.mark.parametrize("path", ["nccl", "peer", "peer_ring"])
+@pytest.mark.parametrize("path", ["nccl", "peer", "peer_ring", "peer_rs1"])
 def test_vocab_parallel_production_widths(cuda_lib, W, path):
     """rl_vocab_parallel_logprob at P = 1 with the per-rank column width of P = 8 (18,992), P = 4
     (37,984) and the whole vocabulary: the kernels' multi-chunk slice geometry of configs[3], on the
@@ -348,6 +348,8 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
         if path.startswith("peer"):
             assert comm.enable_peer_exchange(N)
             rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 2)
+            if path == "peer_rs1":   # the multi-rank configuration: one row parked in shared memory
+                rl.dev_set_option(rl.DEV_VC_ROWS, 2)
         else:
             rl.dev_set_option(rl.DEV_VP_PATH, 1)
         dl = t.empty_like(x)
@@ -364,6 +366,7 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
     finally:
         rl.dev_set_option(rl.DEV_VP_PATH, 0)
         rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
+        rl.dev_set_option(rl.DEV_VC_ROWS, 0)
         comm.destroy()
     g_lp = logp.cpu().numpy()
     assert np.all(np.abs(g_lp - lp_all) <= LOGP_ATOL), np.abs(g_lp - lp_all).max()
@@ -377,7 +380,7 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
 # ------------------------------------------------------------------------------- vocab-parallel edge cases
 @pytest.mark.parametrize("N", [1, 7, 149, 1000])
 @pytest.mark.parametrize("W", [8, 1000, 1004, 18992])
-@pytest.mark.parametrize("path", ["peer", "peer_ring", "nccl"])
+@pytest.mark.parametrize("path", ["peer", "peer_ring", "peer_rs1", "nccl"])
 def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
     """Few rows (fewer than the 148 CTAs: idle CTAs, one row per CTA), a single 16-B vector per row
     (W = 8), widths with and without whole vectors per consumer thread, on both peer kernels and the
@@ -402,6 +405,8 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
         if path.startswith("peer"):
             assert comm.enable_peer_exchange(N)
             rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 2)
+            if path == "peer_rs1":   # the multi-rank configuration: one row parked in shared memory
+                rl.dev_set_option(rl.DEV_VC_ROWS, 2)
         else:
             rl.dev_set_option(rl.DEV_VP_PATH, 1)
         dl = t.empty_like(x)
@@ -415,6 +420,7 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
     finally:
         rl.dev_set_option(rl.DEV_VP_PATH, 0)
         rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
+        rl.dev_set_option(rl.DEV_VC_ROWS, 0)
         comm.destroy()
     out = oracle.policy_loss_fwd_bwd(oracle.decode_bf16(bits), y, old, mask, tseq, adv.astype(np.float64), None,
                                      None, oracle.LossParams(agg=oracle.AGG_SUM))
@@ -437,8 +443,8 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
 
 
 # ------------------------------------------------------------------------------- determinism
-@pytest.mark.parametrize("kind,W", [("sv", 151936), ("peer", 37984), ("peer", 18992), ("peer_ring", 37984),
-                                    ("nccl", 37984)])
+@pytest.mark.parametrize("kind,W", [("sv", 151936), ("peer", 37984), ("peer", 18992), ("peer_rs1", 18992),
+                                    ("peer_ring", 37984), ("nccl", 37984)])
 def test_repeated_calls_bitwise_identical(cuda_lib, kind, W):
     """Five back-to-back calls on the same inputs give bit-identical log-probs, statistics and
     dlogits (the reduction order is fixed, §8(a) a6).  Guards the TMA-ring consumer protocol: a warp
@@ -469,6 +475,8 @@ def test_repeated_calls_bitwise_identical(cuda_lib, kind, W):
             if kind.startswith("peer"):
                 assert comm.enable_peer_exchange(N)
                 rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if kind == "peer_ring" else 2)
+                if kind == "peer_rs1":
+                    rl.dev_set_option(rl.DEV_VC_ROWS, 2)
             else:
                 rl.dev_set_option(rl.DEV_VP_PATH, 1)
             ws = t.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=t.uint8, device="cuda")
@@ -482,6 +490,7 @@ def test_repeated_calls_bitwise_identical(cuda_lib, kind, W):
     finally:
         rl.dev_set_option(rl.DEV_VP_PATH, 0)
         rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
+        rl.dev_set_option(rl.DEV_VC_ROWS, 0)
         if comm is not None:
             comm.destroy()
     for c in range(1, 5):
