@@ -1250,10 +1250,10 @@ extern "C" rl_status rl_vocab_parallel_logprob(
       // rows parked in shared memory (RS): the exchange window is R + RS - 1 rows
       const bool wide = nv > 6 * kVcCons;
       const int rs_opt = dev_option(OPT_VC_ROWS);  // 0 = default, else RS + 1
-      // default: one parked row across GPUs (the exchange window); none on one rank, where the
-      // records are back within a row and the parked row's shared-memory traffic costs 11 % at the
-      // P = 8 width (0.95 vs 1.06 ms; across 4 GPUs RS = 1 is the faster: 1.55 vs 1.59 ms)
-      const int RS = rs_opt > 0 ? std::min(rs_opt - 1, wide ? 1 : 2) : (P > 1 ? 1 : 0);
+      // default: parked rows across GPUs widen the exchange window (P = 8 width on 4 GPUs: RS = 0 /
+      // 1 / 2 -> 1.59 / 1.55 / 1.47 ms; the wide shards have room for one); none on one rank, where
+      // the records are back within a row and parking costs 11 % at the P = 8 width (0.95 vs 1.06 ms)
+      const int RS = rs_opt > 0 ? std::min(rs_opt - 1, wide ? 1 : 2) : (P > 1 ? (wide ? 1 : 2) : 0);
       const int NVc = wide ? 11 : 6;
       const size_t head = (sizeof(VcShared) + 127) & ~(size_t)127;
       const size_t rowc = (size_t)RS * NVc * kVcCons * 16;

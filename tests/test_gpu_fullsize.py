@@ -307,7 +307,7 @@ R2_ABS = 2.0 ** -16
 
 # ------------------------------------------------------------------------------- C4 vocab-parallel
 @pytest.mark.parametrize("W", [18992, 37984, 151936])
-@pytest.mark.parametrize("path", ["nccl", "peer", "peer_ring", "peer_rs1"])
+@pytest.mark.parametrize("path", ["nccl", "peer", "peer_ring", "peer_rs1", "peer_rs2"])
 def test_vocab_parallel_production_widths(cuda_lib, W, path):
     """rl_vocab_parallel_logprob at P = 1 with the per-rank column width of P = 8 (18,992), P = 4
     (37,984) and the whole vocabulary: the kernels' multi-chunk slice geometry of configs[3], on the
@@ -348,8 +348,8 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
         if path.startswith("peer"):
             assert comm.enable_peer_exchange(N)
             rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 2)
-            if path == "peer_rs1":   # the multi-rank configuration: one row parked in shared memory
-                rl.dev_set_option(rl.DEV_VC_ROWS, 2)
+            if path in ("peer_rs1", "peer_rs2"):   # the multi-rank configurations: rows parked in smem
+                rl.dev_set_option(rl.DEV_VC_ROWS, 2 if path == "peer_rs1" else 3)
         else:
             rl.dev_set_option(rl.DEV_VP_PATH, 1)
         dl = t.empty_like(x)
@@ -405,8 +405,8 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
         if path.startswith("peer"):
             assert comm.enable_peer_exchange(N)
             rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 2)
-            if path == "peer_rs1":   # the multi-rank configuration: one row parked in shared memory
-                rl.dev_set_option(rl.DEV_VC_ROWS, 2)
+            if path in ("peer_rs1", "peer_rs2"):   # the multi-rank configurations: rows parked in smem
+                rl.dev_set_option(rl.DEV_VC_ROWS, 2 if path == "peer_rs1" else 3)
         else:
             rl.dev_set_option(rl.DEV_VP_PATH, 1)
         dl = t.empty_like(x)
