@@ -1,6 +1,6 @@
 """Back-to-back determinism of the vocab-parallel peer path across ranks (development):
-    RL_LIB_PATH=... torchrun --nproc-per-node P tools/race_check.py [--opt key=value ...]
-Every rank holds its shard of the same seeded [4096, 151936] logits; 8 calls with no collective in
+    RL_LIB_PATH=... torchrun --nproc-per-node P tools/race_check.py [--vocab V] [KEY=VALUE ...]
+Every rank holds its shard of the same seeded [4096, V] logits (V = 151936 by default); 8 calls with no collective in
 between; prints, on rank 0, how many log-probs of calls 0..6 differ bitwise from call 7."""
 import os
 import sys
@@ -25,7 +25,8 @@ def main():
         k, v = kv.split("=")
         rl.dev_set_option(int(k), int(v))
     comm = rl.Comm.from_torch()
-    V, N = 151936, 4096
+    V = int(sys.argv[sys.argv.index("--vocab") + 1]) if "--vocab" in sys.argv else 151936
+    N = 4096
     xf = torch.empty((N, V), dtype=torch.bfloat16, device=dev)
     y = torch.empty(N, dtype=torch.int32, device=dev)
     synth.device_logits(xf, V, 0, 4, targets_out=y)
