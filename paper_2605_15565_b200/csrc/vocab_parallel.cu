@@ -686,10 +686,12 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
 // (m_w, S_w = sum e') -> the LAST consumer warp to post its record (a shared-memory counter) combines
 // the 14 warps into c2_r = lse2 of the shard and sends (c2_r, z_y) to every rank (LL words, as vp_ring_kernel) -> the collector warp polls the P
 // records of the row, combines them in rank order (identical on every rank), runs the token
-// epilogue and publishes (s_t, c2, dy, target column).  R - 1 rows after a row was loaded its
-// gradient is written from the cache:  dlogits_v = e'_v q_w,  q_w = s_t 2^(m_w - c2)  (q split
-// into bf16 hi + lo, HMUL2 + HFMA2: one rounding in the product, reading R2), target column
-// dy = s_t (p_y - 1).  So the exchange latency hides behind R - 1 rows of streaming.
+// epilogue and publishes (s_t, c2, dy, target column).  R + RS - 1 rows after a row was loaded its
+// gradient is written from the cache (RS older rows parked in shared memory across GPUs):
+// dlogits_v = e'_v q_w,  q_w = s_t 2^(m_w - c2)  (q split into bf16 hi + lo, HMUL2 + HFMA2: one
+// rounding in the product, reading R2), target column dy = s_t (p_y - 1).  So the exchange latency
+// hides behind R + RS - 1 rows of streaming.  Ring slots are released per thread after the data
+// read from them is in registers (sm100::mbar_release_after).
 //   warps 0..13   consumers (thread t holds vectors t + 448 i, i < NV)
 //   warp 14       lane 0: TMA producer (ring of 28 KB slots) — alone in its warp, so a copy is
 //                 issued the moment a slot frees (sharing the warp with polling lanes starved it)
