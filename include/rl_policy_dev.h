@@ -26,6 +26,10 @@
  *                         hand-written lm_gemm_kernel on tcgen05 (with RL_DEV_LM_PAIR = 2: CTA pairs)
  *   9 RL_DEV_VR_DELAY     vp_ring_kernel rows between the two reads of a row slice (0 = the L2-window
  *                         rule, default; else that many, with one row per service group)
+ *  10 RL_DEV_VC_TMEM     vp_cache_kernel: where the rows awaiting their scale are parked: 0 = default
+ *                         (tensor memory for shards of <= 2,688 vectors on more than one rank, else
+ *                         shared memory), 1 = shared memory, 2 = tensor memory (2 rows at the wide,
+ *                         4 at the narrow widths)
  * Options are read at launch time; set them before the calls they should affect.
  */
 #ifndef RL_POLICY_DEV_H_
@@ -44,6 +48,7 @@ extern "C" {
 #define RL_DEV_LM_PAIR 7
 #define RL_DEV_LM_GEMM 8
 #define RL_DEV_VR_DELAY 9
+#define RL_DEV_VC_TMEM 10
 int32_t rl_dev_set_option(int32_t key, int32_t value);
 #ifdef __cplusplus
 }

@@ -127,7 +127,7 @@ def load():
 
 # development options (include/rl_policy_dev.h): alternative kernels kept for A/B parity tests
 DEV_LOSS_KERNEL, DEV_VP_PATH, DEV_LM_SPLITS, DEV_VP_KERNEL, DEV_VC_GROUPS, DEV_VC_ROWS, DEV_VC_PUB, DEV_LM_PAIR, \
-    DEV_LM_GEMM, DEV_VR_DELAY = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9
+    DEV_LM_GEMM, DEV_VR_DELAY, DEV_VC_TMEM = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
 
 
 def dev_set_option(key: int, value: int) -> int:

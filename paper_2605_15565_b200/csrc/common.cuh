@@ -45,7 +45,8 @@ enum DevOpt {
   OPT_LM_PAIR = 7,      // LM-head kernels: 0 = pairs for the gradient kernel only, 1 = single CTAs, 2 = pairs for both
   OPT_LM_GEMM = 8,      // LM-head backward GEMMs: 0 / 1 = cuBLAS (default), 2 = lm_gemm_kernel (tcgen05)
   OPT_VR_DELAY = 9,     // vp_ring_kernel rows between a slice's two reads (0 = L2-window rule; sets G = 1)
-  OPT_COUNT = 10
+  OPT_VC_TMEM = 10,     // vp_cache_kernel parked rows in tensor memory: 0 = default (on for narrow shards on > 1 rank), 1 = off, 2 = on
+  OPT_COUNT = 11
 };
 int dev_option(int key);
 

@@ -701,8 +701,6 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
 // 16 warps = 4 per SM sub-partition, so each thread may use 128 registers (the NV = 11 cache is 88).
 constexpr int kVcWarps = 14, kVcCons = kVcWarps * 32;
 constexpr int kVcThreads = kVcCons + 64;
-constexpr int kVcChunkVec = 4 * kVcCons;      // 16-B vectors per ring slot (4 per consumer thread)
-constexpr int kVcSlot = kVcChunkVec * 16;      // 28 KB
 constexpr int kVcColl = 0;  // first collector lane
 constexpr int kVcStat = 32, kVcScale = 32;
 
@@ -729,7 +727,26 @@ struct VcShared {
   float zyv[kVcStat];
   float4 sc[kVcScale];  // (s, c2, dy, target column or -1)
   double acc[8][RL_LOSS_STATS_N];  // collector groups' statistics
+  uint32_t tmem_base;              // PK: the parked rows' tensor-memory allocation
 };
+
+// parked rows in tensor memory (PK): thread (warp w, lane l) owns TMEM lane 32 (w % 4) + l; the four
+// warps sharing a sub-partition take disjoint column ranges.  Plain 32-bit stores / loads
+// (tcgen05.st / ld .32x32b.x4: one 16-B vector per thread), no tensor-core work.
+__device__ __forceinline__ void tm_st4(uint32_t taddr, uint4 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+// the caller issues tcgen05.wait::ld before using the registers
+__device__ __forceinline__ uint4 tm_ld4(uint32_t taddr) {
+  uint4 v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(taddr)
+               : "memory");
+  return v;
+}
 
 // warp max in one instruction (redux.sync .f32, sm_100a)
 __device__ __forceinline__ float warp_max_redux(float v) {
@@ -738,8 +755,13 @@ __device__ __forceinline__ float warp_max_redux(float v) {
   return r;
 }
 
-template <int NV, int R, int RS>
+// CV: 16-B vectors per consumer thread per ring slot; PK: the RS parked rows live in tensor memory
+// (1) instead of shared memory (0), which leaves all of shared memory to the copy ring
+template <int NV, int R, int RS, int CV = 4, int PK = 0>
 __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a) {
+  static_assert(!PK || (RS > 0 && ((kVcWarps + 3) / 4) * RS * NV * 4 <= 512), "parked rows exceed 512 TMEM columns");
+  constexpr int CHV = CV * kVcCons;  // vectors per ring slot
+  constexpr int SLOT = CHV * 16;     // ring slot bytes (28 KB at CV = 4)
   using V = ClVec<bf16_t>;
   extern __shared__ __align__(128) unsigned char smem[];
   VcShared& sh = *reinterpret_cast<VcShared*>(smem);
@@ -750,7 +772,7 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
   const int64_t nk = blockIdx.x < a.n ? (a.n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t row_bytes = a.ld * 2;
   const int nvec = (int)(a.Vr / 8);
-  const int nch = (nvec + kVcChunkVec - 1) / kVcChunkVec;
+  const int nch = (nvec + CHV - 1) / CHV;
   const float k = a.kn.inv_t * RL_LOG2E;
   auto row_of = [&](int64_t kk) { return (int64_t)blockIdx.x + kk * gridDim.x; };
   if (tid == 0) {
@@ -769,12 +791,22 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     }
     sm100::fence_mbar_init();
   }
+  if constexpr (PK) {
+    if (threadIdx.x < 32) {  // warp 0 allocates 512 columns (one CTA per SM)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sm100::smem_u32(&sh.tmem_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
   __syncthreads();
+  if constexpr (PK) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t full_s = sm100::smem_u32(full), empty_s = sm100::smem_u32(empty);
   const uint32_t ring_s = sm100::smem_u32(ring);
   // RS older rows of e' parked in shared memory after the ring (thread t's vector i of slot s at
   // ((s NV + i) 448 + t) 16: conflict-free, only the owning thread touches it)
-  const uint32_t rowc_s = ring_s + (uint32_t)a.nslots * (uint32_t)kVcSlot;
+  const uint32_t rowc_s = ring_s + (uint32_t)a.nslots * (uint32_t)SLOT;
+  const uint32_t tmem = PK ? sh.tmem_base : 0u;
 
   if (warp == kVcWarps) {
     if (lane == 0) {  // -------------------------------------------------------- TMA producer
@@ -783,9 +815,9 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         const char* src = reinterpret_cast<const char*>(a.logits) + row_of(kk) * row_bytes;
         for (int c = 0; c < nch; ++c) {
           sm100::mbar_wait_a(empty_s + rp.slot * 8, rp.phase ^ 1);
-          const uint32_t bytes = (uint32_t)min(kVcChunkVec, nvec - c * kVcChunkVec) * 16u;
+          const uint32_t bytes = (uint32_t)min(CHV, nvec - c * CHV) * 16u;
           sm100::mbar_arrive_expect_tx(&full[rp.slot], bytes);
-          sm100::bulk_g2s_nohint(ring + (size_t)rp.slot * kVcSlot, src + (size_t)c * kVcSlot, bytes, &full[rp.slot]);
+          sm100::bulk_g2s_nohint(ring + (size_t)rp.slot * SLOT, src + (size_t)c * SLOT, bytes, &full[rp.slot]);
           rp.advance(1, a.nslots);
         }
       }
@@ -963,17 +995,17 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     // the chunk loop
     uint32_t pend = 0;  // empty-barrier address of the slot awaiting release (0: none)
 #pragma unroll
-    for (int c = 0; c < (NV + 3) / 4; ++c) {
+    for (int c = 0; c < (NV + CV - 1) / CV; ++c) {
       if (c < nch) {
         RL_DCHECK(slot < (uint32_t)a.nslots && row_of(kk) < a.n);
         RL_VC_T0(tf0);
         sm100::mbar_wait_a(full_s + slot * 8, rph);
         if (tid == 0) RL_VC_ADD(1, tf0);
-        const uint32_t sb = ring_s + slot * (uint32_t)kVcSlot;
+        const uint32_t sb = ring_s + slot * (uint32_t)SLOT;
         const uint32_t dprev = dep;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = 4 * c + u;
+        for (int u = 0; u < CV; ++u) {
+          const int i = CV * c + u;
           if (i < NV) {
             const bool ok = i * kVcCons + tid < nvec;
             cache[r][i] = ok ? sm100::lds128_a(sb + u * (kVcCons * 16) + my_off) : V::neg_inf_vec();
@@ -989,8 +1021,8 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         }
       } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (4 * c + u < NV) cache[r][4 * c + u] = V::neg_inf_vec();
+        for (int u = 0; u < CV; ++u)
+          if (CV * c + u < NV) cache[r][CV * c + u] = V::neg_inf_vec();
       }
     }
     // z_y from the raw vector that holds it (its owner thread; compile-time vector index)
@@ -1070,9 +1102,25 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
     const uint32_t ql2 = pack_bf16x2(q - qh, q - qh);
     uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<char*>(a.dlogits) + row * row_bytes) + tid;
     RL_DCHECK(row < a.n && ycol < a.Vr);
+    if constexpr (PK) {
+      // parked in tensor memory: four loads in flight per wait (one tcgen05.wait::ld per 4 vectors)
 #pragma unroll
-    for (int i = 0; i < NV; ++i)
-      st_stream_v4_if(out + i * kVcCons, V::grad_sv(getv(i), qb2, ql2, q), i * kVcCons + tid < nvec);
+      for (int i0 = 0; i0 < NV; i0 += 4) {
+        uint4 t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u < NV) t[u] = getv(i0 + u);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u < NV)
+            st_stream_v4_if(out + (i0 + u) * kVcCons, V::grad_sv(t[u], qb2, ql2, q), (i0 + u) * kVcCons + tid < nvec);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+        st_stream_v4_if(out + i * kVcCons, V::grad_sv(getv(i), qb2, ql2, q), i * kVcCons + tid < nvec);
+    }
     if (st != 0.f && ycol >= 0 && ((ycol >> 3) % kVcCons) == tid)  // same thread, after its vector store
       VecTraits<bf16_t>::store1(reinterpret_cast<char*>(a.dlogits) + row * row_bytes, ycol, dy);
     __syncwarp();
@@ -1098,20 +1146,42 @@ __global__ void __launch_bounds__(kVcThreads, 1) vp_cache_kernel(const VrArgs a)
         constexpr int r = decltype(rc)::value;
         const int64_t p = p0 + r;
         const int64_t g = p - R - RS;
-        if (g >= 0 && g < nk) {
-          const uint32_t base = rowc_s + (uint32_t)((g % RS) * NV * kVcCons) * 16u + my_off;
-          RL_DCHECK(base + (uint32_t)((NV - 1) * kVcCons * 16) < rowc_s + (uint32_t)(RS * NV * kVcCons * 16));
-          grad_vecs(g, [&](int i) { return sm100::lds128_a(base + (uint32_t)(i * kVcCons * 16)); });
-        }
-        const int64_t mv = p - R;
-        if (mv >= 0 && mv < nk) {
-          const uint32_t base = rowc_s + (uint32_t)((mv % RS) * NV * kVcCons) * 16u + my_off;
+        if constexpr (PK) {
+          // TMEM lane 32 (warp % 4) + lane, columns ((warp / 4) RS + slot) 4 NV + 4 i
+          const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * RS * NV * 4);
+          if (g >= 0 && g < nk) {
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            const uint32_t tb = tl + (uint32_t)((g % RS) * NV * 4);
+            grad_vecs(g, [&](int i) { return tm_ld4(tb + (uint32_t)(4 * i)); });
+          }
+          const int64_t mv = p - R;
+          if (mv >= 0 && mv < nk) {
+            const uint32_t tb = tl + (uint32_t)((mv % RS) * NV * 4);
 #pragma unroll
-          for (int i = 0; i < NV; ++i) sm100::sts128(base + (uint32_t)(i * kVcCons * 16), cache[r][i]);
+            for (int i = 0; i < NV; ++i) tm_st4(tb + (uint32_t)(4 * i), cache[r][i]);
+          }
+        } else {
+          if (g >= 0 && g < nk) {
+            const uint32_t base = rowc_s + (uint32_t)((g % RS) * NV * kVcCons) * 16u + my_off;
+            RL_DCHECK(base + (uint32_t)((NV - 1) * kVcCons * 16) < rowc_s + (uint32_t)(RS * NV * kVcCons * 16));
+            grad_vecs(g, [&](int i) { return sm100::lds128_a(base + (uint32_t)(i * kVcCons * 16)); });
+          }
+          const int64_t mv = p - R;
+          if (mv >= 0 && mv < nk) {
+            const uint32_t base = rowc_s + (uint32_t)((mv % RS) * NV * kVcCons) * 16u + my_off;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) sm100::sts128(base + (uint32_t)(i * kVcCons * 16), cache[r][i]);
+          }
         }
         if (p < nk) load_row(rc, p);
       });
     }
+  }
+  if constexpr (PK) {  // every consumer warp is done with its parked rows -> warp 0 frees the columns
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(kVcCons) : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 #ifdef RL_VC_TRACE
   if (tid == 0 && blockIdx.x < 256) {  // 6: consumer thread 0's cycles in the kernel, 7: SM id
@@ -1255,14 +1325,24 @@ extern "C" rl_status rl_vocab_parallel_logprob(
       // default: parked rows across GPUs widen the exchange window (P = 8 width on 4 GPUs: RS = 0 /
       // 1 / 2 -> 1.59 / 1.55 / 1.47 ms; the wide shards have room for one); none on one rank, where
       // the records are back within a row and parking costs 11 % at the P = 8 width (0.95 vs 1.06 ms)
-      const int RS = rs_opt > 0 ? std::min(rs_opt - 1, wide ? 1 : 2) : (P > 1 ? (wide ? 1 : 2) : 0);
+      // parked rows in tensor memory (RL_DEV_VC_TMEM: 0 default, 1 off, 2 on): RS = 2 wide / 4 narrow
+      // rows, all of shared memory left to the ring.  Default on more than one rank at the narrow
+      // (P >= 8) widths: P = 8 width on 4 GPUs 1.37 ms against 1.47 with two rows in shared memory
+      // (and 1.54 for the ring); the wide shards lose (2.14 vs 2.12 ms across GPUs, 1.87 vs 1.64 on one)
+      const int tm_opt = dev_option(OPT_VC_TMEM);
+      const bool pk = tm_opt == 2 || (tm_opt == 0 && P > 1 && !wide);
+      const int RS = pk ? (wide ? 2 : 4)
+                        : rs_opt > 0 ? std::min(rs_opt - 1, 2) : (P > 1 ? (wide ? 1 : 2) : 0);
+      // two parked wide rows in shared memory leave 62 KB of ring: 14 KB slots (CV = 2)
+      const int slot_b = (!pk && wide && RS == 2 ? 2 : 4) * kVcCons * 16;
       const int NVc = wide ? 11 : 6;
       const size_t head = (sizeof(VcShared) + 127) & ~(size_t)127;
-      const size_t rowc = (size_t)RS * NVc * kVcCons * 16;
-      v.nslots = (int)((kSmemMax - head - rowc - 256) / (kVcSlot + 16));
+      const size_t rowc = pk ? 0 : (size_t)RS * NVc * kVcCons * 16;
+      v.nslots = (int)((kSmemMax - head - rowc - 256) / (slot_b + 16));
       const size_t smem = ((sizeof(VcShared) + 16 * (size_t)v.nslots + 127) & ~(size_t)127) +
-                          (size_t)v.nslots * kVcSlot + rowc;
-      auto kern = wide ? (RS == 1 ? vp_cache_kernel<11, 2, 1> : vp_cache_kernel<11, 2, 0>)
+                          (size_t)v.nslots * slot_b + rowc;
+      auto kern = pk ? (wide ? vp_cache_kernel<11, 2, 2, 4, 1> : vp_cache_kernel<6, 3, 4, 4, 1>)
+                : wide ? (RS == 2 ? vp_cache_kernel<11, 2, 2, 2> : RS == 1 ? vp_cache_kernel<11, 2, 1> : vp_cache_kernel<11, 2, 0>)
                        : (RS == 2 ? vp_cache_kernel<6, 3, 2> : RS == 1 ? vp_cache_kernel<6, 3, 1>
                                                                       : vp_cache_kernel<6, 3, 0>);
       v.G = std::min(8, std::max(0, dev_option(OPT_VC_GROUPS)));

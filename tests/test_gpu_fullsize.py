@@ -307,7 +307,7 @@ R2_ABS = 2.0 ** -16
 
 # ------------------------------------------------------------------------------- C4 vocab-parallel
 @pytest.mark.parametrize("W", [18992, 37984, 151936])
-@pytest.mark.parametrize("path", ["nccl", "peer", "peer_ring", "peer_rs1", "peer_rs2"])
+@pytest.mark.parametrize("path", ["nccl", "peer", "peer_ring", "peer_rs1", "peer_rs2", "peer_tmem"])
 def test_vocab_parallel_production_widths(cuda_lib, W, path):
     """rl_vocab_parallel_logprob at P = 1 with the per-rank column width of P = 8 (18,992), P = 4
     (37,984) and the whole vocabulary: the kernels' multi-chunk slice geometry of configs[3], on the
@@ -350,6 +350,8 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
             rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 2)
             if path in ("peer_rs1", "peer_rs2"):   # the multi-rank configurations: rows parked in smem
                 rl.dev_set_option(rl.DEV_VC_ROWS, 2 if path == "peer_rs1" else 3)
+            if path == "peer_tmem":   # rows parked in tensor memory
+                rl.dev_set_option(rl.DEV_VC_TMEM, 2)
         else:
             rl.dev_set_option(rl.DEV_VP_PATH, 1)
         dl = t.empty_like(x)
@@ -367,6 +369,7 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
         rl.dev_set_option(rl.DEV_VP_PATH, 0)
         rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
         rl.dev_set_option(rl.DEV_VC_ROWS, 0)
+        rl.dev_set_option(rl.DEV_VC_TMEM, 0)
         comm.destroy()
     g_lp = logp.cpu().numpy()
     assert np.all(np.abs(g_lp - lp_all) <= LOGP_ATOL), np.abs(g_lp - lp_all).max()
@@ -380,7 +383,7 @@ def test_vocab_parallel_production_widths(cuda_lib, W, path):
 # ------------------------------------------------------------------------------- vocab-parallel edge cases
 @pytest.mark.parametrize("N", [1, 7, 149, 1000])
 @pytest.mark.parametrize("W", [8, 1000, 1004, 18992])
-@pytest.mark.parametrize("path", ["peer", "peer_ring", "peer_rs1", "nccl"])
+@pytest.mark.parametrize("path", ["peer", "peer_ring", "peer_rs1", "peer_tmem", "nccl"])
 def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
     """Few rows (fewer than the 148 CTAs: idle CTAs, one row per CTA), a single 16-B vector per row
     (W = 8), widths with and without whole vectors per consumer thread, on both peer kernels and the
@@ -407,6 +410,8 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
             rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if path == "peer_ring" else 2)
             if path in ("peer_rs1", "peer_rs2"):   # the multi-rank configurations: rows parked in smem
                 rl.dev_set_option(rl.DEV_VC_ROWS, 2 if path == "peer_rs1" else 3)
+            if path == "peer_tmem":   # rows parked in tensor memory
+                rl.dev_set_option(rl.DEV_VC_TMEM, 2)
         else:
             rl.dev_set_option(rl.DEV_VP_PATH, 1)
         dl = t.empty_like(x)
@@ -421,6 +426,7 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
         rl.dev_set_option(rl.DEV_VP_PATH, 0)
         rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
         rl.dev_set_option(rl.DEV_VC_ROWS, 0)
+        rl.dev_set_option(rl.DEV_VC_TMEM, 0)
         comm.destroy()
     out = oracle.policy_loss_fwd_bwd(oracle.decode_bf16(bits), y, old, mask, tseq, adv.astype(np.float64), None,
                                      None, oracle.LossParams(agg=oracle.AGG_SUM))
@@ -444,7 +450,7 @@ def test_vocab_parallel_edge_shapes(cuda_lib, N, W, path):
 
 # ------------------------------------------------------------------------------- determinism
 @pytest.mark.parametrize("kind,W", [("sv", 151936), ("peer", 37984), ("peer", 18992), ("peer_rs1", 18992),
-                                    ("peer_ring", 37984), ("nccl", 37984)])
+                                    ("peer_tmem", 37984), ("peer_tmem", 18992), ("peer_ring", 37984), ("nccl", 37984)])
 def test_repeated_calls_bitwise_identical(cuda_lib, kind, W):
     """Five back-to-back calls on the same inputs give bit-identical log-probs, statistics and
     dlogits (the reduction order is fixed, §8(a) a6).  Guards the TMA-ring consumer protocol: a warp
@@ -477,6 +483,8 @@ def test_repeated_calls_bitwise_identical(cuda_lib, kind, W):
                 rl.dev_set_option(rl.DEV_VP_KERNEL, 1 if kind == "peer_ring" else 2)
                 if kind == "peer_rs1":
                     rl.dev_set_option(rl.DEV_VC_ROWS, 2)
+                if kind == "peer_tmem":
+                    rl.dev_set_option(rl.DEV_VC_TMEM, 2)
             else:
                 rl.dev_set_option(rl.DEV_VP_PATH, 1)
             ws = t.empty(rl.vocab_parallel_workspace_size(N, 1), dtype=t.uint8, device="cuda")
@@ -491,6 +499,7 @@ def test_repeated_calls_bitwise_identical(cuda_lib, kind, W):
         rl.dev_set_option(rl.DEV_VP_PATH, 0)
         rl.dev_set_option(rl.DEV_VP_KERNEL, 0)
         rl.dev_set_option(rl.DEV_VC_ROWS, 0)
+        rl.dev_set_option(rl.DEV_VC_TMEM, 0)
         if comm is not None:
             comm.destroy()
     for c in range(1, 5):

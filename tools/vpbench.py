@@ -41,6 +41,8 @@ def main():
             rl.dev_set_option(rl.DEV_VC_PUB, int(sys.argv[sys.argv.index("--pub") + 1]) + 1)
         if "--delay" in sys.argv:  # vp_ring_kernel rows between a slice's two reads
             rl.dev_set_option(rl.DEV_VR_DELAY, int(sys.argv[sys.argv.index("--delay") + 1]))
+        if "--tmem" in sys.argv:  # parked rows in tensor memory
+            rl.dev_set_option(rl.DEV_VC_TMEM, 2)
         if "--rs" in sys.argv:   # rows parked in shared memory
             rl.dev_set_option(rl.DEV_VC_ROWS, int(sys.argv[sys.argv.index("--rs") + 1]) + 1)
     else:
