@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kVtThreads, 1) vp_finish_tma_kernel(
 // after every peer finished call e (finishing e + 1 needs every peer's e + 1 records), so a slot
 // is never rewritten while a peer may still read it.  A peer that never publishes (a dead rank)
 // ends the kernel with __trap() after kVrTimeoutNs, which surfaces as RL_ERR_CUDA.
-constexpr int kVrCons = 480, kVrThreads = 544, kVrVpt = 4;  // 15 consumer warps + producer + service
+constexpr int kVrCons = 480, kVrThreads = 576, kVrVpt = 4;  // 15 consumer warps + producer + 2 service
 constexpr int kVrSlot = kVrVpt * kVrCons * 16;              // 30 KB ring slot
 constexpr int kVrChunkVec = kVrVpt * kVrCons;               // 16-B vectors per slot
 constexpr int kVrStat = 32;                                 // row stats slots
@@ -409,7 +409,10 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
     return;
   }
 
-  if (warp == 16) {  // ------------------------------------------------------------- service
+  if (warp >= 16) {  // ------------------------------------------------ service: warp 16 (A), warp 17 (B)
+    // (A) and (B) run in their own warps, so a row's scale never waits behind the next row's
+    // publication (at D = 1, P = 2, the serial order exposed the service latency every row)
+    const bool pubw = warp == 16;
     const int G = a.G, P = a.P;
     const int rl_ = lane / P, ql = lane % P;  // this lane: row rl_ of a group, rank ql
     const bool lane_on = rl_ < G;
@@ -435,8 +438,8 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
       }
     };
     load_l1(0);
-    for (int64_t g = 0; g < ngr + a.LG; ++g) {
-      if (g < ngr) {  // ---- (A) publish the records of group g
+    for (int64_t g = 0; g < ngr; ++g) {
+      if (pubw) {  // ---- (A) publish the records of group g
         for (int r = 0; r < G; ++r) {
           const int64_t kk = g * G + r;
           if (kk >= nk) break;
@@ -460,8 +463,8 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
           st_ll2(a.xr[ql] + ((int64_t)a.me * a.max_tokens + row_of(kk)) * 2, ep | __float_as_uint(my_c2),
                  ep | __float_as_uint(my_zy));
       }
-      if (g >= a.LG) {  // ---- (B) combine group g - LG, run the epilogue, publish the scales
-        const int64_t gb = g - a.LG;
+      if (!pubw) {  // ---- (B) combine group g, run the epilogue, publish the scales
+        const int64_t gb = g;
         const int64_t kk = gb * G + rl_;
         const bool has = lane_on && kk < nk;
         const int64_t row = has ? row_of(kk) : 0;
@@ -540,6 +543,7 @@ __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) 
         }
       }
     }
+    if (pubw) return;
     for (int i = 0; i < RL_LOSS_STATS_N; ++i) sh.acc[lane][i] = acc.v[i];
     __syncwarp();
     if (lane < RL_LOSS_STATS_N) {  // lane-ordered (deterministic) sum of the row leaders' statistics
