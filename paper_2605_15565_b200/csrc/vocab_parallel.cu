@@ -264,9 +264,7 @@ __global__ void __launch_bounds__(kVtThreads, 1) vp_finish_tma_kernel(
 // after every peer finished call e (finishing e + 1 needs every peer's e + 1 records), so a slot
 // is never rewritten while a peer may still read it.  A peer that never publishes (a dead rank)
 // ends the kernel with __trap() after kVrTimeoutNs, which surfaces as RL_ERR_CUDA.
-constexpr int kVrCons = 480, kVrThreads = 576, kVrVpt = 4;  // 15 consumer warps + producer + 2 service
-constexpr int kVrSlot = kVrVpt * kVrCons * 16;              // 30 KB ring slot
-constexpr int kVrChunkVec = kVrVpt * kVrCons;               // 16-B vectors per slot
+constexpr int kVrCons = 480, kVrThreads = 576;  // 15 consumer warps + producer + 2 service warps
 constexpr int kVrStat = 32;                                 // row stats slots
 constexpr int kVrScale = 32;                                // row scale slots
 constexpr long long kVrTimeoutNs = 30LL * 1000 * 1000 * 1000;
@@ -349,8 +347,14 @@ struct VrGrad<float> {
   }
 };
 
-template <typename T>
+// VPT: 16-B vectors per consumer thread per ring slot (4: 30 KB slots, 5: 37.5 KB), chosen on the host
+// so the slot count covers the row slice with the least idle tail (P = 4 / 8 widths: 5; 2 chunks of
+// 2,400 vectors for 4,748, where 4 left the third chunk 47 % full)
+template <typename T, int VPT>
 __global__ void __launch_bounds__(kVrThreads, 1) vp_ring_kernel(const VrArgs a) {
+  constexpr int kVrVpt = VPT;
+  constexpr int kVrChunkVec = VPT * kVrCons;   // 16-B vectors per slot
+  constexpr int kVrSlot = kVrChunkVec * 16;    // slot bytes
   constexpr int EPV = VecTraits<T>::EPV;
   extern __shared__ __align__(128) unsigned char smem[];
   VrShared& sh = *reinterpret_cast<VrShared*>(smem);
@@ -1362,10 +1366,19 @@ extern "C" rl_status rl_vocab_parallel_logprob(
     }
     const int64_t slice_bytes = (vocab_shard / (16 / eb)) * 16;
     vr_geometry(P, std::max<int64_t>(slice_bytes, 16), grid, &v.G, &v.LG, &v.D);
+    // vectors per thread per slot: the fewest idle tail lanes (ties: the smaller slot, more of them)
+    const int64_t nvec_r = vocab_shard / (16 / eb);
+    auto waste = [&](int vpt) {
+      const int64_t cv = (int64_t)vpt * kVrCons;
+      return ((nvec_r + cv - 1) / cv) * cv - nvec_r;
+    };
+    const int vpt = waste(5) < waste(4) ? 5 : 4;
+    const int slot_b = vpt * kVrCons * 16;
     const size_t head = (sizeof(VrShared) + 127) & ~(size_t)127;
-    v.nslots = (int)((kSmemMax - head - 256) / (kVrSlot + 16));
-    const size_t smem = ((sizeof(VrShared) + 16 * (size_t)v.nslots + 127) & ~(size_t)127) + (size_t)v.nslots * kVrSlot;
-    auto kern = dtype == RL_BF16 ? vp_ring_kernel<bf16_t> : vp_ring_kernel<float>;
+    v.nslots = (int)((kSmemMax - head - 256) / (slot_b + 16));
+    const size_t smem = ((sizeof(VrShared) + 16 * (size_t)v.nslots + 127) & ~(size_t)127) + (size_t)v.nslots * slot_b;
+    auto kern = dtype == RL_BF16 ? (vpt == 5 ? vp_ring_kernel<bf16_t, 5> : vp_ring_kernel<bf16_t, 4>)
+                                 : (vpt == 5 ? vp_ring_kernel<float, 5> : vp_ring_kernel<float, 4>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return check_launch("cudaFuncSetAttribute(vp_ring_kernel)");
     kern<<<grid, kVrThreads, smem, s>>>(v);
