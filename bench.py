@@ -558,10 +558,9 @@ def main():
             parallelism = (f"ONE GPU doing one rank's share of a {args.vp_width_of}-way vocabulary split "
                            f"({wl.Vr} columns as its own vocabulary, exchange with itself)")
         fits = wl.Vr % 8 == 0 and wl.Vr // 8 <= 11 * 448
-        # the library's choice (vocab_parallel.cu): the register cache when the shard fits it, except
-        # wide shards (> 6 x 448 vectors) on more than one rank; --vp-kernel cache / ring force one
-        use_cache = fits and (args.vp_kernel == "cache" or
-                              (args.vp_kernel == "auto" and (world == 1 or wl.Vr // 8 <= 6 * 448)))
+        # the library's choice (vocab_parallel.cu): the register cache on one rank when the shard fits
+        # it, the ring on more; --vp-kernel cache / ring force one
+        use_cache = fits and (args.vp_kernel == "cache" or (args.vp_kernel == "auto" and world == 1))
         vk = "vp_cache_kernel" if use_cache else "vp_ring_kernel"
         kname = "rl_vocab_parallel_logprob (" + (f"{vk}, in-kernel peer exchange" if fused_vp
                                                  else "vp_stats + NCCL all-gather + vp_finish") + ")"

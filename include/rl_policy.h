@@ -265,11 +265,10 @@ rl_status rl_comm_allreduce_f64(rl_comm* c, double* buf, size_t n, rl_stream str
  * the same path.  Afterwards rl_vocab_parallel_logprob with the fused loss runs as ONE kernel per
  * rank that sends each row's shard record (log2-domain lse of the shard, target logit) to every
  * rank as two 8-byte words tagged with the call's epoch (slots double-buffered by epoch parity)
- * and polls the peers' records inside the kernel: vp_cache_kernel for bf16 shards of <= 4,928
- * whole 16-B vectors (row slices held in registers: logits read once, one exp per element) —
- * on more than one rank only for shards of <= 2,688 vectors (the P >= 8 widths of V = 151936) —
- * vp_ring_kernel otherwise (slices re-read from L2: a ~14 us exchange window that absorbs the
- * cross-GPU lockstep jitter).  A rank that never publishes makes its peers
+ * and polls the peers' records inside the kernel: vp_ring_kernel (slices re-read from L2: a ~14 us
+ * exchange window that absorbs the cross-GPU lockstep jitter); on a single rank
+ * vp_cache_kernel for bf16 shards of <= 4,928 whole 16-B vectors (row slices held in registers:
+ * logits read once, one exp per element).  A rank that never publishes makes its peers
  * trap after 30 s (RL_ERR_CUDA) instead of hanging.  Returns RL_ERR_UNSUPPORTED (and leaves the
  * NCCL path in use on every rank) if a peer is not P2P-accessible; > 8 ranks are unsupported.
  * The buffers are released by rl_comm_destroy; calling it again re-maps (collective). */

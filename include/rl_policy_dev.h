@@ -11,10 +11,10 @@
  *                         rl_comm_enable_peer_exchange succeeded (default), 1 = NCCL path
  *   2 RL_DEV_LM_SPLITS    rl_lmhead_logprob vocabulary splits: 0 = cost model (default), else
  *                         the split count (clamped to what the workspace holds)
- *   3 RL_DEV_VP_KERNEL    peer-exchange vocab-parallel kernel: 0 = default (register-cache kernel
- *                         when the shard fits it, except shards of > 2,688 vectors on > 1 rank,
- *                         which take the ring), 1 = the L2 re-read ring kernel, 2 = the register-
- *                         cache kernel whenever the shard fits it
+ *   3 RL_DEV_VP_KERNEL    peer-exchange vocab-parallel kernel: 0 = default (the L2 re-read ring
+ *                         kernel on more than one rank; on one rank the register-cache kernel when
+ *                         the shard fits it), 1 = the ring kernel, 2 = the register-cache kernel
+ *                         whenever the shard fits it
  *   4 RL_DEV_VC_GROUPS    vp_cache_kernel collector groups (0 = min(8, 32 / P))
  *   5 RL_DEV_VC_ROWS      vp_cache_kernel rows parked in shared memory + 1 (0 = default)
  *   6 RL_DEV_VC_PUB       vp_cache_kernel record send + 1: 0 collector (strong stores), 1 last

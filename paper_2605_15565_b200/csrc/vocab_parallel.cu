@@ -1320,12 +1320,13 @@ extern "C" rl_status rl_vocab_parallel_logprob(
     // bf16 shards of <= 4800 whole vectors: the register-cache kernel (one read, one exp2 per
     // element); anything else: the L2 re-read ring kernel (same exchange protocol)
     const int64_t nv = vocab_shard / 8;
-    // Across GPUs the register cache's exchange window (R + RS - 1 rows) is too short for the wide
-    // (NV = 11, P <= 4) shards: the L2 ring's window is ~48 MB (4 x B200, P = 4: ring 2.13 ms, cache
-    // 2.24 ms; one GPU: cache 1.68-1.74 ms, ring 2.12 ms) — so wide shards take the ring on P > 1
+    // Across GPUs the register cache's exchange window (R + RS - 1 rows) does not absorb the ranks'
+    // lockstep jitter, the L2 ring's (~14 us) does: 4 x B200, P = 4 width: ring 1.84 ms, cache 2.12;
+    // P = 8 width: ring 1.09, cache 1.37 (rows parked in tensor memory).  One rank: cache 1.64 / 0.95,
+    // ring 1.83 / 1.10.  So the cache on one rank, the ring on more.
     const int vk = dev_option(OPT_VP_KERNEL);  // 0 default, 1 ring, 2 cache whenever it fits
     const bool cache_fits = dtype == RL_BF16 && vocab_shard % 8 == 0 && nv >= 1 && nv <= 11 * kVcCons;
-    const bool use_cache = cache_fits && (vk == 2 || (vk == 0 && (P == 1 || nv <= 6 * kVcCons)));
+    const bool use_cache = cache_fits && (vk == 2 || (vk == 0 && P == 1));
     if (use_cache) {
       // rows parked in shared memory (RS): the exchange window is R + RS - 1 rows
       const bool wide = nv > 6 * kVcCons;
