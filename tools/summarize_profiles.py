@@ -25,11 +25,12 @@ KERNELS = {
                            "(tools/vpbench.py --peer)", rows=65536, bytes_per_row=2 * 18992 * 2 + 17, bench_rows=65536),
     "vpcache4": dict(title="vp_cache_kernel<11,2>: one rank's shard at P = 4, 65,536 rows x 37,984 columns",
                      rows=65536, bytes_per_row=2 * 37984 * 2 + 17, bench_rows=65536),
-    "ring4": dict(title="vp_ring_kernel (L2 re-read, D = 3): one rank's shard at P = 4, 65,536 rows x 37,984 "
-                        "columns (tools/vpbench.py --peer --ring; the default across 4 GPUs)",
+    "ring4": dict(title="vp_ring_kernel (L2 re-read, D = 3, 5-vector slots, two service warps): one rank's shard "
+                        "at P = 4, 65,536 rows x 37,984 columns (tools/vpbench.py --peer --ring; the default "
+                        "across 4 GPUs)",
                   rows=65536, bytes_per_row=2 * 37984 * 2 + 17, bench_rows=65536),
-    "ring2": dict(title="vp_ring_kernel (L2 re-read, D = 1): one rank's shard at P = 2, 65,536 rows x 75,968 "
-                        "columns (the default across 2 GPUs)",
+    "ring2": dict(title="vp_ring_kernel (L2 re-read, D = 1, two service warps): one rank's shard at P = 2, "
+                        "65,536 rows x 75,968 columns (the default across 2 GPUs)",
                   rows=65536, bytes_per_row=2 * 75968 * 2 + 17, bench_rows=65536),
     "lmgrad": dict(title="lmhead_kernel<grad>: logits recompute + G = s (p - onehot), 8,192 tokens x d 4,096 x "
                          "V 151,936 (one backward chunk of tools/lmbench.py --bwd)", tokens=8192, d=4096, V=151936),
